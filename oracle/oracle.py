@@ -1,0 +1,165 @@
+"""ctypes wrapper of the CPU oracle (oracle/mem_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.  The product package
+(paper_2309_16818_b200) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "mem_oracle.c")
+LIB = os.path.join(HERE, "libmem_oracle.so")
+# D29: IEEE fp32/fp64, round-to-nearest, no FMA contraction, no fast-math.
+CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math", "-fopenmp"]
+
+AVERAGE, GAUSSIAN, CLASS_AVERAGE, CLASS_BAYESIAN, CLASS_MAX, COLOR = range(6)
+INLIER, OUTLIER, NONFINITE, RANGE, HEIGHT, OOB = range(6)
+STAT_NAMES = ["n_input", "n_nonfinite", "n_range", "n_height", "n_oob", "n_inlier", "n_outlier",
+              "n_cells_touched"]
+
+
+class _Spec(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("rule", C.c_int), ("n_channels", C.c_int), ("w", C.c_float),
+                ("sigma_f2", C.c_float), ("mu0", C.c_float), ("sigma0_2", C.c_float), ("alpha0", C.c_float)]
+
+
+class _Bind(C.Structure):
+    _fields_ = [("ch_offset", C.c_int), ("n_ch", C.c_int), ("group", C.c_int)]
+
+
+class _Noise(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("a", "b", "r_min", "r_max", "h_min", "h_max", "tau2", "v_out")]
+
+
+def build(force=False):
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", LIB, SRC, "-lm"])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        vp = C.c_void_p
+        L.om_create.restype = vp
+        L.om_create.argtypes = [C.c_float, C.c_int, C.c_int, C.POINTER(_Spec), C.c_int, C.POINTER(C.c_int)]
+        L.om_destroy.argtypes = [vp]
+        L.om_input_pointcloud.argtypes = [vp, vp, C.c_long, C.c_int, C.POINTER(_Bind), C.c_int,
+                                          C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(_Noise),
+                                          vp, vp]
+        L.om_input_image.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(_Bind), C.c_int,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.om_move_to.argtypes = [vp, C.c_double, C.c_double]
+        L.om_get_layer.argtypes = [vp, C.c_char_p, vp]
+        L.om_set_layer.argtypes = [vp, C.c_char_p, vp]
+        L.om_get_stats.argtypes = [vp, vp]
+        L.om_get_center.argtypes = [vp, vp]
+        _lib = L
+    return _lib
+
+
+def _dbl(a, n):
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    assert a.size == n
+    return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, what):
+        super().__init__(f"{what}: oracle status {status}")
+        self.status = status
+
+
+def make_binds(bindings):
+    arr = (_Bind * max(1, len(bindings)))()
+    for i, (off, n, g) in enumerate(bindings):
+        arr[i] = _Bind(off, n, g)
+    return arr
+
+
+class OracleMap:
+    """One map of the oracle. groups: list of dicts(name, rule, n_channels, w, sigma_f2, mu0, sigma0_2, alpha0)."""
+
+    def __init__(self, res, rows, cols, groups=()):
+        L = lib()
+        self.rows, self.cols, self.res = rows, cols, res
+        self._names = [g["name"].encode() for g in groups]
+        specs = (_Spec * max(1, len(groups)))()
+        for i, g in enumerate(groups):
+            specs[i] = _Spec(self._names[i], g["rule"], g.get("n_channels", 1), g.get("w", 1.0),
+                             g.get("sigma_f2", 1.0), g.get("mu0", 0.0), g.get("sigma0_2", 1.0),
+                             g.get("alpha0", 1.0))
+        st = C.c_int(0)
+        self._h = L.om_create(C.c_float(res), rows, cols, specs, len(groups), C.byref(st))
+        if not self._h:
+            raise OracleError(st.value, "om_create")
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().om_destroy(self._h)
+            self._h = None
+
+    def input_pointcloud(self, pts, bindings, R, t, noise, debug=False):
+        pts = np.ascontiguousarray(pts, np.float32)
+        n, stride = pts.shape
+        Rr, Rp = _dbl(R, 9)
+        tt, tp = _dbl(t, 3)
+        nz = _Noise(**noise)
+        cell = np.empty(n, np.int32) if debug else None
+        code = np.empty(n, np.uint8) if debug else None
+        st = lib().om_input_pointcloud(self._h, pts.ctypes.data, n, stride, make_binds(bindings), len(bindings),
+                                       Rp, tp, C.byref(nz), cell.ctypes.data if debug else None,
+                                       code.ctypes.data if debug else None)
+        if st != 0:
+            raise OracleError(st, "om_input_pointcloud")
+        return (cell, code) if debug else None
+
+    def input_image(self, img, bindings, K, R, t):
+        img = np.ascontiguousarray(img, np.float32)
+        Cc, H, W = img.shape
+        Kr, Kp = _dbl(K, 9)
+        Rr, Rp = _dbl(R, 9)
+        tt, tp = _dbl(t, 3)
+        st = lib().om_input_image(self._h, img.ctypes.data, Cc, H, W, make_binds(bindings), len(bindings),
+                                  Kp, Rp, tp)
+        if st != 0:
+            raise OracleError(st, "om_input_image")
+
+    def move_to(self, x, y):
+        st = lib().om_move_to(self._h, C.c_double(x), C.c_double(y))
+        if st != 0:
+            raise OracleError(st, "om_move_to")
+
+    def get_layer(self, name):
+        out = np.empty((self.rows, self.cols), np.float32)
+        st = lib().om_get_layer(self._h, name.encode(), out.ctypes.data)
+        if st != 0:
+            raise OracleError(st, f"om_get_layer({name})")
+        return out
+
+    def set_layer(self, name, values):
+        v = np.ascontiguousarray(np.broadcast_to(np.asarray(values, np.float32), (self.rows, self.cols)))
+        st = lib().om_set_layer(self._h, name.encode(), v.ctypes.data)
+        if st != 0:
+            raise OracleError(st, f"om_set_layer({name})")
+
+    def stats(self):
+        out = np.zeros(8, np.uint64)
+        lib().om_get_stats(self._h, out.ctypes.data)
+        return dict(zip(STAT_NAMES, (int(x) for x in out)))
+
+    def center(self):
+        out = np.zeros(2, np.int64)
+        lib().om_get_center(self._h, out.ctypes.data)
+        return int(out[0]), int(out[1])

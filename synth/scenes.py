@@ -1,0 +1,294 @@
+"""Seeded synthetic scenes and sensors for the MEM hot path (SURVEY.md §8(d) recipes).
+
+This module is the ONLY code shared by the oracle side and the CUDA side of the tests:
+it makes input bytes (points, images, poses, trajectories) and holds none of the
+method's arithmetic (no binning, no filtering, no fusion).  Every generator takes an
+explicit seed and returns float32 arrays in the layouts the C-ABI takes:
+
+* point cloud: (N, stride) float32, AoS, xyz in the SENSOR frame then channels;
+  a packed colour channel is 0x00RRGGBB bit-cast into float32 (reading D20);
+* image: (C, H, W) float32, CHW;
+* pose: R (3x3 float64, sensor->map), t (3, float64).
+
+Scenes are 2.5D analytic height fields: a ground plane z = 0 plus
+axis-aligned boxes and one ramp, each with a class id and an RGB colour.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GROUND_CLASS = 0
+
+
+@dataclass
+class Box:
+    x0: float
+    x1: float
+    y0: float
+    y1: float
+    height: float
+    cls: int
+    rgb: tuple
+
+
+@dataclass
+class Ramp:
+    """Inclined patch z = slope * (x - x0) over [x0, x1] x [y0, y1] (top surface only)."""
+    x0: float
+    x1: float
+    y0: float
+    y1: float
+    slope: float
+    cls: int
+    rgb: tuple
+
+
+@dataclass
+class Scene:
+    boxes: list = field(default_factory=list)
+    ramps: list = field(default_factory=list)
+    ground_rgb: tuple = (90, 140, 60)
+    ground_rgb2: tuple = (110, 160, 80)  # checker texture on the ground (1 m squares)
+
+    # ---- height field and per-location attributes (world frame) ----
+    def height(self, x, y):
+        x = np.asarray(x, np.float64)
+        y = np.asarray(y, np.float64)
+        h = np.zeros(np.broadcast(x, y).shape)
+        for b in self.boxes:
+            inside = (x >= b.x0) & (x < b.x1) & (y >= b.y0) & (y < b.y1)
+            h = np.where(inside, np.maximum(h, b.height), h)
+        for r in self.ramps:
+            inside = (x >= r.x0) & (x < r.x1) & (y >= r.y0) & (y < r.y1)
+            h = np.where(inside, np.maximum(h, r.slope * (x - r.x0)), h)
+        return h
+
+    def attributes(self, x, y, z):
+        """class id and rgb (uint8 x3) of the surface point (x, y, z)."""
+        x = np.asarray(x, np.float64)
+        y = np.asarray(y, np.float64)
+        checker = ((np.floor(x) + np.floor(y)) % 2 == 0)
+        cls = np.full(x.shape, GROUND_CLASS, np.int32)
+        rgb = np.where(checker[..., None], np.array(self.ground_rgb), np.array(self.ground_rgb2))
+        for r in self.ramps:
+            inside = (x >= r.x0) & (x < r.x1) & (y >= r.y0) & (y < r.y1) & (z > 0.02)
+            cls = np.where(inside, r.cls, cls)
+            rgb = np.where(inside[..., None], np.array(r.rgb), rgb)
+        for b in self.boxes:
+            # points on or in the box (its top or its sides)
+            inside = (x >= b.x0 - 1e-6) & (x <= b.x1 + 1e-6) & (y >= b.y0 - 1e-6) & (y <= b.y1 + 1e-6) & (z > 0.02)
+            cls = np.where(inside, b.cls, cls)
+            rgb = np.where(inside[..., None], np.array(b.rgb), rgb)
+        return cls, rgb.astype(np.uint8)
+
+    # ---- analytic ray casting (sensor simulation, not the method) ----
+    def raycast(self, o, d, t_max=100.0):
+        """first hit distance along unit rays d (N,3) from origin o (3,); inf if none."""
+        o = np.asarray(o, np.float64)
+        d = np.asarray(d, np.float64)
+        n = d.shape[0]
+        best = np.full(n, np.inf)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            # ground plane z = 0
+            t = -o[2] / d[:, 2]
+            ok = (d[:, 2] < 0) & (t > 0)
+            best = np.where(ok, np.minimum(best, t), best)
+            for b in self.boxes:
+                lo = np.array([b.x0, b.y0, 0.0])
+                hi = np.array([b.x1, b.y1, b.height])
+                t1 = (lo - o) / d
+                t2 = (hi - o) / d
+                tmin = np.nanmax(np.minimum(t1, t2), axis=1)
+                tmax = np.nanmin(np.maximum(t1, t2), axis=1)
+                ok = (tmax >= tmin) & (tmin > 0)
+                best = np.where(ok, np.minimum(best, tmin), best)
+            for r in self.ramps:
+                # plane z = slope (x - x0)  <=>  slope*x - z = slope*x0
+                nrm = np.array([r.slope, 0.0, -1.0])
+                den = d @ nrm
+                t = (r.slope * r.x0 - o @ nrm) / den
+                p = o + t[:, None] * d
+                ok = (t > 0) & (p[:, 0] >= r.x0) & (p[:, 0] < r.x1) & (p[:, 1] >= r.y0) & (p[:, 1] < r.y1)
+                best = np.where(ok, np.minimum(best, t), best)
+        best = np.where(best <= t_max, best, np.inf)
+        return best
+
+
+def rot_z(yaw):
+    c, s = math.cos(yaw), math.sin(yaw)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
+def rot_y(a):
+    c, s = math.cos(a), math.sin(a)
+    return np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+
+
+def rot_x(a):
+    c, s = math.cos(a), math.sin(a)
+    return np.array([[1.0, 0.0, 0.0], [0.0, c, -s], [0.0, s, c]])
+
+
+def pack_rgb(rgb_u8):
+    """(N,3) uint8 -> (N,) float32 whose bits are 0x00RRGGBB (reading D20)."""
+    rgb = rgb_u8.astype(np.uint32)
+    bits = (rgb[:, 0] << 16) | (rgb[:, 1] << 8) | rgb[:, 2]
+    return bits.astype(np.uint32).view(np.float32)
+
+
+def assert_tie_guard(x, res, guard=0.05):
+    """every trajectory position must stay >= `guard` cell from a snap tie (D14)."""
+    f = x / res + 0.5
+    frac = f - math.floor(f)
+    assert min(frac, 1.0 - frac) >= guard, f"position {x} within {guard} cell of a snap tie"
+
+
+# --------------------------------------------------------------------------------------
+# C1: 64x64 @ 0.1 m, plane + box, uniform points, 1 average-fused feature
+# --------------------------------------------------------------------------------------
+C1 = dict(res=0.1, rows=64, cols=64, n_points=10_000, frames=10, w=0.5,
+          noise=dict(a=1e-4, b=1e-4, r_min=0.1, r_max=10.0, h_min=-3.0, h_max=0.5, tau2=9.0, v_out=0.01))
+
+
+def c1_scene():
+    return Scene(boxes=[Box(0.5, 1.5, -0.5, 0.5, 0.4, 1, (200, 30, 30))])
+
+
+def c1_frame(frame, seed=1, n_points=C1["n_points"]):
+    """One C1 frame: returns dict(points (N,4) f32 sensor frame, R, t, move=(x, y))."""
+    rng = np.random.default_rng([seed, frame])
+    scene = c1_scene()
+    sensor = np.array([0.12 * frame, 0.0, 1.5])
+    assert_tie_guard(sensor[0], C1["res"])
+    assert_tie_guard(sensor[1], C1["res"])
+    xy = sensor[:2] + rng.uniform(-3.4, 3.4, size=(n_points, 2))
+    z = scene.height(xy[:, 0], xy[:, 1]) + rng.normal(0.0, 0.01, n_points)
+    feat = (scene.height(xy[:, 0], xy[:, 1]) > 0.2).astype(np.float64) + rng.normal(0.0, 0.05, n_points)
+    kind = rng.uniform(size=n_points)
+    z = np.where(kind < 0.01, z + rng.uniform(0.5, 1.0, n_points), z)  # 1% outliers
+    p = np.stack([xy[:, 0], xy[:, 1], z], 1) - sensor  # R = I
+    far = (kind >= 0.01) & (kind < 0.015)
+    p[far] *= 20.0  # 0.5% beyond r_max
+    nanm = (kind >= 0.015) & (kind < 0.02)
+    p[nanm, rng.integers(0, 3, nanm.sum())] = np.nan  # 0.5% non-finite
+    pts = np.concatenate([p, feat[:, None]], 1).astype(np.float32)
+    return dict(points=pts, R=np.eye(3), t=sensor.copy(), move=(sensor[0], sensor[1]))
+
+
+# --------------------------------------------------------------------------------------
+# C2: 200x200 @ 0.04 m, 128x1024 LiDAR with packed RGB, colour fusion, shift on motion
+# --------------------------------------------------------------------------------------
+C2 = dict(res=0.04, rows=200, cols=200, rings=128, azimuths=1024, frames=10, w=0.5,
+          noise=dict(a=1e-4, b=2.5e-5, r_min=0.3, r_max=60.0, h_min=-2.5, h_max=1.0, tau2=9.0, v_out=0.01))
+
+
+def c2_scene(seed=2):
+    rng = np.random.default_rng([seed, 999])
+    boxes = []
+    colours = [(200, 40, 40), (40, 40, 200), (220, 200, 40), (160, 60, 200)]
+    for k, (cx, cy) in enumerate([(2.0, 1.0), (-1.5, 2.2), (1.0, -2.5), (-2.5, -1.0)]):
+        sx, sy = rng.uniform(0.4, 0.9, 2)
+        boxes.append(Box(cx - sx, cx + sx, cy - sy, cy + sy, float(rng.uniform(0.2, 0.8)), 1 + k, colours[k]))
+    ramps = [Ramp(3.0, 5.0, -1.0, 1.0, 0.25, 5, (130, 130, 130))]
+    return Scene(boxes=boxes, ramps=ramps)
+
+
+def c2_pose(frame):
+    """trajectory: 0.046 m/frame along heading 30 deg, +0.1 rad/frame yaw, 1.0 m high.
+
+    The trajectory repeats every 16 frames (the robot jumps back to the start, a large
+    shift), because the tie guard cannot hold for longer straight runs at this speed."""
+    frame = frame % 16
+    x0, y0 = 0.0, 0.005
+    hd = math.radians(30.0)
+    x = x0 + 0.046 * frame * math.cos(hd)
+    y = y0 + 0.046 * frame * math.sin(hd)
+    assert_tie_guard(x, C2["res"])
+    assert_tie_guard(y, C2["res"])
+    return rot_z(0.1 * frame), np.array([x, y, 1.0])
+
+
+def lidar_dirs(rings, azimuths, elev_deg=(-22.5, 22.5), az_offset=0.0):
+    el = np.radians(np.linspace(elev_deg[0], elev_deg[1], rings))
+    az = az_offset + 2.0 * math.pi * np.arange(azimuths) / azimuths
+    el, az = np.meshgrid(el, az, indexing="ij")  # ring-major: row = ring
+    d = np.stack([np.cos(el) * np.cos(az), np.cos(el) * np.sin(az), np.sin(el)], -1)
+    return d.reshape(-1, 3)
+
+
+def lidar_frame(scene, R, t, rng, rings, azimuths, noise_a, noise_b, outlier_frac=0.005, with_rgb=True,
+                feature=None):
+    """simulate an organised LiDAR scan; no-return rays are NaN. Returns (N, 4) float32."""
+    d_s = lidar_dirs(rings, azimuths, az_offset=float(rng.uniform(0, 2 * math.pi / azimuths)))
+    d_w = d_s @ R.T
+    rng_t = scene.raycast(t, d_w)
+    hit = np.isfinite(rng_t)
+    r_true = np.where(hit, rng_t, 0.0)
+    sigma = np.sqrt(noise_a + noise_b * r_true ** 2)
+    r_meas = r_true + rng.normal(0.0, 1.0, r_true.shape) * sigma
+    p_s = d_s * r_meas[:, None]
+    pw = t + d_w * r_true[:, None]
+    out = rng.uniform(size=r_true.shape) < outlier_frac
+    p_s[out, 2] += rng.uniform(0.3, 1.0, out.sum())
+    p_s[~hit] = np.nan
+    if with_rgb:
+        _, rgb = scene.attributes(pw[:, 0], pw[:, 1], pw[:, 2])
+        ch = pack_rgb(rgb)
+    else:
+        ch = (feature(pw) if feature is not None else np.zeros(len(p_s))).astype(np.float32)
+    pts = np.empty((p_s.shape[0], 4), np.float32)
+    pts[:, :3] = p_s.astype(np.float32)
+    pts[:, 3] = ch
+    return pts
+
+
+def c2_frame(frame, seed=2):
+    rng = np.random.default_rng([seed, frame])
+    scene = c2_scene(seed)
+    R, t = c2_pose(frame)
+    pts = lidar_frame(scene, R, t, rng, C2["rings"], C2["azimuths"], C2["noise"]["a"], C2["noise"]["b"])
+    return dict(points=pts, R=R, t=t, move=(t[0], t[1]))
+
+
+# --------------------------------------------------------------------------------------
+# small random cases for parity tests (several tiles + ragged tails)
+# --------------------------------------------------------------------------------------
+def random_cloud(seed, n, stride, rows, cols, res, centre=(0.0, 0.0), z_sigma=0.05, nan_frac=0.02,
+                 channel_kind="feature", n_classes=0, sensor_h=1.0):
+    """uniform points over (slightly more than) the window; sensor frame with R = I at (centre, sensor_h)."""
+    rng = np.random.default_rng(seed)
+    ex, ey = rows * res / 2 * 1.1, cols * res / 2 * 1.1
+    x = rng.uniform(-ex, ex, n)
+    y = rng.uniform(-ey, ey, n)
+    z = 0.3 * np.sin(x) * np.cos(y) + rng.normal(0, z_sigma, n)
+    pts = np.zeros((n, stride), np.float32)
+    pts[:, 0] = x
+    pts[:, 1] = y
+    pts[:, 2] = z - sensor_h
+    nanm = rng.uniform(size=n) < nan_frac
+    pts[nanm, 0] = np.nan
+    if stride > 3:
+        if channel_kind == "feature":
+            pts[:, 3:] = rng.normal(0, 1, (n, stride - 3))
+        elif channel_kind == "probs":
+            k = n_classes
+            logits = rng.normal(0, 1, (n, k))
+            p = np.exp(logits)
+            p /= p.sum(1, keepdims=True)
+            pts[:, 3:3 + k] = p
+        elif channel_kind == "rgb":
+            pts[:, 3] = pack_rgb(rng.integers(0, 256, (n, 3)).astype(np.uint8))
+    return pts
+
+
+def softmax_image(labels, n_classes, rng, scale=4.0):
+    """(H,W) int labels -> (K,H,W) float32 softmax of scale*onehot + N(0,1) logits (C3 recipe)."""
+    H, W = labels.shape
+    logits = rng.normal(0.0, 1.0, (n_classes, H, W))
+    logits[labels, np.arange(H)[:, None], np.arange(W)[None, :]] += scale
+    logits -= logits.max(0, keepdims=True)
+    e = np.exp(logits)
+    return (e / e.sum(0, keepdims=True)).astype(np.float32)

@@ -1,0 +1,524 @@
+"""Pins of the CPU oracle against what the paper / SPEC and the mathematics fix.
+
+None of these re-types the oracle's own formula: each checks a printed worked example
+(tests/golden/spec_examples.json), a closed form in a DIFFERENT algebraic form (e.g. the
+information form of a Kalman/Gaussian update vs the oracle's Eq.(6)-(7) form), an
+invariant, or brute force on tiny inputs.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.oracle import (AVERAGE, CLASS_AVERAGE, CLASS_BAYESIAN, CLASS_MAX, COLOR, GAUSSIAN, HEIGHT,
+                           INLIER, NONFINITE, OOB, OUTLIER, RANGE, OracleError, OracleMap)
+from synth.scenes import pack_rgb, rot_z
+
+NOISE = dict(a=0.25, b=0.0, r_min=0.0, r_max=1e6, h_min=-1e6, h_max=1e6, tau2=1e30, v_out=0.01)
+EYE = np.eye(3)
+
+
+def put(points_world, sensor=(0.0, 0.0, 0.0), ch=None):
+    """points given in the map frame (R = I) -> sensor-frame float32 rows (+ channels)."""
+    p = np.asarray(points_world, np.float64) - np.asarray(sensor)
+    if ch is not None:
+        p = np.concatenate([p, np.asarray(ch, np.float64).reshape(len(p), -1)], 1)
+    return p.astype(np.float32)
+
+
+# ---------------------------------------------------------------- data association
+def test_cell_index_spec_examples(golden):
+    g = golden["cell_index"]
+    m = OracleMap(g["res"], g["rows"], g["cols"])
+    pts = put([[c["xy"][0], c["xy"][1], 0.0] for c in g["cases"]], sensor=(0, 0, 1))
+    cell, code = m.input_pointcloud(pts, [], EYE, [0, 0, 1], NOISE, debug=True)
+    for c, ci, co in zip(g["cases"], cell, code):
+        if c["cell"] is None:
+            assert co == OOB and ci == -1
+        else:
+            assert ci == c["cell"][0] * g["cols"] + c["cell"][1] and co == INLIER
+
+
+@pytest.mark.parametrize("rows,cols,res", [(3, 3, 1.0), (64, 48, 0.125), (7, 10, 0.25), (200, 200, 0.0625)])
+def test_cell_centre_round_trip(rows, cols, res):
+    """cell_index(cell_center(idx)) == idx; half-open edges: a point at the
+    max edge of a cell belongs to the next one. Dyadic resolutions make every
+    centre and edge exact in fp32, so the expected index follows from geometry alone."""
+    m = OracleMap(res, rows, cols)
+    rng = np.random.default_rng(0)
+    ii = rng.integers(0, rows, 500)
+    jj = rng.integers(0, cols, 500)
+    # cell centre / lower edge in the map frame: row <-> +x, col <-> +y, centred window (D13)
+    cx = (ii + 0.5 - rows / 2) * res
+    cy = (jj + 0.5 - cols / 2) * res
+    ex = (ii - rows / 2) * res
+    ey = (jj - cols / 2) * res
+    for X, Y in ((cx, cy), (ex, ey)):
+        pts = put(np.stack([X, Y, np.zeros_like(X)], 1), sensor=(0, 0, 1))
+        cell, code = m.input_pointcloud(pts, [], EYE, [0, 0, 1], NOISE, debug=True)
+        assert (code == INLIER).all()
+        assert (cell == ii * cols + jj).all()
+    # the upper edge of the window is outside (half-open)
+    pts = put([[rows / 2 * res, 0, 0], [0, cols / 2 * res, 0], [-rows / 2 * res - res / 4, 0, 0]], sensor=(0, 0, 1))
+    _, code = m.input_pointcloud(pts, [], EYE, [0, 0, 1], NOISE, debug=True)
+    assert list(code) == [OOB, OOB, OOB]
+
+
+def test_transform_spec_examples(golden):
+    """SPEC.md:156-158 through the binning: the transformed point lands in the cell of q."""
+    res, n = 0.25, 16
+    for c in golden["transform"]["cases"]:
+        R = EYE if c["R"] == "identity" else rot_z(math.pi / 2)
+        m = OracleMap(res, n, n)
+        t = np.array(c["t"], float) + np.array([0, 0, 0.5])  # lift so that z stays inside filters
+        pts = np.array([c["p"]], np.float32)
+        cell, code = m.input_pointcloud(pts, [], R, t, NOISE, debug=True)
+        q = np.array(c["q"]) + np.array([0, 0, 0.5])
+        row = math.floor(q[0] / res + n / 2)
+        col = math.floor(q[1] / res + n / 2)
+        assert code[0] == INLIER and cell[0] == row * n + col
+        assert m.get_layer("elevation")[row, col] == np.float32(q[2])
+
+
+def test_transform_preserves_distances():
+    """SPEC.md:179 rigid transform: fused heights of random points under a random rotation
+    equal z of R p + t (checked per point in cells hit once)."""
+    rng = np.random.default_rng(3)
+    A = rng.normal(size=(3, 3))
+    Q, _ = np.linalg.qr(A)
+    if np.linalg.det(Q) < 0:
+        Q[:, 0] *= -1
+    p = rng.uniform(-1, 1, (50, 3)).astype(np.float32)
+    t = np.array([0.1, -0.2, 0.3])
+    m = OracleMap(0.01, 400, 400)
+    cell, code = m.input_pointcloud(p, [], Q, t, NOISE, debug=True)
+    q = p.astype(np.float64) @ Q.T + t
+    assert (code == INLIER).all()
+    elev = m.get_layer("elevation").reshape(-1)
+    uniq, cnt = np.unique(cell, return_counts=True)
+    once = set(uniq[cnt == 1])
+    for i in range(50):
+        if cell[i] in once:
+            assert abs(elev[cell[i]] - q[i, 2]) < 1e-6
+    assert np.allclose(np.linalg.norm(q[1:] - q[:-1], axis=1), np.linalg.norm(p[1:] - p[:-1], axis=1), atol=1e-6)
+
+
+def test_filter_boundaries_inclusive():
+    """D9: points exactly at r_min, r_max, h_min, h_max are kept; just beyond are dropped."""
+    m = OracleMap(1.0, 8, 8)
+    nz = dict(NOISE, r_min=2.0, r_max=4.0, h_min=-4.0, h_max=-2.0)
+    pts = np.array([[0, 0, -2.0], [0, 0, -4.0], [0, 0, np.nextafter(np.float32(-2), np.float32(0))],
+                    [0, 0, np.nextafter(np.float32(-4), np.float32(-5))], [0, 2.0, 0.0],
+                    [np.nan, 0, 0], [0, np.inf, 0], [0, 0, -3.0]], np.float32)
+    nz2 = dict(nz, h_min=-1.0, h_max=1.0)
+    _, code = m.input_pointcloud(pts, [], EYE, [0, 0, 5], nz, debug=True)
+    assert list(code) == [INLIER, INLIER, RANGE, RANGE, HEIGHT, NONFINITE, NONFINITE, INLIER]
+    _, code = m.input_pointcloud(pts[:2], [], EYE, [0, 0, 5], nz2, debug=True)
+    assert list(code) == [HEIGHT, HEIGHT]
+
+
+def test_binning_invariant_and_far_point(golden):
+    """SPEC.md:219 (1e9,0,0) is dropped; SPEC.md:241 n_input = sum(drops) + n_in + n_out."""
+    m = OracleMap(0.1, 32, 32)
+    pts = put([golden["binning"]["far_point"]] + [[0.05, 0.05, 0.0]], sensor=(0, 0, 1))
+    _, code = m.input_pointcloud(pts, [], EYE, [0, 0, 1], dict(NOISE, r_max=100.0), debug=True)
+    assert code[0] == RANGE and code[1] == INLIER
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(-3, 3, (5000, 3)).astype(np.float32)
+    pts[rng.uniform(size=5000) < 0.05, 1] = np.nan
+    m.input_pointcloud(pts, [], EYE, [0, 0, 0], dict(NOISE, r_min=0.5, r_max=4.0, h_min=-2.0, h_max=2.0, tau2=1.0))
+    s = m.stats()
+    assert s["n_input"] == s["n_nonfinite"] + s["n_range"] + s["n_height"] + s["n_oob"] + s["n_inlier"] + s["n_outlier"]
+    assert s["n_nonfinite"] > 0 and s["n_range"] > 0 and s["n_height"] > 0 and s["n_oob"] > 0
+
+
+# ---------------------------------------------------------------- height update
+def test_single_point_empty_cell():
+    """north_star: a single point into an empty cell yields height z and the modelled variance
+    v = a + b r^2 (dyadic numbers, exact)."""
+    m = OracleMap(1.0, 4, 4)
+    nz = dict(NOISE, a=0.25, b=0.0625)
+    p = np.array([[0.0, 0.0, -2.0]], np.float32)  # r^2 = 4 -> v = 0.25 + 0.25 = 0.5
+    m.input_pointcloud(p, [], EYE, [0.25, 0.25, 3.5], nz)
+    assert m.get_layer("elevation")[2, 2] == 1.5
+    assert m.get_layer("variance")[2, 2] == 0.5
+    assert m.get_layer("valid").sum() == 1
+
+
+def test_height_first_touch_spec(golden):
+    g = golden["height_first_touch"]
+    m = OracleMap(1.0, 4, 4)
+    nz = dict(NOISE, a=g["sigma_z2"], b=0.0)
+    z = np.array([0.875, 1.125, 0.9375, 1.0625])  # mean 1.0, dyadic
+    assert len(z) == g["N"] and z.mean() == g["zbar"]
+    pts = put([[0.1, 0.1, zz] for zz in z], sensor=(0, 0, 2))
+    m.input_pointcloud(pts, [], EYE, [0, 0, 2], nz)
+    assert abs(m.get_layer("elevation")[2, 2] - g["h"]) < 1e-6
+    assert abs(m.get_layer("variance")[2, 2] - g["var"]) < 1e-9
+
+
+def test_two_measurement_kalman_closed_form(golden):
+    """SPEC.md:329 and the textbook scalar Kalman update h = (v2 z1 + v1 z2)/(v1+v2),
+    sigma^2 = v1 v2/(v1+v2) (a different algebraic form than the oracle's information form)."""
+    g = golden["height_equal_var"]
+    m = OracleMap(1.0, 4, 4)
+    m.set_layer("elevation", g["h_old"])
+    m.set_layer("variance", 0.25)
+    m.set_layer("valid", 1)
+    m.input_pointcloud(put([[0.1, 0.1, g["z"]]], sensor=(0, 0, 3)), [], EYE, [0, 0, 3], dict(NOISE, a=0.25))
+    assert m.get_layer("elevation")[2, 2] == g["h"]
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        z1, z2 = rng.normal(0, 1, 2)
+        v1, v2 = rng.uniform(0.01, 1.0, 2)
+        m = OracleMap(1.0, 4, 4)
+        m.input_pointcloud(put([[0.1, 0.1, z1]], sensor=(0, 0, 3)), [], EYE, [0, 0, 3], dict(NOISE, a=v1))
+        z1f, v1f = m.get_layer("elevation")[2, 2], m.get_layer("variance")[2, 2]
+        m.input_pointcloud(put([[0.1, 0.1, z2]], sensor=(0, 0, 3)), [], EYE, [0, 0, 3], dict(NOISE, a=v2))
+        v2f = np.float64(np.float32(1.0) / np.float32(np.float32(1.0) / np.float32(v2)))
+        z2f = np.float32(z2 - 3) + np.float32(3)
+        h = (v2f * z1f + v1f * z2f) / (v1f + v2f)
+        s2 = v1f * v2f / (v1f + v2f)
+        assert abs(m.get_layer("elevation")[2, 2] - h) < 1e-6 * max(1, abs(h))
+        assert abs(m.get_layer("variance")[2, 2] - s2) < 1e-6 * s2
+
+
+def test_sequential_equals_batch_height():
+    """10 sequential frames equal one batch precision-weighted mean (fp32 state
+    between frames -> 1e-6 relative instead of the fp64 1e-9)."""
+    rng = np.random.default_rng(11)
+    m = OracleMap(1.0, 4, 4)
+    allz, allv = [], []
+    for f in range(10):
+        n = int(rng.integers(1, 6))
+        z = rng.normal(0.5, 0.1, n)
+        a = float(rng.uniform(0.01, 0.1))
+        m.input_pointcloud(put([[0.2, 0.3, zz] for zz in z], sensor=(0, 0, 2)), [], EYE, [0, 0, 2], dict(NOISE, a=a))
+        allz += list(np.float32(np.float32(z - 2) + np.float32(2)))
+        allv += [a] * n
+    w = 1.0 / np.array(allv)
+    h = (w * np.array(allz)).sum() / w.sum()
+    assert abs(m.get_layer("elevation")[2, 2] - h) < 1e-6
+    assert abs(m.get_layer("variance")[2, 2] - 1.0 / w.sum()) < 1e-6 / w.sum()
+
+
+def test_outlier_boundary():
+    """D10: h=0, sigma^2=0.5, v=0.5, tau^2=9: z=3 inlier (equality), nextafter(3,4) outlier, -3 inlier."""
+    for z, expect in ((3.0, INLIER), (float(np.nextafter(np.float32(3), np.float32(4))), OUTLIER), (-3.0, INLIER)):
+        m = OracleMap(1.0, 4, 4)
+        m.set_layer("elevation", 0.0)
+        m.set_layer("variance", 0.5)
+        m.set_layer("valid", 1)
+        p = np.array([[0.0, 0.0, np.float32(z)]], np.float32)
+        _, code = m.input_pointcloud(p, [], EYE, [0.1, 0.1, 0.0], dict(NOISE, a=0.5, tau2=9.0), debug=True)
+        assert code[0] == expect
+        if expect == OUTLIER:  # D11: inflation only
+            assert m.get_layer("variance")[2, 2] == np.float32(0.5 + 0.01)
+            assert m.get_layer("elevation")[2, 2] == 0.0
+
+
+# ---------------------------------------------------------------- multimodal rules
+def test_latest_and_binning_mean(golden):
+    g, b = golden["latest"], golden["binning"]
+    m = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    m.set_layer("f", g["old"])
+    m.set_layer("f_observed", 1)
+    pts = put([[0.1, 0.1, 0.0]] * 2, sensor=(0, 0, 1), ch=g["values"])
+    m.input_pointcloud(pts, [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    f = m.get_layer("f")
+    assert f[2, 2] == g["result"]
+    assert (f[np.arange(4) != 2] == g["old"]).all()  # untouched cells bit-identical
+    m2 = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    m2.input_pointcloud(put([[0.1, 0.1, 0.0]] * 3, sensor=(0, 0, 1), ch=b["values"]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m2.get_layer("f")[2, 2] == b["mean"]
+
+
+def test_exponential(golden):
+    g = golden["exponential"]
+    m = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=g["w"])])
+    m.set_layer("f", g["old"])
+    m.set_layer("f_observed", 1)
+    m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[g["a"]]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m.get_layer("f")[2, 2] == g["result"]
+    s = g["series"]  # D3: theta_0 preset with observed = 1
+    m = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=s["w"])])
+    m.set_layer("f", s["theta0"])
+    m.set_layer("f_observed", 1)
+    for _ in range(s["steps"]):
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[s["a"]]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert abs(m.get_layer("f")[2, 2] - eval(s["result_expr"])) < 1e-6
+    # first touch initialises to the measurement (D3)
+    m = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=0.3)])
+    m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[7.0]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m.get_layer("f")[2, 2] == 7.0
+
+
+def test_exponential_convergence_rate():
+    """constant input converges geometrically with ratio (1 - w)."""
+    w = 0.25
+    m = OracleMap(1.0, 4, 4, [dict(name="f", rule=AVERAGE, n_channels=1, w=w)])
+    m.set_layer("f", 0.0)
+    m.set_layer("f_observed", 1)
+    errs = []
+    for _ in range(8):
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[2.0]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+        errs.append(2.0 - float(m.get_layer("f")[2, 2]))
+    ratios = np.array(errs[1:]) / np.array(errs[:-1])
+    assert np.allclose(ratios, 1 - w, atol=1e-5)
+
+
+def test_gaussian_spec_and_conjugacy(golden):
+    g = golden["gaussian"]
+    sf2 = g["sigma_f2_eq_sigma0_2"]
+    spec = dict(name="g", rule=GAUSSIAN, n_channels=1, sigma_f2=sf2, mu0=g["mu0"], sigma0_2=sf2)
+    m = OracleMap(1.0, 4, 4, [spec])
+    m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[g["f"]]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m.get_layer("g")[2, 2] == g["mu"]
+    assert m.get_layer("g_var")[2, 2] == sf2 * g["var_over_sigma_f2"]
+    # N = 0: unchanged
+    m.input_pointcloud(put([[1.1, 1.1, 0.0]], sensor=(0, 0, 1), ch=[5.0]), [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m.get_layer("g")[2, 2] == g["mu"]
+    # 5 messages sequential vs batch, batch in the INFORMATION form (Bishop 2.141-2.142):
+    # precision = 1/s0 + N/sf, mean = (mu0/s0 + sum f / sf) / precision
+    rng = np.random.default_rng(13)
+    d = 3
+    spec = dict(name="g", rule=GAUSSIAN, n_channels=d, sigma_f2=0.3, mu0=0.5, sigma0_2=2.0)
+    m = OracleMap(1.0, 4, 4, [spec])
+    allf = []
+    for _ in range(5):
+        n = int(rng.integers(1, 7))
+        f = rng.normal(1.0, 0.5, (n, d)).astype(np.float32)
+        allf.append(f)
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]] * n, sensor=(0, 0, 1), ch=f), [(0, d, 0)], EYE, [0, 0, 1], NOISE)
+    F = np.concatenate(allf).astype(np.float64)
+    prec = 1 / np.float64(np.float32(2.0)) + len(F) / np.float64(np.float32(0.3))
+    mean = (0.5 / np.float64(np.float32(2.0)) + F.sum(0) / np.float64(np.float32(0.3))) / prec
+    for k in range(d):
+        assert abs(m.get_layer(f"g_{k}")[2, 2] - mean[k]) < 1e-6
+        assert abs(m.get_layer(f"g_var_{k}")[2, 2] - 1 / prec) < 1e-6 / prec
+
+
+def test_dirichlet_spec(golden):
+    g = golden["dirichlet"]
+    K = len(g["alpha_prior"])
+    m = OracleMap(1.0, 4, 4, [dict(name="s", rule=CLASS_BAYESIAN, n_channels=K, alpha0=g["alpha_prior"][0])])
+    m.input_pointcloud(put([[0.1, 0.1, 0.0]] * len(g["obs"]), sensor=(0, 0, 1), ch=g["obs"]), [(0, K, 0)], EYE,
+                       [0, 0, 1], NOISE)
+    for k in range(K):
+        assert m.get_layer(f"s_alpha_{k}")[2, 2] == g["alpha"][k]
+        assert abs(m.get_layer(f"s_{k}")[2, 2] - g["theta"][k]) < 1e-7
+
+
+def test_dirichlet_batch_conjugacy_simplex_monotone():
+    """5 messages of soft labels == alpha0 + total sum (batch); theta on the
+    simplex; alpha monotone."""
+    rng = np.random.default_rng(17)
+    K = 5
+    m = OracleMap(1.0, 4, 4, [dict(name="s", rule=CLASS_BAYESIAN, n_channels=K, alpha0=1.0)])
+    tot = np.zeros(K)
+    prev = np.zeros(K)
+    for _ in range(5):
+        n = int(rng.integers(1, 40))
+        p = rng.dirichlet(np.ones(K), n).astype(np.float32)
+        tot += p.astype(np.float64).sum(0)
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]] * n, sensor=(0, 0, 1), ch=p), [(0, K, 0)], EYE, [0, 0, 1], NOISE)
+        al = np.array([m.get_layer(f"s_alpha_{k}")[2, 2] for k in range(K)])
+        assert (al >= prev).all()
+        prev = al
+        th = np.array([m.get_layer(f"s_{k}")[2, 2] for k in range(K)], np.float64)
+        assert abs(th.sum() - 1) < 1e-6
+    assert np.allclose(prev, 1.0 + tot, rtol=1e-6)
+
+
+def test_class_average_simplex_and_brute_force():
+    rng = np.random.default_rng(19)
+    K, w = 4, 0.5
+    m = OracleMap(1.0, 2, 2, [dict(name="c", rule=CLASS_AVERAGE, n_channels=K, w=w)])
+    theta = None
+    for _ in range(4):
+        n = int(rng.integers(1, 10))
+        p = rng.dirichlet(np.ones(K), n).astype(np.float32)
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]] * n, sensor=(0, 0, 1), ch=p), [(0, K, 0)], EYE, [0, 0, 1], NOISE)
+        a = p.astype(np.float64).mean(0)
+        theta = a if theta is None else w * a + (1 - w) * theta
+        got = np.array([m.get_layer(f"c_{k}")[1, 1] for k in range(K)])
+        assert np.allclose(got, theta, atol=1e-6)
+        assert abs(got.astype(np.float64).sum() - 1) < 1e-6
+
+
+def test_class_max_brute_force_ties_permutation(golden):
+    for c in golden["semantic_argmax"]["cases"]:
+        m = OracleMap(1.0, 2, 2, [dict(name="m", rule=CLASS_MAX, n_channels=2)])
+        m.input_pointcloud(put([[0.1, 0.1, 0.0]], sensor=(0, 0, 1), ch=[c["theta"]]), [(0, 2, 0)], EYE, [0, 0, 1], NOISE)
+        assert m.get_layer("m_label")[1, 1] == c["id"]
+        assert m.get_layer("m_conf")[1, 1] == np.float32(c["conf"])
+        assert m.get_layer("m_label")[0, 0] == -1
+    rng = np.random.default_rng(23)
+    K = 6
+    for trial in range(10):
+        n = 40
+        xy = rng.uniform(-1, 1, (n, 2))
+        p = np.round(rng.uniform(0, 1, (n, K)) * 4) / 4  # many ties
+        pts = put(np.concatenate([xy, np.zeros((n, 1))], 1), sensor=(0, 0, 1), ch=p)
+        res = []
+        for perm in (np.arange(n), rng.permutation(n)):
+            m = OracleMap(1.0, 2, 2, [dict(name="m", rule=CLASS_MAX, n_channels=K)])
+            m.input_pointcloud(pts[perm], [(0, K, 0)], EYE, [0, 0, 1], NOISE)
+            res.append((m.get_layer("m_label"), m.get_layer("m_conf")))
+        assert (res[0][0] == res[1][0]).all() and (res[0][1] == res[1][1]).all()
+        # brute force: per cell the point with the largest max prob; ties -> lowest class
+        for r in range(2):
+            for c in range(2):
+                sel = (np.floor(xy[:, 0] + 1) == r) & (np.floor(xy[:, 1] + 1) == c)
+                if not sel.any():
+                    assert res[0][0][r, c] == -1
+                    continue
+                q = pts[sel, 3:]
+                best = max((q[i].max(), -int(np.argmax(q[i]))) for i in range(len(q)))
+                assert res[0][1][r, c] == best[0] and res[0][0][r, c] == -best[1]
+
+
+def test_color_brute_force():
+    rng = np.random.default_rng(29)
+    rgb = rng.integers(0, 256, (60, 3)).astype(np.uint8)
+    xy = rng.uniform(-1, 1, (60, 2))
+    pts = put(np.concatenate([xy, np.zeros((60, 1))], 1), sensor=(0, 0, 1), ch=pack_rgb(rgb).view(np.float32))
+    m = OracleMap(1.0, 2, 2, [dict(name="rgb", rule=COLOR, n_channels=3, w=1.0)])
+    m.input_pointcloud(pts, [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    for r in range(2):
+        for c in range(2):
+            sel = (np.floor(xy[:, 0] + 1) == r) & (np.floor(xy[:, 1] + 1) == c)
+            mean = rgb[sel].astype(np.float64).mean(0)
+            for k, nm in enumerate("rgb"):
+                assert m.get_layer(f"rgb_{nm}")[r, c] == np.float32(mean[k])
+
+
+def test_nonfinite_channel_skips_group_only():
+    """D31: a non-finite channel value skips the group but the point still fuses height."""
+    m = OracleMap(1.0, 2, 2, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    pts = put([[0.1, 0.1, 0.0], [0.2, 0.2, 0.0]], sensor=(0, 0, 1), ch=[np.nan, 4.0])
+    m.input_pointcloud(pts, [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    assert m.get_layer("f")[1, 1] == 4.0 and m.get_layer("valid")[1, 1] == 1
+
+
+# ---------------------------------------------------------------- image association
+def down_camera(tx, ty, tz):
+    """camera looking straight down: x_c = +x, y_c = -y, z_c = -z (det +1)."""
+    R = np.array([[1.0, 0, 0], [0, -1.0, 0], [0, 0, -1.0]])
+    return R, np.array([tx, ty, tz])
+
+
+def test_pixel_spec_examples(golden):
+    """SPEC.md:165-167 via the image path: a valid cell whose centre is at p_cam = (0.5, 0, 1)
+    samples pixel (100, 50); one at (0, 0, 1) samples (cx, cy)."""
+    g = golden["pixel"]
+    K = np.array([[g["fx"], 0, g["cx"]], [0, g["fy"], g["cy"]], [0, 0, 1.0]])
+    res, n = 0.25, 8
+    m = OracleMap(res, n, n, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    m.set_layer("elevation", 0.0)
+    m.set_layer("variance", 1.0)
+    m.set_layer("valid", 1)
+    img = np.zeros((1, 101, 201), np.float32)
+    img[0, 50, 100] = 5.0
+    img[0, 50, 50] = 3.0
+    # cell (row 6, col 4) centre = (0.625, 0.125); camera above (0.125, 0.125) at height 1
+    R, t = down_camera(0.125, 0.125, 1.0)
+    m.input_image(img, [(0, 1, 0)], K, R, t)
+    f = m.get_layer("f")
+    assert f[6, 4] == 5.0  # p_cam = (0.5, 0, 1) -> (100, 50)
+    assert f[4, 4] == 3.0  # p_cam = (0, 0, 1)   -> (cx, cy)
+    # behind the camera: facing up -> nothing changes
+    m2 = OracleMap(res, n, n, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    m2.set_layer("elevation", 0.0)
+    m2.set_layer("valid", 1)
+    Rup = np.array([[1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0]])
+    m2.input_image(np.ones((1, 101, 201), np.float32), [(0, 1, 0)], K, Rup, np.array([0.0, 0.0, -1.0]) * -1)
+    assert (m2.get_layer("f") == 0).all() and (m2.get_layer("f_observed") == 0).all()
+
+
+def test_image_uniform_and_analytic_projection():
+    """uniform image on a flat map -> every in-frustum valid cell gets the value;
+    the set of updated cells equals the analytic frustum (brute force in fp64 with a margin)."""
+    res, n = 0.1, 40
+    fx = fy = 50.0
+    W_img, H_img = 64, 48
+    K = np.array([[fx, 0, 31.5], [0, fy, 23.5], [0, 0, 1.0]])
+    m = OracleMap(res, n, n, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    m.set_layer("elevation", 0.0)
+    m.set_layer("variance", 1.0)
+    valid = np.ones((n, n), np.float32)
+    valid[:, :3] = 0
+    m.set_layer("valid", valid)
+    R, t = down_camera(0.0, 0.0, 1.5)
+    m.input_image(np.full((1, H_img, W_img), 2.5, np.float32), [(0, 1, 0)], K, R, t)
+    f = m.get_layer("f")
+    xs = (np.arange(n) + 0.5 - n / 2) * res
+    u = fx * (xs[:, None] - 0.0) / 1.5 + 31.5 + 0 * xs[None, :]
+    v = fy * (-(xs[None, :] - 0.0)) / 1.5 + 23.5 + 0 * xs[:, None]
+    inside = (u > -0.5 + 1e-3) & (u < W_img - 0.5 - 1e-3) & (v > -0.5 + 1e-3) & (v < H_img - 0.5 - 1e-3)
+    outside = (u < -0.5 - 1e-3) | (u > W_img - 0.5 + 1e-3) | (v < -0.5 - 1e-3) | (v > H_img - 0.5 + 1e-3)
+    assert (f[inside & (valid > 0)] == 2.5).all()
+    assert (f[outside] == 0).all() and (f[valid == 0] == 0).all()
+    assert (m.get_layer("elevation")[valid > 0] == 0).all()  # elevation untouched by images
+    assert (m.get_layer("valid") == valid).all()
+
+
+# ---------------------------------------------------------------- map shift
+def naive_shift(a, sr, sc, fill):
+    """independent oracle of the recentre: numpy slicing copy."""
+    out = np.full_like(a, fill)
+    H, W = a.shape
+    for i in range(H):
+        for j in range(W):
+            oi, oj = i + sr, j + sc
+            if 0 <= oi < H and 0 <= oj < W:
+                out[i, j] = a[oi, oj]
+    return out
+
+
+def test_move_to_shift_properties():
+    res, n = 0.5, 10
+    rng = np.random.default_rng(31)
+    m = OracleMap(res, n, n, [dict(name="f", rule=AVERAGE, n_channels=1, w=1.0)])
+    pts = put(np.concatenate([rng.uniform(-2.5, 2.5, (300, 2)), rng.normal(0, 0.1, (300, 1))], 1), sensor=(0, 0, 1),
+              ch=rng.normal(0, 1, 300))
+    m.input_pointcloud(pts, [(0, 1, 0)], EYE, [0, 0, 1], NOISE)
+    before = {k: m.get_layer(k) for k in ("elevation", "valid", "f", "f_observed")}
+    m.move_to(0.2, -0.2)  # snaps to (0, 0): s = 0 -> bit-identical
+    for k, v in before.items():
+        assert np.array_equal(m.get_layer(k), v, equal_nan=True)
+    m.move_to(1.1, -0.6)  # k = (2, -1)
+    assert m.center() == (2, -1)
+    exp = {k: naive_shift(v, 2, -1, np.nan if k == "elevation" else 0) for k, v in before.items()}
+    for k in exp:
+        assert np.array_equal(m.get_layer(k), exp[k], equal_nan=True)
+    assert (m.get_layer("valid")[-2:, :] == 0).all() and (m.get_layer("valid")[:, 0] == 0).all()
+    m.move_to(1.1, -0.6)  # idempotent
+    for k in exp:
+        assert np.array_equal(m.get_layer(k), exp[k], equal_nan=True)
+    m.move_to(1.1 + n * res, -0.6)  # shift >= size -> everything invalid
+    assert (m.get_layer("valid") == 0).all() and np.isnan(m.get_layer("elevation")).all()
+
+
+def test_snap_rule_round_half_up():
+    """D14: k = floor(x/res + 1/2)."""
+    m = OracleMap(1.0, 4, 4)
+    for x, k in ((0.49, 0), (0.5, 1), (-0.5, 0), (-0.51, -1), (2.5, 3)):
+        m.move_to(x, 0.0)
+        assert m.center()[0] == k
+
+
+def test_errors():
+    with pytest.raises(OracleError):
+        OracleMap(0.0, 4, 4)
+    with pytest.raises(OracleError) as e:
+        OracleMap(1.0, 4, 4, [dict(name="a", rule=AVERAGE), dict(name="a", rule=AVERAGE)])
+    assert e.value.status == -2
+    m = OracleMap(1.0, 4, 4)
+    R = np.eye(3)
+    R[0, 0] = 1.001
+    with pytest.raises(OracleError) as e:
+        m.input_pointcloud(np.zeros((1, 3), np.float32), [], R, [0, 0, 1], NOISE)
+    assert e.value.status == -5
+    m.input_pointcloud(np.zeros((0, 3), np.float32), [], EYE, [0, 0, 1], NOISE)  # empty is legal
+    assert np.isnan(m.get_layer("elevation")).all()
