@@ -1,0 +1,924 @@
+// mem_api.cu -- host side of the libmem C-ABI (include/mem.h): argument validation, the
+// layer registry, device state allocation, per-call parameter staging and kernel launches.
+// No compute happens here: every step of the path runs in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace memk;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+mem_status fail(mem_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CU(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(MEM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+enum LayerKind { LK_ELEV, LK_VAR, LK_VALID, LK_WORD, LK_LABEL, LK_FLAG, LK_THETA };
+
+struct Layer {
+  std::string name;
+  int kind, idx;          // word or flag layer index
+  int first, K, flag;     // theta only
+};
+
+// pinned host staging slots with events: the host writes a slot immediately, the H2D copy
+// reads it later in stream order, so a slot is reused only after its copy has executed.
+struct PinnedRing {
+  static constexpr int kSlots = 8;
+  void *host[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  size_t cap = 0;
+  int next = 0;
+};
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[MEM_N_STAGES];
+  double ms[MEM_N_STAGES] = {};
+  uint64_t count[MEM_N_STAGES] = {};
+};
+
+}  // namespace
+
+struct mem_map {
+  int B = 1, H = 0, W = 0;
+  float res = 0.f;
+  unsigned flags = 0;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int ng = 0;
+  GroupDesc g[kMaxGroups];
+  std::string gname[kMaxGroups];
+  int n_word = 0, n_flag = 0, n_acc = 0;
+  int n_label = 0, label_word[kMaxGroups] = {};
+  std::vector<Layer> layers;
+  State st{};
+  int2 *ring = nullptr;
+  std::vector<long long> kx, ky;
+  std::vector<int> r0, c0;
+  // staging
+  void *dparam = nullptr;
+  size_t dparam_cap = 0;
+  PinnedRing pin;
+  void *din = nullptr;
+  size_t din_cap = 0;
+  float *dout = nullptr;
+  size_t dout_cap = 0;
+  unsigned long long *dstats = nullptr;
+  int *dbg_cell = nullptr;
+  uint8_t *dbg_code = nullptr;
+  size_t dbg_cap = 0;
+  long long dbg_n = 0;
+  Prof prof;
+
+  Geometry geo() const {
+    Geometry gg;
+    gg.H = H;
+    gg.W = W;
+    gg.HW = H * W;
+    gg.n_maps = B;
+    gg.BHW = (long long)B * H * W;
+    gg.res = res;
+    gg.hH = (float)H / 2.0f;
+    gg.hW = (float)W / 2.0f;
+    return gg;
+  }
+};
+
+namespace {
+
+cudaEvent_t prof_event(mem_map *m) {
+  if (!m->prof.pool.empty()) {
+    cudaEvent_t e = m->prof.pool.back();
+    m->prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+// runs one launch / copy of `stage`, bracketed by events when profiling is on
+template <class F>
+mem_status timed(mem_map *m, int stage, const char *what, F &&op) {
+  m->prof.count[stage]++;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (m->prof.on) {
+    a = prof_event(m);
+    b = prof_event(m);
+    if (!a || !b) return fail(MEM_ECUDA, "cudaEventCreate failed");
+    CU(cudaEventRecord(a, m->stream));
+  }
+  const cudaError_t e = op();
+  if (e != cudaSuccess) return fail(MEM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  if (m->prof.on) {
+    CU(cudaEventRecord(b, m->stream));
+    m->prof.pending[stage].emplace_back(a, b);
+  }
+  return MEM_OK;
+}
+
+#define TIMED(stage, expr)                                                   \
+  do {                                                                       \
+    mem_status ts_ = timed(m, stage, #expr, [&]() { return (expr); });       \
+    if (ts_ != MEM_OK) return ts_;                                           \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+mem_status grow(void **buf, size_t *cap, size_t need, cudaStream_t s) {
+  if (need <= *cap) return MEM_OK;
+  CU(cudaStreamSynchronize(s));
+  if (*buf) CU(cudaFree(*buf));
+  *buf = nullptr;
+  *cap = 0;
+  size_t c = need < 4096 ? 4096 : need + need / 4;
+  if (cudaMalloc(buf, c) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MEM_ENOMEM, "cudaMalloc(%zu) failed", c);
+  }
+  *cap = c;
+  return MEM_OK;
+}
+
+// copies `bytes` of host data to the map's device parameter buffer (stream-ordered).
+mem_status stage_params(mem_map *m, const void *src, size_t bytes, void **dptr) {
+  mem_status s = grow(&m->dparam, &m->dparam_cap, bytes, m->stream);
+  if (s != MEM_OK) return s;
+  PinnedRing &p = m->pin;
+  if (bytes > p.cap) {
+    CU(cudaStreamSynchronize(m->stream));
+    for (int i = 0; i < PinnedRing::kSlots; ++i) {
+      if (p.host[i]) CU(cudaFreeHost(p.host[i]));
+      p.host[i] = nullptr;
+    }
+    size_t c = bytes < 4096 ? 4096 : bytes + bytes / 4;
+    for (int i = 0; i < PinnedRing::kSlots; ++i) {
+      if (cudaMallocHost(&p.host[i], c) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MEM_ENOMEM, "cudaMallocHost(%zu) failed", c);
+      }
+      if (!p.ev[i]) CU(cudaEventCreateWithFlags(&p.ev[i], cudaEventDisableTiming));
+    }
+    p.cap = c;
+  }
+  const int k = p.next;
+  p.next = (p.next + 1) % PinnedRing::kSlots;
+  CU(cudaEventSynchronize(p.ev[k]));
+  memcpy(p.host[k], src, bytes);
+  CU(cudaMemcpyAsync(m->dparam, p.host[k], bytes, cudaMemcpyHostToDevice, m->stream));
+  CU(cudaEventRecord(p.ev[k], m->stream));
+  *dptr = m->dparam;
+  return MEM_OK;
+}
+
+// returns a device pointer holding `bytes` of the caller's input (copied if it is host memory).
+mem_status stage_input(mem_map *m, const void *src, size_t bytes, const void **dptr) {
+  if (bytes == 0 || is_device_ptr(src)) {
+    *dptr = src;
+    return MEM_OK;
+  }
+  mem_status s = grow(&m->din, &m->din_cap, bytes, m->stream);
+  if (s != MEM_OK) return s;
+  TIMED(MEM_STAGE_H2D, cudaMemcpyAsync(m->din, src, bytes, cudaMemcpyHostToDevice, m->stream));
+  *dptr = m->din;
+  return MEM_OK;
+}
+
+// R^T R = I within 1e-6 and det(R) = +1 within 1e-6 (host, fp64).
+bool rotation_ok(const double *R) {
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double d = R[a] * R[b] + R[3 + a] * R[3 + b] + R[6 + a] * R[6 + b];
+      double e = (a == b) ? 1.0 : 0.0;
+      if (!std::isfinite(d) || std::fabs(d - e) > 1e-6) return false;
+    }
+  const double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                     R[2] * (R[3] * R[7] - R[4] * R[6]);
+  return std::fabs(det - 1.0) <= 1e-6;
+}
+
+// a1: frame setup on the host -- t relative to the map centre in fp64, then fp32 (D13)
+MapFrame make_frame(const mem_map *m, int map, const double *R, const double *t, const double *K) {
+  MapFrame f;
+  memset(&f, 0, sizeof f);
+  for (int k = 0; k < 9; ++k) f.R[k] = (float)R[k];
+  const double cx = (double)m->kx[map] * (double)m->res, cy = (double)m->ky[map] * (double)m->res;
+  f.t[0] = (float)(t[0] - cx);
+  f.t[1] = (float)(t[1] - cy);
+  f.t[2] = (float)t[2];
+  if (K) {
+    f.K[0] = (float)K[0];
+    f.K[1] = (float)K[1];
+    f.K[2] = (float)K[2];
+    f.K[3] = (float)K[4];
+    f.K[4] = (float)K[5];
+  }
+  return f;
+}
+
+mem_status resolve_bindings(const mem_map *m, const mem_binding *bind, int nb, bool image, int stride_or_C,
+                            BindDesc *out) {
+  if (nb < 0 || nb > kMaxBind) return fail(MEM_EINVAL, "n_bind %d out of [0, %d]", nb, kMaxBind);
+  if (nb > 0 && !bind) return fail(MEM_EINVAL, "bindings NULL");
+  for (int i = 0; i < nb; ++i) {
+    const mem_binding &b = bind[i];
+    if (b.group < 0 || b.group >= m->ng) return fail(MEM_EINVAL, "binding %d: group %d out of range", i, b.group);
+    const GroupDesc &g = m->g[b.group];
+    const int avail = image ? stride_or_C : stride_or_C - 3;
+    if (b.ch_offset < 0 || b.n_ch < 1 || b.ch_offset + b.n_ch > avail)
+      return fail(MEM_EINVAL, "binding %d: channels [%d, %d) outside the %d input channels", i, b.ch_offset,
+                  b.ch_offset + b.n_ch, avail);
+    const int want = g.rule == MEM_COLOR ? (image ? 3 : 1) : g.nch;
+    if (b.n_ch != want)
+      return fail(MEM_EINVAL, "binding %d: group '%s' takes %d channel(s), got %d", i, m->gname[b.group].c_str(),
+                  want, b.n_ch);
+    for (int j = 0; j < i; ++j)
+      if (bind[j].group == b.group) return fail(MEM_EINVAL, "group '%s' bound twice", m->gname[b.group].c_str());
+    out[i].ch_offset = b.ch_offset;
+    out[i].nch = b.n_ch;
+    out[i].group = b.group;
+    out[i].g = g;
+  }
+  return MEM_OK;
+}
+
+mem_status check_map(const mem_map *m) {
+  if (!m) return fail(MEM_EINVAL, "map is NULL");
+  return MEM_OK;
+}
+
+mem_status set_device(const mem_map *m) {
+  CU(cudaSetDevice(m->device));
+  return MEM_OK;
+}
+
+void add_layer(mem_map *m, const std::string &name, int kind, int idx, int first = 0, int K = 0, int flag = 0) {
+  Layer l;
+  l.name = name;
+  l.kind = kind;
+  l.idx = idx;
+  l.first = first;
+  l.K = K;
+  l.flag = flag;
+  m->layers.push_back(l);
+}
+
+mem_status reset_all(mem_map *m) {
+  ShiftArgs a;
+  memset(&a, 0, sizeof a);
+  a.geo = m->geo();
+  a.st = m->st;
+  a.recs = nullptr;
+  a.rec0.sr = m->H;  // |s| >= size: every cell
+  a.rec0.sc = 0;
+  a.rec0.r0 = 0;
+  a.rec0.c0 = 0;
+  a.ring = m->ring;
+  a.n_word = m->n_word;
+  a.n_flag = m->n_flag;
+  a.n_label = m->n_label;
+  for (int i = 0; i < m->n_label; ++i) a.label_word[i] = m->label_word[i];
+  a.max_count = m->H * m->W;
+  CU(launch_shift(a, m->stream));
+  return MEM_OK;
+}
+
+void free_map(mem_map *m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  cudaFree(m->st.words);
+  cudaFree(m->st.flags);
+  cudaFree(m->st.acc);
+  cudaFree(m->ring);
+  cudaFree(m->dparam);
+  cudaFree(m->din);
+  cudaFree(m->dout);
+  cudaFree(m->dstats);
+  cudaFree(m->dbg_cell);
+  cudaFree(m->dbg_code);
+  for (int i = 0; i < PinnedRing::kSlots; ++i) {
+    if (m->pin.host[i]) cudaFreeHost(m->pin.host[i]);
+    if (m->pin.ev[i]) cudaEventDestroy(m->pin.ev[i]);
+  }
+  for (cudaEvent_t e : m->prof.pool) cudaEventDestroy(e);
+  for (auto &v : m->prof.pending)
+    for (auto &pr : v) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  cudaGetLastError();
+  delete m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mem_last_error(void) { return g_err.c_str(); }
+
+const char *mem_version(void) { return "libmem 0.1.0 (sm_100a)"; }
+
+mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, const mem_layer_spec *groups,
+                            int n_groups, unsigned flags, mem_stream stream, mem_map **out) {
+  if (!out) return fail(MEM_EINVAL, "out is NULL");
+  if (n_maps < 1 || n_maps > 65535) return fail(MEM_EINVAL, "n_maps %d out of [1, 65535]", n_maps);
+  if (!(resolution > 0.0f) || !std::isfinite(resolution)) return fail(MEM_EINVAL, "resolution must be > 0");
+  if (rows < 1 || cols < 1 || (long long)rows * cols > (1LL << 31) - 1)
+    return fail(MEM_EINVAL, "rows x cols = %d x %d invalid", rows, cols);
+  if (n_groups < 0 || n_groups > kMaxGroups) return fail(MEM_EINVAL, "n_groups %d out of [0, %d]", n_groups, kMaxGroups);
+  if (n_groups > 0 && !groups) return fail(MEM_EINVAL, "groups is NULL");
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    cudaGetLastError();
+    return fail(MEM_ECUDA, "no CUDA device (libmem has no CPU fallback)");
+  }
+  // validate every spec before allocating anything
+  for (int i = 0; i < n_groups; ++i) {
+    const mem_layer_spec &s = groups[i];
+    if (!s.name || !s.name[0] || strlen(s.name) >= 40) return fail(MEM_EINVAL, "group %d: name must be 1..39 chars", i);
+    if (!strcmp(s.name, "elevation") || !strcmp(s.name, "variance") || !strcmp(s.name, "valid"))
+      return fail(MEM_EDUPNAME, "group name '%s' is reserved", s.name);
+    for (int j = 0; j < i; ++j)
+      if (!strcmp(groups[j].name, s.name)) return fail(MEM_EDUPNAME, "duplicate group name '%s'", s.name);
+    if (s.rule < MEM_AVERAGE || s.rule > MEM_COLOR) return fail(MEM_ERULE, "group '%s': unknown rule %d", s.name, s.rule);
+    if (s.rule == MEM_COLOR) {
+      if (s.n_channels != 3) return fail(MEM_EINVAL, "group '%s': color takes n_channels = 3", s.name);
+    } else if (s.n_channels < 1 || s.n_channels > kMaxCh) {
+      return fail(MEM_EINVAL, "group '%s': n_channels %d out of [1, %d]", s.name, s.n_channels, kMaxCh);
+    }
+    if ((s.rule == MEM_CLASS_AVERAGE || s.rule == MEM_CLASS_BAYESIAN || s.rule == MEM_CLASS_MAX) && s.n_channels < 2)
+      return fail(MEM_ERULE, "group '%s': class rules need >= 2 classes", s.name);
+    if ((s.rule == MEM_AVERAGE || s.rule == MEM_CLASS_AVERAGE || s.rule == MEM_COLOR) && !(s.w > 0.0f && s.w <= 1.0f))
+      return fail(MEM_EINVAL, "group '%s': w must be in (0, 1]", s.name);
+    if (s.rule == MEM_GAUSSIAN && !(s.sigma_f2 > 0.0f && s.sigma0_2 > 0.0f))
+      return fail(MEM_EINVAL, "group '%s': variances must be > 0", s.name);
+    if (s.rule == MEM_CLASS_BAYESIAN && !(s.alpha0 > 0.0f)) return fail(MEM_EINVAL, "group '%s': alpha0 must be > 0", s.name);
+  }
+  mem_map *m = new mem_map();
+  m->B = n_maps;
+  m->H = rows;
+  m->W = cols;
+  m->res = resolution;
+  m->flags = flags;
+  m->stream = (cudaStream_t)stream;
+  if (cudaGetDevice(&m->device) != cudaSuccess) {
+    cudaGetLastError();
+    delete m;
+    return fail(MEM_ECUDA, "cudaGetDevice failed");
+  }
+  m->kx.assign(n_maps, 0);
+  m->ky.assign(n_maps, 0);
+  m->r0.assign(n_maps, 0);
+  m->c0.assign(n_maps, 0);
+  // layer registry (names: include/mem.h)
+  m->n_word = 2;
+  m->n_flag = 1;
+  m->n_acc = 3;
+  add_layer(m, "elevation", LK_ELEV, kWordElev);
+  add_layer(m, "variance", LK_VAR, kWordVar);
+  add_layer(m, "valid", LK_VALID, kFlagValid);
+  m->ng = n_groups;
+  for (int i = 0; i < n_groups; ++i) {
+    const mem_layer_spec &s = groups[i];
+    GroupDesc &g = m->g[i];
+    g.rule = s.rule;
+    g.nch = s.n_channels;
+    g.w = s.w;
+    g.sf2 = s.sigma_f2;
+    g.mu0 = s.mu0;
+    g.s02 = s.sigma0_2;
+    g.a0 = s.alpha0;
+    g.word0 = m->n_word;
+    g.label = -1;
+    g.flag = -1;
+    g.acc0 = m->n_acc;
+    const std::string nm = s.name;
+    m->gname[i] = nm;
+    auto sfx = [&](int k) { return g.nch == 1 ? nm : nm + "_" + std::to_string(k); };
+    switch (s.rule) {
+      case MEM_AVERAGE:
+      case MEM_CLASS_AVERAGE:
+        for (int k = 0; k < g.nch; ++k) add_layer(m, sfx(k), LK_WORD, g.word0 + k);
+        m->n_word += g.nch;
+        m->n_acc += 1 + g.nch;
+        break;
+      case MEM_GAUSSIAN:
+        for (int k = 0; k < g.nch; ++k) add_layer(m, sfx(k), LK_WORD, g.word0 + k);
+        for (int k = 0; k < g.nch; ++k)
+          add_layer(m, g.nch == 1 ? nm + "_var" : nm + "_var_" + std::to_string(k), LK_WORD, g.word0 + g.nch + k);
+        m->n_word += 2 * g.nch;
+        m->n_acc += 1 + g.nch;
+        break;
+      case MEM_CLASS_BAYESIAN:
+        for (int k = 0; k < g.nch; ++k) add_layer(m, nm + "_" + std::to_string(k), LK_THETA, g.word0 + k, g.word0, g.nch, m->n_flag);
+        for (int k = 0; k < g.nch; ++k) add_layer(m, nm + "_alpha_" + std::to_string(k), LK_WORD, g.word0 + k);
+        m->n_word += g.nch;
+        m->n_acc += 1 + g.nch;
+        break;
+      case MEM_CLASS_MAX:
+        g.label = m->n_word + 1;
+        add_layer(m, nm + "_label", LK_LABEL, g.label);
+        add_layer(m, nm + "_conf", LK_WORD, g.word0);
+        m->label_word[m->n_label++] = g.label;
+        m->n_word += 2;
+        m->n_acc += 1;
+        break;
+      case MEM_COLOR:
+        add_layer(m, nm + "_r", LK_WORD, g.word0);
+        add_layer(m, nm + "_g", LK_WORD, g.word0 + 1);
+        add_layer(m, nm + "_b", LK_WORD, g.word0 + 2);
+        m->n_word += 3;
+        m->n_acc += 2;
+        break;
+    }
+    if (s.rule != MEM_CLASS_MAX) {
+      g.flag = m->n_flag++;
+      add_layer(m, nm + "_observed", LK_FLAG, g.flag);
+    }
+  }
+  // device state
+  const long long BHW = (long long)n_maps * rows * cols;
+  auto alloc = [&](void **p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
+      !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
+      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * BHW * m->n_acc) ||
+      !alloc((void **)&m->ring, sizeof(int2) * n_maps) || !alloc((void **)&m->dstats, sizeof(unsigned long long) * 8)) {
+    free_map(m);
+    return fail(MEM_ENOMEM, "device allocation of the map state failed");
+  }
+  mem_status s = MEM_OK;
+  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * BHW * m->n_acc, m->stream) != cudaSuccess ||
+      cudaMemsetAsync(m->dstats, 0, sizeof(unsigned long long) * 8, m->stream) != cudaSuccess) {
+    s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  if (s == MEM_OK) s = reset_all(m);
+  if (s == MEM_OK && cudaStreamSynchronize(m->stream) != cudaSuccess)
+    s = fail(MEM_ECUDA, "create: %s", cudaGetErrorString(cudaGetLastError()));
+  if (s != MEM_OK) {
+    free_map(m);
+    return s;
+  }
+  *out = m;
+  return MEM_OK;
+}
+
+mem_status mem_create(float resolution, int rows, int cols, const mem_layer_spec *groups, int n_groups,
+                      unsigned flags, mem_stream stream, mem_map **out) {
+  return mem_create_batch(1, resolution, rows, cols, groups, n_groups, flags, stream, out);
+}
+
+mem_status mem_destroy(mem_map *m) {
+  free_map(m);
+  return MEM_OK;
+}
+
+mem_status mem_set_stream(mem_map *m, mem_stream s) {
+  if (check_map(m)) return MEM_EINVAL;
+  CU(cudaStreamSynchronize(m->stream));
+  m->stream = (cudaStream_t)s;
+  return MEM_OK;
+}
+
+mem_status mem_synchronize(mem_map *m) {
+  if (check_map(m)) return MEM_EINVAL;
+  CU(cudaStreamSynchronize(m->stream));
+  return MEM_OK;
+}
+
+static mem_status input_points(mem_map *m, const float *pts, const int64_t *offsets, int64_t n_single, int stride,
+                               const mem_binding *bind, int nb, const double *R, const double *t,
+                               const mem_noise *np) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (stride < 3) return fail(MEM_EINVAL, "stride %d < 3", stride);
+  if (!R || !t || !np) return fail(MEM_EINVAL, "R, t and noise must be non-NULL");
+  if (!(np->a > 0.0f) || !(np->b >= 0.0f))
+    return fail(MEM_EINVAL, "noise: need a > 0 and b >= 0 (v = a + b r^2 > 0)");
+  const int B = m->B;
+  long long total = 0, max_n = 0;
+  if (offsets) {
+    if (offsets[0] != 0) return fail(MEM_EINVAL, "offsets[0] must be 0");
+    for (int i = 0; i < B; ++i) {
+      const long long c = offsets[i + 1] - offsets[i];
+      if (c < 0) return fail(MEM_EINVAL, "offsets must be non-decreasing");
+      if (c > max_n) max_n = c;
+    }
+    total = offsets[B];
+  } else {
+    if (B != 1) return fail(MEM_EINVAL, "batched map: use mem_input_pointcloud_batch");
+    if (n_single < 0) return fail(MEM_EINVAL, "n = %lld < 0", (long long)n_single);
+    total = max_n = n_single;
+  }
+  if (total > 0 && !pts) return fail(MEM_EINVAL, "pts is NULL");
+  for (int i = 0; i < B; ++i)
+    if (!rotation_ok(R + 9 * i)) return fail(MEM_EPOSE, "map %d: R is not a rotation (SPEC.md:128)", i);
+  for (int i = 0; i < 3 * B; ++i)
+    if (!std::isfinite(t[i])) return fail(MEM_EINVAL, "t must be finite");
+  PointArgs a;
+  memset(&a, 0, sizeof a);
+  mem_status s = resolve_bindings(m, bind, nb, false, stride, a.b);
+  if (s != MEM_OK) return s;
+  if (set_device(m)) return MEM_ECUDA;
+  CU(cudaMemsetAsync(m->dstats, 0, sizeof(unsigned long long) * 8, m->stream));
+  if (m->flags & MEM_FLAG_DEBUG_POINTS) {
+    if ((size_t)total > m->dbg_cap) {
+      CU(cudaStreamSynchronize(m->stream));
+      cudaFree(m->dbg_cell);
+      cudaFree(m->dbg_code);
+      m->dbg_cell = nullptr;
+      m->dbg_code = nullptr;
+      m->dbg_cap = 0;
+      const size_t c = total + total / 4 + 1024;
+      if (cudaMalloc(&m->dbg_cell, c * sizeof(int)) != cudaSuccess || cudaMalloc(&m->dbg_code, c) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MEM_ENOMEM, "debug buffers");
+      }
+      m->dbg_cap = c;
+    }
+    m->dbg_n = total;
+  }
+  if (total == 0) return MEM_OK;  // legal; the map is unchanged
+  const void *dpts = nullptr;
+  s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
+  if (s != MEM_OK) return s;
+  a.pts = (const float *)dpts;
+  a.stride = stride;
+  a.vec4 = (stride == 4 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
+  a.n_single = n_single;
+  a.max_n = max_n;
+  a.ring = m->ring;
+  a.geo = m->geo();
+  a.st = m->st;
+  a.np = *np;
+  a.nb = nb;
+  a.stats = m->dstats;
+  if (m->flags & MEM_FLAG_DEBUG_POINTS) {
+    a.dbg_cell = m->dbg_cell;
+    a.dbg_code = m->dbg_code;
+  }
+  if (B == 1 && !offsets) {
+    a.f0 = make_frame(m, 0, R, t, nullptr);
+  } else {
+    std::vector<unsigned char> blob(sizeof(MapFrame) * B + sizeof(long long) * (B + 1) + 16);
+    MapFrame *fr = reinterpret_cast<MapFrame *>(blob.data());
+    for (int i = 0; i < B; ++i) fr[i] = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
+    const size_t off_at = sizeof(MapFrame) * B;
+    memcpy(blob.data() + off_at, offsets, sizeof(long long) * (B + 1));
+    void *d = nullptr;
+    s = stage_params(m, blob.data(), blob.size(), &d);
+    if (s != MEM_OK) return s;
+    a.frames = reinterpret_cast<const MapFrame *>(d);
+    a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
+  }
+  TIMED(MEM_STAGE_POINT, launch_point(a, m->stream));
+  CellArgs c;
+  memset(&c, 0, sizeof c);
+  c.geo = a.geo;
+  c.st = m->st;
+  c.v_out = np->v_out;
+  c.nb = nb;
+  for (int i = 0; i < nb; ++i) c.b[i] = a.b[i];
+  c.stats = m->dstats;
+  TIMED(MEM_STAGE_CELL, launch_cell(c, m->stream));
+  return MEM_OK;
+}
+
+mem_status mem_input_pointcloud(mem_map *m, const float *pts, int64_t n, int stride, const mem_binding *bind,
+                                int n_bind, const double R[9], const double t[3], const mem_noise *np) {
+  return input_points(m, pts, nullptr, n, stride, bind, n_bind, R, t, np);
+}
+
+mem_status mem_input_pointcloud_batch(mem_map *m, const float *pts, const int64_t *offsets, int stride,
+                                      const mem_binding *bind, int n_bind, const double *R, const double *t,
+                                      const mem_noise *np) {
+  if (!offsets) return fail(MEM_EINVAL, "offsets is NULL");
+  return input_points(m, pts, offsets, 0, stride, bind, n_bind, R, t, np);
+}
+
+static mem_status input_image(mem_map *m, const float *img, int C, int IH, int IW, const mem_binding *bind, int nb,
+                              const double *K, const double *R, const double *t, bool batched) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (C < 1 || IH < 1 || IW < 1) return fail(MEM_EINVAL, "image size %d x %d x %d invalid", C, IH, IW);
+  if (!img || !K || !R || !t) return fail(MEM_EINVAL, "img, K, R, t must be non-NULL");
+  if (!batched && m->B != 1) return fail(MEM_EINVAL, "batched map: use mem_input_image_batch");
+  const int B = m->B;
+  for (int i = 0; i < B; ++i) {
+    const double *k = K + 9 * i;
+    if (!(k[0] > 0.0 && k[4] > 0.0) || k[3] != 0.0 || k[6] != 0.0 || k[7] != 0.0 || k[8] != 1.0 ||
+        !std::isfinite(k[1]) || !std::isfinite(k[2]) || !std::isfinite(k[5]))
+      return fail(MEM_EINVAL, "map %d: K must be [[fx,s,cx],[0,fy,cy],[0,0,1]] with fx, fy > 0", i);
+    if (!rotation_ok(R + 9 * i)) return fail(MEM_EPOSE, "map %d: R is not a rotation (SPEC.md:128)", i);
+  }
+  for (int i = 0; i < 3 * B; ++i)
+    if (!std::isfinite(t[i])) return fail(MEM_EINVAL, "t must be finite");
+  ImageArgs a;
+  memset(&a, 0, sizeof a);
+  mem_status s = resolve_bindings(m, bind, nb, true, C, a.b);
+  if (s != MEM_OK) return s;
+  if (set_device(m)) return MEM_ECUDA;
+  const long long per = (long long)C * IH * IW;
+  const void *dimg = nullptr;
+  s = stage_input(m, img, sizeof(float) * (size_t)per * B, &dimg);
+  if (s != MEM_OK) return s;
+  a.img = (const float *)dimg;
+  a.C = C;
+  a.IH = IH;
+  a.IW = IW;
+  a.map_stride = per;
+  a.ring = m->ring;
+  a.geo = m->geo();
+  a.st = m->st;
+  a.nb = nb;
+  if (B == 1) {
+    a.f0 = make_frame(m, 0, R, t, K);
+  } else {
+    std::vector<MapFrame> fr(B);
+    for (int i = 0; i < B; ++i) fr[i] = make_frame(m, i, R + 9 * i, t + 3 * i, K + 9 * i);
+    void *d = nullptr;
+    s = stage_params(m, fr.data(), sizeof(MapFrame) * B, &d);
+    if (s != MEM_OK) return s;
+    a.frames = reinterpret_cast<const MapFrame *>(d);
+  }
+  TIMED(MEM_STAGE_IMAGE, launch_image(a, m->stream));
+  return MEM_OK;
+}
+
+mem_status mem_input_image(mem_map *m, const float *img, int C, int H, int W, const mem_binding *bind, int n_bind,
+                           const double K[9], const double R[9], const double t[3]) {
+  return input_image(m, img, C, H, W, bind, n_bind, K, R, t, false);
+}
+
+mem_status mem_input_image_batch(mem_map *m, const float *img, int C, int H, int W, const mem_binding *bind,
+                                 int n_bind, const double *K, const double *R, const double *t) {
+  return input_image(m, img, C, H, W, bind, n_bind, K, R, t, true);
+}
+
+static mem_status move_to(mem_map *m, const double *xy) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (!xy) return fail(MEM_EINVAL, "xy is NULL");
+  const int B = m->B;
+  for (int i = 0; i < 2 * B; ++i)
+    if (!std::isfinite(xy[i])) return fail(MEM_EINVAL, "position must be finite");
+  if (set_device(m)) return MEM_ECUDA;
+  std::vector<ShiftRec> recs(B);
+  int max_count = 0;
+  bool any = false;
+  for (int i = 0; i < B; ++i) {
+    // D14: k = floor(x/res + 1/2) in fp64
+    const long long kx = (long long)std::floor(xy[2 * i] / (double)m->res + 0.5);
+    const long long ky = (long long)std::floor(xy[2 * i + 1] / (double)m->res + 0.5);
+    long long sr = kx - m->kx[i], sc = ky - m->ky[i];
+    m->kx[i] = kx;
+    m->ky[i] = ky;
+    const bool all = sr >= m->H || -sr >= m->H || sc >= m->W || -sc >= m->W;
+    if (all) {
+      sr = m->H;
+      sc = 0;
+      m->r0[i] = 0;
+      m->c0[i] = 0;
+    } else {
+      m->r0[i] = (int)(((m->r0[i] + sr) % m->H + m->H) % m->H);
+      m->c0[i] = (int)(((m->c0[i] + sc) % m->W + m->W) % m->W);
+    }
+    recs[i].sr = (int)sr;
+    recs[i].sc = (int)sc;
+    recs[i].r0 = m->r0[i];
+    recs[i].c0 = m->c0[i];
+    const int cnt = all ? m->H * m->W : (int)((sr < 0 ? -sr : sr) * m->W + (sc < 0 ? -sc : sc) * m->H);
+    if (cnt > max_count) max_count = cnt;
+    any |= (sr != 0 || sc != 0);
+  }
+  if (!any) return MEM_OK;  // s = 0 everywhere: bit-identical
+  ShiftArgs a;
+  memset(&a, 0, sizeof a);
+  a.geo = m->geo();
+  a.st = m->st;
+  a.ring = m->ring;
+  a.n_word = m->n_word;
+  a.n_flag = m->n_flag;
+  a.n_label = m->n_label;
+  for (int i = 0; i < m->n_label; ++i) a.label_word[i] = m->label_word[i];
+  a.max_count = max_count;
+  if (B == 1) {
+    a.rec0 = recs[0];
+  } else {
+    void *d = nullptr;
+    mem_status s = stage_params(m, recs.data(), sizeof(ShiftRec) * B, &d);
+    if (s != MEM_OK) return s;
+    a.recs = reinterpret_cast<const ShiftRec *>(d);
+  }
+  TIMED(MEM_STAGE_SHIFT, launch_shift(a, m->stream));
+  return MEM_OK;
+}
+
+mem_status mem_move_to(mem_map *m, double x, double y) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (m->B != 1) return fail(MEM_EINVAL, "batched map: use mem_move_to_batch");
+  const double xy[2] = {x, y};
+  return move_to(m, xy);
+}
+
+mem_status mem_move_to_batch(mem_map *m, const double *xy) { return move_to(m, xy); }
+
+static const Layer *find_layer(const mem_map *m, const char *name) {
+  if (!name) return nullptr;
+  for (const Layer &l : m->layers)
+    if (l.name == name) return &l;
+  return nullptr;
+}
+
+static ReadArgs read_args(const mem_map *m, const Layer &l) {
+  ReadArgs a;
+  memset(&a, 0, sizeof a);
+  a.geo = m->geo();
+  a.st = m->st;
+  a.ring = m->ring;
+  a.idx = l.idx;
+  a.first = l.first;
+  a.K = l.K;
+  a.flag = l.flag;
+  switch (l.kind) {
+    case LK_ELEV: a.kind = RK_ELEV; break;
+    case LK_VAR: a.kind = RK_VAR; break;
+    case LK_VALID: a.kind = RK_FLAG; break;
+    case LK_WORD: a.kind = RK_WORD; break;
+    case LK_LABEL: a.kind = RK_LABEL; break;
+    case LK_FLAG: a.kind = RK_FLAG; break;
+    case LK_THETA: a.kind = RK_THETA; break;
+  }
+  return a;
+}
+
+mem_status mem_get_layer(const mem_map *cm, const char *name, float *out) {
+  mem_map *m = const_cast<mem_map *>(cm);
+  if (check_map(m)) return MEM_EINVAL;
+  if (!out) return fail(MEM_EINVAL, "out is NULL");
+  const Layer *l = find_layer(m, name);
+  if (!l) return fail(MEM_ENOTFOUND, "no layer named '%s'", name ? name : "(null)");
+  if (set_device(m)) return MEM_ECUDA;
+  ReadArgs a = read_args(m, *l);
+  const size_t bytes = sizeof(float) * (size_t)m->B * m->H * m->W;
+  const bool dev = is_device_ptr(out);
+  if (dev) {
+    a.out = out;
+  } else {
+    mem_status s = grow((void **)&m->dout, &m->dout_cap, bytes, m->stream);
+    if (s != MEM_OK) return s;
+    a.out = m->dout;
+  }
+  TIMED(MEM_STAGE_READ, launch_read(a, m->stream));
+  if (!dev) {
+    TIMED(MEM_STAGE_D2H, cudaMemcpyAsync(out, m->dout, bytes, cudaMemcpyDeviceToHost, m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+  }
+  return MEM_OK;
+}
+
+mem_status mem_set_layer(mem_map *m, const char *name, const float *src) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (!src) return fail(MEM_EINVAL, "src is NULL");
+  const Layer *l = find_layer(m, name);
+  if (!l) return fail(MEM_ENOTFOUND, "no layer named '%s'", name ? name : "(null)");
+  if (l->kind == LK_THETA) return fail(MEM_EINVAL, "layer '%s' is derived (alpha / sum alpha)", name);
+  if (set_device(m)) return MEM_ECUDA;
+  ReadArgs a = read_args(m, *l);
+  const void *d = nullptr;
+  mem_status s = stage_input(m, src, sizeof(float) * (size_t)m->B * m->H * m->W, &d);
+  if (s != MEM_OK) return s;
+  a.src = (const float *)d;
+  TIMED(MEM_STAGE_WRITE, launch_write(a, m->stream));
+  return MEM_OK;
+}
+
+mem_status mem_get_layer_names(const mem_map *m, char *buf, size_t cap) {
+  if (!m || !buf) return fail(MEM_EINVAL, "NULL argument");
+  std::string s;
+  for (const Layer &l : m->layers) s += l.name + "\n";
+  if (s.size() + 1 > cap) return fail(MEM_EINVAL, "buffer too small: need %zu bytes", s.size() + 1);
+  memcpy(buf, s.c_str(), s.size() + 1);
+  return MEM_OK;
+}
+
+mem_status mem_memory_footprint(const mem_map *m, uint64_t *bytes) {
+  if (!m || !bytes) return fail(MEM_EINVAL, "NULL argument");
+  const uint64_t cells = (uint64_t)m->B * m->H * m->W;
+  *bytes = cells * (4ull * m->n_word + (uint64_t)m->n_flag);
+  return MEM_OK;
+}
+
+mem_status mem_get_info(const mem_map *m, int *n_maps, int *rows, int *cols, float *resolution) {
+  if (!m) return fail(MEM_EINVAL, "map is NULL");
+  if (n_maps) *n_maps = m->B;
+  if (rows) *rows = m->H;
+  if (cols) *cols = m->W;
+  if (resolution) *resolution = m->res;
+  return MEM_OK;
+}
+
+mem_status mem_get_center(const mem_map *m, int64_t *kxy) {
+  if (!m || !kxy) return fail(MEM_EINVAL, "NULL argument");
+  for (int i = 0; i < m->B; ++i) {
+    kxy[2 * i] = m->kx[i];
+    kxy[2 * i + 1] = m->ky[i];
+  }
+  return MEM_OK;
+}
+
+mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
+  if (!m || !out) return fail(MEM_EINVAL, "NULL argument");
+  if (set_device(m)) return MEM_ECUDA;
+  unsigned long long h[8];
+  CU(cudaMemcpyAsync(h, m->dstats, sizeof h, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  h[0] = h[1] + h[2] + h[3] + h[4] + h[5] + h[6];
+  out->n_input = h[0];
+  out->n_nonfinite = h[1];
+  out->n_range = h[2];
+  out->n_height = h[3];
+  out->n_oob = h[4];
+  out->n_inlier = h[5];
+  out->n_outlier = h[6];
+  out->n_cells_touched = h[7];
+  return MEM_OK;
+}
+
+mem_status mem_profile(mem_map *m, int enable) {
+  if (check_map(m)) return MEM_EINVAL;
+  m->prof.on = enable != 0;
+  return MEM_OK;
+}
+
+mem_status mem_profile_read(mem_map *m, double *ms, uint64_t *counts, int reset) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (set_device(m)) return MEM_ECUDA;
+  CU(cudaStreamSynchronize(m->stream));
+  for (int st = 0; st < MEM_N_STAGES; ++st) {
+    for (auto &pr : m->prof.pending[st]) {
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, pr.first, pr.second));
+      m->prof.ms[st] += t;
+      m->prof.pool.push_back(pr.first);
+      m->prof.pool.push_back(pr.second);
+    }
+    m->prof.pending[st].clear();
+    if (ms) ms[st] = m->prof.ms[st];
+    if (counts) counts[st] = m->prof.count[st];
+    if (reset) {
+      m->prof.ms[st] = 0.0;
+      m->prof.count[st] = 0;
+    }
+  }
+  return MEM_OK;
+}
+
+mem_status mem_debug_point_codes(const mem_map *m, int32_t *cell, uint8_t *code) {
+  if (!m) return fail(MEM_EINVAL, "map is NULL");
+  if (!(m->flags & MEM_FLAG_DEBUG_POINTS)) return fail(MEM_EINVAL, "map created without MEM_FLAG_DEBUG_POINTS");
+  if (set_device(m)) return MEM_ECUDA;
+  if (m->dbg_n == 0) return MEM_OK;
+  if (cell) CU(cudaMemcpyAsync(cell, m->dbg_cell, sizeof(int) * m->dbg_n, cudaMemcpyDefault, m->stream));
+  if (code) CU(cudaMemcpyAsync(code, m->dbg_code, m->dbg_n, cudaMemcpyDefault, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return MEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,303 @@
+"""GPU parity: libmem (CUDA, through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Integer outputs (per-point cell + code, counters, valid, observed flags, class_max labels,
+ring/shift indexing) must be bit-exact; fp32 layers within 1e-5 rel / 1e-6 abs after 10
+fused frames (north_star).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2309_16818_b200 import mem as M  # noqa: E402
+from synth import scenes as S  # noqa: E402
+from tests.helpers import compare_layers, copy_state_to_oracle  # noqa: E402
+
+
+def make_pair(res, rows, cols, groups, debug=True):
+    g = M.Map(res, rows, cols, groups, debug_points=debug)
+    o = O.OracleMap(res, rows, cols, groups)
+    return g, o
+
+
+def step_points(g, o, pts, binds, R, t, noise, check_codes=True, device=True):
+    src = torch.from_numpy(pts).cuda() if device else pts
+    g.input_pointcloud(src, binds, R, t, noise)
+    oc = o.input_pointcloud(pts, binds, R, t, noise, debug=check_codes)
+    if check_codes:
+        cell, code = g.debug_codes()
+        assert np.array_equal(code, oc[1]), f"codes differ at {np.argwhere(code != oc[1])[:5].ravel()}"
+        assert np.array_equal(cell, oc[0]), f"cells differ at {np.argwhere(cell != oc[0])[:5].ravel()}"
+    gs, os_ = g.stats(), o.stats()
+    assert gs == os_, (gs, os_)
+    return gs
+
+
+# ---------------------------------------------------------------- C1 (configs[0])
+def test_c1_chained_10_frames():
+    c = S.C1
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    for f in range(c["frames"]):
+        fr = S.c1_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        assert tuple(g.center()[0]) == o.center()
+        st = step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        assert st["n_outlier"] > 0 or f == 0
+        compare_layers(g, o, where=f"frame {f}: ")
+
+
+# ---------------------------------------------------------------- all six rules, ragged map
+ALL_GROUPS = [
+    dict(name="feat", rule=M.MEM_AVERAGE, n_channels=3, w=0.5),
+    dict(name="gf", rule=M.MEM_GAUSSIAN, n_channels=2, sigma_f2=0.2, mu0=0.1, sigma0_2=1.5),
+    dict(name="cavg", rule=M.MEM_CLASS_AVERAGE, n_channels=4, w=0.3),
+    dict(name="sem", rule=M.MEM_CLASS_BAYESIAN, n_channels=4, alpha0=1.0),
+    dict(name="top", rule=M.MEM_CLASS_MAX, n_channels=4),
+    dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5),
+]
+ALL_BINDS = [(0, 3, 0), (3, 2, 1), (5, 4, 2), (5, 4, 3), (5, 4, 4), (9, 1, 5)]
+NOISE_R = dict(a=1e-3, b=1e-4, r_min=0.05, r_max=6.0, h_min=-3.0, h_max=1.0, tau2=4.0, v_out=0.02)
+
+
+def random_all_channels(seed, n, rows, cols, res):
+    rng = np.random.default_rng(seed)
+    pts = S.random_cloud(seed, n, 13, rows, cols, res, channel_kind="feature")
+    p = rng.dirichlet(np.ones(4) * 0.7, n)
+    tie = rng.uniform(size=n) < 0.1
+    p[tie] = np.round(p[tie] * 4) / 4  # exact ties exercise the lowest-index rule (D19)
+    pts[:, 8:12] = p.astype(np.float32)
+    pts[:, 12] = S.pack_rgb(rng.integers(0, 256, (n, 3)).astype(np.uint8))
+    bad = rng.uniform(size=n) < 0.01
+    pts[bad, 3] = np.nan  # D31: non-finite channel skips only that group
+    outl = rng.uniform(size=n) < 0.03
+    pts[outl, 2] += 1.5
+    return pts
+
+
+@pytest.mark.parametrize("rows,cols,res", [(37, 53, 0.1), (64, 64, 0.05)])
+def test_all_rules_chained_with_shifts(rows, cols, res):
+    g, o = make_pair(res, rows, cols, ALL_GROUPS)
+    moves = [(0.0, 0.0), (0.12, 0.0), (0.31, -0.22), (-0.4, 0.05), (-0.4, 0.05), (3.0, 2.0), (2.95, 2.1),
+             (2.7, 2.3), (2.5, 2.2), (2.52, 2.18)]
+    for f, (x, y) in enumerate(moves):
+        g.move_to(x, y)
+        o.move_to(x, y)
+        pts = random_all_channels(100 + f, 5000 + 137 * f, rows, cols, res)
+        R = S.rot_z(0.3 * f)
+        t = np.array([x + 0.01, y - 0.02, 1.0])
+        step_points(g, o, pts, ALL_BINDS, R, t, NOISE_R)
+        compare_layers(g, o, where=f"frame {f}: ")
+
+
+# ---------------------------------------------------------------- C2 (configs[1]) full size
+def test_c2_lidar_10_frames():
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    for f in range(c["frames"]):
+        fr = S.c2_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        compare_layers(g, o, where=f"frame {f}: ")
+    assert g.get_layer("valid").sum() > 5000
+
+
+def test_host_buffers_equal_device_buffers():
+    """the e2e path (host pointers through the C-ABI) gives bit-identical maps."""
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    a = M.Map(c["res"], c["rows"], c["cols"], groups)
+    b = M.Map(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):
+        fr = S.c2_frame(f)
+        for m, dev in ((a, True), (b, False)):
+            m.move_to(*fr["move"])
+            m.input_pointcloud(torch.from_numpy(fr["points"]).cuda() if dev else fr["points"], [(0, 1, 0)],
+                               fr["R"], fr["t"], c["noise"])
+    for nm in a.layer_names():
+        assert np.array_equal(a.get_layer(nm), b.get_layer(nm), equal_nan=True), nm
+
+
+# ---------------------------------------------------------------- image path
+def camera_looking_at(eye, target):
+    """R (camera->map): z_c toward target, x_c right, y_c down."""
+    z = np.asarray(target, float) - np.asarray(eye, float)
+    z /= np.linalg.norm(z)
+    up = np.array([0.0, 0.0, 1.0])
+    x = np.cross(z, up)
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    return np.stack([x, y, z], 1)
+
+
+IMG_GROUPS = [
+    dict(name="sem", rule=M.MEM_CLASS_BAYESIAN, n_channels=5, alpha0=1.0),
+    dict(name="top", rule=M.MEM_CLASS_MAX, n_channels=5),
+    dict(name="feat", rule=M.MEM_AVERAGE, n_channels=3, w=0.5),
+    dict(name="gf", rule=M.MEM_GAUSSIAN, n_channels=2, sigma_f2=0.3, mu0=0.0, sigma0_2=1.0),
+    dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5),
+    dict(name="cavg", rule=M.MEM_CLASS_AVERAGE, n_channels=5, w=0.4),
+]
+IMG_BINDS = [(0, 5, 0), (0, 5, 1), (5, 3, 2), (8, 2, 3), (10, 3, 4), (0, 5, 5)]
+
+
+def test_image_fusion_chained():
+    rows, cols, res = 60, 70, 0.05
+    g, o = make_pair(res, rows, cols, IMG_GROUPS)
+    rng = np.random.default_rng(41)
+    noise = dict(a=1e-3, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=9.0, v_out=0.01)
+    K = np.array([[120.0, 0.5, 79.5], [0, 118.0, 59.5], [0, 0, 1.0]])
+    for f in range(10):
+        pts = S.random_cloud(200 + f, 20000, 3, rows, cols, res)
+        step_points(g, o, pts, [], np.eye(3), [0.0, 0.0, 1.0], noise)
+        eye = np.array([rng.uniform(-3, -2), rng.uniform(-1, 1), rng.uniform(1.0, 2.0)])
+        R = camera_looking_at(eye, [rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), 0.0])
+        img = np.concatenate([S.softmax_image(rng.integers(0, 5, (120, 160)), 5, rng),
+                              rng.normal(0, 1, (5, 120, 160)).astype(np.float32),
+                              rng.uniform(0, 255, (3, 120, 160)).astype(np.float32)])
+        img[5, rng.integers(0, 120, 50), rng.integers(0, 160, 50)] = np.nan
+        src = torch.from_numpy(img).cuda() if f % 2 == 0 else img
+        g.input_image(src, IMG_BINDS, K, R, eye)
+        o.input_image(img, IMG_BINDS, K, R, eye)
+        compare_layers(g, o, where=f"frame {f}: ")
+        if f == 4:
+            g.move_to(0.33, -0.27)
+            o.move_to(0.33, -0.27)
+    assert (g.get_layer("top_label") >= 0).sum() > 500
+
+
+# ---------------------------------------------------------------- batched maps
+def test_batched_equals_single_and_oracle():
+    rows, cols, res = 48, 40, 0.1
+    B = 5
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5),
+              dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5)]
+    gb = M.Map(res, rows, cols, groups, n_maps=B)
+    singles = [M.Map(res, rows, cols, groups) for _ in range(B)]
+    oras = [O.OracleMap(res, rows, cols, groups) for _ in range(2)]
+    rng = np.random.default_rng(43)
+    binds = [(0, 1, 0), (1, 1, 1)]
+    for f in range(4):
+        counts = rng.integers(0, 3000, B)
+        counts[f % B] = 0  # an empty map in the batch
+        clouds = []
+        for b in range(B):
+            p = S.random_cloud(1000 * f + b, int(counts[b]), 5, rows, cols, res)
+            p[:, 4] = S.pack_rgb(rng.integers(0, 256, (len(p), 3)).astype(np.uint8))
+            clouds.append(p)
+        off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        allp = np.concatenate(clouds) if off[-1] else np.zeros((0, 5), np.float32)
+        Rs = np.stack([S.rot_z(0.1 * b + f) for b in range(B)])
+        ts = np.stack([[0.05 * b, -0.03 * f, 1.0] for b in range(B)])
+        xy = np.stack([[0.1 * f * (b + 1), -0.07 * f] for b in range(B)])
+        gb.move_to_batch(xy)
+        gb.input_pointcloud_batch(torch.from_numpy(allp).cuda(), off, binds, Rs, ts, NOISE_R)
+        for b in range(B):
+            singles[b].move_to(*xy[b])
+            singles[b].input_pointcloud(clouds[b], binds, Rs[b], ts[b], NOISE_R)
+        for b in range(2):
+            oras[b].move_to(*xy[b])
+            oras[b].input_pointcloud(clouds[b], binds, Rs[b], ts[b], NOISE_R)
+    for nm in gb.layer_names():
+        allb = gb.get_layer(nm)
+        for b in range(B):
+            assert np.array_equal(allb[b], singles[b].get_layer(nm), equal_nan=True), (nm, b)
+    for b in range(2):
+        compare_layers(singles[b], oras[b], where=f"map {b}: ")
+
+
+# ---------------------------------------------------------------- single-step parity, run-twice identity
+def test_single_step_parity_and_determinism():
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    runs = []
+    for rep in range(2):
+        g = M.Map(c["res"], c["rows"], c["cols"], groups, debug_points=True)
+        for f in range(6):
+            fr = S.c2_frame(f)
+            g.move_to(*fr["move"])
+            if f == 5 and rep == 0:  # single step from the GPU's own pre-frame state
+                o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+                o.move_to(*fr["move"])
+                copy_state_to_oracle(g, o)
+                step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+                compare_layers(g, o, where="single step: ")
+            else:
+                g.input_pointcloud(torch.from_numpy(fr["points"]).cuda(), [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        runs.append({nm: g.get_layer(nm) for nm in g.layer_names()})
+    for nm in runs[0]:
+        assert np.array_equal(runs[0][nm], runs[1][nm], equal_nan=True), nm  # run-twice bit identity
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_cases():
+    noise = dict(a=1e-2, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=9.0, v_out=0.01)
+    groups = [dict(name="f", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)]
+    # 1x1 map
+    g, o = make_pair(0.5, 1, 1, groups)
+    pts = np.array([[0.1, 0.1, -1.0, 2.0], [0.3, 0.0, -1.0, 3.0], [np.nan, 0, 0, 1.0]], np.float32)
+    step_points(g, o, pts, [(0, 1, 0)], np.eye(3), [0, 0, 1.0], noise)
+    compare_layers(g, o)
+    # empty cloud: map unchanged, stats zero
+    before = {nm: g.get_layer(nm) for nm in g.layer_names()}
+    g.input_pointcloud(np.zeros((0, 4), np.float32), [(0, 1, 0)], np.eye(3), [0, 0, 1.0], noise)
+    assert g.stats()["n_input"] == 0
+    for nm, v in before.items():
+        assert np.array_equal(g.get_layer(nm), v, equal_nan=True)
+    # all non-finite / all out of bounds
+    g, o = make_pair(0.1, 16, 16, groups)
+    for pts in (np.full((1000, 4), np.nan, np.float32),
+                np.tile(np.array([[50.0, 0.0, -1.0, 1.0]], np.float32), (777, 1))):
+        step_points(g, o, pts, [(0, 1, 0)], np.eye(3), [0, 0, 1.0], noise)
+        compare_layers(g, o)
+    # one point per cell on a dense grid (no within-cell aggregation), odd tail
+    g, o = make_pair(0.25, 33, 31, groups)
+    ii, jj = np.meshgrid(np.arange(33), np.arange(31), indexing="ij")
+    pts = np.stack([(ii.ravel() + 0.5 - 16.5) * 0.25, (jj.ravel() + 0.5 - 15.5) * 0.25,
+                    np.full(ii.size, -1.0), np.arange(ii.size, dtype=float)], 1).astype(np.float32)
+    step_points(g, o, pts, [(0, 1, 0)], np.eye(3), [0, 0, 1.0], noise)
+    compare_layers(g, o)
+    assert g.get_layer("valid").all()
+    # many points in one cell (heavy atomic contention)
+    g, o = make_pair(1.0, 4, 4, groups)
+    rng = np.random.default_rng(47)
+    pts = np.concatenate([rng.uniform(0.01, 0.99, (100000, 2)), rng.normal(-1, 0.01, (100000, 1)),
+                          rng.normal(0, 1, (100000, 1))], 1).astype(np.float32)
+    step_points(g, o, pts, [(0, 1, 0)], np.eye(3), [0, 0, 1.0], noise)
+    compare_layers(g, o)
+
+
+def test_errors_and_info():
+    g = M.Map(0.1, 10, 12, [dict(name="f", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)])
+    with pytest.raises(M.MemError) as e:
+        R = np.eye(3)
+        R[0, 1] = 0.01
+        g.input_pointcloud(np.zeros((3, 4), np.float32), [(0, 1, 0)], R, [0, 0, 0], NOISE_R)
+    assert e.value.status == M.MEM_EPOSE
+    with pytest.raises(M.MemError) as e:
+        g.input_pointcloud(np.zeros((3, 4), np.float32), [(1, 1, 0)], np.eye(3), [0, 0, 0], NOISE_R)
+    assert e.value.status == M.MEM_EINVAL
+    with pytest.raises(M.MemError) as e:
+        g.get_layer("nope")
+    assert e.value.status == M.MEM_ENOTFOUND
+    with pytest.raises(M.MemError) as e:
+        M.Map(0.1, 10, 10, [dict(name="a", rule=M.MEM_AVERAGE), dict(name="a", rule=M.MEM_AVERAGE)])
+    assert e.value.status == M.MEM_EDUPNAME
+    with pytest.raises(M.MemError) as e:
+        M.Map(0.1, 10, 10, [dict(name="c", rule=M.MEM_CLASS_BAYESIAN, n_channels=1)])
+    assert e.value.status == M.MEM_ERULE
+    # memory accounting: each fp32 layer is rows x cols x 4 bytes
+    base = M.Map(0.04, 200, 200, [])
+    one = M.Map(0.04, 200, 200, [dict(name="f", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)])
+    assert one.footprint() - base.footprint() == 160000 + 40000  # + 1-byte observed flag
+    assert "elevation" in base.layer_names() and "f_observed" in one.layer_names()
