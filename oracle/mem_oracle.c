@@ -387,10 +387,11 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
     if (m->valid[j]) {
       const double sp = (double)m->s2[j] + (double)n_out[j] * (double)np->v_out;
       if (n_in[j] > 0) {
-        const double den = 1.0 / sp + P[j];
-        const double h_new = ((double)m->h[j] / sp + S[j]) / den;
-        m->h[j] = (float)h_new;
-        m->s2[j] = (float)(1.0 / den);
+        /* information form h' = (h/sp + S)/(1/sp + P), sigma2' = 1/(1/sp + P), written with
+           numerator and denominator multiplied by sp (reading D7): */
+        const double den = 1.0 + P[j] * sp;
+        m->h[j] = (float)(((double)m->h[j] + S[j] * sp) / den);
+        m->s2[j] = (float)(sp / den);
       } else {
         m->s2[j] = (float)sp;
       }
