@@ -279,7 +279,9 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
   const double cx = (double)m->kx * (double)m->res, cy = (double)m->ky * (double)m->res;
   const float tx = (float)(t[0] - cx), ty = (float)(t[1] - cy), tz = (float)t[2];
   const float hH = (float)H / 2.0f, hW = (float)W / 2.0f;
-  const float res = m->res;
+  /* binning multiplies by 1/res rounded once to fp32 (reading D13) */
+  const float inv_res = (float)(1.0 / (double)m->res);
+  const float rmin2 = np->r_min * np->r_min, rmax2 = np->r_max * np->r_max;
 
   /* per-cell, per-frame sufficient statistics */
   unsigned long long *n_in = calloc(cells, sizeof *n_in), *n_out = calloc(cells, sizeof *n_out);
@@ -306,9 +308,10 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
     if (!isfinite(px) || !isfinite(py) || !isfinite(pz)) {
       code = OM_NONFINITE; /* 2.1 */
     } else {
-      const float r2 = (px * px + py * py) + pz * pz; /* 2.2 */
-      const float r = sqrtf(r2);
-      if (!(np->r_min <= r && r <= np->r_max)) {
+      /* 2.2: range filter r_min <= |p| <= r_max, tested on the square (reading D9):
+         r_min^2 <= r2 <= r_max^2 with the squares rounded once to fp32 */
+      const float r2 = (px * px + py * py) + pz * pz;
+      if (!(rmin2 <= r2 && r2 <= rmax2)) {
         code = OM_RANGE;
       } else {
         /* 2.3: q = R p ("point trsf.") */
@@ -322,7 +325,7 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
           const float x = qx + tx, y = qy + ty;
           z = qz + tz;
           /* 2.5: bin by horizontal coordinates, half-open cells */
-          const float fr = x / res + hH, fc = y / res + hW;
+          const float fr = x * inv_res + hH, fc = y * inv_res + hW; /* reading D13 */
           if (!(0.0f <= fr && fr < (float)H && 0.0f <= fc && fc < (float)W)) {
             code = OM_OOB;
           } else {
