@@ -39,7 +39,7 @@ POOL = 16  # trajectory period of synth.c2_pose; also the number of distinct ste
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="mem", choices=["mem", "reference"])
     ap.add_argument("--maps", type=int, default=64, help="maps per GPU")
@@ -86,7 +86,12 @@ class Clocks:
 
     def _read(self):
         for line in self.p.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.monotonic()
+        while self.p and not self.samples and time.monotonic() - t0 < timeout:
+            time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.p:
@@ -94,8 +99,9 @@ class Clocks:
             self.p.wait()
             self.t.join(timeout=2)
 
-    def summary(self):
-        rows = [r for r in self.samples if len(r) >= 8]
+    def summary(self, t0=None, t1=None):
+        """samples inside [t0, t1] (the timed region, widened by one sampling period)."""
+        rows = [r for t, r in self.samples if len(r) >= 8 and (t0 is None or t0 - 0.02 <= t <= t1 + 0.02)]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -222,21 +228,24 @@ def run_mem(a):
         mp.input_pointcloud_batch(batches[k] if src is None else src[k % len(src)], offsets, binds, Rs[k], ts[k],
                                   c["noise"])
 
-    for s in range(a.warmup):
-        step(s)
-    torch.cuda.synchronize()
-    mp.profile_read(reset=True)
-    mp.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
+        clk.wait_first()
+        for s in range(a.warmup):
+            step(s)
+        torch.cuda.synchronize()
+        mp.profile_read(reset=True)
+        mp.profile(True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        t_on = time.monotonic()
         ev0.record(stream)
         for s in range(a.warmup, a.warmup + a.steps):
             step(s)
         ev1.record(stream)
         torch.cuda.synchronize()
+        t_off = time.monotonic()
         if world > 1:
             dist.barrier()
     mp.profile(False)
@@ -250,19 +259,19 @@ def run_mem(a):
     total_pts = npts * M_ * a.steps * world
     value = total_pts / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (k_point), timed live with CUDA events
-    point_ms, point_n = prof["point"]
-    cell_ms, cell_n = prof["cell"]
+    # ---- roofline of the dominant kernel (k_fused: points + cell update), CUDA events live
+    fused_ms, fused_n = prof["point"]
     pk, pk_src = peaks()
-    bytes_point = M_ * npts * 16  # algorithmic: every point read once (16 B)
-    achieved = bytes_point / (point_ms / point_n * 1e-3) / 1e9 if point_n else None
+    # algorithmic bytes per launch: every point read once (16 B) + read and
+    # write of the stored state of every touched cell (C2 colour map: 22 B per cell)
+    bytes_fused = M_ * npts * 16 + 2 * 22 * stats["n_cells_touched"]
+    achieved = bytes_fused / (fused_ms / fused_n * 1e-3) / 1e9 if fused_n else None
     tr = traffic_record()
     traffic = None
     if tr and tr.get("maps") == M_ and tr.get("points_per_map") == npts:
-        traffic = tr.get("k_point_dram_bytes_per_launch")
+        traffic = tr.get("k_fused_dram_bytes_per_launch")
     launches = sum(prof[k][1] for k in ("shift", "point", "cell", "image", "read", "write"))
-    # whole-step algorithmic bytes: points + read/write of the touched cells' state (22 B/cell)
-    step_bytes = M_ * npts * 16 + 2 * 22 * stats["n_cells_touched"]
+    step_bytes = bytes_fused
 
     # ---- e2e: through the C-ABI with HOST (pinned) buffers, H2D + D2H inside the timed region
     e2e = None
@@ -327,13 +336,13 @@ def run_mem(a):
                        "l2": "inputs > L2: 134 MB of points per step from a 16-step rotating pool (2.1 GB)"},
             "map_updates_per_s": M_ * a.steps * world / (ms_max * 1e-3),
             "step_hbm_gbs": step_bytes / (ms_max / a.steps * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_point", "achieved": achieved, "peak": pk,
+            "roofline": {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": pk,
                          "peak_source": pk_src, "unit": "GB/s",
                          "frac": (achieved / pk) if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": bytes_point},
-            "stages_ms_per_step": {k: v[0] / a.steps for k, v in prof.items() if v[1]},
+                         "algorithmic_bytes_per_launch": bytes_fused},
+            "stages_ms_per_step": {("fused" if k == "point" else k): v[0] / a.steps for k, v in prof.items() if v[1]},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(t_on, t_off),
             "e2e": e2e,
             "single_map_c2": single,
             "cpu_baseline": cpu,

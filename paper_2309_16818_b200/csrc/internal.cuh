@@ -50,9 +50,9 @@ struct BindDesc {  // one binding of a call, resolved against its group
 struct MapFrame {  // per-map, per-call point/image frame parameters
   float R[9];      // sensor->map rotation (fp32 of the host doubles)
   float t[3];      // t.xy relative to the map centre (fp64 subtraction, then fp32), t.z
-  int r0, c0;      // ring offsets
   float K[5];      // images: fx, skew, cx, fy, cy
-  int pad;
+  int sr, sc;      // pending (lazy) shift of the preceding mem_move_to: strips to reset first
+  int r0, c0;      // ring offsets after that shift
 };
 
 struct ShiftRec {  // per-map shift of one move_to call
@@ -64,8 +64,9 @@ struct Geometry {
   int H, W;
   int HW;
   int n_maps;
-  long long BHW;  // n_maps * HW: stride between layers
+  long long BHW;  // n_maps * HW: stride between layers (< 2^31, so cell indices fit in int)
   float res, hH, hW;
+  float inv_res;  // (float)(1.0 / res): binning multiplies (reading D13)
 };
 
 struct State {

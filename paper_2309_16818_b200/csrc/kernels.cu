@@ -1,13 +1,17 @@
 // kernels.cu -- the sm_100a kernels of the MEM hot path.
 //
-//   k_point  a2-a8   one thread per point: load, finiteness/range/height filters, transform,
-//                    bin, noise variance, Mahalanobis test against the pre-frame state,
-//                    scatter-accumulate the sufficient statistics (native 64-bit REDs)
-//   k_cell   a9-a10  one thread per touched cell: Kalman height fusion, per-group rules,
-//                    re-zero the statistics it consumed
-//   k_image  a11-a12 one thread per valid cell: project, frustum, gather, fuse (N_j = 1)
-//   k_shift  a13     reset the scrolled-in strips of the ring buffer, advance ring offsets
-//   k_read   a14     unroll the ring into logical row-major fp32, derive theta / NaN
+//   k_points a2-a8  persistent grid-stride over 128-point warp-items of one wave of maps:
+//                   coalesced float4 loads (4 in flight per lane), filters, transform, bin,
+//                   noise, one batched state gather for the Mahalanobis test, and
+//                   warp-aggregated native 64-bit REDs into L2-resident per-cell scratch
+//   k_cells  a9-a10 + lazy a13  grid-stride over 128-cell warp-items of the same wave: strip
+//                   reset of a pending shift, Kalman height fusion, per-group rules (fp64),
+//                   re-zero the scratch.  k_cells(w) runs on a side stream concurrently with
+//                   k_points(w+1); waves alternate between the two halves of the scratch pool.
+//   k_image  a11-a12  one thread per valid cell: project, frustum, gather, fuse (N_j = 1)
+//   k_shift  a13      eager strip reset (only when a shift cannot be folded into k_fused)
+//   k_read   a14      unroll the ring into logical row-major fp32, derive theta / NaN
+//   k_write           the inverse of k_read (state injection for single-step parity)
 //
 // Everything is stream-ordered; no kernel synchronises the host.
 #include <cmath>
@@ -16,244 +20,592 @@
 
 namespace memk {
 
-// ---------------------------------------------------------------- loads
-__device__ __forceinline__ float4 ld_stream_f4(const float *p) {
+// ---------------------------------------------------------------- memory helpers
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// read-once point data: no L1 allocation, evict-first in L2 so the scratch of the maps in
+// flight keeps its L2 residency
+__device__ __forceinline__ float4 ld_stream_f4(const float *p, unsigned long long pol) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return r;
 }
-
-__device__ __forceinline__ bool finite3(float a, float b, float c) {
-  return isfinite(a) && isfinite(b) && isfinite(c);
-}
+__device__ __forceinline__ bool finite3(float a, float b, float c) { return isfinite(a) && isfinite(b) && isfinite(c); }
 
 __device__ __forceinline__ int stat_slot(int code) {
   // mem_stats order: n_input, nonfinite, range, height, oob, inlier, outlier, touched
   return code == MEM_CODE_INLIER ? 5 : code == MEM_CODE_OUTLIER ? 6 : code - 1;
 }
 
-// ---------------------------------------------------------------- k_point (a2-a8)
-template <bool kDebug>
-__global__ void __launch_bounds__(kPointThreads) k_point(const __grid_constant__ PointArgs a) {
-  const int m = blockIdx.y;
-  long long beg = 0, end = a.n_single;
-  if (a.offsets) {
-    beg = a.offsets[m];
-    end = a.offsets[m + 1];
-  }
-  const long long base = beg + (long long)blockIdx.x * kPointsPerBlock;
-  if (base >= end) return;  // block-uniform
-
-  __shared__ unsigned s_cnt[6];
-  if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-
-  const MapFrame &f = a.frames ? a.frames[m] : a.f0;
-  const int2 ring = a.ring[m];
-  const Geometry &g = a.geo;
-  const mem_noise &np = a.np;
-  const long long map_base = (long long)m * g.HW;
-  const float *vals = reinterpret_cast<const float *>(a.st.words);
-  const uint8_t *valid = a.st.flags + (long long)kFlagValid * g.BHW;
-  unsigned long long *acc = a.st.acc;
-  const int lane = threadIdx.x & 31;
-
-#pragma unroll
-  for (int u = 0; u < kPointsPerThread; ++u) {
-    const long long i = base + (long long)u * kPointThreads + threadIdx.x;
-    const bool live = i < end;
-    int code = MEM_CODE_NONFINITE;
-    int lcell = -1;
-    long long cell = -1;
-    float z = 0.0f, v = 0.0f;
-    float ch0 = 0.0f;  // stride-4 points: the one channel arrives with the float4
-    const float *p = a.pts + i * (long long)a.stride;
-    if (live) {
-      float px, py, pz;
-      if (a.vec4) {
-        const float4 q = ld_stream_f4(p);
-        px = q.x; py = q.y; pz = q.z; ch0 = q.w;
-      } else {
-        px = __ldg(p); py = __ldg(p + 1); pz = __ldg(p + 2);
-      }
-      if (finite3(px, py, pz)) {                          // a2: finiteness
-        const float r2 = (px * px + py * py) + pz * pz;    // a2: range in the sensor frame (D9)
-        const float r = sqrtf(r2);
-        if (!(np.r_min <= r && r <= np.r_max)) {
-          code = MEM_CODE_RANGE;
-        } else {
-          // a3: q = R p, fixed order, no FMA ("point trsf.")
-          const float qx = (f.R[0] * px + f.R[1] * py) + f.R[2] * pz;
-          const float qy = (f.R[3] * px + f.R[4] * py) + f.R[5] * pz;
-          const float qz = (f.R[6] * px + f.R[7] * py) + f.R[8] * pz;
-          if (!(np.h_min <= qz && qz <= np.h_max)) {       // a4: height filter (D9)
-            code = MEM_CODE_HEIGHT;
-          } else {
-            const float x = qx + f.t[0], y = qy + f.t[1];
-            z = qz + f.t[2];
-            const float fr = x / g.res + g.hH;              // a5: bin (D13)
-            const float fc = y / g.res + g.hW;
-            if (!(0.0f <= fr && fr < (float)g.H && 0.0f <= fc && fc < (float)g.W)) {
-              code = MEM_CODE_OOB;
-            } else {
-              const int row = (int)floorf(fr), col = (int)floorf(fc);
-              lcell = row * g.W + col;
-              cell = map_base + (long long)wrap(row + ring.x, g.H) * g.W + wrap(col + ring.y, g.W);
-              v = np.a + np.b * r2;                         // a6: noise variance (D8)
-              bool outlier = false;                         // a7: Mahalanobis test (D10)
-              if (valid[cell]) {
-                const float d = z - vals[(long long)kWordElev * g.BHW + cell];
-                outlier = d * d > np.tau2 * (vals[(long long)kWordVar * g.BHW + cell] + v);
-              }
-              code = outlier ? MEM_CODE_OUTLIER : MEM_CODE_INLIER;
-            }
-          }
-        }
-      }
-      if (kDebug) {
-        a.dbg_cell[i] = lcell;
-        a.dbg_code[i] = (uint8_t)code;
-      }
-    }
-    // per-code counters: one ballot per code per warp, one smem add per code per warp
-#pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      const unsigned bal = __ballot_sync(0xffffffffu, live && code == c);
-      if (lane == 0 && bal) atomicAdd(&s_cnt[c], (unsigned)__popc(bal));
-    }
-    if (cell < 0) continue;
-
-    // a8: scatter-accumulate (hard part #7: native 64-bit global REDs)
-    if (code == MEM_CODE_OUTLIER) {
-      atomicAdd(&acc[(long long)kAccCnt * g.BHW + cell], 1ull << 32);
-    } else {
-      const float w = 1.0f / v;
-      atomicAdd(&acc[(long long)kAccCnt * g.BHW + cell], 1ull);
-      atomicAdd(reinterpret_cast<double *>(&acc[(long long)kAccP * g.BHW + cell]), (double)w);
-      atomicAdd(reinterpret_cast<double *>(&acc[(long long)kAccS * g.BHW + cell]), (double)(z * w));
-    }
-    for (int bi = 0; bi < a.nb; ++bi) {  // every filtered in-bounds point feeds the groups (D12)
-      const BindDesc &b = a.b[bi];
-      const float *ch = p + 3 + b.ch_offset;
-      unsigned long long *ga = acc + (long long)b.g.acc0 * g.BHW + cell;
-      if (a.vec4) {  // stride 4: the single channel is ch0 (bindings were validated against stride)
-        if (b.g.rule == MEM_COLOR) {
-          const uint32_t bits = __float_as_uint(ch0);
-          const unsigned long long rr = (bits >> 16) & 255u, gg = (bits >> 8) & 255u, bb = bits & 255u;
-          atomicAdd(ga, rr | (gg << 32));
-          atomicAdd(ga + g.BHW, bb | (1ull << 32));
-        } else if (isfinite(ch0)) {  // nch == 1 (class rules need >= 2 channels)
-          atomicAdd(ga, 1ull);
-          atomicAdd(reinterpret_cast<double *>(ga + g.BHW), (double)ch0);
-        }
-        continue;
-      }
-      if (b.g.rule == MEM_COLOR) {  // D20: packed 0x00RRGGBB; exact integer sums packed in u64
-        const uint32_t bits = __float_as_uint(__ldg(ch));
-        const unsigned long long rr = (bits >> 16) & 255u, gg = (bits >> 8) & 255u, bb = bits & 255u;
-        atomicAdd(ga, rr | (gg << 32));
-        atomicAdd(ga + g.BHW, bb | (1ull << 32));
-        continue;
-      }
-      bool fin = true;
-      for (int k = 0; k < b.nch; ++k) fin &= (bool)isfinite(__ldg(ch + k));
-      if (!fin) continue;  // D31
-      if (b.g.rule == MEM_CLASS_MAX) {  // D19
-        int best = 0;
-        float bv = __ldg(ch);
-        for (int k = 1; k < b.nch; ++k) {
-          const float c = __ldg(ch + k);
-          if (c > bv) { bv = c; best = k; }
-        }
-        const unsigned long long key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
-        atomicMax(ga, key);
-        continue;
-      }
-      atomicAdd(ga, 1ull);
-      for (int k = 0; k < b.nch; ++k)
-        atomicAdd(reinterpret_cast<double *>(ga + (long long)(1 + k) * g.BHW), (double)__ldg(ch + k));
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 6 && s_cnt[threadIdx.x]) atomicAdd(&a.stats[stat_slot(threadIdx.x)], (unsigned long long)s_cnt[threadIdx.x]);
+// is logical cell (row, col) in the strips that scrolled in with the pending shift (D14)?
+__device__ __forceinline__ bool in_strip(int row, int col, const MapFrame &f, const Geometry &g) {
+  if (f.sr == 0 && f.sc == 0) return false;
+  const int ar = f.sr < 0 ? -f.sr : f.sr, ac = f.sc < 0 ? -f.sc : f.sc;
+  if (ar >= g.H || ac >= g.W) return true;
+  const bool rs = f.sr > 0 ? row >= g.H - f.sr : row < -f.sr;
+  const bool cs = f.sc > 0 ? col >= g.W - f.sc : col < -f.sc;
+  return rs || cs;
 }
 
-// ---------------------------------------------------------------- k_cell (a9-a10)
-__global__ void __launch_bounds__(256) k_cell(const __grid_constant__ CellArgs a) {
-  const Geometry &g = a.geo;
-  unsigned long long *acc = a.st.acc;
-  float *vals = reinterpret_cast<float *>(a.st.words);
-  uint8_t *valid = a.st.flags + (long long)kFlagValid * g.BHW;
-  unsigned touched = 0;
-  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.BHW;
-       c += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long cnt = __ldcg(&acc[(long long)kAccCnt * g.BHW + c]);
-    if (cnt == 0) continue;  // untouched cells stay bit-identical
-    ++touched;
-    const double n_in = (double)(uint32_t)(cnt & 0xffffffffull);
-    const double n_out = (double)(uint32_t)(cnt >> 32);
-    const double P = __longlong_as_double((long long)__ldcg(&acc[(long long)kAccP * g.BHW + c]));
-    const double S = __longlong_as_double((long long)__ldcg(&acc[(long long)kAccS * g.BHW + c]));
-    float *h = vals + (long long)kWordElev * g.BHW + c;
-    float *s2 = vals + (long long)kWordVar * g.BHW + c;
-    // a9: Kalman height fusion, information form (D7), outliers inflate first (D11)
-    if (valid[c]) {
-      const double sp = (double)*s2 + n_out * (double)a.v_out;
-      if (n_in > 0.0) {
-        const double den = 1.0 / sp + P;
-        const double hn = ((double)*h / sp + S) / den;
-        *h = __double2float_rn(hn);
-        *s2 = __double2float_rn(1.0 / den);
-      } else {
-        *s2 = __double2float_rn(sp);
-      }
-    } else if (n_in > 0.0) {  // first touch
-      *h = __double2float_rn(S / P);
-      *s2 = __double2float_rn(1.0 / P);
-      valid[c] = 1;
-    }
-    acc[(long long)kAccCnt * g.BHW + c] = 0ull;
-    acc[(long long)kAccP * g.BHW + c] = 0ull;
-    acc[(long long)kAccS * g.BHW + c] = 0ull;
-    // a10: each bound group by its rule
-    for (int bi = 0; bi < a.nb; ++bi) {
-      const GroupDesc &gd = a.b[bi].g;
-      unsigned long long *ga = acc + (long long)gd.acc0 * g.BHW + c;
-      if (gd.rule == MEM_CLASS_MAX) {
-        const unsigned long long key = __ldcg(ga);
-        if (key == 0ull) continue;
-        apply_group(a.st, g.BHW, c, gd, 1.0, [](int) { return 0.0; }, key);
-        *ga = 0ull;
-      } else if (gd.rule == MEM_COLOR) {
-        const unsigned long long rg = __ldcg(ga), bn = __ldcg(ga + g.BHW);
-        const uint32_t n = (uint32_t)(bn >> 32);
-        if (n == 0) continue;
-        const double sr = (double)(uint32_t)(rg & 0xffffffffull), sg = (double)(uint32_t)(rg >> 32),
-                     sb = (double)(uint32_t)(bn & 0xffffffffull);
-        apply_group(a.st, g.BHW, c, gd, (double)n,
-                    [&](int k) { return k == 0 ? sr : k == 1 ? sg : sb; }, 0ull);
-        ga[0] = 0ull;
-        ga[g.BHW] = 0ull;
-      } else {
-        const unsigned long long n = __ldcg(ga);
-        if (n == 0ull) continue;
-        apply_group(a.st, g.BHW, c, gd, (double)n,
-                    [&](int k) { return __longlong_as_double((long long)__ldcg(ga + (long long)(1 + k) * g.BHW)); },
-                    0ull);
-        ga[0] = 0ull;
-        for (int k = 0; k < gd.nch; ++k) ga[(long long)(1 + k) * g.BHW] = 0ull;
-      }
+// the state of a never-observed cell (D15)
+__device__ __forceinline__ void reset_cell(const State &st, long long BHW, long long cell, const ResetInfo &r) {
+  float *vals = reinterpret_cast<float *>(st.words);
+  vals[(long long)kWordElev * BHW + cell] = __int_as_float(0x7fc00000);
+  vals[(long long)kWordVar * BHW + cell] = __int_as_float(0x7fc00000);
+  for (int w = 2; w < r.n_word; ++w) st.words[(long long)w * BHW + cell] = 0u;
+  for (int l = 0; l < r.n_label; ++l) reinterpret_cast<int *>(st.words)[(long long)r.label_word[l] * BHW + cell] = -1;
+  for (int fl = 0; fl < r.n_flag; ++fl) st.flags[(long long)fl * BHW + cell] = 0;
+}
+
+// ---------------------------------------------------------------- a2-a8 for one point
+struct PointOut {
+  int code;
+  int lcell;        // logical row*W+col, -1 if dropped
+  int cell;         // global physical cell m*HW + phys, -1 if dropped
+  float z, v;
+  bool test;        // in the window and not in a scrolled-in strip: Mahalanobis test applies
+};
+
+// a2-a6 for one point: no memory access (the state gather of a7 is batched by the caller)
+__device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const MapFrame &f, const Geometry &g,
+                                              const mem_noise &np, float rmin2, float rmax2, int map_base) {
+  PointOut o;
+  o.code = MEM_CODE_NONFINITE;
+  o.lcell = -1;
+  o.cell = -1;
+  o.z = 0.0f;
+  o.v = 0.0f;
+  o.test = false;
+  if (!finite3(px, py, pz)) return o;                   // a2: finiteness
+  const float r2 = (px * px + py * py) + pz * pz;       // a2: sensor-frame range on r^2 (D9)
+  if (!(rmin2 <= r2 && r2 <= rmax2)) {
+    o.code = MEM_CODE_RANGE;
+    return o;
+  }
+  // a3: q = R p, fixed order, no FMA ("point trsf.")
+  const float qx = (f.R[0] * px + f.R[1] * py) + f.R[2] * pz;
+  const float qy = (f.R[3] * px + f.R[4] * py) + f.R[5] * pz;
+  const float qz = (f.R[6] * px + f.R[7] * py) + f.R[8] * pz;
+  if (!(np.h_min <= qz && qz <= np.h_max)) {             // a4: height filter (D9)
+    o.code = MEM_CODE_HEIGHT;
+    return o;
+  }
+  const float x = qx + f.t[0], y = qy + f.t[1];
+  o.z = qz + f.t[2];
+  const float fr = x * g.inv_res + g.hH;                 // a5: bin (D13)
+  const float fc = y * g.inv_res + g.hW;
+  if (!(0.0f <= fr && fr < (float)g.H && 0.0f <= fc && fc < (float)g.W)) {
+    o.code = MEM_CODE_OOB;
+    return o;
+  }
+  const int row = (int)floorf(fr), col = (int)floorf(fc);
+  o.lcell = row * g.W + col;
+  o.cell = map_base + wrap(row + f.r0, g.H) * g.W + wrap(col + f.c0, g.W);
+  o.v = np.a + np.b * r2;                                // a6: noise variance (D8)
+  o.code = MEM_CODE_INLIER;                              // a7 decided after the gather
+  o.test = !in_strip(row, col, f, g);                    // scrolled-in cells are fresh (invalid)
+  return o;
+}
+
+// a7 for a batch of points: issue every state gather first (one round trip), then decide
+template <int N>
+__device__ __forceinline__ void mahalanobis(PointOut (&o)[N], const State &st, const Geometry &g, float tau2) {
+  const float *elev = reinterpret_cast<const float *>(st.words) + (long long)kWordElev * g.BHW;
+  const float *var = reinterpret_cast<const float *>(st.words) + (long long)kWordVar * g.BHW;
+  const uint8_t *valid = st.flags + (long long)kFlagValid * g.BHW;
+  uint8_t vl[N];
+  float hv[N], sv[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    vl[u] = 0;
+    hv[u] = sv[u] = 0.0f;
+    if (o[u].test) {
+      vl[u] = valid[o[u].cell];
+      hv[u] = elev[o[u].cell];
+      sv[u] = var[o[u].cell];
     }
   }
-  // n_cells_touched: warp reduce, one atomic per warp
-  for (int o = 16; o > 0; o >>= 1) touched += __shfl_xor_sync(0xffffffffu, touched, o);
-  if ((threadIdx.x & 31) == 0 && touched) atomicAdd(&a.stats[7], (unsigned long long)touched);
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    if (o[u].test && vl[u]) {  // outlier iff valid and (z - h)^2 > tau^2 (sigma^2 + v) (D10)
+      const float d = o[u].z - hv[u];
+      if (d * d > tau2 * (sv[u] + o[u].v)) o[u].code = MEM_CODE_OUTLIER;
+    }
+  }
+}
+
+// explicit fire-and-forget reductions (RED, never ATOM with a return)
+__device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_f64(unsigned long long *p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- warp aggregation
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Segmented reduction over the lanes of `peers` (the lanes holding the same cell): the lowest
+// lane of each peer group ends with the group's total.  Tree over the rank within the group:
+// ceil(log2(group size)) rounds, every lane participates in every shuffle (after E. Westphal,
+// "warp-aggregated atomics").  `Op` is + or max.
+template <class T, class Op>
+__device__ __forceinline__ T reduce_peers(unsigned peers, T x, Op op) {
+  const int lane = threadIdx.x & 31;
+  unsigned rel = (unsigned)__popc(peers & lanemask_lt());
+  unsigned rest = peers & ~(lanemask_lt() | (1u << lane));  // peers above me
+  while (__any_sync(0xffffffffu, rest != 0u)) {
+    const int next = __ffs(rest);
+    const T t = __shfl_sync(0xffffffffu, x, next > 0 ? next - 1 : lane);
+    if (next) x = op(x, t);
+    rest &= ~__ballot_sync(0xffffffffu, rel & 1u);  // odd ranks are folded into their neighbour
+    rel >>= 1;
+  }
+  return x;
+}
+
+struct OpAdd {
+  template <class T>
+  __device__ T operator()(T a, T b) const { return a + b; }
+};
+struct OpMax {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a > b ? a : b; }
+};
+
+// a8: scatter-accumulate the sufficient statistics of the warp's current points (one per lane,
+// `o.cell < 0` = dropped) into their scratch cells `sc`.  Lanes hitting the same cell are
+// combined first (__match_any_sync + reduce_peers) so that one lane issues the REDs of the
+// group: fewer L2 atomics, no same-address serialisation.  All 32 lanes must call this.
+__device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, const float *p,
+                                                float ch0) {
+  const long long F = a.SHW;
+  unsigned long long *acc = a.st.acc;
+  const bool act = o.cell >= 0;
+  const unsigned act_b = __ballot_sync(0xffffffffu, act);
+  if (act_b == 0u) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned key = act ? (unsigned)sc : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const bool single = __all_sync(0xffffffffu, __popc(peers) == 1 || !act);  // no two lanes share a cell
+  const bool leader = act && (__ffs(peers) - 1 == lane);
+  const bool inl = act && o.code == MEM_CODE_INLIER;
+  const unsigned in_b = __ballot_sync(0xffffffffu, inl);
+  // height statistics (inliers): n_in | n_out << 32, sum 1/v, sum z/v
+  double w = 0.0, zw = 0.0;
+  if (inl) {
+    const float wf = 1.0f / o.v;
+    w = (double)wf;
+    zw = (double)(o.z * wf);
+  }
+  if (!single) {
+    w = reduce_peers(peers, w, OpAdd());
+    zw = reduce_peers(peers, zw, OpAdd());
+  }
+  if (leader) {
+    const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+    red_add_u64(&acc[(long long)kAccCnt * F + sc], (unsigned long long)n_in |
+                                                          ((unsigned long long)(n_all - n_in) << 32));
+    if (n_in) {
+      red_add_f64(&acc[(long long)kAccP * F + sc], w);
+      red_add_f64(&acc[(long long)kAccS * F + sc], zw);
+    }
+  }
+  for (int bi = 0; bi < a.nb; ++bi) {  // every filtered in-bounds point feeds the groups (D12)
+    const BindDesc &b = a.b[bi];
+    unsigned long long *ga = acc + (long long)b.g.acc0 * F + sc;
+    const float *ch = p + 3 + b.ch_offset;
+    if (b.g.rule == MEM_COLOR) {  // D20: packed 0x00RRGGBB; exact integer sums
+      unsigned rg = 0u, bb = 0u;  // r | g << 16 (a warp sums <= 32 * 255 per channel)
+      if (act) {
+        const uint32_t bits = __float_as_uint(a.vec4 ? ch0 : ch[0]);
+        rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
+        bb = bits & 255u;
+      }
+      if (!single) {
+        rg = reduce_peers(peers, rg, OpAdd());
+        bb = reduce_peers(peers, bb, OpAdd());
+      }
+      if (leader) {
+        red_add_u64(ga, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
+        red_add_u64(ga + F, (unsigned long long)bb | ((unsigned long long)__popc(peers) << 32));
+      }
+      continue;
+    }
+    bool fin = act;
+    if (act) {
+      if (a.vec4) {
+        fin = isfinite(ch0);
+      } else {
+        for (int k = 0; k < b.nch; ++k) fin &= (bool)isfinite(ch[k]);
+      }
+    }
+    const unsigned fin_b = __ballot_sync(0xffffffffu, fin);  // D31: non-finite channels skip the group
+    if ((fin_b & act_b) == 0u) continue;
+    if (b.g.rule == MEM_CLASS_MAX) {  // D19: (conf, lowest index) as one u64 max
+      unsigned long long kv = 0ull;
+      if (fin) {
+        int best = 0;
+        float bv = ch[0];
+        for (int k = 1; k < b.nch; ++k) {
+          const float c = ch[k];
+          if (c > bv) {
+            bv = c;
+            best = k;
+          }
+        }
+        kv = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
+      }
+      if (!single) kv = reduce_peers(peers, kv, OpMax());
+      if (leader && kv) red_max_u64(ga, kv);
+      continue;
+    }
+    const unsigned ng = (unsigned)__popc(peers & fin_b);
+    if (leader && ng) red_add_u64(ga, (unsigned long long)ng);
+    for (int k = 0; k < b.nch; ++k) {
+      double v = fin ? (double)(a.vec4 ? ch0 : ch[k]) : 0.0;
+      if (!single) v = reduce_peers(peers, v, OpAdd());
+      if (leader && ng) red_add_f64(ga + (long long)(1 + k) * F, v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a9-a10, batched
+// One lane fuses up to N touched cells (phys[u] >= 0) of map m.  Every phase issues all of its
+// loads for the N cells before any math or store (the compiler cannot hoist loads over stores
+// to possibly aliasing layers), so a lane keeps N independent round trips in flight.
+template <int N>
+__device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, const int (&phys)[N],
+                                           const unsigned long long (&cnt)[N]) {
+  const Geometry &g = a.geo;
+  const long long BHW = g.BHW, F = a.SHW;
+  unsigned long long *acc = a.st.acc;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
+  uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
+  unsigned long long *accP = acc + (long long)kAccP * F, *accS = acc + (long long)kAccS * F;
+  unsigned long long *accN = acc + (long long)kAccCnt * F;
+  int c[N], sc[N];
+  unsigned hit = 0;
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    c[u] = m * g.HW + phys[u];
+    sc[u] = sb + phys[u];
+    hit |= phys[u] >= 0 ? (1u << u) : 0u;
+  }
+  // ---- a9: Kalman height fusion (D7: h' = (h + S sp)/(1 + P sp), s2' = sp/(1 + P sp))
+  {
+    double P[N], S[N];
+    float h[N], s2[N];
+    uint8_t vd[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      if (!(hit >> u & 1u)) continue;
+      P[u] = __longlong_as_double((long long)__ldcg(accP + sc[u]));
+      S[u] = __longlong_as_double((long long)__ldcg(accS + sc[u]));
+      h[u] = elev[c[u]];
+      s2[u] = var[c[u]];
+      vd[u] = validp[c[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      if (!(hit >> u & 1u)) continue;
+      const double n_in = (double)(uint32_t)(cnt[u] & 0xffffffffull);
+      const double n_out = (double)(uint32_t)(cnt[u] >> 32);
+      if (vd[u]) {
+        const double sp = (double)s2[u] + n_out * (double)a.np.v_out;  // outliers inflate first (D11)
+        if (n_in > 0.0) {
+          const double den = 1.0 + P[u] * sp;
+          elev[c[u]] = __double2float_rn(((double)h[u] + S[u] * sp) / den);
+          var[c[u]] = __double2float_rn(sp / den);
+        } else {
+          var[c[u]] = __double2float_rn(sp);
+        }
+      } else if (n_in > 0.0) {  // first touch: h = S/P, s2 = 1/P
+        elev[c[u]] = __double2float_rn(S[u] / P[u]);
+        var[c[u]] = __double2float_rn(1.0 / P[u]);
+        validp[c[u]] = 1;
+      }
+      __stcg(accN + sc[u], 0ull);  // re-zero the scratch for the slot's next map
+      __stcg(accP + sc[u], 0ull);
+      __stcg(accS + sc[u], 0ull);
+    }
+  }
+  // ---- a10: each bound group by its rule, batched over the N cells
+  for (int bi = 0; bi < a.nb; ++bi) {
+    const GroupDesc &gd = a.b[bi].g;
+    unsigned long long *ga = acc + (long long)gd.acc0 * F;
+    if (gd.rule == MEM_CLASS_MAX) {  // D19: the frame's winner overwrites (label, conf)
+      unsigned long long key[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) key[u] = (hit >> u & 1u) ? __ldcg(ga + sc[u]) : 0ull;
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        if (key[u] == 0ull) continue;
+        reinterpret_cast<int *>(a.st.words)[(long long)gd.label * BHW + c[u]] =
+            gd.nch - 1 - (int)(uint32_t)(key[u] & 0xffffffffull);
+        vals[(long long)gd.word0 * BHW + c[u]] = f32_of_ord((uint32_t)(key[u] >> 32));
+        __stcg(ga + sc[u], 0ull);
+      }
+      continue;
+    }
+    uint8_t *obsp = a.st.flags + (long long)gd.flag * BHW;
+    unsigned long long w0[N], w1[N];  // count (or color r|g<<32) and color b|n<<32
+    unsigned obs = 0, any = 0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      w0[u] = w1[u] = 0ull;
+      if (!(hit >> u & 1u)) continue;
+      w0[u] = __ldcg(ga + sc[u]);
+      if (gd.rule == MEM_COLOR) w1[u] = __ldcg(ga + F + sc[u]);
+      obs |= obsp[c[u]] ? (1u << u) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      const unsigned long long nn = gd.rule == MEM_COLOR ? (w1[u] >> 32) : w0[u];
+      any |= nn != 0ull ? (1u << u) : 0u;
+    }
+    for (int k = 0; k < gd.nch; ++k) {
+      double sum[N];
+      float th[N], th2[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) {  // loads for channel k of every cell first
+        if (!(any >> u & 1u)) continue;
+        if (gd.rule == MEM_COLOR) {
+          const uint32_t v = k == 0 ? (uint32_t)(w0[u] & 0xffffffffull) : k == 1 ? (uint32_t)(w0[u] >> 32)
+                                                                          : (uint32_t)(w1[u] & 0xffffffffull);
+          sum[u] = (double)v;  // exact integer colour sums (D20)
+        } else {
+          sum[u] = __longlong_as_double((long long)__ldcg(ga + (long long)(1 + k) * F + sc[u]));
+        }
+        th[u] = vals[(long long)(gd.word0 + k) * BHW + c[u]];
+        if (gd.rule == MEM_GAUSSIAN) th2[u] = vals[(long long)(gd.word0 + gd.nch + k) * BHW + c[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        if (!(any >> u & 1u)) continue;
+        const double n = (double)(gd.rule == MEM_COLOR ? (w1[u] >> 32) : w0[u]);
+        const bool ob = obs >> u & 1u;
+        float *dst = vals + (long long)(gd.word0 + k) * BHW + c[u];
+        switch (gd.rule) {
+          case MEM_AVERAGE:
+          case MEM_CLASS_AVERAGE:
+          case MEM_COLOR: *dst = rule_average(th[u], ob, sum[u], n, gd.w); break;
+          case MEM_GAUSSIAN: {
+            float mu = th[u], vv = th2[u];
+            rule_gaussian(mu, vv, ob, sum[u], n, gd);
+            *dst = mu;
+            vals[(long long)(gd.word0 + gd.nch + k) * BHW + c[u]] = vv;
+            break;
+          }
+          case MEM_CLASS_BAYESIAN: *dst = rule_dirichlet(th[u], ob, sum[u], gd.a0); break;
+          default: break;
+        }
+        if (gd.rule != MEM_COLOR) __stcg(ga + (long long)(1 + k) * F + sc[u], 0ull);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      if (!(any >> u & 1u)) continue;
+      obsp[c[u]] = 1;
+      __stcg(ga + sc[u], 0ull);
+      if (gd.rule == MEM_COLOR) __stcg(ga + F + sc[u], 0ull);
+    }
+  }
+}
+
+// scratch cell base of map m: its map-slot in its wave's half of the pool
+__device__ __forceinline__ long long scratch_base(const PassArgs &a, int m) {
+  const int w = m / a.wave_maps;
+  return (long long)((w & 1) * a.wave_maps + (m - w * a.wave_maps)) * a.geo.HW;
+}
+
+// per-CTA counters: warp reduce, one smem add per warp, one global add per counter
+__device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cnt)[8], unsigned long long *out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const unsigned v = __reduce_add_sync(0xffffffffu, cnt[c]);
+    if (lane == 0 && v) atomicAdd(&s_cnt[c], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && s_cnt[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------- k_points (a2-a8)
+// Persistent grid-stride over the 128-point warp-items of one wave.  Per lane: 4 float4 point
+// loads in flight, then binning, one batched state gather (a7), then warp-aggregated REDs.
+template <bool kDebug>
+__global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ PassArgs a) {
+  __shared__ unsigned s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // by mem_stats slot
+  const Geometry &g = a.geo;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (kThreads / 32);
+  const int gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int i0 = a.pstart ? __ldg(&a.pstart[a.m0]) : 0;
+  const int i1 = a.pstart ? __ldg(&a.pstart[a.m1]) : a.p_single;
+  const unsigned long long pol = evict_first_policy();
+  const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
+  for (int it = i0 + gw; it < i1; it += nwarps) {
+    int m = a.m0;
+    if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
+      int lo = a.m0, hi = a.m1 - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&a.pstart[mid]) <= it) lo = mid; else hi = mid - 1;
+      }
+      m = lo;
+    }
+    long long beg = 0, end = a.n_single;
+    if (a.offsets) {
+      beg = __ldg(&a.offsets[m]);
+      end = __ldg(&a.offsets[m + 1]);
+    }
+    const long long base = beg + (long long)(it - (a.pstart ? __ldg(&a.pstart[m]) : 0)) * kWarpPoints;
+    float px[kWarpPtsPerLane], py[kWarpPtsPerLane], pz[kWarpPtsPerLane], pw[kWarpPtsPerLane];
+#pragma unroll
+    for (int u = 0; u < kWarpPtsPerLane; ++u) {  // all loads first (memory-level parallelism)
+      const long long i = base + u * 32 + lane;
+      px[u] = py[u] = pz[u] = pw[u] = 0.0f;
+      if (i < end) {
+        const float *q = a.pts + i * (long long)a.stride;
+        if (a.vec4) {
+          const float4 v = ld_stream_f4(q, pol);
+          px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
+        } else {
+          px[u] = __ldg(q); py[u] = __ldg(q + 1); pz[u] = __ldg(q + 2);
+        }
+      }
+    }
+    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    const int map_base = m * g.HW;
+    const int sb = (int)scratch_base(a, m);
+    PointOut o[kWarpPtsPerLane];
+#pragma unroll
+    for (int u = 0; u < kWarpPtsPerLane; ++u) {
+      const long long i = base + u * 32 + lane;
+      if (i < end && !(a.ablate & 8u)) {
+        o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
+      } else {
+        o[u].code = i < end ? MEM_CODE_NONFINITE : -1;
+        o[u].cell = -1;
+        o[u].test = false;
+      }
+    }
+    if (!(a.ablate & 4u)) mahalanobis(o, a.st, g, a.np.tau2);
+#pragma unroll
+    for (int u = 0; u < kWarpPtsPerLane; ++u) {
+      const long long i = base + u * 32 + lane;
+      if (i < end) {
+        if (kDebug) {
+          a.dbg_cell[i] = o[u].lcell;
+          a.dbg_code[i] = (uint8_t)o[u].code;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {  // per-code counters: one ballot per code per warp
+        const unsigned bc = __ballot_sync(0xffffffffu, o[u].code == c);
+        if (lane == 0) cnt[stat_slot(c)] += (unsigned)__popc(bc);
+      }
+      if (!(a.ablate & 2u))
+        accumulate_warp(a, o[u], sb + (o[u].cell - map_base), a.pts + (i < end ? i : beg) * (long long)a.stride, pw[u]);
+    }
+  }
+  flush_stats(s_cnt, cnt, a.ctl->stats);
+}
+
+// ---------------------------------------------------------------- k_cells (a9-a10, lazy a13)
+// Persistent grid-stride over 1024-cell tiles of one wave.  Phase 1 reads every cell's count
+// (coalesced), applies the pending strip reset and compacts the touched cells into shared
+// memory; phase 2 fuses the touched cells densely (2 per lane in flight), so no lane idles on
+// untouched cells.
+constexpr int kCellTile = kThreads * 4;
+
+__global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ PassArgs a) {
+  __shared__ int s_phys[kCellTile];
+  __shared__ unsigned long long s_cntv[kCellTile];
+  __shared__ int s_n;
+  __shared__ unsigned s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const Geometry &g = a.geo;
+  const int lane = threadIdx.x & 31;
+  const int tpm = (g.HW + kCellTile - 1) / kCellTile;  // tiles per map
+  const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * tpm;
+  const unsigned long long *accN = a.st.acc + (long long)kAccCnt * a.SHW;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int m = a.m0 + tile / tpm;
+    const int t0 = (tile - (tile / tpm) * tpm) * kCellTile;
+    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    const int sb = (int)scratch_base(a, m);
+    if (threadIdx.x == 0) {
+      s_n = 0;
+      if (t0 == 0) a.ring[m] = make_int2(f.r0, f.c0);
+    }
+    __syncthreads();
+    unsigned long long cv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // counts first (memory-level parallelism)
+      const int phys = t0 + u * kThreads + threadIdx.x;
+      cv[u] = phys < g.HW ? __ldcg(accN + sb + phys) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int phys = t0 + u * kThreads + threadIdx.x;
+      if (phys < g.HW && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
+        const int prow = phys / g.W, pcol = phys - (phys / g.W) * g.W;
+        int row = prow - f.r0, col = pcol - f.c0;
+        row += row < 0 ? g.H : 0;
+        col += col < 0 ? g.W : 0;
+        if (in_strip(row, col, f, g)) reset_cell(a.st, g.BHW, (long long)m * g.HW + phys, a.reset);
+      }
+      const bool t = cv[u] != 0ull;  // untouched cells stay bit-identical
+      const unsigned b = __ballot_sync(0xffffffffu, t);
+      int base = 0;
+      if (lane == 0 && b) base = atomicAdd(&s_n, __popc(b));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (t) {
+        const int k = base + __popc(b & lanemask_lt());
+        s_phys[k] = phys;
+        s_cntv[k] = cv[u];
+      }
+    }
+    __syncthreads();
+    const int n = s_n;
+    cnt[7] += threadIdx.x == 0 ? (unsigned)n : 0u;
+    for (int k0 = 0; k0 < n; k0 += 2 * kThreads) {
+      int ph[2];
+      unsigned long long cc[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u * kThreads + threadIdx.x;
+        ph[u] = k < n ? s_phys[k] : -1;
+        cc[u] = k < n ? s_cntv[k] : 0ull;
+      }
+      fuse_cells<2>(a, m, sb, ph, cc);
+    }
+    __syncthreads();  // s_phys / s_n are rewritten by the next tile
+  }
+  __syncthreads();
+  flush_stats(s_cnt, cnt, a.ctl->stats);
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)
-__global__ void __launch_bounds__(256) k_image(const __grid_constant__ ImageArgs a) {
+__global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ ImageArgs a) {
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -293,7 +645,10 @@ __global__ void __launch_bounds__(256) k_image(const __grid_constant__ ImageArgs
       float bv = __ldg(ch);
       for (int k = 1; k < b.nch; ++k) {
         const float c = __ldg(ch + k * plane);
-        if (c > bv) { bv = c; best = k; }
+        if (c > bv) {
+          bv = c;
+          best = k;
+        }
       }
       key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
     }
@@ -301,19 +656,8 @@ __global__ void __launch_bounds__(256) k_image(const __grid_constant__ ImageArgs
   }
 }
 
-// ---------------------------------------------------------------- reset of a cell
-__device__ __forceinline__ void reset_cell(const State &st, long long BHW, long long cell, int n_word, int n_flag,
-                                           const int *label_word, int n_label) {
-  float *vals = reinterpret_cast<float *>(st.words);
-  vals[(long long)kWordElev * BHW + cell] = __int_as_float(0x7fc00000);
-  vals[(long long)kWordVar * BHW + cell] = __int_as_float(0x7fc00000);
-  for (int w = 2; w < n_word; ++w) st.words[(long long)w * BHW + cell] = 0u;
-  for (int l = 0; l < n_label; ++l) reinterpret_cast<int *>(st.words)[(long long)label_word[l] * BHW + cell] = -1;
-  for (int fl = 0; fl < n_flag; ++fl) st.flags[(long long)fl * BHW + cell] = 0;
-}
-
-// ---------------------------------------------------------------- k_shift (a13)
-__global__ void __launch_bounds__(256) k_shift(const __grid_constant__ ShiftArgs a) {
+// ---------------------------------------------------------------- k_shift (eager a13)
+__global__ void __launch_bounds__(kThreads) k_shift(const __grid_constant__ ShiftArgs a) {
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
   const ShiftRec r = a.recs ? a.recs[m] : a.rec0;
@@ -338,11 +682,11 @@ __global__ void __launch_bounds__(256) k_shift(const __grid_constant__ ShiftArgs
     return;
   }
   const long long cell = (long long)m * g.HW + (long long)wrap(row + r.r0, g.H) * g.W + wrap(col + r.c0, g.W);
-  reset_cell(a.st, g.BHW, cell, a.n_word, a.n_flag, a.label_word, a.n_label);
+  reset_cell(a.st, g.BHW, cell, a.reset);
 }
 
 // ---------------------------------------------------------------- k_read / k_write (a14)
-__global__ void __launch_bounds__(256) k_read(const __grid_constant__ ReadArgs a) {
+__global__ void __launch_bounds__(kThreads) k_read(const __grid_constant__ ReadArgs a) {
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -361,7 +705,7 @@ __global__ void __launch_bounds__(256) k_read(const __grid_constant__ ReadArgs a
     case RK_WORD: out = vals[(long long)a.idx * g.BHW + cell]; break;
     case RK_LABEL: out = (float)reinterpret_cast<const int *>(a.st.words)[(long long)a.idx * g.BHW + cell]; break;
     case RK_FLAG: out = (float)a.st.flags[(long long)a.idx * g.BHW + cell]; break;
-    case RK_THETA: {  // Eq.(11) posterior mean, derived at readout (D5); idx = alpha layer of class k
+    case RK_THETA: {  // Eq.(11) posterior mean, derived at readout (D5)
       if (!a.st.flags[(long long)a.flag * g.BHW + cell]) break;  // unobserved -> 0 (D15)
       double tot = 0.0;
       for (int k = 0; k < a.K; ++k) tot += (double)vals[(long long)(a.first + k) * g.BHW + cell];
@@ -372,7 +716,7 @@ __global__ void __launch_bounds__(256) k_read(const __grid_constant__ ReadArgs a
   a.out[(long long)m * g.HW + t] = out;
 }
 
-__global__ void __launch_bounds__(256) k_write(const __grid_constant__ ReadArgs a) {
+__global__ void __launch_bounds__(kThreads) k_write(const __grid_constant__ ReadArgs a) {
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -394,41 +738,52 @@ __global__ void __launch_bounds__(256) k_write(const __grid_constant__ ReadArgs 
 // ---------------------------------------------------------------- launchers
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-cudaError_t launch_point(const PointArgs &a, cudaStream_t s) {
-  const unsigned bx = cdiv(a.max_n > 0 ? a.max_n : 1, kPointsPerBlock);
-  const dim3 grid(bx, a.geo.n_maps);
-  if (a.dbg_cell)
-    k_point<true><<<grid, kPointThreads, 0, s>>>(a);
+int points_blocks_per_sm(bool debug) {
+  int n = 0;
+  if (debug)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true>, kThreads, 0);
   else
-    k_point<false><<<grid, kPointThreads, 0, s>>>(a);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false>, kThreads, 0);
+  return n > 0 ? n : 1;
+}
+
+int cells_blocks_per_sm() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_cells, kThreads, 0);
+  return n > 0 ? n : 1;
+}
+
+cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
+  if (a.dbg_cell)
+    k_points<true><<<grid, kThreads, 0, s>>>(a);
+  else
+    k_points<false><<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cell(const CellArgs &a, cudaStream_t s) {
-  const long long blocks = (a.geo.BHW + 255) / 256;
-  const unsigned grid = (unsigned)(blocks < 148LL * 16 ? blocks : 148LL * 16);
-  k_cell<<<grid, 256, 0, s>>>(a);
+cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
+  k_cells<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
-  k_image<<<dim3(cdiv(a.geo.HW, 256), a.geo.n_maps), 256, 0, s>>>(a);
+  k_image<<<dim3(cdiv(a.geo.HW, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
   const int cnt = a.max_count > 0 ? a.max_count : 1;
-  k_shift<<<dim3(cdiv(cnt, 256), a.geo.n_maps), 256, 0, s>>>(a);
+  k_shift<<<dim3(cdiv(cnt, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s) {
-  k_read<<<dim3(cdiv(a.geo.HW, 256), a.geo.n_maps), 256, 0, s>>>(a);
+  k_read<<<dim3(cdiv(a.geo.HW, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s) {
-  k_write<<<dim3(cdiv(a.geo.HW, 256), a.geo.n_maps), 256, 0, s>>>(a);
+  k_write<<<dim3(cdiv(a.geo.HW, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -4,39 +4,58 @@
 
 namespace memk {
 
-struct PointArgs {
+constexpr int kThreads = 256;           // 8 warps per CTA
+constexpr int kWarpPtsPerLane = 4;      // point warp-item = 128 points (4 float4 loads in flight per lane)
+constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
+constexpr int kWarpCellsPerLane = 4;    // cell warp-item = 128 physical cells
+constexpr int kWarpCells = 32 * kWarpCellsPerLane;
+
+// Control block of one point input (zeroed by one cudaMemsetAsync per call).
+struct Control {
+  unsigned long long stats[8];  // mem_stats order (n_input is derived on the host)
+};
+
+// reset description shared by k_cells (lazy strips) and k_shift
+struct ResetInfo {
+  int n_word, n_flag, n_label;
+  int label_word[kMaxGroups];
+};
+
+// Arguments of one wave (maps [m0, m1)) of a point input, shared by k_points and k_cells
+// (DESIGN.md §4.2).  Per-cell scratch of map m lives in map-slot scratch_slot(m) of the pool:
+// waves alternate between the two halves so that k_cells(w) overlaps k_points(w+1).
+struct PassArgs {
   const float *pts;
   int stride;
-  int vec4;                   // 1: stride == 4 and 16-B aligned -> one float4 load per point
-  const long long *offsets;   // device, n_maps+1 (batched) or nullptr (single map: [0, n_single))
+  int vec4;                    // stride == 4 and 16-B aligned: one float4 per point
+  const long long *offsets;    // device [n_maps+1] (batched) or nullptr (single map: [0, n_single))
   long long n_single;
-  long long max_n;            // max points of any map (grid x extent)
-  const MapFrame *frames;     // device, n_maps (batched) or nullptr (single map: f0)
+  const int *pstart;           // device [n_maps+1] prefix sums of point warp-items (batched) or nullptr
+  int p_single;                // point warp-items of the single map
+  int m0, m1;                  // maps of this wave
+  int wave_maps;               // maps per wave
+  int q_per_map;               // cell warp-items per map
+  long long SHW;               // scratch map-slots * HW: stride between scratch fields
+  const MapFrame *frames;      // device [n_maps] (batched) or nullptr (single map: f0)
   MapFrame f0;
-  const int2 *ring;           // device ring offsets per map
+  int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)
   Geometry geo;
-  State st;
+  State st;                    // st.acc: [n_acc][map-slots][HW]
   mem_noise np;
   int nb;
   BindDesc b[kMaxBind];
-  unsigned long long *stats;  // [8]: per-code counters (index = code + 1 as in mem_stats minus n_input)
-  int *dbg_cell;              // optional, per point
+  Control *ctl;
+  ResetInfo reset;
+  int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;
-};
-
-struct CellArgs {
-  Geometry geo;
-  State st;
-  float v_out;
-  int nb;
-  BindDesc b[kMaxBind];
-  unsigned long long *stats;
+  unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE; results are wrong when != 0):
+                               // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math
 };
 
 struct ImageArgs {
   const float *img;
   int C, IH, IW;
-  long long map_stride;       // floats between consecutive maps' images
+  long long map_stride;        // floats between consecutive maps' images
   const MapFrame *frames;
   MapFrame f0;
   const int2 *ring;
@@ -49,13 +68,11 @@ struct ImageArgs {
 struct ShiftArgs {
   Geometry geo;
   State st;
-  const ShiftRec *recs;       // device, n_maps (batched) or nullptr (single map: rec0)
+  const ShiftRec *recs;        // device, n_maps (batched) or nullptr (single map: rec0)
   ShiftRec rec0;
-  int2 *ring;                 // updated in place to the records' (r0, c0)
-  int n_word, n_flag;
-  int n_label;
-  int label_word[kMaxGroups];
-  int max_count;              // max over maps of the number of cells to reset
+  int2 *ring;                  // updated in place to the records' (r0, c0)
+  ResetInfo reset;
+  int max_count;               // max over maps of the number of cells to reset
 };
 
 enum ReadKind { RK_ELEV = 0, RK_VAR = 1, RK_WORD = 2, RK_LABEL = 3, RK_FLAG = 4, RK_THETA = 5 };
@@ -64,21 +81,19 @@ struct ReadArgs {
   Geometry geo;
   State st;
   const int2 *ring;
-  int kind, idx;              // layer kind and index (word or flag layer)
-  int first, K, flag;         // theta: first alpha word layer, class count, observed flag layer
-  float *out;                 // read: logical row-major [n_maps][H][W]
-  const float *src;           // write
+  int kind, idx;               // layer kind and index (word or flag layer)
+  int first, K, flag;          // theta: first alpha word layer, class count, observed flag layer
+  float *out;                  // read: logical row-major [n_maps][H][W]
+  const float *src;            // write
 };
 
-cudaError_t launch_point(const PointArgs &a, cudaStream_t s);
-cudaError_t launch_cell(const CellArgs &a, cudaStream_t s);
+cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s);
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s);
-
-constexpr int kPointThreads = 256;
-constexpr int kPointsPerThread = 2;
-constexpr int kPointsPerBlock = kPointThreads * kPointsPerThread;
+int points_blocks_per_sm(bool debug);
+int cells_blocks_per_sm();
 
 }  // namespace memk

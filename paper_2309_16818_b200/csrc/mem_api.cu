@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,6 +17,9 @@
 using namespace memk;
 
 namespace {
+
+// L2 budget for the per-cell scratch of the maps in flight (2 waves); B200 L2 = 126 MB
+static const size_t kScratchBudget = getenv("MEM_SCRATCH_MB") ? (size_t)atol(getenv("MEM_SCRATCH_MB")) << 20 : 48ull << 20;
 
 thread_local std::string g_err = "no error";
 
@@ -86,12 +91,31 @@ struct mem_map {
   size_t din_cap = 0;
   float *dout = nullptr;
   size_t dout_cap = 0;
-  unsigned long long *dstats = nullptr;
+  Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
+  size_t ctl_bytes = 0;
+  int points_grid = 0;      // resident CTAs of k_points (persistent grid)
+  int cells_grid = 0;       // resident CTAs of k_cells
+  cudaStream_t side = nullptr;  // k_cells of wave w overlaps k_points of wave w+1
+  std::vector<cudaEvent_t> ev_pts, ev_cells;
+  int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
+  bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
+  unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see FusedArgs::ablate)
+  std::vector<ShiftRec> pend;
   int *dbg_cell = nullptr;
   uint8_t *dbg_code = nullptr;
   size_t dbg_cap = 0;
   long long dbg_n = 0;
   Prof prof;
+
+  ResetInfo reset_info() const {
+    ResetInfo r;
+    memset(&r, 0, sizeof r);
+    r.n_word = n_word;
+    r.n_flag = n_flag;
+    r.n_label = n_label;
+    for (int i = 0; i < n_label; ++i) r.label_word[i] = label_word[i];
+    return r;
+  }
 
   Geometry geo() const {
     Geometry gg;
@@ -103,6 +127,7 @@ struct mem_map {
     gg.res = res;
     gg.hH = (float)H / 2.0f;
     gg.hW = (float)W / 2.0f;
+    gg.inv_res = (float)(1.0 / (double)res);  // reading D13
     return gg;
   }
 };
@@ -125,29 +150,30 @@ cudaEvent_t prof_event(mem_map *m) {
 
 // runs one launch / copy of `stage`, bracketed by events when profiling is on
 template <class F>
-mem_status timed(mem_map *m, int stage, const char *what, F &&op) {
+mem_status timed(mem_map *m, cudaStream_t st, int stage, const char *what, F &&op) {
   m->prof.count[stage]++;
   cudaEvent_t a = nullptr, b = nullptr;
   if (m->prof.on) {
     a = prof_event(m);
     b = prof_event(m);
     if (!a || !b) return fail(MEM_ECUDA, "cudaEventCreate failed");
-    CU(cudaEventRecord(a, m->stream));
+    CU(cudaEventRecord(a, st));
   }
   const cudaError_t e = op();
   if (e != cudaSuccess) return fail(MEM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   if (m->prof.on) {
-    CU(cudaEventRecord(b, m->stream));
+    CU(cudaEventRecord(b, st));
     m->prof.pending[stage].emplace_back(a, b);
   }
   return MEM_OK;
 }
 
-#define TIMED(stage, expr)                                                   \
+#define TIMED_ON(st, stage, expr)                                            \
   do {                                                                       \
-    mem_status ts_ = timed(m, stage, #expr, [&]() { return (expr); });       \
+    mem_status ts_ = timed(m, st, stage, #expr, [&]() { return (expr); });   \
     if (ts_ != MEM_OK) return ts_;                                           \
   } while (0)
+#define TIMED(stage, expr) TIMED_ON(m->stream, stage, expr)
 
 bool is_device_ptr(const void *p) {
   cudaPointerAttributes at;
@@ -307,12 +333,39 @@ mem_status reset_all(mem_map *m) {
   a.rec0.r0 = 0;
   a.rec0.c0 = 0;
   a.ring = m->ring;
-  a.n_word = m->n_word;
-  a.n_flag = m->n_flag;
-  a.n_label = m->n_label;
-  for (int i = 0; i < m->n_label; ++i) a.label_word[i] = m->label_word[i];
+  a.reset = m->reset_info();
   a.max_count = m->H * m->W;
   CU(launch_shift(a, m->stream));
+  return MEM_OK;
+}
+
+// applies a pending (lazy) shift eagerly with k_shift; every call other than a point input
+// does this first, so kernels that read the map never see an unapplied shift.
+mem_status flush_shift(mem_map *m) {
+  if (!m->pending) return MEM_OK;
+  m->pending = false;
+  ShiftArgs a;
+  memset(&a, 0, sizeof a);
+  a.geo = m->geo();
+  a.st = m->st;
+  a.ring = m->ring;
+  a.reset = m->reset_info();
+  int max_count = 0;
+  for (const ShiftRec &r : m->pend) {
+    const int ar = r.sr < 0 ? -r.sr : r.sr, ac = r.sc < 0 ? -r.sc : r.sc;
+    const int cnt = (ar >= m->H || ac >= m->W) ? m->H * m->W : ar * m->W + ac * m->H;
+    if (cnt > max_count) max_count = cnt;
+  }
+  a.max_count = max_count;
+  if (m->B == 1) {
+    a.rec0 = m->pend[0];
+  } else {
+    void *d = nullptr;
+    mem_status s = stage_params(m, m->pend.data(), sizeof(ShiftRec) * m->B, &d);
+    if (s != MEM_OK) return s;
+    a.recs = reinterpret_cast<const ShiftRec *>(d);
+  }
+  TIMED(MEM_STAGE_SHIFT, launch_shift(a, m->stream));
   return MEM_OK;
 }
 
@@ -320,6 +373,12 @@ void free_map(mem_map *m) {
   if (!m) return;
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
+  if (m->side) {
+    cudaStreamSynchronize(m->side);
+    cudaStreamDestroy(m->side);
+  }
+  for (cudaEvent_t e : m->ev_pts) cudaEventDestroy(e);
+  for (cudaEvent_t e : m->ev_cells) cudaEventDestroy(e);
   cudaFree(m->st.words);
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
@@ -327,7 +386,7 @@ void free_map(mem_map *m) {
   cudaFree(m->dparam);
   cudaFree(m->din);
   cudaFree(m->dout);
-  cudaFree(m->dstats);
+  cudaFree(m->ctl);
   cudaFree(m->dbg_cell);
   cudaFree(m->dbg_code);
   for (int i = 0; i < PinnedRing::kSlots; ++i) {
@@ -357,8 +416,8 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (!out) return fail(MEM_EINVAL, "out is NULL");
   if (n_maps < 1 || n_maps > 65535) return fail(MEM_EINVAL, "n_maps %d out of [1, 65535]", n_maps);
   if (!(resolution > 0.0f) || !std::isfinite(resolution)) return fail(MEM_EINVAL, "resolution must be > 0");
-  if (rows < 1 || cols < 1 || (long long)rows * cols > (1LL << 31) - 1)
-    return fail(MEM_EINVAL, "rows x cols = %d x %d invalid", rows, cols);
+  if (rows < 1 || cols < 1 || (long long)n_maps * rows * cols > (1LL << 31) - 1)
+    return fail(MEM_EINVAL, "n_maps x rows x cols = %d x %d x %d invalid (must be < 2^31 cells)", n_maps, rows, cols);
   if (n_groups < 0 || n_groups > kMaxGroups) return fail(MEM_EINVAL, "n_groups %d out of [0, %d]", n_groups, kMaxGroups);
   if (n_groups > 0 && !groups) return fail(MEM_EINVAL, "groups is NULL");
   int dev_count = 0;
@@ -400,6 +459,20 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
     delete m;
     return fail(MEM_ECUDA, "cudaGetDevice failed");
   }
+  {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+    m->points_grid = points_blocks_per_sm((flags & MEM_FLAG_DEBUG_POINTS) != 0) * (sms > 0 ? sms : 1);
+    m->cells_grid = cells_blocks_per_sm() * (sms > 0 ? sms : 1);
+    cudaGetLastError();
+  }
+  m->pend.assign(n_maps, ShiftRec{0, 0, 0, 0});
+  if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    delete m;
+    return fail(MEM_ECUDA, "cudaStreamCreate failed");
+  }
+  if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -481,14 +554,16 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   };
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
-      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * BHW * m->n_acc) ||
-      !alloc((void **)&m->ring, sizeof(int2) * n_maps) || !alloc((void **)&m->dstats, sizeof(unsigned long long) * 8)) {
+      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * m->n_acc) ||
+      !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
+      !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
     return fail(MEM_ENOMEM, "device allocation of the map state failed");
   }
   mem_status s = MEM_OK;
-  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * BHW * m->n_acc, m->stream) != cudaSuccess ||
-      cudaMemsetAsync(m->dstats, 0, sizeof(unsigned long long) * 8, m->stream) != cudaSuccess) {
+  m->scratch_maps = 1;
+  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * m->n_acc, m->stream) != cudaSuccess ||
+      cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }
   if (s == MEM_OK) s = reset_all(m);
@@ -553,12 +628,11 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     if (!rotation_ok(R + 9 * i)) return fail(MEM_EPOSE, "map %d: R is not a rotation (SPEC.md:128)", i);
   for (int i = 0; i < 3 * B; ++i)
     if (!std::isfinite(t[i])) return fail(MEM_EINVAL, "t must be finite");
-  PointArgs a;
+  PassArgs a;
   memset(&a, 0, sizeof a);
   mem_status s = resolve_bindings(m, bind, nb, false, stride, a.b);
   if (s != MEM_OK) return s;
   if (set_device(m)) return MEM_ECUDA;
-  CU(cudaMemsetAsync(m->dstats, 0, sizeof(unsigned long long) * 8, m->stream));
   if (m->flags & MEM_FLAG_DEBUG_POINTS) {
     if ((size_t)total > m->dbg_cap) {
       CU(cudaStreamSynchronize(m->stream));
@@ -576,49 +650,122 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     }
     m->dbg_n = total;
   }
-  if (total == 0) return MEM_OK;  // legal; the map is unchanged
+  CU(cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream));  // stats + work queue
+  if (total == 0) return flush_shift(m);  // legal; only a pending shift changes the map
   const void *dpts = nullptr;
   s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
   if (s != MEM_OK) return s;
   a.pts = (const float *)dpts;
   a.stride = stride;
-  a.vec4 = (stride == 4 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
   a.n_single = n_single;
-  a.max_n = max_n;
   a.ring = m->ring;
   a.geo = m->geo();
   a.st = m->st;
   a.np = *np;
   a.nb = nb;
-  a.stats = m->dstats;
+  a.ctl = m->ctl;
+  a.reset = m->reset_info();
+  a.ablate = m->ablate;
+  const int HW = m->H * m->W;
+  a.q_per_map = (HW + kWarpCells - 1) / kWarpCells;
   if (m->flags & MEM_FLAG_DEBUG_POINTS) {
     a.dbg_cell = m->dbg_cell;
     a.dbg_code = m->dbg_code;
   }
+  auto frame = [&](int i) {
+    MapFrame f = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
+    // fold the pending shift of the preceding mem_move_to into this launch (lazy a13)
+    f.sr = m->pending ? m->pend[i].sr : 0;
+    f.sc = m->pending ? m->pend[i].sc : 0;
+    f.r0 = m->r0[i];
+    f.c0 = m->c0[i];
+    return f;
+  };
+  // ---- wave schedule: waves of Wm maps, scratch pool = 2 waves
+  a.vec4 = (stride == 4 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
+  std::vector<int> pstart(B + 1);
+  pstart[0] = 0;
+  for (int i = 0; i < B; ++i) {
+    const long long ni = offsets ? offsets[i + 1] - offsets[i] : total;
+    const long long pi = pstart[i] + (ni + kWarpPoints - 1) / kWarpPoints;
+    if (pi > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
+    pstart[i + 1] = (int)pi;
+  }
+  const size_t per_map = sizeof(unsigned long long) * (size_t)HW * m->n_acc;
+  long long wm = (long long)(kScratchBudget / 2 / per_map);
+  if (wm < 1) wm = 1;
+  if (wm > B) wm = B;
+  const int n_waves = (int)((B + wm - 1) / wm);
+  wm = (B + n_waves - 1) / n_waves;  // balanced waves
+  const int slots = (int)(n_waves == 1 ? wm : 2 * wm);  // one wave uses half 0 only
+  if (slots > m->scratch_maps) {  // grow the scratch pool (zeroed)
+    CU(cudaStreamSynchronize(m->stream));
+    CU(cudaStreamSynchronize(m->side));
+    CU(cudaFree(m->st.acc));
+    m->st.acc = nullptr;
+    const size_t bytes = per_map * slots;
+    if (cudaMalloc((void **)&m->st.acc, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      m->scratch_maps = 0;
+      return fail(MEM_ENOMEM, "scratch allocation (%zu bytes) failed", bytes);
+    }
+    CU(cudaMemsetAsync(m->st.acc, 0, bytes, m->stream));
+    m->scratch_maps = slots;
+  }
+  if ((int)m->ev_pts.size() < n_waves) {
+    for (int i = (int)m->ev_pts.size(); i < n_waves; ++i) {
+      cudaEvent_t e1 = nullptr, e2 = nullptr;
+      CU(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      m->ev_pts.push_back(e1);
+      m->ev_cells.push_back(e2);
+    }
+  }
+  a.st = m->st;
+  a.wave_maps = (int)wm;
+  a.SHW = (long long)m->scratch_maps * HW;
   if (B == 1 && !offsets) {
-    a.f0 = make_frame(m, 0, R, t, nullptr);
+    a.f0 = frame(0);
+    a.p_single = pstart[1];
   } else {
-    std::vector<unsigned char> blob(sizeof(MapFrame) * B + sizeof(long long) * (B + 1) + 16);
+    // parameter blob: frames [B] | offsets [B+1] (i64) | pstart [B+1] (i32)
+    const size_t off_at = (sizeof(MapFrame) * B + 15) & ~(size_t)15;  // int64 alignment
+    const size_t ps_at = off_at + sizeof(long long) * (B + 1);
+    std::vector<unsigned char> blob(ps_at + sizeof(int) * (B + 1));
     MapFrame *fr = reinterpret_cast<MapFrame *>(blob.data());
-    for (int i = 0; i < B; ++i) fr[i] = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
-    const size_t off_at = sizeof(MapFrame) * B;
+    for (int i = 0; i < B; ++i) fr[i] = frame(i);
     memcpy(blob.data() + off_at, offsets, sizeof(long long) * (B + 1));
+    memcpy(blob.data() + ps_at, pstart.data(), sizeof(int) * (B + 1));
     void *d = nullptr;
     s = stage_params(m, blob.data(), blob.size(), &d);
     if (s != MEM_OK) return s;
     a.frames = reinterpret_cast<const MapFrame *>(d);
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
+    a.pstart = reinterpret_cast<const int *>((char *)d + ps_at);
   }
-  TIMED(MEM_STAGE_POINT, launch_point(a, m->stream));
-  CellArgs c;
-  memset(&c, 0, sizeof c);
-  c.geo = a.geo;
-  c.st = m->st;
-  c.v_out = np->v_out;
-  c.nb = nb;
-  for (int i = 0; i < nb; ++i) c.b[i] = a.b[i];
-  c.stats = m->dstats;
-  TIMED(MEM_STAGE_CELL, launch_cell(c, m->stream));
+  // k_points(w) on the caller's stream; k_cells(w) on the side stream after it; k_points(w+2)
+  // reuses the scratch half of wave w, so it waits for k_cells(w).  The call ends joined.
+  for (int w = 0; w < n_waves; ++w) {
+    a.m0 = (int)(w * wm);
+    a.m1 = (int)((w + 1) * wm < B ? (w + 1) * wm : B);
+    const long long pitems = pstart[a.m1] - pstart[a.m0];
+    const long long citems = (long long)(a.m1 - a.m0) * a.q_per_map;
+    const int gp = (int)std::max(1LL, std::min<long long>(m->points_grid, (pitems + 7) / 8));
+    const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
+    if (n_waves == 1) {
+      TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
+      TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
+      break;
+    }
+    if (w >= 2) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[w - 2], 0));
+    TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
+    CU(cudaEventRecord(m->ev_pts[w], m->stream));
+    CU(cudaStreamWaitEvent(m->side, m->ev_pts[w], 0));
+    TIMED_ON(m->side, MEM_STAGE_CELL, launch_cells(a, gc, m->side));
+    CU(cudaEventRecord(m->ev_cells[w], m->side));
+  }
+  if (n_waves > 1) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
+  m->pending = false;
   return MEM_OK;
 }
 
@@ -655,6 +802,8 @@ static mem_status input_image(mem_map *m, const float *img, int C, int IH, int I
   mem_status s = resolve_bindings(m, bind, nb, true, C, a.b);
   if (s != MEM_OK) return s;
   if (set_device(m)) return MEM_ECUDA;
+  s = flush_shift(m);
+  if (s != MEM_OK) return s;
   const long long per = (long long)C * IH * IW;
   const void *dimg = nullptr;
   s = stage_input(m, img, sizeof(float) * (size_t)per * B, &dimg);
@@ -699,8 +848,10 @@ static mem_status move_to(mem_map *m, const double *xy) {
   for (int i = 0; i < 2 * B; ++i)
     if (!std::isfinite(xy[i])) return fail(MEM_EINVAL, "position must be finite");
   if (set_device(m)) return MEM_ECUDA;
-  std::vector<ShiftRec> recs(B);
-  int max_count = 0;
+  // two shifts cannot be composed into one strip reset (data scrolled out is gone), so an
+  // earlier pending shift is applied first
+  mem_status st = flush_shift(m);
+  if (st != MEM_OK) return st;
   bool any = false;
   for (int i = 0; i < B; ++i) {
     // D14: k = floor(x/res + 1/2) in fp64
@@ -710,7 +861,7 @@ static mem_status move_to(mem_map *m, const double *xy) {
     m->kx[i] = kx;
     m->ky[i] = ky;
     const bool all = sr >= m->H || -sr >= m->H || sc >= m->W || -sc >= m->W;
-    if (all) {
+    if (all) {  // |s| >= size: every cell scrolls in
       sr = m->H;
       sc = 0;
       m->r0[i] = 0;
@@ -719,34 +870,12 @@ static mem_status move_to(mem_map *m, const double *xy) {
       m->r0[i] = (int)(((m->r0[i] + sr) % m->H + m->H) % m->H);
       m->c0[i] = (int)(((m->c0[i] + sc) % m->W + m->W) % m->W);
     }
-    recs[i].sr = (int)sr;
-    recs[i].sc = (int)sc;
-    recs[i].r0 = m->r0[i];
-    recs[i].c0 = m->c0[i];
-    const int cnt = all ? m->H * m->W : (int)((sr < 0 ? -sr : sr) * m->W + (sc < 0 ? -sc : sc) * m->H);
-    if (cnt > max_count) max_count = cnt;
+    m->pend[i] = ShiftRec{(int)sr, (int)sc, m->r0[i], m->c0[i]};
     any |= (sr != 0 || sc != 0);
   }
-  if (!any) return MEM_OK;  // s = 0 everywhere: bit-identical
-  ShiftArgs a;
-  memset(&a, 0, sizeof a);
-  a.geo = m->geo();
-  a.st = m->st;
-  a.ring = m->ring;
-  a.n_word = m->n_word;
-  a.n_flag = m->n_flag;
-  a.n_label = m->n_label;
-  for (int i = 0; i < m->n_label; ++i) a.label_word[i] = m->label_word[i];
-  a.max_count = max_count;
-  if (B == 1) {
-    a.rec0 = recs[0];
-  } else {
-    void *d = nullptr;
-    mem_status s = stage_params(m, recs.data(), sizeof(ShiftRec) * B, &d);
-    if (s != MEM_OK) return s;
-    a.recs = reinterpret_cast<const ShiftRec *>(d);
-  }
-  TIMED(MEM_STAGE_SHIFT, launch_shift(a, m->stream));
+  // s = 0 everywhere: bit-identical, nothing to do.  Otherwise the strip reset is applied
+  // lazily by the next point input's k_fused (or eagerly by flush_shift before any other call).
+  m->pending = any;
   return MEM_OK;
 }
 
@@ -795,6 +924,10 @@ mem_status mem_get_layer(const mem_map *cm, const char *name, float *out) {
   const Layer *l = find_layer(m, name);
   if (!l) return fail(MEM_ENOTFOUND, "no layer named '%s'", name ? name : "(null)");
   if (set_device(m)) return MEM_ECUDA;
+  {
+    mem_status fs = flush_shift(m);
+    if (fs != MEM_OK) return fs;
+  }
   ReadArgs a = read_args(m, *l);
   const size_t bytes = sizeof(float) * (size_t)m->B * m->H * m->W;
   const bool dev = is_device_ptr(out);
@@ -820,6 +953,10 @@ mem_status mem_set_layer(mem_map *m, const char *name, const float *src) {
   if (!l) return fail(MEM_ENOTFOUND, "no layer named '%s'", name ? name : "(null)");
   if (l->kind == LK_THETA) return fail(MEM_EINVAL, "layer '%s' is derived (alpha / sum alpha)", name);
   if (set_device(m)) return MEM_ECUDA;
+  {
+    mem_status fs = flush_shift(m);
+    if (fs != MEM_OK) return fs;
+  }
   ReadArgs a = read_args(m, *l);
   const void *d = nullptr;
   mem_status s = stage_input(m, src, sizeof(float) * (size_t)m->B * m->H * m->W, &d);
@@ -867,7 +1004,7 @@ mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   if (!m || !out) return fail(MEM_EINVAL, "NULL argument");
   if (set_device(m)) return MEM_ECUDA;
   unsigned long long h[8];
-  CU(cudaMemcpyAsync(h, m->dstats, sizeof h, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaMemcpyAsync(h, m->ctl->stats, sizeof h, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   h[0] = h[1] + h[2] + h[3] + h[4] + h[5] + h[6];
   out->n_input = h[0];

@@ -54,7 +54,7 @@ def test_sm100a_cubin_only():
                                os.path.join(build.CSRC, "kernels.cu"), "-o", ptx])
         txt = open(ptx).read()
     assert not re.search(r"\b(fma|mad)\.(rn\.)?f(32|64)", txt), "floating-point fma in PTX"
-    assert "div.rn.f32" in txt and "sqrt.rn.f32" in txt
+    assert "div.rn.f32" in txt and "div.rn.f64" in txt  # IEEE divisions, never approximate
 
 
 def test_product_and_oracle_share_nothing():
