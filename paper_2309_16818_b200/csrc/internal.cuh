@@ -5,8 +5,9 @@
 //   words [n_word_layers][n_maps][rows*cols]  fp32 layers (elevation, variance, group values)
 //                                               and int32 class_max labels
 //   flags [n_flag_layers][n_maps][rows*cols]  u8 (valid, per-group observed)
-//   acc   [n_acc_fields][n_maps][rows*cols]   u64/f64 per-frame sufficient statistics (zero
-//                                               between frames; K_cell re-zeroes what it reads)
+//   acc   scratch pool of per-frame sufficient statistics for the maps in flight: counts
+//         [slots][rows*cols] then records [slots][rows*cols][R] (zero between frames;
+//         k_cells re-zeroes what it reads)
 // Logical cell (i, j) of map m lives at physical ((i + r0[m]) % rows, (j + c0[m]) % cols).
 //
 // Numerics (reading D29): the library is compiled with -fmad=false (no FFMA/DFMA
@@ -28,10 +29,11 @@ constexpr int kMaxCh = 256;
 constexpr int kWordElev = 0;
 constexpr int kWordVar = 1;
 constexpr int kFlagValid = 0;
-// acc fields 0..2 are the height statistics
-constexpr int kAccCnt = 0;  // u64: n_in (low 32) | n_out (high 32)
-constexpr int kAccP = 1;    // f64: sum 1/v over inliers
-constexpr int kAccS = 2;    // f64: sum z/v over inliers
+// per-cell scratch: a count array (SoA, u64 n_in | n_out << 32, scanned
+// densely) and one AoS record of R u64 words per cell, so a touched cell's sums share one
+// or two 32-B sectors.  Record words 0, 1 are the height statistics:
+constexpr int kRecP = 0;    // f64: sum 1/v over inliers
+constexpr int kRecS = 1;    // f64: sum z/v over inliers
 
 struct GroupDesc {
   int rule, nch;
@@ -39,7 +41,7 @@ struct GroupDesc {
   int word0;  // first word layer (theta / mu then var / alpha / conf)
   int label;  // word layer of class_max labels, -1 otherwise
   int flag;   // observed flag layer, -1 for class_max
-  int acc0;   // first acc field (average etc.: n then nch sums; color: rg, bn; class_max: key)
+  int acc0;   // first record word (average etc.: n then nch sums; color: r|g<<32, b|n<<32; class_max: key)
 };
 
 struct BindDesc {  // one binding of a call, resolved against its group

@@ -190,15 +190,19 @@ struct OpMax {
 // group: fewer L2 atomics, no same-address serialisation.  All 32 lanes must call this.
 __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, const float *p,
                                                 float ch0) {
-  const long long F = a.SHW;
-  unsigned long long *acc = a.st.acc;
+  unsigned long long *rec = a.rec + (long long)sc * a.R;
   const bool act = o.cell >= 0;
   const unsigned act_b = __ballot_sync(0xffffffffu, act);
   if (act_b == 0u) return;
   const int lane = threadIdx.x & 31;
   const unsigned key = act ? (unsigned)sc : 0xffffffffu;
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  const bool single = __all_sync(0xffffffffu, __popc(peers) == 1 || !act);  // no two lanes share a cell
+  // aggregate only when it pays: >= 16 lanes repeat their neighbour's cell (dense clouds; a
+  // LiDAR scan line has ~1.5 points per cell and is faster with one RED set per lane)
+  const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const unsigned dup = __ballot_sync(0xffffffffu, act && lane > 0 && prev == key);
+  const bool agg = __popc(dup) >= 16 && !(a.ablate & 64u);
+  const unsigned peers = agg ? __match_any_sync(0xffffffffu, key) : (1u << lane);
+  const bool single = !agg;
   const bool leader = act && (__ffs(peers) - 1 == lane);
   const bool inl = act && o.code == MEM_CODE_INLIER;
   const unsigned in_b = __ballot_sync(0xffffffffu, inl);
@@ -215,16 +219,15 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
   }
   if (leader) {
     const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
-    red_add_u64(&acc[(long long)kAccCnt * F + sc], (unsigned long long)n_in |
-                                                          ((unsigned long long)(n_all - n_in) << 32));
+    red_add_u64(&a.cnt[sc], (unsigned long long)n_in | ((unsigned long long)(n_all - n_in) << 32));
     if (n_in) {
-      red_add_f64(&acc[(long long)kAccP * F + sc], w);
-      red_add_f64(&acc[(long long)kAccS * F + sc], zw);
+      red_add_f64(rec + kRecP, w);
+      red_add_f64(rec + kRecS, zw);
     }
   }
   for (int bi = 0; bi < a.nb; ++bi) {  // every filtered in-bounds point feeds the groups (D12)
     const BindDesc &b = a.b[bi];
-    unsigned long long *ga = acc + (long long)b.g.acc0 * F + sc;
+    unsigned long long *ga = rec + b.g.acc0;
     const float *ch = p + 3 + b.ch_offset;
     if (b.g.rule == MEM_COLOR) {  // D20: packed 0x00RRGGBB; exact integer sums
       unsigned rg = 0u, bb = 0u;  // r | g << 16 (a warp sums <= 32 * 255 per channel)
@@ -239,7 +242,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       }
       if (leader) {
         red_add_u64(ga, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
-        red_add_u64(ga + F, (unsigned long long)bb | ((unsigned long long)__popc(peers) << 32));
+        red_add_u64(ga + 1, (unsigned long long)bb | ((unsigned long long)__popc(peers) << 32));
       }
       continue;
     }
@@ -276,7 +279,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     for (int k = 0; k < b.nch; ++k) {
       double v = fin ? (double)(a.vec4 ? ch0 : ch[k]) : 0.0;
       if (!single) v = reduce_peers(peers, v, OpAdd());
-      if (leader && ng) red_add_f64(ga + (long long)(1 + k) * F, v);
+      if (leader && ng) red_add_f64(ga + 1 + k, v);
     }
   }
 }
@@ -289,13 +292,10 @@ template <int N>
 __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, const int (&phys)[N],
                                            const unsigned long long (&cnt)[N]) {
   const Geometry &g = a.geo;
-  const long long BHW = g.BHW, F = a.SHW;
-  unsigned long long *acc = a.st.acc;
+  const long long BHW = g.BHW;
   float *vals = reinterpret_cast<float *>(a.st.words);
   float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
   uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
-  unsigned long long *accP = acc + (long long)kAccP * F, *accS = acc + (long long)kAccS * F;
-  unsigned long long *accN = acc + (long long)kAccCnt * F;
   int c[N], sc[N];
   unsigned hit = 0;
 #pragma unroll
@@ -312,8 +312,9 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
 #pragma unroll
     for (int u = 0; u < N; ++u) {
       if (!(hit >> u & 1u)) continue;
-      P[u] = __longlong_as_double((long long)__ldcg(accP + sc[u]));
-      S[u] = __longlong_as_double((long long)__ldcg(accS + sc[u]));
+      const unsigned long long *r = a.rec + (long long)sc[u] * a.R;
+      P[u] = __longlong_as_double((long long)__ldcg(r + kRecP));
+      S[u] = __longlong_as_double((long long)__ldcg(r + kRecS));
       h[u] = elev[c[u]];
       s2[u] = var[c[u]];
       vd[u] = validp[c[u]];
@@ -337,26 +338,29 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
         var[c[u]] = __double2float_rn(1.0 / P[u]);
         validp[c[u]] = 1;
       }
-      __stcg(accN + sc[u], 0ull);  // re-zero the scratch for the slot's next map
-      __stcg(accP + sc[u], 0ull);
-      __stcg(accS + sc[u], 0ull);
+      unsigned long long *r = a.rec + (long long)sc[u] * a.R;  // re-zero for the slot's next map
+      __stcg(a.cnt + sc[u], 0ull);
+      __stcg(r + kRecP, 0ull);
+      __stcg(r + kRecS, 0ull);
     }
   }
   // ---- a10: each bound group by its rule, batched over the N cells
   for (int bi = 0; bi < a.nb; ++bi) {
     const GroupDesc &gd = a.b[bi].g;
-    unsigned long long *ga = acc + (long long)gd.acc0 * F;
+    unsigned long long *ga[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) ga[u] = a.rec + (long long)sc[u] * a.R + gd.acc0;
     if (gd.rule == MEM_CLASS_MAX) {  // D19: the frame's winner overwrites (label, conf)
       unsigned long long key[N];
 #pragma unroll
-      for (int u = 0; u < N; ++u) key[u] = (hit >> u & 1u) ? __ldcg(ga + sc[u]) : 0ull;
+      for (int u = 0; u < N; ++u) key[u] = (hit >> u & 1u) ? __ldcg(ga[u]) : 0ull;
 #pragma unroll
       for (int u = 0; u < N; ++u) {
         if (key[u] == 0ull) continue;
         reinterpret_cast<int *>(a.st.words)[(long long)gd.label * BHW + c[u]] =
             gd.nch - 1 - (int)(uint32_t)(key[u] & 0xffffffffull);
         vals[(long long)gd.word0 * BHW + c[u]] = f32_of_ord((uint32_t)(key[u] >> 32));
-        __stcg(ga + sc[u], 0ull);
+        __stcg(ga[u], 0ull);
       }
       continue;
     }
@@ -367,8 +371,8 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
     for (int u = 0; u < N; ++u) {
       w0[u] = w1[u] = 0ull;
       if (!(hit >> u & 1u)) continue;
-      w0[u] = __ldcg(ga + sc[u]);
-      if (gd.rule == MEM_COLOR) w1[u] = __ldcg(ga + F + sc[u]);
+      w0[u] = __ldcg(ga[u]);
+      if (gd.rule == MEM_COLOR) w1[u] = __ldcg(ga[u] + 1);
       obs |= obsp[c[u]] ? (1u << u) : 0u;
     }
 #pragma unroll
@@ -387,7 +391,7 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
                                                                           : (uint32_t)(w1[u] & 0xffffffffull);
           sum[u] = (double)v;  // exact integer colour sums (D20)
         } else {
-          sum[u] = __longlong_as_double((long long)__ldcg(ga + (long long)(1 + k) * F + sc[u]));
+          sum[u] = __longlong_as_double((long long)__ldcg(ga[u] + 1 + k));
         }
         th[u] = vals[(long long)(gd.word0 + k) * BHW + c[u]];
         if (gd.rule == MEM_GAUSSIAN) th2[u] = vals[(long long)(gd.word0 + gd.nch + k) * BHW + c[u]];
@@ -412,23 +416,33 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
           case MEM_CLASS_BAYESIAN: *dst = rule_dirichlet(th[u], ob, sum[u], gd.a0); break;
           default: break;
         }
-        if (gd.rule != MEM_COLOR) __stcg(ga + (long long)(1 + k) * F + sc[u], 0ull);
+        if (gd.rule != MEM_COLOR) __stcg(ga[u] + 1 + k, 0ull);
       }
     }
 #pragma unroll
     for (int u = 0; u < N; ++u) {
       if (!(any >> u & 1u)) continue;
       obsp[c[u]] = 1;
-      __stcg(ga + sc[u], 0ull);
-      if (gd.rule == MEM_COLOR) __stcg(ga + F + sc[u], 0ull);
+      __stcg(ga[u], 0ull);
+      if (gd.rule == MEM_COLOR) __stcg(ga[u] + 1, 0ull);
     }
   }
 }
 
-// scratch cell base of map m: its map-slot in its wave's half of the pool
+// scratch cell base of map m of this wave: its map-slot in the wave's half of the pool
 __device__ __forceinline__ long long scratch_base(const PassArgs &a, int m) {
-  const int w = m / a.wave_maps;
-  return (long long)((w & 1) * a.wave_maps + (m - w * a.wave_maps)) * a.geo.HW;
+  return (long long)(a.slot0 + m - a.m0) * a.geo.HW;
+}
+
+// per-lane code counters packed in one u64: 10 bits per code, flushed before they can wrap
+__device__ __forceinline__ void count_code(unsigned long long &packed, unsigned &n, int code, unsigned (&cnt)[8]) {
+  if (code >= 0) packed += 1ull << (10 * code);
+  if (++n == 1000u) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
+    packed = 0ull;
+    n = 0;
+  }
 }
 
 // per-CTA counters: warp reduce, one smem add per warp, one global add per counter
@@ -460,9 +474,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
   const int i1 = a.pstart ? __ldg(&a.pstart[a.m1]) : a.p_single;
   const unsigned long long pol = evict_first_policy();
   const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
+  unsigned long long packed = 0ull;
+  unsigned npk = 0;
   for (int it = i0 + gw; it < i1; it += nwarps) {
     int m = a.m0;
-    if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
+    if (a.p_uniform > 0) {
+      m = a.m0 + (it - i0) / a.p_uniform;
+    } else if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
       int lo = a.m0, hi = a.m1 - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -515,16 +533,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
           a.dbg_cell[i] = o[u].lcell;
           a.dbg_code[i] = (uint8_t)o[u].code;
         }
-      }
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {  // per-code counters: one ballot per code per warp
-        const unsigned bc = __ballot_sync(0xffffffffu, o[u].code == c);
-        if (lane == 0) cnt[stat_slot(c)] += (unsigned)__popc(bc);
+        count_code(packed, npk, o[u].code, cnt);
       }
       if (!(a.ablate & 2u))
         accumulate_warp(a, o[u], sb + (o[u].cell - map_base), a.pts + (i < end ? i : beg) * (long long)a.stride, pw[u]);
     }
   }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
   flush_stats(s_cnt, cnt, a.ctl->stats);
 }
 
@@ -546,8 +562,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
   const int lane = threadIdx.x & 31;
   const int tpm = (g.HW + kCellTile - 1) / kCellTile;  // tiles per map
   const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * tpm;
-  const unsigned long long *accN = a.st.acc + (long long)kAccCnt * a.SHW;
-  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  const unsigned long long *accN = a.cnt;
+  for (int rt = blockIdx.x; rt < total; rt += gridDim.x) {
+    // newest-first: k_points walked the maps in order, so the last maps' scratch is the most
+    // recently touched (L2-resident); the next k_points starts with the lines zeroed last here
+    const int tile = (a.ablate & 32u) ? rt : total - 1 - rt;
     const int m = a.m0 + tile / tpm;
     const int t0 = (tile - (tile / tpm) * tpm) * kCellTile;
     const MapFrame f = a.frames ? a.frames[m] : a.f0;

@@ -33,9 +33,13 @@ struct PassArgs {
   const int *pstart;           // device [n_maps+1] prefix sums of point warp-items (batched) or nullptr
   int p_single;                // point warp-items of the single map
   int m0, m1;                  // maps of this wave
-  int wave_maps;               // maps per wave
+  int p_uniform;               // > 0: every map of the wave has exactly this many point warp-items
+  int slot0;                   // scratch map-slot of map m0 (map m -> slot slot0 + m - m0)
   int q_per_map;               // cell warp-items per map
-  long long SHW;               // scratch map-slots * HW: stride between scratch fields
+  long long SHW;               // scratch map-slots * HW
+  unsigned long long *cnt;     // scratch counts [SHW]
+  unsigned long long *rec;     // scratch records [SHW][R]
+  int R;                       // record words per cell
   const MapFrame *frames;      // device [n_maps] (batched) or nullptr (single map: f0)
   MapFrame f0;
   int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)
@@ -49,7 +53,8 @@ struct PassArgs {
   int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;
   unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE; results are wrong when != 0):
-                               // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math
+                               // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math,
+                               // 32 forward (not newest-first) cell tile order, 64 no warp aggregation
 };
 
 struct ImageArgs {

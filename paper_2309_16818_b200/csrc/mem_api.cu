@@ -99,7 +99,8 @@ struct mem_map {
   std::vector<cudaEvent_t> ev_pts, ev_cells;
   int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
-  unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see FusedArgs::ablate)
+  unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see PassArgs::ablate)
+  int l2_persist_mb = 0;    // DIAGNOSTICS: env MEM_L2_PERSIST_MB at create
   std::vector<ShiftRec> pend;
   int *dbg_cell = nullptr;
   uint8_t *dbg_code = nullptr;
@@ -467,12 +468,15 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
     cudaGetLastError();
   }
   m->pend.assign(n_maps, ShiftRec{0, 0, 0, 0});
-  if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) {
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     cudaGetLastError();
     delete m;
     return fail(MEM_ECUDA, "cudaStreamCreate failed");
   }
   if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
+  if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -480,7 +484,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   // layer registry (names: include/mem.h)
   m->n_word = 2;
   m->n_flag = 1;
-  m->n_acc = 3;
+  m->n_acc = 2;  // record words: P, S, then the groups' fields
   add_layer(m, "elevation", LK_ELEV, kWordElev);
   add_layer(m, "variance", LK_VAR, kWordVar);
   add_layer(m, "valid", LK_VALID, kFlagValid);
@@ -554,7 +558,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   };
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
-      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * m->n_acc) ||
+      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc)) ||
       !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
       !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
@@ -562,7 +566,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   }
   mem_status s = MEM_OK;
   m->scratch_maps = 1;
-  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * m->n_acc, m->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc), m->stream) != cudaSuccess ||
       cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -691,7 +695,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     if (pi > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
     pstart[i + 1] = (int)pi;
   }
-  const size_t per_map = sizeof(unsigned long long) * (size_t)HW * m->n_acc;
+  const size_t per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
   long long wm = (long long)(kScratchBudget / 2 / per_map);
   if (wm < 1) wm = 1;
   if (wm > B) wm = B;
@@ -722,8 +726,25 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     }
   }
   a.st = m->st;
-  a.wave_maps = (int)wm;
   a.SHW = (long long)m->scratch_maps * HW;
+  a.cnt = m->st.acc;
+  a.rec = m->st.acc + a.SHW;
+  a.R = m->n_acc;
+  if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool in an L2 persisting window
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof v);
+    const size_t win = per_map * m->scratch_maps;
+    const size_t setaside = (size_t)m->l2_persist_mb << 20;
+    v.accessPolicyWindow.base_ptr = m->st.acc;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = win <= setaside ? 1.0f : (float)setaside / (float)win;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+    cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaStreamSetAttribute(m->side, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+  }
   if (B == 1 && !offsets) {
     a.f0 = frame(0);
     a.p_single = pstart[1];
@@ -748,6 +769,10 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   for (int w = 0; w < n_waves; ++w) {
     a.m0 = (int)(w * wm);
     a.m1 = (int)((w + 1) * wm < B ? (w + 1) * wm : B);
+    a.slot0 = (w & 1) * (int)wm;
+    a.p_uniform = pstart[a.m0 + 1] - pstart[a.m0];  // > 0 only if every map of the wave has it
+    for (int i = a.m0; i < a.m1 && a.p_uniform > 0; ++i)
+      if (pstart[i + 1] - pstart[i] != a.p_uniform) a.p_uniform = 0;
     const long long pitems = pstart[a.m1] - pstart[a.m0];
     const long long citems = (long long)(a.m1 - a.m0) * a.q_per_map;
     const int gp = (int)std::max(1LL, std::min<long long>(m->points_grid, (pitems + 7) / 8));

@@ -42,20 +42,50 @@ def sass_lines(lib, kernel):
     return out
 
 
+def kernel_rows(rep, kernel):
+    """rows (kernel line, header, data...) of the first kernel block whose demangled name
+    contains the unmangled kernel name."""
+    csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(csvtxt)))
+    short = re.sub(r"^_ZN\d+\w+?\d+", "", kernel)
+    m = re.match(r"_ZN(\d+)(\w+)", kernel)
+    want = None
+    if m:  # _ZN4memk8k_pointsI... -> "k_points"
+        rest = kernel[len("_ZN"):]
+        names = []
+        while rest and rest[0].isdigit():
+            n = int(re.match(r"\d+", rest).group(0))
+            rest = rest[len(str(n)):]
+            names.append(rest[:n])
+            rest = rest[n:]
+        want = names[-1] if names else None
+    blocks, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = [r]
+            blocks.append(cur)
+        elif cur is not None:
+            cur.append(r)
+    for b in blocks:
+        if want is None or want in b[0][1]:
+            return b
+    return blocks[0]
+
+
 def main():
     rep, lib, kernel = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+    col = sys.argv[5] if len(sys.argv) > 5 else "Warp Stall Sampling (All Samples)"
     lines = sass_lines(lib, kernel)
-    csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(csvtxt)))
+    rows = kernel_rows(rep, kernel)
     hdr = rows[1]
-    si = hdr.index("Warp Stall Sampling (All Samples)")
+    si = hdr.index(col)
     data = rows[2:]
     base = int(data[0][0], 16)
     agg = collections.Counter()
     tot = 0
     for r in data:
-        n = int(r[si] or 0)
+        n = int(float(r[si] or 0))
         tot += n
         agg[lines.get(int(r[0], 16) - base, ("?", 0))] += n
     src = {}
@@ -74,8 +104,7 @@ if __name__ == "__main__":
 def groups(rep, lib, kernel, ranges):
     """sum samples over named (file, first, last) line ranges."""
     lines = sass_lines(lib, kernel)
-    csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(csvtxt)))
+    rows = kernel_rows(rep, kernel)
     hdr = rows[1]
     si = hdr.index("Warp Stall Sampling (All Samples)")
     data = rows[2:]
