@@ -121,7 +121,7 @@ def peaks():
 
 
 def traffic_record():
-    """dram bytes per k_point launch from the committed ncu --set full capture (or None)."""
+    """dram bytes per k_points launch from the committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         return json.load(open(p))
@@ -259,19 +259,22 @@ def run_mem(a):
     total_pts = npts * M_ * a.steps * world
     value = total_pts / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (k_fused: points + cell update), CUDA events live
-    fused_ms, fused_n = prof["point"]
+    # ---- roofline of the dominant kernel (k_points), timed live with CUDA events on its stream
+    pts_ms, pts_n = prof["point"]
+    cell_ms, cell_n = prof["cell"]
     pk, pk_src = peaks()
-    # algorithmic bytes per launch: every point read once (16 B) + read and
-    # write of the stored state of every touched cell (C2 colour map: 22 B per cell)
-    bytes_fused = M_ * npts * 16 + 2 * 22 * stats["n_cells_touched"]
-    achieved = bytes_fused / (fused_ms / fused_n * 1e-3) / 1e9 if fused_n else None
+    # algorithmic bytes per launch: k_points reads every point once (16 B);
+    # k_cells reads and writes the stored state of every touched cell (C2 colour map: 22 B)
+    bytes_pts = M_ * npts * 16
+    bytes_cells = 2 * 22 * stats["n_cells_touched"]
+    achieved = bytes_pts / (pts_ms / pts_n * 1e-3) / 1e9 if pts_n else None
+    achieved_cells = bytes_cells / (cell_ms / cell_n * 1e-3) / 1e9 if cell_n else None
     tr = traffic_record()
     traffic = None
     if tr and tr.get("maps") == M_ and tr.get("points_per_map") == npts:
-        traffic = tr.get("k_fused_dram_bytes_per_launch")
+        traffic = tr.get("k_points_dram_bytes_per_launch")
     launches = sum(prof[k][1] for k in ("shift", "point", "cell", "image", "read", "write"))
-    step_bytes = bytes_fused
+    step_bytes = bytes_pts + bytes_cells
 
     # ---- e2e: through the C-ABI with HOST (pinned) buffers, H2D + D2H inside the timed region
     e2e = None
@@ -336,11 +339,15 @@ def run_mem(a):
                        "l2": "inputs > L2: 134 MB of points per step from a 16-step rotating pool (2.1 GB)"},
             "map_updates_per_s": M_ * a.steps * world / (ms_max * 1e-3),
             "step_hbm_gbs": step_bytes / (ms_max / a.steps * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": pk,
+            "roofline": {"bound": "hbm", "kernel": "k_points", "achieved": achieved, "peak": pk,
                          "peak_source": pk_src, "unit": "GB/s",
                          "frac": (achieved / pk) if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": bytes_fused},
-            "stages_ms_per_step": {("fused" if k == "point" else k): v[0] / a.steps for k, v in prof.items() if v[1]},
+                         "algorithmic_bytes_per_launch": bytes_pts,
+                         "k_cells": {"achieved": achieved_cells, "frac": (achieved_cells / pk) if achieved_cells else None,
+                                     "algorithmic_bytes_per_launch": bytes_cells},
+                         "step": {"achieved": step_bytes / (ms_max / a.steps * 1e-3) / 1e9,
+                                  "frac": step_bytes / (ms_max / a.steps * 1e-3) / 1e9 / pk}},
+            "stages_ms_per_step": {k: v[0] / a.steps for k, v in prof.items() if v[1]},
             "gpu_launches": launches,
             "clocks": clk.summary(t_on, t_off),
             "e2e": e2e,

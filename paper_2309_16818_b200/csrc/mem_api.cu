@@ -19,7 +19,7 @@ using namespace memk;
 namespace {
 
 // L2 budget for the per-cell scratch of the maps in flight (2 waves); B200 L2 = 126 MB
-static const size_t kScratchBudget = getenv("MEM_SCRATCH_MB") ? (size_t)atol(getenv("MEM_SCRATCH_MB")) << 20 : 48ull << 20;
+static const size_t kScratchBudget = getenv("MEM_SCRATCH_MB") ? (size_t)atol(getenv("MEM_SCRATCH_MB")) << 20 : 2048ull << 20;
 
 thread_local std::string g_err = "no error";
 
