@@ -454,7 +454,8 @@ __device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cn
     if (lane == 0 && v) atomicAdd(&s_cnt[c], v);
   }
   __syncthreads();
-  if (threadIdx.x < 8 && s_cnt[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+  if (threadIdx.x < 8 && s_cnt[threadIdx.x])
+    atomicAdd(&out[(blockIdx.x % kStatSlots) * 8 + threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- k_points (a2-a8)
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
   }
 #pragma unroll
   for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
-  flush_stats(s_cnt, cnt, a.ctl->stats);
+  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
 }
 
 // ---------------------------------------------------------------- k_cells (a9-a10, lazy a13)
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
     __syncthreads();  // s_phys / s_n are rewritten by the next tile
   }
   __syncthreads();
-  flush_stats(s_cnt, cnt, a.ctl->stats);
+  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)

@@ -11,8 +11,9 @@ constexpr int kWarpCellsPerLane = 4;    // cell warp-item = 128 physical cells
 constexpr int kWarpCells = 32 * kWarpCellsPerLane;
 
 // Control block of one point input (zeroed by one cudaMemsetAsync per call).
+constexpr int kStatSlots = 64;  // CTAs add their counters to slot blockIdx % 64 (no hot address)
 struct Control {
-  unsigned long long stats[8];  // mem_stats order (n_input is derived on the host)
+  unsigned long long stats[kStatSlots][8];  // mem_stats order (n_input is derived on the host)
 };
 
 // reset description shared by k_cells (lazy strips) and k_shift

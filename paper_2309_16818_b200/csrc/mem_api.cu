@@ -775,7 +775,11 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
       if (pstart[i + 1] - pstart[i] != a.p_uniform) a.p_uniform = 0;
     const long long pitems = pstart[a.m1] - pstart[a.m0];
     const long long citems = (long long)(a.m1 - a.m0) * a.q_per_map;
-    const int gp = (int)std::max(1LL, std::min<long long>(m->points_grid, (pitems + 7) / 8));
+    // one wave: persistent grid; several waves: short-lived CTAs (~2 items per warp) so that
+    // the high-priority k_cells of the previous wave is scheduled as they retire
+    const long long per_cta = n_waves == 1 ? 8 : 16;
+    const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
+    const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
     if (n_waves == 1) {
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
@@ -1028,9 +1032,11 @@ mem_status mem_get_center(const mem_map *m, int64_t *kxy) {
 mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   if (!m || !out) return fail(MEM_EINVAL, "NULL argument");
   if (set_device(m)) return MEM_ECUDA;
-  unsigned long long h[8];
-  CU(cudaMemcpyAsync(h, m->ctl->stats, sizeof h, cudaMemcpyDeviceToHost, m->stream));
+  unsigned long long hs[kStatSlots][8], h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  CU(cudaMemcpyAsync(hs, m->ctl->stats, sizeof hs, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
+  for (int i = 0; i < kStatSlots; ++i)
+    for (int k = 0; k < 8; ++k) h[k] += hs[i][k];
   h[0] = h[1] + h[2] + h[3] + h[4] + h[5] + h[6];
   out->n_input = h[0];
   out->n_nonfinite = h[1];
