@@ -301,3 +301,49 @@ def test_errors_and_info():
     one = M.Map(0.04, 200, 200, [dict(name="f", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)])
     assert one.footprint() - base.footprint() == 160000 + 40000  # + 1-byte observed flag
     assert "elevation" in base.layer_names() and "f_observed" in one.layer_names()
+
+
+def test_uniform_batch_sweep_vs_oracle():
+    """uniform batches (every map the same point count) take the fused sweep kernel; every map
+    must match its own oracle map (codes bit-exact via stats, layers within tolerance)."""
+    rows, cols, res = 40, 36, 0.1
+    B, n = 9, 4000
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5),
+              dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5)]
+    gb = M.Map(res, rows, cols, groups, n_maps=B, debug_points=True)
+    oras = [O.OracleMap(res, rows, cols, groups) for _ in range(B)]
+    rng = np.random.default_rng(53)
+    binds = [(0, 1, 0), (1, 1, 1)]
+    for f in range(6):
+        clouds = []
+        for b in range(B):
+            p = S.random_cloud(7000 * f + b, n, 5, rows, cols, res)
+            p[:, 4] = S.pack_rgb(rng.integers(0, 256, (n, 3)).astype(np.uint8))
+            p[rng.uniform(size=n) < 0.05, 2] += 1.0  # outliers
+            clouds.append(p)
+        off = np.arange(B + 1, dtype=np.int64) * n
+        Rs = np.stack([S.rot_z(0.2 * b - 0.3 * f) for b in range(B)])
+        ts = np.stack([[0.03 * b, 0.02 * f, 1.0] for b in range(B)])
+        xy = np.stack([[0.13 * f * (b % 3 + 1), -0.11 * f] for b in range(B)])
+        gb.move_to_batch(xy)
+        gb.input_pointcloud_batch(torch.from_numpy(np.concatenate(clouds)).cuda(), off, binds, Rs, ts, NOISE_R)
+        cell, code = gb.debug_codes()
+        tot = dict.fromkeys(O.STAT_NAMES, 0)
+        for b in range(B):
+            oras[b].move_to(*xy[b])
+            oc, ok = oras[b].input_pointcloud(clouds[b], binds, Rs[b], ts[b], NOISE_R, debug=True)
+            assert np.array_equal(code[b * n:(b + 1) * n], ok), (f, b)
+            assert np.array_equal(cell[b * n:(b + 1) * n], oc), (f, b)
+            for k, v in oras[b].stats().items():
+                tot[k] += v
+        assert gb.stats() == tot
+    for b in range(B):
+        for nm in gb.layer_names():
+            g = gb.get_layer(nm)[b]
+            o = oras[b].get_layer(nm)
+            assert np.array_equal(np.isnan(g), np.isnan(o)), (b, nm)
+            fin = ~np.isnan(o)
+            if nm.endswith("_observed") or nm == "valid":
+                assert np.array_equal(g, o), (b, nm)
+            else:
+                assert np.all(np.abs(g[fin].astype(np.float64) - o[fin]) <= 1e-6 + 1e-5 * np.abs(o[fin])), (b, nm)
