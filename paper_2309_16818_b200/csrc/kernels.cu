@@ -429,6 +429,90 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
   }
 }
 
+// Fast path of fuse_cells for the common configuration "one average or colour group with
+// nch <= 3 channels bound" (C1, C2, C5a): every load of a cell (scratch record, h, s2, valid,
+// observed, theta_k) is issued in ONE round for both cells before any math or store.
+template <int N, int NCH, bool kColor>
+__device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb, const int (&phys)[N],
+                                               const unsigned long long (&cnt)[N]) {
+  const Geometry &g = a.geo;
+  const long long BHW = g.BHW;
+  const GroupDesc &gd = a.b[0].g;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
+  uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
+  uint8_t *obsp = a.st.flags + (long long)gd.flag * BHW;
+  double P[N], S[N], sum[N][NCH];
+  unsigned long long w0[N], w1[N];
+  float h[N], s2[N], th[N][NCH];
+  uint8_t vd[N], ob[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {  // one round of loads
+    if (phys[u] < 0) continue;
+    const int c = m * g.HW + phys[u];
+    const unsigned long long *r = a.rec + (long long)(sb + phys[u]) * a.R;
+    P[u] = __longlong_as_double((long long)__ldcg(r + kRecP));
+    S[u] = __longlong_as_double((long long)__ldcg(r + kRecS));
+    w0[u] = __ldcg(r + gd.acc0);
+    if (kColor) {
+      w1[u] = __ldcg(r + gd.acc0 + 1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) sum[u][k] = __longlong_as_double((long long)__ldcg(r + gd.acc0 + 1 + k));
+    }
+    h[u] = elev[c];
+    s2[u] = var[c];
+    vd[u] = validp[c];
+    ob[u] = obsp[c];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) th[u][k] = vals[(long long)(gd.word0 + k) * BHW + c];
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    if (phys[u] < 0) continue;
+    const int c = m * g.HW + phys[u];
+    unsigned long long *r = a.rec + (long long)(sb + phys[u]) * a.R;
+    // a9: Kalman height fusion (D7), outliers inflate first (D11)
+    const double n_in = (double)(uint32_t)(cnt[u] & 0xffffffffull);
+    const double n_out = (double)(uint32_t)(cnt[u] >> 32);
+    if (vd[u]) {
+      const double sp = (double)s2[u] + n_out * (double)a.np.v_out;
+      if (n_in > 0.0) {
+        const double den = 1.0 + P[u] * sp;
+        elev[c] = __double2float_rn(((double)h[u] + S[u] * sp) / den);
+        var[c] = __double2float_rn(sp / den);
+      } else {
+        var[c] = __double2float_rn(sp);
+      }
+    } else if (n_in > 0.0) {
+      elev[c] = __double2float_rn(S[u] / P[u]);
+      var[c] = __double2float_rn(1.0 / P[u]);
+      validp[c] = 1;
+    }
+    // a10: Eq.(1)+(2) per channel
+    const unsigned long long nn = kColor ? (w1[u] >> 32) : w0[u];
+    if (nn != 0ull) {
+      const double n = (double)nn;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        double sk;
+        if (kColor) {
+          const uint32_t v = k == 0 ? (uint32_t)(w0[u] & 0xffffffffull)
+                                    : k == 1 ? (uint32_t)(w0[u] >> 32) : (uint32_t)(w1[u] & 0xffffffffull);
+          sk = (double)v;  // exact integer colour sums (D20)
+        } else {
+          sk = sum[u][k];
+        }
+        vals[(long long)(gd.word0 + k) * BHW + c] = rule_average(th[u][k], ob[u] != 0, sk, n, gd.w);
+      }
+      obsp[c] = 1;
+    }
+    // re-zero the scratch for the slot's next map
+    __stcg(a.cnt + sb + phys[u], 0ull);
+    for (int k = 0; k < a.R; ++k) __stcg(r + k, 0ull);
+  }
+}
+
 // scratch cell base of map m of this wave: its map-slot in the wave's half of the pool
 __device__ __forceinline__ long long scratch_base(const PassArgs &a, int m) {
   return (long long)(a.slot0 + m - a.m0) * a.geo.HW;
@@ -552,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
 // untouched cells.
 constexpr int kCellTile = kThreads * 4;
 
+template <int kFast>
 __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ PassArgs a) {
   __shared__ int s_phys[kCellTile];
   __shared__ unsigned long long s_cntv[kCellTile];
@@ -607,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
     __syncthreads();
     const int n = s_n;
     cnt[7] += threadIdx.x == 0 ? (unsigned)n : 0u;
-    for (int k0 = 0; k0 < n; k0 += 2 * kThreads) {
+    for (int k0 = 0; k0 < ((a.ablate & 512u) ? 0 : n); k0 += 2 * kThreads) {
       int ph[2];
       unsigned long long cc[2];
 #pragma unroll
@@ -616,7 +701,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
         ph[u] = k < n ? s_phys[k] : -1;
         cc[u] = k < n ? s_cntv[k] : 0ull;
       }
-      fuse_cells<2>(a, m, sb, ph, cc);
+      if (kFast == 1)
+        fuse_cells_avg<2, 3, true>(a, m, sb, ph, cc);
+      else if (kFast == 2)
+        fuse_cells_avg<2, 1, false>(a, m, sb, ph, cc);
+      else
+        fuse_cells<2>(a, m, sb, ph, cc);
     }
     __syncthreads();  // s_phys / s_n are rewritten by the next tile
   }
@@ -769,7 +859,7 @@ int points_blocks_per_sm(bool debug) {
 
 int cells_blocks_per_sm() {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_cells, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_cells<0>, kThreads, 0);
   return n > 0 ? n : 1;
 }
 
@@ -782,7 +872,12 @@ cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
 }
 
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
-  k_cells<<<grid, kThreads, 0, s>>>(a);
+  if (a.fast == 1)
+    k_cells<1><<<grid, kThreads, 0, s>>>(a);
+  else if (a.fast == 2)
+    k_cells<2><<<grid, kThreads, 0, s>>>(a);
+  else
+    k_cells<0><<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -41,6 +41,7 @@ struct PassArgs {
   unsigned long long *cnt;     // scratch counts [SHW]
   unsigned long long *rec;     // scratch records [SHW][R]
   int R;                       // record words per cell
+  int fast;                    // k_cells fast path: 1 = one colour group, 2 = one 1-channel average group
   const MapFrame *frames;      // device [n_maps] (batched) or nullptr (single map: f0)
   MapFrame f0;
   int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)

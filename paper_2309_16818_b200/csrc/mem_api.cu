@@ -101,6 +101,7 @@ struct mem_map {
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see PassArgs::ablate)
   int l2_persist_mb = 0;    // DIAGNOSTICS: env MEM_L2_PERSIST_MB at create
+  bool single_stream = false;  // DIAGNOSTICS: env MEM_SINGLE_STREAM=1: waves run P0 C0 P1 C1 ... in order
   std::vector<ShiftRec> pend;
   int *dbg_cell = nullptr;
   uint8_t *dbg_code = nullptr;
@@ -477,6 +478,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   }
   if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
   if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
+  if (const char *ss = getenv("MEM_SINGLE_STREAM")) m->single_stream = atoi(ss) != 0;
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -730,6 +732,11 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.cnt = m->st.acc;
   a.rec = m->st.acc + a.SHW;
   a.R = m->n_acc;
+  a.fast = 0;
+  if (nb == 1 && m->ng == 1 && !(m->ablate & 1024u)) {  // every group bound (no stale group state)
+    if (a.b[0].g.rule == MEM_COLOR) a.fast = 1;
+    else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) a.fast = 2;
+  }
   if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool in an L2 persisting window
     cudaStreamAttrValue v;
     memset(&v, 0, sizeof v);
@@ -781,10 +788,11 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
     const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
-    if (n_waves == 1) {
+    if (n_waves == 1 || m->single_stream) {
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
       TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
-      break;
+      if (n_waves == 1) break;
+      continue;
     }
     if (w >= 2) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[w - 2], 0));
     TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
@@ -793,7 +801,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     TIMED_ON(m->side, MEM_STAGE_CELL, launch_cells(a, gc, m->side));
     CU(cudaEventRecord(m->ev_cells[w], m->side));
   }
-  if (n_waves > 1) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
+  if (n_waves > 1 && !m->single_stream) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
   m->pending = false;
   return MEM_OK;
 }
