@@ -188,6 +188,8 @@ struct OpMax {
 // `o.cell < 0` = dropped) into their scratch cells `sc`.  Lanes hitting the same cell are
 // combined first (__match_any_sync + reduce_peers) so that one lane issues the REDs of the
 // group: fewer L2 atomics, no same-address serialisation.  All 32 lanes must call this.
+// kFast (stride-4 points, one group bound): 1 = colour, 2 = 1-channel average; 0 = generic
+template <int kFast>
 __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, const float *p,
                                                 float ch0) {
   unsigned long long *rec = a.rec + (long long)sc * a.R;
@@ -224,6 +226,38 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       red_add_f64(rec + kRecP, w);
       red_add_f64(rec + kRecS, zw);
     }
+  }
+  if (kFast != 0) {  // one group, channel in ch0 (the float4's w)
+    unsigned long long *ga = rec + a.b[0].g.acc0;
+    if (kFast == 1) {  // D20 colour: exact integer sums
+      unsigned rg = 0u, bb = 0u;
+      if (act) {
+        const uint32_t bits = __float_as_uint(ch0);
+        rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
+        bb = bits & 255u;
+      }
+      if (!single) {
+        rg = reduce_peers(peers, rg, OpAdd());
+        bb = reduce_peers(peers, bb, OpAdd());
+      }
+      if (leader) {
+        red_add_u64(ga, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
+        red_add_u64(ga + 1, (unsigned long long)bb | ((unsigned long long)__popc(peers) << 32));
+      }
+    } else {  // Eq.(1) sums of one channel; non-finite values skip the group (D31)
+      const bool fin = act && isfinite(ch0);
+      double v = fin ? (double)ch0 : 0.0;
+      unsigned ng = fin ? 1u : 0u;
+      if (!single) {
+        ng = (unsigned)__popc(peers & __ballot_sync(0xffffffffu, fin));
+        v = reduce_peers(peers, v, OpAdd());
+      }
+      if (leader && ng) {
+        red_add_u64(ga, (unsigned long long)ng);
+        red_add_f64(ga + 1, v);
+      }
+    }
+    return;
   }
   for (int bi = 0; bi < a.nb; ++bi) {  // every filtered in-bounds point feeds the groups (D12)
     const BindDesc &b = a.b[bi];
@@ -545,7 +579,7 @@ __device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cn
 // ---------------------------------------------------------------- k_points (a2-a8)
 // Persistent grid-stride over the 128-point warp-items of one wave.  Per lane: 4 float4 point
 // loads in flight, then binning, one batched state gather (a7), then warp-aggregated REDs.
-template <bool kDebug>
+template <bool kDebug, int kFast>
 __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
@@ -586,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
       px[u] = py[u] = pz[u] = pw[u] = 0.0f;
       if (i < end) {
         const float *q = a.pts + i * (long long)a.stride;
-        if (a.vec4) {
+        if (kFast != 0 || a.vec4) {
           const float4 v = ld_stream_f4(q, pol);
           px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
         } else {
@@ -621,7 +655,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
         count_code(packed, npk, o[u].code, cnt);
       }
       if (!(a.ablate & 2u))
-        accumulate_warp(a, o[u], sb + (o[u].cell - map_base), a.pts + (i < end ? i : beg) * (long long)a.stride, pw[u]);
+        accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), a.pts + (i < end ? i : beg) * (long long)a.stride,
+                               pw[u]);
     }
   }
 #pragma unroll
@@ -851,9 +886,9 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 int points_blocks_per_sm(bool debug) {
   int n = 0;
   if (debug)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0>, kThreads, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0>, kThreads, 0);
   return n > 0 ? n : 1;
 }
 
@@ -864,10 +899,17 @@ int cells_blocks_per_sm() {
 }
 
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
-  if (a.dbg_cell)
-    k_points<true><<<grid, kThreads, 0, s>>>(a);
-  else
-    k_points<false><<<grid, kThreads, 0, s>>>(a);
+  // the fast variants need the channel in the float4's w (vec4) and exactly one group bound
+  const int f = a.vec4 ? a.fast : 0;
+  if (a.dbg_cell) {
+    if (f == 1) k_points<true, 1><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2) k_points<true, 2><<<grid, kThreads, 0, s>>>(a);
+    else k_points<true, 0><<<grid, kThreads, 0, s>>>(a);
+  } else {
+    if (f == 1) k_points<false, 1><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2) k_points<false, 2><<<grid, kThreads, 0, s>>>(a);
+    else k_points<false, 0><<<grid, kThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
