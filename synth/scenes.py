@@ -292,3 +292,117 @@ def softmax_image(labels, n_classes, rng, scale=4.0):
     logits -= logits.max(0, keepdims=True)
     e = np.exp(logits)
     return (e / e.sum(0, keepdims=True)).astype(np.float32)
+
+
+# --------------------------------------------------------------------------------------
+# cameras (D17: optical axis +z_c, x right, y down; R = camera -> map)
+# --------------------------------------------------------------------------------------
+def camera_looking_at(eye, target):
+    z = np.asarray(target, float) - np.asarray(eye, float)
+    z /= np.linalg.norm(z)
+    up = np.array([0.0, 0.0, 1.0])
+    x = np.cross(z, up)
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    return np.stack([x, y, z], 1)
+
+
+def camera_yaw_pitch(eye, yaw, pitch_down):
+    """camera at `eye` looking along heading `yaw`, tilted `pitch_down` rad below horizontal."""
+    d = np.array([math.cos(yaw) * math.cos(pitch_down), math.sin(yaw) * math.cos(pitch_down), -math.sin(pitch_down)])
+    return camera_looking_at(eye, np.asarray(eye, float) + d)
+
+
+def pinhole_rays(W, H, fx, fy, cx, cy):
+    """unit ray directions (H*W, 3) in the camera frame, row-major over (v, u)."""
+    u, v = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    d = np.stack([(u - cx) / fx, (v - cy) / fy, np.ones_like(u)], -1).reshape(-1, 3)
+    return d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+def depth_frame(scene, R, t, rng, W=640, H=480, f=385.0, noise_a=1e-6, noise_b=4e-6):
+    """depth camera cloud (H*W, 3) float32 in the camera frame; no-hit pixels are NaN."""
+    d_c = pinhole_rays(W, H, f, f, W / 2.0, H / 2.0)
+    d_w = d_c @ R.T
+    rng_t = scene.raycast(t, d_w, t_max=20.0)
+    hit = np.isfinite(rng_t)
+    r = np.where(hit, rng_t, 0.0)
+    r_meas = r + rng.normal(0.0, 1.0, r.shape) * np.sqrt(noise_a + noise_b * r ** 2)
+    p = d_c * r_meas[:, None]
+    p[~hit] = np.nan
+    return p.astype(np.float32), hit, (t + d_w * r[:, None])
+
+
+# --------------------------------------------------------------------------------------
+# C3: 250x250 @ 0.04 m, three 640x480 depth clouds + a 20-class softmax image
+# --------------------------------------------------------------------------------------
+C3 = dict(res=0.04, rows=250, cols=250, n_classes=20, frames=10, W=640, H=480, f=385.0, cam_h=0.7,
+          pitch=math.radians(30.0),
+          noise=dict(a=1e-6, b=4e-6, r_min=0.2, r_max=8.0, h_min=-1.5, h_max=1.5, tau2=9.0, v_out=0.01))
+
+
+def c3_scene(seed=3):
+    rng = np.random.default_rng([seed, 999])
+    boxes = []
+    for k in range(9):
+        cx, cy = rng.uniform(-4.5, 4.5, 2)
+        sx, sy = rng.uniform(0.2, 0.6, 2)
+        boxes.append(Box(cx - sx, cx + sx, cy - sy, cy + sy, float(rng.uniform(0.1, 0.7)), 1 + k,
+                         tuple(int(c) for c in rng.integers(0, 256, 3))))
+    ramps = [Ramp(1.5, 3.5, 2.5, 4.0, 0.2, 10, (120, 120, 120))]
+    return Scene(boxes=boxes, ramps=ramps)
+
+
+def c3_frame(frame, seed=3, cameras=3):
+    """three depth clouds (yaw 0, +-120 deg) and the front camera's 20-class softmax image."""
+    rng = np.random.default_rng([seed, frame])
+    scene = c3_scene(seed)
+    c = C3
+    x0, y0 = 0.009 + 0.029 * frame, 0.009 - 0.013 * frame
+    assert_tie_guard(x0, c["res"])
+    assert_tie_guard(y0, c["res"])
+    heading = 0.05 * frame
+    K = np.array([[c["f"], 0.0, c["W"] / 2.0], [0.0, c["f"], c["H"] / 2.0], [0.0, 0.0, 1.0]])
+    clouds = []
+    for k, dy in enumerate((0.0, 2 * math.pi / 3, -2 * math.pi / 3)[:cameras]):
+        eye = np.array([x0, y0, c["cam_h"]])
+        R = camera_yaw_pitch(eye, heading + dy, c["pitch"])
+        pts, hit, pw = depth_frame(scene, R, eye, rng, c["W"], c["H"], c["f"], c["noise"]["a"], c["noise"]["b"])
+        clouds.append(dict(points=pts, R=R, t=eye))
+        if k == 0:
+            cls, _ = scene.attributes(pw[:, 0], pw[:, 1], pw[:, 2])
+            labels = np.where(hit, cls, 0).reshape(c["H"], c["W"])
+            img = softmax_image(labels, c["n_classes"], rng)
+            image = dict(img=img, K=K, R=R, t=eye)
+    return dict(clouds=clouds, image=image, move=(x0, y0))
+
+
+# --------------------------------------------------------------------------------------
+# C4: 250x250 @ 0.04 m, 64-channel feature image (one C3 depth frame for geometry first)
+# --------------------------------------------------------------------------------------
+C4 = dict(res=0.04, rows=250, cols=250, d=64, frames=10, W=640, H=480, w=0.5)
+
+
+def c4_class_features(seed=4, n_classes=20, d=64):
+    rng = np.random.default_rng([seed, 12345])
+    v = rng.normal(0.0, 1.0, (n_classes, d))
+    return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+
+def c4_image(frame, seed=4):
+    """64 x 480 x 640 feature image from the C3 front camera at frame 0: per-class unit vector +
+    N(0, 0.1^2) per channel."""
+    rng = np.random.default_rng([seed, frame])
+    scene = c3_scene(3)
+    c3 = c3_frame(0)
+    im = c3["image"]
+    d_c = pinhole_rays(C3["W"], C3["H"], C3["f"], C3["f"], C3["W"] / 2.0, C3["H"] / 2.0)
+    d_w = d_c @ im["R"].T
+    t = scene.raycast(im["t"], d_w, t_max=20.0)
+    hit = np.isfinite(t)
+    pw = im["t"] + d_w * np.where(hit, t, 0.0)[:, None]
+    cls, _ = scene.attributes(pw[:, 0], pw[:, 1], pw[:, 2])
+    cls = np.where(hit, cls, 0).reshape(C3["H"], C3["W"])
+    feats = c4_class_features(seed)
+    img = feats[cls].transpose(2, 0, 1) + rng.normal(0.0, 0.1, (C4["d"], C3["H"], C3["W"]))
+    return dict(img=img.astype(np.float32), K=im["K"], R=im["R"], t=im["t"])

@@ -347,3 +347,43 @@ def test_uniform_batch_sweep_vs_oracle():
                 assert np.array_equal(g, o), (b, nm)
             else:
                 assert np.all(np.abs(g[fin].astype(np.float64) - o[fin]) <= 1e-6 + 1e-5 * np.abs(o[fin])), (b, nm)
+
+
+# ---------------------------------------------------------------- C3 / C4 (configs[2], configs[3]) full size
+def test_c3_rgbd_semantic_full_size():
+    """three 640x480 depth clouds (stride 3) + a 20-class softmax image per frame, class_bayesian
+    and class_max from the same channels."""
+    c = S.C3
+    groups = [dict(name="sem", rule=M.MEM_CLASS_BAYESIAN, n_channels=c["n_classes"], alpha0=1.0),
+              dict(name="top", rule=M.MEM_CLASS_MAX, n_channels=c["n_classes"])]
+    binds = [(0, c["n_classes"], 0), (0, c["n_classes"], 1)]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):
+        fr = S.c3_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        for cl in fr["clouds"]:
+            step_points(g, o, cl["points"], [], cl["R"], cl["t"], c["noise"])
+        im = fr["image"]
+        g.input_image(torch.from_numpy(im["img"]).cuda(), binds, im["K"], im["R"], im["t"])
+        o.input_image(im["img"], binds, im["K"], im["R"], im["t"])
+        compare_layers(g, o, where=f"C3 frame {f}: ")
+    assert (g.get_layer("top_label") >= 0).sum() > 5000
+
+
+def test_c4_feature_image_full_size():
+    """64-channel 480x640 feature image, 64 x average(w=0.5)."""
+    c, c3 = S.C4, S.C3
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=c["d"], w=c["w"])]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    fr = S.c3_frame(0)
+    g.move_to(*fr["move"])
+    o.move_to(*fr["move"])
+    for cl in fr["clouds"]:
+        step_points(g, o, cl["points"], [], cl["R"], cl["t"], c3["noise"], check_codes=False)
+    for f in range(3):
+        im = S.c4_image(f)
+        g.input_image(torch.from_numpy(im["img"]).cuda(), [(0, c["d"], 0)], im["K"], im["R"], im["t"])
+        o.input_image(im["img"], [(0, c["d"], 0)], im["K"], im["R"], im["t"])
+    compare_layers(g, o, where="C4: ")
+    assert g.get_layer("feat_observed").sum() > 5000
