@@ -636,3 +636,80 @@ int om_set_layer(om_map *m, const char *name, const float *src) {
 
 void om_get_stats(const om_map *m, unsigned long long out[8]) { memcpy(out, m->stats, sizeof m->stats); }
 void om_get_center(const om_map *m, long long out[2]) { out[0] = m->kx; out[1] = m->ky; }
+
+/* ---- PCA readout of a feature group (reading D28) ----
+ * Over the cells where the group is observed: mean mu and covariance
+ * C = (1/n) sum (x - mu)(x - mu)^T in fp64 (plain loops); eigenvectors by power iteration
+ * with deflation in long double (the library uses a different solver); each component's
+ * sign makes its largest-|coefficient| positive (D25); projections p = (x - mu) . e in fp64;
+ * min-max scaled to [0, 1] over the observed cells, 0 when max == min;
+ * unobserved cells and components beyond the rank get 0. out: k x rows x cols. */
+int om_pca_readout(const om_map *m, const char *group, int k, float *out) {
+  int gi = -1;
+  for (int i = 0; i < m->ng; ++i)
+    if (!strcmp(m->g[i].name, group)) gi = i;
+  if (gi < 0) return OM_ENOTFOUND;
+  const om_group *g = &m->g[gi];
+  if (!(g->rule == OM_AVERAGE || g->rule == OM_CLASS_AVERAGE || g->rule == OM_GAUSSIAN) || k < 1) return OM_EINVAL;
+  const int d = g->nch;
+  const long cells = ncells(m);
+  double *mu = calloc(d, sizeof(double)), *C = calloc((size_t)d * d, sizeof(double));
+  long n = 0;
+  for (long j = 0; j < cells; ++j) {
+    if (!g->observed[j]) continue;
+    ++n;
+    for (int a = 0; a < d; ++a) mu[a] += (double)g->val[(long)a * cells + j];
+  }
+  for (long j = 0; j < (long)k * cells; ++j) out[j] = 0.0f;
+  if (n == 0) { free(mu); free(C); return OM_OK; }
+  for (int a = 0; a < d; ++a) mu[a] /= (double)n;
+  for (long j = 0; j < cells; ++j) {
+    if (!g->observed[j]) continue;
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b)
+        C[a * d + b] += ((double)g->val[(long)a * cells + j] - mu[a]) * ((double)g->val[(long)b * cells + j] - mu[b]);
+  }
+  for (int a = 0; a < d * d; ++a) C[a] /= (double)n;
+  long double *A = malloc(sizeof(long double) * d * d), *v = malloc(sizeof(long double) * d),
+              *w = malloc(sizeof(long double) * d);
+  for (int a = 0; a < d * d; ++a) A[a] = C[a];
+  double *comp = calloc((size_t)k * d, sizeof(double));
+  for (int c = 0; c < k && c < d; ++c) {
+    for (int a = 0; a < d; ++a) v[a] = 1.0L / sqrtl((long double)d) + (long double)a * 1e-3L;
+    long double lam = 0.0L;
+    for (int it = 0; it < 200000; ++it) {
+      long double nrm = 0.0L;
+      for (int a = 0; a < d; ++a) {
+        w[a] = 0.0L;
+        for (int b = 0; b < d; ++b) w[a] += A[a * d + b] * v[b];
+        nrm += w[a] * w[a];
+      }
+      nrm = sqrtl(nrm);
+      if (nrm == 0.0L) { lam = 0.0L; break; }
+      long double diff = 0.0L;
+      for (int a = 0; a < d; ++a) { const long double x = w[a] / nrm; diff += fabsl(x - v[a]); v[a] = x; }
+      lam = nrm;
+      if (diff < 1e-16L) break;
+    }
+    if (lam <= 0.0L) break;  /* rank exhausted: remaining components stay 0 */
+    int big = 0;
+    for (int a = 1; a < d; ++a) if (fabsl(v[a]) > fabsl(v[big])) big = a;
+    const long double sg = v[big] < 0.0L ? -1.0L : 1.0L;
+    for (int a = 0; a < d; ++a) comp[(long)c * d + a] = (double)(sg * v[a]);
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b) A[a * d + b] -= lam * v[a] * v[b];
+  }
+  for (int c = 0; c < k; ++c) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int pass = 0; pass < 2; ++pass)
+      for (long j = 0; j < cells; ++j) {
+        if (!g->observed[j]) continue;
+        double p = 0.0;
+        for (int a = 0; a < d; ++a) p += ((double)g->val[(long)a * cells + j] - mu[a]) * comp[(long)c * d + a];
+        if (pass == 0) { if (p < lo) lo = p; if (p > hi) hi = p; }
+        else out[(long)c * cells + j] = hi > lo ? (float)((p - lo) / (hi - lo)) : 0.0f;
+      }
+  }
+  free(mu); free(C); free(A); free(v); free(w); free(comp);
+  return OM_OK;
+}

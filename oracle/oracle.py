@@ -65,6 +65,7 @@ def lib():
         L.om_set_layer.argtypes = [vp, C.c_char_p, vp]
         L.om_get_stats.argtypes = [vp, vp]
         L.om_get_center.argtypes = [vp, vp]
+        L.om_pca_readout.argtypes = [vp, C.c_char_p, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -153,6 +154,13 @@ class OracleMap:
         st = lib().om_set_layer(self._h, name.encode(), v.ctypes.data)
         if st != 0:
             raise OracleError(st, f"om_set_layer({name})")
+
+    def pca_readout(self, group, k=3):
+        out = np.empty((k, self.rows, self.cols), np.float32)
+        st = lib().om_pca_readout(self._h, group.encode(), k, out.ctypes.data)
+        if st != 0:
+            raise OracleError(st, f"om_pca_readout({group})")
+        return out
 
     def stats(self):
         out = np.zeros(8, np.uint64)

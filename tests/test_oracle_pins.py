@@ -522,3 +522,64 @@ def test_errors():
     assert e.value.status == -5
     m.input_pointcloud(np.zeros((0, 3), np.float32), [], EYE, [0, 0, 1], NOISE)  # empty is legal
     assert np.isnan(m.get_layer("elevation")).all()
+
+
+# ---------------------------------------------------------------- PCA readout (D28)
+def pca_map(feats, observed=None):
+    """map whose 'f' group holds the given (d, rows, cols) features (observed everywhere)."""
+    d, rows, cols = feats.shape
+    m = OracleMap(1.0, rows, cols, [dict(name="f", rule=AVERAGE, n_channels=d, w=0.5)])
+    for k in range(d):
+        m.set_layer(f"f_{k}" if d > 1 else "f", feats[k])
+    m.set_layer("f_observed", np.ones((rows, cols)) if observed is None else observed)
+    return m
+
+
+def test_pca_axis_aligned_recovers_axes():
+    """d = 3, variances x > y > z -> the components are the axes (sign fixed by D25),
+    so component c equals the min-max scaled feature c."""
+    rng = np.random.default_rng(61)
+    rows, cols = 20, 30
+    f = np.stack([rng.normal(0, 3.0, (rows, cols)), rng.normal(0, 1.0, (rows, cols)),
+                  rng.normal(0, 0.3, (rows, cols))]).astype(np.float32)
+    f -= f.reshape(3, -1).mean(1)[:, None, None]
+    # decorrelate exactly so that the axes ARE the eigenvectors
+    flat = f.reshape(3, -1).astype(np.float64)
+    q, _ = np.linalg.qr(flat.T)
+    flat = (q[:, :3] * np.array([3.0, 1.0, 0.3]) * np.sqrt(flat.shape[1])).T
+    f = flat.reshape(3, rows, cols).astype(np.float32)
+    out = pca_map(f).pca_readout("f", 3)
+    for c in range(3):
+        x = f[c].astype(np.float64)
+        x = x - x.mean()
+        exp = (x - x.min()) / (x.max() - x.min())
+        # the component is +/- axis c; D25 fixes the sign of the largest coefficient (+1)
+        assert np.allclose(out[c], exp, atol=2e-4), c
+
+
+def test_pca_constant_and_clusters_and_eigh():
+    rng = np.random.default_rng(67)
+    rows, cols, d = 16, 16, 8
+    # constant features -> 0 (SPEC.md:419)
+    out = pca_map(np.full((d, rows, cols), 0.7, np.float32)).pca_readout("f", 3)
+    assert (out == 0).all()
+    # two clusters separate on the first component (SPEC.md:420)
+    lab = rng.integers(0, 2, (rows, cols))
+    cen = rng.normal(0, 1, (2, d))
+    f = (cen[lab].transpose(2, 0, 1) + rng.normal(0, 0.05, (d, rows, cols))).astype(np.float32)
+    out = pca_map(f).pca_readout("f", 3)
+    a, b = out[0][lab == 0], out[0][lab == 1]
+    assert a.max() < b.min() or b.max() < a.min()
+    # the first component against numpy's symmetric eigensolver on the same covariance
+    x = f.reshape(d, -1).astype(np.float64)
+    cov = np.cov(x, bias=True)
+    wv, vv = np.linalg.eigh(cov)
+    e = vv[:, -1] * np.sign(vv[np.argmax(np.abs(vv[:, -1])), -1])
+    p = (x - x.mean(1, keepdims=True)).T @ e
+    exp = ((p - p.min()) / (p.max() - p.min())).reshape(rows, cols)
+    assert np.allclose(out[0], exp, atol=1e-4)
+    # unobserved cells are 0 and excluded
+    obs = np.ones((rows, cols))
+    obs[:3] = 0
+    out2 = pca_map(f, obs).pca_readout("f", 2)
+    assert (out2[:, :3] == 0).all() and out2[0, 3:].max() == 1.0
