@@ -674,6 +674,7 @@ int om_pca_readout(const om_map *m, const char *group, int k, float *out) {
               *w = malloc(sizeof(long double) * d);
   for (int a = 0; a < d * d; ++a) A[a] = C[a];
   double *comp = calloc((size_t)k * d, sizeof(double));
+  long double lam_max = 0.0L;
   for (int c = 0; c < k && c < d; ++c) {
     for (int a = 0; a < d; ++a) v[a] = 1.0L / sqrtl((long double)d) + (long double)a * 1e-3L;
     long double lam = 0.0L;
@@ -691,7 +692,9 @@ int om_pca_readout(const om_map *m, const char *group, int k, float *out) {
       lam = nrm;
       if (diff < 1e-16L) break;
     }
-    if (lam <= 0.0L) break;  /* rank exhausted: remaining components stay 0 */
+    if (c == 0) lam_max = lam;
+    /* rank exhausted: components with lambda <= 1e-12 lambda_max stay 0 */
+    if (lam <= 0.0L || lam <= 1e-12L * lam_max) break;
     int big = 0;
     for (int a = 1; a < d; ++a) if (fabsl(v[a]) > fabsl(v[big])) big = a;
     const long double sg = v[big] < 0.0L ? -1.0L : 1.0L;
