@@ -189,6 +189,16 @@ MEM_API mem_status mem_get_layer(const mem_map *map, const char *name, float *ou
  * EINVAL.  Used for single-step parity and resume. */
 MEM_API mem_status mem_set_layer(mem_map *map, const char *name, const float *src);
 
+/* PCA readout of a feature group (BASELINE configs[3]):
+ * per map, over the cells where the group is observed: covariance of the group's values
+ * (average / class_average: theta; gaussian: means) from fp64 moments, top-k eigenvectors
+ * (cyclic Jacobi on the host; each sign makes its largest-|coefficient| positive), projections
+ * min-max scaled to [0, 1] (0 when the component is constant or beyond the covariance's rank,
+ * and on unobserved cells).  out: n_maps x k x rows x cols float32, logical row-major, host
+ * or device.  Synchronises the stream (the eigenproblem is solved on the host).
+ * Errors: ENOTFOUND (no such group), EINVAL (rule without values, k < 1 or k > n_channels). */
+MEM_API mem_status mem_pca_readout(mem_map *map, const char *group, int k, float *out);
+
 /* Newline-separated layer names into buf (NUL-terminated); EINVAL if cap is too small. */
 MEM_API mem_status mem_get_layer_names(const mem_map *map, char *buf, size_t cap);
 

@@ -227,7 +227,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       red_add_f64(rec + kRecS, zw);
     }
   }
-  if (kFast != 0) {  // one group, channel in ch0 (the float4's w)
+  if constexpr (kFast != 0) {  // one group, channel in ch0 (the float4's w)
     unsigned long long *ga = rec + a.b[0].g.acc0;
     if (kFast == 1) {  // D20 colour: exact integer sums
       unsigned rg = 0u, bb = 0u;
@@ -257,8 +257,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
         red_add_f64(ga + 1, v);
       }
     }
-    return;
-  }
+  } else {
   for (int bi = 0; bi < a.nb; ++bi) {  // every filtered in-bounds point feeds the groups (D12)
     const BindDesc &b = a.b[bi];
     unsigned long long *ga = rec + b.g.acc0;
@@ -315,6 +314,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       if (!single) v = reduce_peers(peers, v, OpAdd());
       if (leader && ng) red_add_f64(ga + 1 + k, v);
     }
+  }
   }
 }
 
@@ -880,6 +880,85 @@ __global__ void __launch_bounds__(kThreads) k_write(const __grid_constant__ Read
   }
 }
 
+// ---------------------------------------------------------------- PCA readout (a14, C4)
+// Moments over the observed cells of one map: sum x and the upper triangle of sum x x^T in
+// fp64 (a tile of cells staged in shared memory, one thread per (a, b) pair, native fp64 REDs).
+constexpr int kPcaTileBytes = 32768;
+__global__ void __launch_bounds__(kThreads) k_pca_moments(const __grid_constant__ PcaArgs a) {
+  extern __shared__ float s_x[];  // [d][tile]
+  __shared__ int s_n;
+  const Geometry &g = a.geo;
+  const int d = a.d;
+  const int tile = kPcaTileBytes / (4 * d);
+  const int c0 = blockIdx.x * tile;
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  const long long mb = (long long)a.map * g.HW;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < tile; t += blockDim.x) {  // physical cells: order is irrelevant
+    const int phys = c0 + t;
+    const bool obs = phys < g.HW && a.st.flags[(long long)a.flag * g.BHW + mb + phys];
+    for (int k = 0; k < d; ++k) s_x[k * tile + t] = obs ? vals[(long long)(a.word0 + k) * g.BHW + mb + phys] : 0.0f;
+    if (obs) atomicAdd(&s_n, 1);
+  }
+  __syncthreads();
+  const int pairs = d * (d + 1) / 2;
+  for (int p = threadIdx.x; p < d + pairs; p += blockDim.x) {
+    double acc = 0.0;
+    if (p < d) {
+      for (int t = 0; t < tile; ++t) acc += (double)s_x[p * tile + t];
+    } else {
+      int q = p - d, ra = 0;  // q -> (ra, rb), ra <= rb, row-major upper triangle
+      while (q >= d - ra) {
+        q -= d - ra;
+        ++ra;
+      }
+      const int rb = ra + q;
+      for (int t = 0; t < tile; ++t) acc += (double)s_x[ra * tile + t] * (double)s_x[rb * tile + t];
+    }
+    if (acc != 0.0) atomicAdd(&a.sums[p], acc);
+  }
+  if (threadIdx.x == 0 && s_n) atomicAdd(&a.sums[d + pairs], (double)s_n);
+}
+
+__device__ __forceinline__ unsigned long long ord_f64(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double f64_of_ord(unsigned long long o) {
+  return __longlong_as_double((long long)((o >> 63) ? (o & 0x7fffffffffffffffull) : ~o));
+}
+
+// pass 0: projections p_c = (x - mu) . e_c in fp64 (sequential over d), min/max per component;
+// pass 1: min-max scaling to [0, 1] (0 when max == min); unobserved cells 0.
+__global__ void __launch_bounds__(kThreads) k_pca_project(const __grid_constant__ PcaArgs a, int pass) {
+  const Geometry &g = a.geo;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.HW) return;
+  const int row = t / g.W, col = t - (t / g.W) * g.W;
+  const int2 ring = a.ring[a.map];
+  const long long cell = (long long)a.map * g.HW + (long long)wrap(row + ring.x, g.H) * g.W + wrap(col + ring.y, g.W);
+  const bool obs = a.st.flags[(long long)a.flag * g.BHW + cell] != 0;
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  for (int c = 0; c < a.k; ++c) {
+    float *o = a.out + (long long)c * g.HW + t;
+    if (!obs) {
+      if (pass == 1) *o = 0.0f;
+      continue;
+    }
+    double p = 0.0;
+    for (int k = 0; k < a.d; ++k)
+      p += ((double)vals[(long long)(a.word0 + k) * g.BHW + cell] - a.mean[k]) * a.comp[c * a.d + k];
+    if (pass == 0) {
+      atomicMin(&a.minmax[2 * c], ord_f64(p));
+      atomicMax(&a.minmax[2 * c + 1], ord_f64(p));
+    } else {
+      const double lo = f64_of_ord(a.minmax[2 * c]), hi = f64_of_ord(a.minmax[2 * c + 1]);
+      *o = hi > lo ? __double2float_rn((p - lo) / (hi - lo)) : 0.0f;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
@@ -931,6 +1010,17 @@ cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
   const int cnt = a.max_count > 0 ? a.max_count : 1;
   k_shift<<<dim3(cdiv(cnt, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
+  const int tile = kPcaTileBytes / (4 * a.d);
+  k_pca_moments<<<cdiv(a.geo.HW, tile), kThreads, kPcaTileBytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s) {
+  k_pca_project<<<cdiv(a.geo.HW, kThreads), kThreads, 0, s>>>(a, pass);
   return cudaGetLastError();
 }
 

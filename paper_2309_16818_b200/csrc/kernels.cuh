@@ -98,6 +98,22 @@ cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
+// PCA readout: moments of one map's feature group, then projections
+struct PcaArgs {
+  Geometry geo;
+  State st;
+  const int2 *ring;
+  int map;                     // map index
+  int word0, d, flag;          // feature layers [word0, word0 + d), observed flag layer
+  double *sums;                // [d] sum x, then [d (d + 1) / 2] sum x_a x_b (a <= b), then count
+  int k;                       // components
+  const double *mean;          // [d]
+  const double *comp;          // [k][d]
+  unsigned long long *minmax;  // [k][2] order-preserving keys of min and max projections
+  float *out;                  // [k][H][W] logical
+};
+cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s);
+cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s);
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s);
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s);
 int points_blocks_per_sm(bool debug);

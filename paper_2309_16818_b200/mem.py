@@ -32,7 +32,7 @@ EXPORTS = ["mem_create", "mem_create_batch", "mem_destroy", "mem_set_stream", "m
            "mem_input_pointcloud", "mem_input_pointcloud_batch", "mem_input_image", "mem_input_image_batch",
            "mem_move_to", "mem_move_to_batch", "mem_get_layer", "mem_set_layer", "mem_get_layer_names",
            "mem_memory_footprint", "mem_get_info", "mem_get_center", "mem_frame_stats", "mem_debug_point_codes",
-           "mem_profile", "mem_profile_read", "mem_last_error", "mem_version"]
+           "mem_profile", "mem_profile_read", "mem_pca_readout", "mem_last_error", "mem_version"]
 STAGES = ["shift", "point", "cell", "image", "read", "write", "h2d", "d2h"]
 
 
@@ -91,6 +91,7 @@ _sig = {
     "mem_frame_stats": [_vp, _P(mem_stats)],
     "mem_debug_point_codes": [_vp, _vp, _vp],
     "mem_profile": [_vp, C.c_int],
+    "mem_pca_readout": [_vp, C.c_char_p, C.c_int, _vp],
     "mem_profile_read": [_vp, _P(C.c_double), _P(C.c_uint64), C.c_int],
 }
 for _n, _a in _sig.items():
@@ -286,6 +287,14 @@ def mem_debug_point_codes(h, n):
     return cell, code
 
 
+def mem_pca_readout(h, group, k=3, out=None):
+    if out is None:
+        B, H, W, _ = mem_get_info(h)
+        out = np.empty((B, k, H, W) if B > 1 else (k, H, W), np.float32)
+    _check(_lib.mem_pca_readout(h, group.encode(), k, _ptr(out)), f"mem_pca_readout({group})")
+    return out
+
+
 def mem_profile(h, enable):
     _check(_lib.mem_profile(h, int(enable)), "mem_profile")
 
@@ -368,6 +377,9 @@ class Map:
 
     def synchronize(self):
         mem_synchronize(self.h)
+
+    def pca_readout(self, group, k=3, out=None):
+        return mem_pca_readout(self.h, group, k, out)
 
     def profile(self, enable=True):
         mem_profile(self.h, enable)

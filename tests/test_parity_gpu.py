@@ -387,3 +387,34 @@ def test_c4_feature_image_full_size():
         o.input_image(im["img"], [(0, c["d"], 0)], im["K"], im["R"], im["t"])
     compare_layers(g, o, where="C4: ")
     assert g.get_layer("feat_observed").sum() > 5000
+    # PCA readout (a14): top-3 components min-max scaled, 1e-4 abs on [0, 1] outputs (D28)
+    gp, op = np.asarray(g.pca_readout("feat", 3)), o.pca_readout("feat", 3)
+    assert np.abs(gp - op).max() <= 1e-4, np.abs(gp - op).max()
+    assert (gp[:, g.get_layer("feat_observed") == 0] == 0).all()
+
+
+def test_pca_readout_random_and_degenerate():
+    rng = np.random.default_rng(71)
+    rows, cols, d = 33, 47, 6
+    groups = [dict(name="f", rule=M.MEM_AVERAGE, n_channels=d, w=0.5)]
+    for case in ("random", "constant", "rank2"):
+        g, o = make_pair(0.1, rows, cols, groups)
+        if case == "random":
+            f = (rng.normal(0, 1, (d, 1, 1)) * rng.normal(0, 1, (d, rows, cols)) + rng.normal(0, 1, (d, 1, 1)))
+        elif case == "constant":
+            f = np.full((d, rows, cols), 0.25)
+        else:
+            base = rng.normal(0, 1, (2, rows, cols))
+            f = np.einsum("kd,krc->drc", rng.normal(0, 1, (2, d)), base)
+        obs = (rng.uniform(size=(rows, cols)) < 0.8).astype(np.float32)
+        for k in range(d):
+            g.set_layer(f"f_{k}", f[k].astype(np.float32))
+            o.set_layer(f"f_{k}", f[k].astype(np.float32))
+        g.set_layer("f_observed", obs)
+        o.set_layer("f_observed", obs)
+        gp, op = np.asarray(g.pca_readout("f", 3)), o.pca_readout("f", 3)
+        assert np.abs(gp - op).max() <= 1e-4, (case, np.abs(gp - op).max())
+        if case == "constant":
+            assert (gp == 0).all()
+        if case == "rank2":
+            assert (gp[2] == 0).all()  # beyond the rank: zero-filled
