@@ -406,3 +406,64 @@ def c4_image(frame, seed=4):
     feats = c4_class_features(seed)
     img = feats[cls].transpose(2, 0, 1) + rng.normal(0.0, 0.1, (C4["d"], C3["H"], C3["W"]))
     return dict(img=img.astype(np.float32), K=im["K"], R=im["R"], t=im["t"])
+
+
+# --------------------------------------------------------------------------------------
+# C5a: batched learning workload, B independent 128x128 @ 0.1 m maps x 32,768 points
+# --------------------------------------------------------------------------------------
+C5A = dict(res=0.1, rows=128, cols=128, points=32768, w=0.5, n_boxes=3,
+           noise=dict(a=1e-4, b=1e-4, r_min=0.1, r_max=12.0, h_min=-3.0, h_max=1.0, tau2=9.0, v_out=0.01))
+
+
+def c5a_batch(frame, first_map, n_maps, seed=1000, points=C5A["points"]):
+    """points (n_maps*points, 4) f32 [x y z feature] in each map's sensor frame, per-map R (n,3,3),
+    t (n,3), move (n,2).  Map m: its own plane + 3 boxes (seed 1000 + m), sensor 1.5 m high at a
+    per-map start moving 0.07 m/frame along its own heading with yaw += 0.05 rad/frame; points
+    uniform over +-7 m around the sensor (the window is +-6.4 m), z = height + N(0, 0.02^2), 1%
+    outliers, 0.5% NaN; feature = box id / 3 + N(0, 0.05^2)."""
+    nb, P = C5A["n_boxes"], points
+    maps = np.arange(first_map, first_map + n_maps)
+    # per-map scene parameters (deterministic in the map id)
+    bx = np.empty((n_maps, nb, 5))
+    heading = np.empty(n_maps)
+    start = np.empty((n_maps, 2))
+    for i, mm in enumerate(maps):
+        r = np.random.default_rng([seed + int(mm), 7])
+        c = r.uniform(-5, 5, (nb, 2))
+        sz = r.uniform(0.3, 1.2, (nb, 2))
+        bx[i, :, 0], bx[i, :, 1] = c[:, 0] - sz[:, 0], c[:, 0] + sz[:, 0]
+        bx[i, :, 2], bx[i, :, 3] = c[:, 1] - sz[:, 1], c[:, 1] + sz[:, 1]
+        bx[i, :, 4] = r.uniform(0.2, 0.9, nb)
+        heading[i] = r.uniform(0, 2 * math.pi)
+        start[i] = r.uniform(-0.5, 0.5, 2)
+    rng = np.random.default_rng([seed, frame, first_map, n_maps])
+    pos = start + 0.07 * frame * np.stack([np.cos(heading), np.sin(heading)], 1)
+    # keep every snap >= 0.05 cell from a tie (D14 tie guard): nudge by a quarter cell if needed
+    for ax in range(2):
+        q = pos[:, ax] / C5A["res"] + 0.5
+        fr = q - np.floor(q)
+        bad = np.minimum(fr, 1 - fr) < 0.05
+        pos[bad, ax] += 0.25 * C5A["res"]
+    yaw = heading + 0.05 * frame
+    xy = pos[:, None, :] + rng.uniform(-7.0, 7.0, (n_maps, P, 2))
+    h = np.zeros((n_maps, P))
+    fid = np.zeros((n_maps, P))
+    for k in range(nb):
+        inside = ((xy[..., 0] >= bx[:, None, k, 0]) & (xy[..., 0] < bx[:, None, k, 1]) &
+                  (xy[..., 1] >= bx[:, None, k, 2]) & (xy[..., 1] < bx[:, None, k, 3]))
+        h = np.where(inside, np.maximum(h, bx[:, None, k, 4]), h)
+        fid = np.where(inside, k + 1, fid)
+    z = h + rng.normal(0.0, 0.02, h.shape)
+    kind = rng.uniform(size=h.shape)
+    z = np.where(kind < 0.01, z + rng.uniform(0.5, 1.0, h.shape), z)
+    t = np.concatenate([pos, np.full((n_maps, 1), 1.5)], 1)
+    c, s = np.cos(yaw), np.sin(yaw)
+    R = np.zeros((n_maps, 3, 3))
+    R[:, 0, 0], R[:, 0, 1], R[:, 1, 0], R[:, 1, 1], R[:, 2, 2] = c, -s, s, c, 1.0
+    d = np.stack([xy[..., 0] - t[:, None, 0], xy[..., 1] - t[:, None, 1], z - 1.5], -1)
+    p = np.einsum("mji,mpj->mpi", R, d)  # R^T (world - t)
+    nanm = (kind >= 0.01) & (kind < 0.015)
+    p[nanm, 0] = np.nan
+    feat = fid / 3.0 + rng.normal(0.0, 0.05, h.shape)
+    pts = np.concatenate([p, feat[..., None]], -1).astype(np.float32).reshape(-1, 4)
+    return dict(points=pts, R=R, t=t, move=pos.copy(), offsets=np.arange(n_maps + 1, dtype=np.int64) * P)

@@ -418,3 +418,34 @@ def test_pca_readout_random_and_degenerate():
             assert (gp == 0).all()
         if case == "rank2":
             assert (gp[2] == 0).all()  # beyond the rank: zero-filled
+
+
+# ---------------------------------------------------------------- C5a (configs[4]) batched maps
+def test_c5a_batched_maps_subset():
+    """C5a shape (128x128 @ 0.1 m maps, 32,768 points each, height + average), 24 maps x 4 frames
+    in one batched call per frame; every 8th map checked against its own oracle."""
+    c = S.C5A
+    B = 24
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    gb = M.Map(c["res"], c["rows"], c["cols"], groups, n_maps=B)
+    check = list(range(0, B, 8))
+    oras = {b: O.OracleMap(c["res"], c["rows"], c["cols"], groups) for b in check}
+    for f in range(4):
+        bt = S.c5a_batch(f, 0, B)
+        gb.move_to_batch(bt["move"])
+        gb.input_pointcloud_batch(torch.from_numpy(bt["points"]).cuda(), bt["offsets"], [(0, 1, 0)], bt["R"],
+                                  bt["t"], c["noise"])
+        for b in check:
+            oras[b].move_to(*bt["move"][b])
+            oras[b].input_pointcloud(bt["points"][bt["offsets"][b]:bt["offsets"][b + 1]], [(0, 1, 0)], bt["R"][b],
+                                     bt["t"][b], c["noise"])
+    for b in check:
+        for nm in gb.layer_names():
+            g, o = gb.get_layer(nm)[b], oras[b].get_layer(nm)
+            assert np.array_equal(np.isnan(g), np.isnan(o)), (b, nm)
+            fin = ~np.isnan(o)
+            if nm in ("valid", "feat_observed"):
+                assert np.array_equal(g, o), (b, nm)
+            else:
+                assert np.all(np.abs(g[fin].astype(np.float64) - o[fin]) <= 1e-6 + 1e-5 * np.abs(o[fin])), (b, nm)
+        assert (gb.get_layer("valid")[b] > 0).sum() > 8000
