@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--maps", type=int, default=64, help="maps per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sides", action="store_true", help="skip the C3 / C4 / C5a side lines")
     return ap.parse_args()
 
 
@@ -193,6 +194,111 @@ def run_reference(a):
     return 0
 
 
+# ------------------------------------------------------------------ side lines (other configs)
+def timed_loop(torch, stream, n, fn):
+    """device time of n calls of fn() (CUDA events on the caller's stream), after 2 warm-ups."""
+    fn(0)
+    fn(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(n):
+        fn(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+def side_c5a(torch, M, stream, rank, world, steps=20):
+    """BASELINE configs[4] batched learning workload: 4096 maps split over the ranks (strong
+    scaling), one 32,768-point frame per map per step.  Inputs: 256 generated maps x 2 frames
+    tiled to the rank's maps (map m uses generated map m % 256)."""
+    c = S.C5A
+    total_maps = 4096
+    mine = total_maps // world
+    first = rank * mine
+    pool = [S.c5a_batch(f, 0, 256) for f in range(2)]
+    idx = (np.arange(first, first + mine) % 256)
+    P = c["points"]
+    batches, Rs, ts, xys = [], [], [], []
+    for fr in pool:
+        pts = fr["points"].reshape(256, P, 4)[idx].reshape(-1, 4)
+        batches.append(torch.from_numpy(pts).cuda())
+        Rs.append(fr["R"][idx])
+        ts.append(fr["t"][idx])
+        xys.append(fr["move"][idx])
+    offsets = np.arange(mine + 1, dtype=np.int64) * P
+    mp = M.Map(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])], n_maps=mine)
+
+    def step(i):
+        k = i % 2
+        mp.move_to_batch(xys[k])
+        mp.input_pointcloud_batch(batches[k], offsets, [(0, 1, 0)], Rs[k], ts[k], c["noise"])
+
+    ms = timed_loop(torch, stream, steps, step)
+    mp.close()
+    return {"workload": f"C5a: 4096 maps 128x128@0.1m x 32768 pts, {mine} maps on this rank", "ms_per_step": ms,
+            "maps_per_rank": mine, "points_per_s_rank": mine * P / (ms * 1e-3),
+            "map_updates_per_s_rank": mine / (ms * 1e-3), "scaling": "strong (4096 maps total)"}
+
+
+def side_c3_c4(torch, M, stream, frames=2):
+    out = {}
+    c = S.C3
+    fr = [S.c3_frame(f) for f in range(frames)]
+    groups = [dict(name="sem", rule=3, n_channels=c["n_classes"], alpha0=1.0),
+              dict(name="top", rule=4, n_channels=c["n_classes"])]
+    binds = [(0, c["n_classes"], 0), (0, c["n_classes"], 1)]
+    mp = M.Map(c["res"], c["rows"], c["cols"], groups)
+    dev = [dict(clouds=[torch.from_numpy(cl["points"]).cuda() for cl in f["clouds"]],
+                img=torch.from_numpy(f["image"]["img"]).cuda()) for f in fr]
+
+    def c3_step(i):
+        f, d = fr[i % frames], dev[i % frames]
+        mp.move_to(*f["move"])
+        for cl, dp in zip(f["clouds"], d["clouds"]):
+            mp.input_pointcloud(dp, [], cl["R"], cl["t"], c["noise"])
+        im = f["image"]
+        mp.input_image(d["img"], binds, im["K"], im["R"], im["t"])
+
+    ms = timed_loop(torch, stream, 20, c3_step)
+    npts = sum(cl["points"].shape[0] for cl in fr[0]["clouds"])
+    out["c3"] = {"workload": "C3: 250x250@0.04m, 3 x 640x480 depth clouds + 20-class 640x480 softmax image per frame",
+                 "ms_per_frame": ms, "points_per_s": npts / (ms * 1e-3), "frames_per_s": 1e3 / ms}
+    mp.profile_read(reset=True)
+    mp.profile(True)
+    c3_step(0)
+    torch.cuda.synchronize()
+    mp.profile(False)
+    prof = mp.profile_read(reset=True)
+    out["c3"]["stage_ms"] = {k: v[0] for k, v in prof.items() if v[1]}
+    mp.close()
+    c4 = S.C4
+    m4 = M.Map(c4["res"], c4["rows"], c4["cols"], [dict(name="feat", rule=0, n_channels=c4["d"], w=c4["w"])])
+    f0 = fr[0]
+    m4.move_to(*f0["move"])
+    for cl, dp in zip(f0["clouds"], dev[0]["clouds"]):
+        m4.input_pointcloud(dp, [], cl["R"], cl["t"], c["noise"])
+    ims = [S.c4_image(f) for f in range(2)]
+    dims = [torch.from_numpy(im["img"]).cuda() for im in ims]
+
+    def c4_step(i):
+        im = ims[i % 2]
+        m4.input_image(dims[i % 2], [(0, c4["d"], 0)], im["K"], im["R"], im["t"])
+
+    ms4 = timed_loop(torch, stream, 20, c4_step)
+    pca_out = torch.empty((3, c4["rows"], c4["cols"]), device="cuda")
+    t0 = time.perf_counter()
+    for _ in range(5):
+        m4.pca_readout("feat", 3, pca_out)
+    pca_ms = (time.perf_counter() - t0) / 5 * 1e3
+    out["c4"] = {"workload": "C4: 250x250@0.04m, 64-channel 480x640 feature image, 64 x average + PCA readout",
+                 "ms_per_image": ms4, "images_per_s": 1e3 / ms4, "pca_readout_ms_wall": pca_ms,
+                 "image_bytes": int(dims[0].numel() * 4)}
+    m4.close()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_mem(a):
     import torch
@@ -321,6 +427,18 @@ def run_mem(a):
         single = {"us_per_frame": l0.elapsed_time(l1) * 10.0, "points_per_s": 100 * npts / (l0.elapsed_time(l1) * 1e-3)}
         sm.close()
 
+    sides = {}
+    if not a.no_sides:
+        sides["c5a"] = side_c5a(torch, M, stream, rank, world)
+        t5 = torch.tensor([sides["c5a"]["ms_per_step"]], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        sides["c5a"]["ms_per_step_max_over_ranks"] = float(t5.item())
+        sides["c5a"]["points_per_s"] = 4096 * S.C5A["points"] / (float(t5.item()) * 1e-3)
+        sides["c5a"]["map_updates_per_s"] = 4096 / (float(t5.item()) * 1e-3)
+        if rank == 0:
+            sides.update(side_c3_c4(torch, M, stream))
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         pts_s, maps_s, cores, nf, dt = oracle_rate(frames, budget_s=12.0)
@@ -353,6 +471,7 @@ def run_mem(a):
             "e2e": e2e,
             "single_map_c2": single,
             "cpu_baseline": cpu,
+            "side_lines": sides,
             "frame_stats_last_step": stats,
         }
         print(json.dumps(line), flush=True)
