@@ -143,6 +143,30 @@ MEM_API mem_status mem_set_stream(mem_map *map, mem_stream stream);
 /* Blocks until all work enqueued on the map's stream has finished. */
 MEM_API mem_status mem_synchronize(mem_map *map);
 
+/* ---- one big map sharded across ranks ----------------------------
+ * Every rank holds the full map state and fuses its own shard of each frame's points; the
+ * per-cell statistics are moved to the owner of each physical row band (rows divisible by
+ * nranks; band r = physical rows [r*rows/nranks, (r+1)*rows/nranks)), folded there by a typed
+ * merge kernel (f64 sums, u64 sums, u64 max) and fused for the band only; elevation,
+ * variance and valid are then all-gathered so that every rank's next Mahalanobis test sees
+ * the whole pre-frame map.  Transport:
+ *  - NCCL (nccl_id != NULL, one process per GPU): grouped ncclSend/ncclRecv of the bands and
+ *    ncclAllGather, stream-ordered on the map's stream.  Every call on a sharded map is
+ *    collective (all ranks, same order); mem_get_layer all-gathers every layer first.
+ *  - local (nccl_id == NULL): the nranks shards live in one process on one device (testing
+ *    and single-GPU emulation); mem_input_pointcloud only accumulates, and
+ *    mem_shard_local_sync(shards) performs the exchange, the band fusion and a full state
+ *    replication with device copies; call it after every input (point cloud or image), with
+ *    every shard having taken the same sequence of calls.  All shards must use the same stream.
+ * Images: every rank takes the whole image and fuses the cells of its own band (the image
+ * fusion is per cell, PAPER §3.3); moves are replicated (every rank calls mem_move_to).
+ * Errors: EINVAL (rows % nranks, rank range, shards out of step), ENOMEM, ECOMM (NCCL), ECUDA. */
+MEM_API mem_status mem_nccl_unique_id(void *id128);
+MEM_API mem_status mem_create_sharded(float resolution, int rows, int cols, const mem_layer_spec *groups,
+                                      int n_groups, unsigned flags, mem_stream stream, const void *nccl_id128,
+                                      int rank, int nranks, mem_map **out);
+MEM_API mem_status mem_shard_local_sync(mem_map **shards, int nranks);
+
 /* ---- inputs ---------------------------------------------------------------------- */
 
 /* Fuses one point cloud: n points of `stride` floats (xyz in the

@@ -259,17 +259,62 @@ static void store_class_max(om_group *g, long j, uint64_t key) {
   g->val[j] = float_of_ord((uint32_t)(key >> 32));
 }
 
-/* ---- point-cloud input: SURVEY §8(c) N2 steps 1-3 ---- */
-int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const om_binding *bind, int nb,
+/* ---- point-cloud input: SURVEY §8(c) N2 steps 1-3 ----
+ * Split in two so that the sharded big map can be checked on CPU:
+ * om_accumulate runs steps 1-2 and returns the frame's per-cell sufficient statistics;
+ * om_fuse_rows runs step 3 on the rows [row_lo, row_hi).  om_input_pointcloud is the two
+ * in sequence over all rows.  The statistics are plain sums / counts / maxima of
+ * per-point terms, so statistics of disjoint point subsets add up (max for class_max keys). */
+typedef struct om_frame {
+  long cells;
+  int nb;
+  om_binding bind[16];
+  om_noise noise;
+  unsigned long long *n_in, *n_out;
+  double *P, *S;
+  unsigned long long *ng[16];
+  double *gsum[16];
+  unsigned long long *gkey[16];
+  int nsum[16]; /* sums per cell of binding b = the group's width (3 for colour) */
+  unsigned long long st[8];
+} om_frame;
+
+void om_frame_free(om_frame *f) {
+  if (!f) return;
+  free(f->n_in); free(f->n_out); free(f->P); free(f->S);
+  for (int b = 0; b < f->nb; ++b) { free(f->ng[b]); free(f->gsum[b]); free(f->gkey[b]); }
+  free(f);
+}
+
+/* raw access to a frame's statistics (field 0 n_in, 1 n_out, 2 P, 3 S, 4 group count,
+   5 group sums [n_ch][cells], 6 class_max keys, 7 the 8 counters); *len = element count */
+void *om_frame_array(om_frame *f, int field, int b, long *len) {
+  *len = f->cells;
+  switch (field) {
+    case 0: return f->n_in;
+    case 1: return f->n_out;
+    case 2: return f->P;
+    case 3: return f->S;
+    case 4: return f->ng[b];
+    case 5: *len = f->cells * f->nsum[b]; return f->gsum[b];
+    case 6: if (!f->gkey[b]) *len = 0; return f->gkey[b];
+    case 7: *len = 8; return f->st;
+  }
+  *len = 0;
+  return NULL;
+}
+
+om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const om_binding *bind, int nb,
                         const double R[9], const double t[3], const om_noise *np, int *cell_out,
-                        unsigned char *code_out) {
-  if (n < 0 || stride < 3 || nb < 0 || nb > 16 || !np) return OM_EINVAL;
-  if (!pose_ok(R)) return OM_EPOSE;
+                        unsigned char *code_out, int *status) {
+  *status = OM_EINVAL;
+  if (n < 0 || stride < 3 || nb < 0 || nb > 16 || !np) return NULL;
+  if (!pose_ok(R)) { *status = OM_EPOSE; return NULL; }
   for (int b = 0; b < nb; ++b) {
-    if (bind[b].group < 0 || bind[b].group >= m->ng) return OM_EINVAL;
-    if (bind[b].ch_offset < 0 || 3 + bind[b].ch_offset + bind[b].n_ch > stride) return OM_EINVAL;
-    if (!binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 0)) return OM_EINVAL;
-    for (int c = 0; c < b; ++c) if (bind[c].group == bind[b].group) return OM_EINVAL;
+    if (bind[b].group < 0 || bind[b].group >= m->ng) return NULL;
+    if (bind[b].ch_offset < 0 || 3 + bind[b].ch_offset + bind[b].n_ch > stride) return NULL;
+    if (!binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 0)) return NULL;
+    for (int c = 0; c < b; ++c) if (bind[c].group == bind[b].group) return NULL;
   }
   const long cells = ncells(m);
   const int H = m->rows, W = m->cols;
@@ -284,18 +329,24 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
   const float rmin2 = np->r_min * np->r_min, rmax2 = np->r_max * np->r_max;
 
   /* per-cell, per-frame sufficient statistics */
-  unsigned long long *n_in = calloc(cells, sizeof *n_in), *n_out = calloc(cells, sizeof *n_out);
-  double *P = calloc(cells, sizeof *P), *S = calloc(cells, sizeof *S);
-  unsigned long long *ng[16];
-  double *gsum[16];
-  unsigned long long *gkey[16];
+  om_frame *f = (om_frame *)calloc(1, sizeof(om_frame));
+  f->cells = cells;
+  f->nb = nb;
+  memcpy(f->bind, bind, sizeof(om_binding) * (size_t)nb);
+  f->noise = *np;
+  unsigned long long *n_in = f->n_in = calloc(cells, sizeof *n_in), *n_out = f->n_out = calloc(cells, sizeof *n_out);
+  double *P = f->P = calloc(cells, sizeof *P), *S = f->S = calloc(cells, sizeof *S);
+  unsigned long long **ng = f->ng;
+  double **gsum = f->gsum;
+  unsigned long long **gkey = f->gkey;
   for (int b = 0; b < nb; ++b) {
     const om_group *g = &m->g[bind[b].group];
     ng[b] = calloc(cells, sizeof(unsigned long long));
     gsum[b] = calloc((size_t)cells * g->nch, sizeof(double));
     gkey[b] = g->rule == OM_CLASS_MAX ? calloc(cells, sizeof(unsigned long long)) : NULL;
+    f->nsum[b] = g->nch;
   }
-  unsigned long long st[8] = {0};
+  unsigned long long *st = f->st;
   st[0] = (unsigned long long)n;
 
   /* step 2: for each point, in input order */
@@ -381,9 +432,23 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
     }
   }
 
+  *status = OM_OK;
+  return f;
+}
+
+int om_fuse_rows(om_map *m, om_frame *f, int row_lo, int row_hi) {
+  if (row_lo < 0 || row_hi > m->rows || row_lo > row_hi || f->cells != ncells(m)) return OM_EINVAL;
+  const long cells = f->cells;
+  const int nb = f->nb;
+  const om_binding *bind = f->bind;
+  const om_noise *np = &f->noise;
+  const unsigned long long *n_in = f->n_in, *n_out = f->n_out;
+  const double *P = f->P, *S = f->S;
+  unsigned long long st[8];
+  memcpy(st, f->st, sizeof st);
   /* step 3: per cell; cells with no points stay bit-untouched */
   double sums[256];
-  for (long j = 0; j < cells; ++j) {
+  for (long j = (long)row_lo * m->cols; j < (long)row_hi * m->cols; ++j) {
     if (n_in[j] + n_out[j] == 0) continue;
     st[7]++;
     /* a9: Kalman height fusion in information form (D7, D11) */
@@ -406,22 +471,31 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
     /* a10: each bound group by its rule */
     for (int b = 0; b < nb; ++b) {
       om_group *g = &m->g[bind[b].group];
-      if (ng[b][j] == 0) continue;
-      for (int k = 0; k < g->nch; ++k) sums[k] = gsum[b][(long)k * cells + j];
+      if (f->ng[b][j] == 0) continue;
+      for (int k = 0; k < g->nch; ++k) sums[k] = f->gsum[b][(long)k * cells + j];
       switch (g->rule) {
         case OM_AVERAGE:
         case OM_CLASS_AVERAGE:
-        case OM_COLOR: fuse_average(g, j, cells, (long)ng[b][j], sums); break;
-        case OM_GAUSSIAN: fuse_gaussian(g, j, cells, (long)ng[b][j], sums); break;
+        case OM_COLOR: fuse_average(g, j, cells, (long)f->ng[b][j], sums); break;
+        case OM_GAUSSIAN: fuse_gaussian(g, j, cells, (long)f->ng[b][j], sums); break;
         case OM_CLASS_BAYESIAN: fuse_dirichlet(g, j, cells, sums); break;
-        case OM_CLASS_MAX: store_class_max(g, j, gkey[b][j]); break;
+        case OM_CLASS_MAX: store_class_max(g, j, f->gkey[b][j]); break;
       }
     }
   }
   memcpy(m->stats, st, sizeof st);
-  free(n_in); free(n_out); free(P); free(S);
-  for (int b = 0; b < nb; ++b) { free(ng[b]); free(gsum[b]); free(gkey[b]); }
   return OM_OK;
+}
+
+int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const om_binding *bind, int nb,
+                        const double R[9], const double t[3], const om_noise *np, int *cell_out,
+                        unsigned char *code_out) {
+  int status;
+  om_frame *f = om_accumulate(m, pts, n, stride, bind, nb, R, t, np, cell_out, code_out, &status);
+  if (!f) return status;
+  status = om_fuse_rows(m, f, 0, m->rows);
+  om_frame_free(f);
+  return status;
 }
 
 /* ---- image input: SURVEY §8(c) N2 step 4 (a11 + a12), PAPER.md:232-239 ---- */

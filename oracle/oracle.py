@@ -66,6 +66,12 @@ def lib():
         L.om_get_stats.argtypes = [vp, vp]
         L.om_get_center.argtypes = [vp, vp]
         L.om_pca_readout.argtypes = [vp, C.c_char_p, C.c_int, vp]
+        L.om_accumulate.restype = vp
+        L.om_accumulate.argtypes = L.om_input_pointcloud.argtypes + [C.POINTER(C.c_int)]
+        L.om_fuse_rows.argtypes = [vp, vp, C.c_int, C.c_int]
+        L.om_frame_free.argtypes = [vp]
+        L.om_frame_array.restype = vp
+        L.om_frame_array.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_long)]
         _lib = L
     return _lib
 
@@ -87,6 +93,47 @@ def make_binds(bindings):
     for i, (off, n, g) in enumerate(bindings):
         arr[i] = _Bind(off, n, g)
     return arr
+
+
+class OracleFrame:
+    """one frame's per-cell sufficient statistics (om_accumulate), as writable numpy views:
+    n_in, n_out (u64), P, S (f64), and per binding b: count[b] (u64), sums[b] (f64,
+    [n_ch][cells]), keys[b] (u64 class_max keys or None); counters (u64[8])."""
+
+    _FIELDS = {0: ("n_in", np.uint64), 1: ("n_out", np.uint64), 2: ("P", np.float64), 3: ("S", np.float64)}
+
+    def __init__(self, handle, nb):
+        self._h = handle
+        L = lib()
+
+        def view(field, b, dtype):
+            n = C.c_long(0)
+            ptr = L.om_frame_array(self._h, field, b, C.byref(n))
+            if not ptr or n.value == 0:
+                return None
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint64 if dtype == np.uint64 else C.c_double)),
+                                         (n.value,))
+
+        for f, (name, dt) in self._FIELDS.items():
+            setattr(self, name, view(f, 0, dt))
+        self.count = [view(4, b, np.uint64) for b in range(nb)]
+        self.sums = [view(5, b, np.float64) for b in range(nb)]
+        self.keys = [view(6, b, np.uint64) for b in range(nb)]
+        self.counters = view(7, 0, np.uint64)
+
+    def arrays(self):
+        """every statistic array with its merge operation ('sum' or 'max')"""
+        out = [(self.n_in, "sum"), (self.n_out, "sum"), (self.P, "sum"), (self.S, "sum")]
+        for c, s, k in zip(self.count, self.sums, self.keys):
+            out += [(c, "sum"), (s, "sum")]
+            if k is not None:
+                out.append((k, "max"))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().om_frame_free(self._h)
+            self._h = None
 
 
 class OracleMap:
@@ -125,6 +172,26 @@ class OracleMap:
         if st != 0:
             raise OracleError(st, "om_input_pointcloud")
         return (cell, code) if debug else None
+
+    def accumulate(self, pts, bindings, R, t, noise):
+        """steps 1-2 only (per-point filtering and binning against the current state)."""
+        pts = np.ascontiguousarray(pts, np.float32)
+        n, stride = pts.shape
+        Rr, Rp = _dbl(R, 9)
+        tt, tp = _dbl(t, 3)
+        nz = _Noise(**noise)
+        st = C.c_int(0)
+        h = lib().om_accumulate(self._h, pts.ctypes.data, n, stride, make_binds(bindings), len(bindings), Rp, tp,
+                                C.byref(nz), None, None, C.byref(st))
+        if not h:
+            raise OracleError(st.value, "om_accumulate")
+        return OracleFrame(h, len(bindings))
+
+    def fuse_rows(self, frame, row_lo, row_hi):
+        """step 3 on rows [row_lo, row_hi)."""
+        st = lib().om_fuse_rows(self._h, frame._h, row_lo, row_hi)
+        if st != 0:
+            raise OracleError(st, "om_fuse_rows")
 
     def input_image(self, img, bindings, K, R, t):
         img = np.ascontiguousarray(img, np.float32)

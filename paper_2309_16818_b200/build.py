@@ -17,9 +17,17 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL 2.28 (the copy torch ships in the venv; the system 2.27 is the fallback), for the
+# sharded big map's band exchange
+_VENV_NCCL = os.path.join(sys.prefix, "lib", f"python{sys.version_info[0]}.{sys.version_info[1]}", "site-packages",
+                          "nvidia", "nccl")
+NCCL_DIR = os.environ.get("MEM_NCCL_DIR", _VENV_NCCL if os.path.isdir(_VENV_NCCL) else "/usr")
+NCCL_INC = os.path.join(NCCL_DIR, "include")
+NCCL_LIB = os.path.join(NCCL_DIR, "lib") if os.path.isdir(os.path.join(NCCL_DIR, "lib")) else "/usr/lib/x86_64-linux-gnu"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--extended-lambda", "-shared",
          "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden", "-Xptxas", "-warn-spills",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include"), "-I", NCCL_INC]
+LIBS = ["-L", NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
 
 
 def sources():
@@ -41,7 +49,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *sources(), *LIBS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

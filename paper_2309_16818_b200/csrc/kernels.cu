@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const Geometry &g = a.geo;
   const int lane = threadIdx.x & 31;
-  const int tpm = (g.HW + kCellTile - 1) / kCellTile;  // tiles per map
+  const int tpm = (a.cell_hi - a.cell_lo + kCellTile - 1) / kCellTile;  // tiles per map (band)
   const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * tpm;
   const unsigned long long *accN = a.cnt;
   for (int rt = blockIdx.x; rt < total; rt += gridDim.x) {
@@ -689,24 +689,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
     // recently touched (L2-resident); the next k_points starts with the lines zeroed last here
     const int tile = (a.ablate & 32u) ? rt : total - 1 - rt;
     const int m = a.m0 + tile / tpm;
-    const int t0 = (tile - (tile / tpm) * tpm) * kCellTile;
+    const int t0 = a.cell_lo + (tile - (tile / tpm) * tpm) * kCellTile;
     const MapFrame f = a.frames ? a.frames[m] : a.f0;
     const int sb = (int)scratch_base(a, m);
     if (threadIdx.x == 0) {
       s_n = 0;
-      if (t0 == 0) a.ring[m] = make_int2(f.r0, f.c0);
+      if (t0 == a.cell_lo) a.ring[m] = make_int2(f.r0, f.c0);
     }
     __syncthreads();
     unsigned long long cv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {  // counts first (memory-level parallelism)
       const int phys = t0 + u * kThreads + threadIdx.x;
-      cv[u] = phys < g.HW ? __ldcg(accN + sb + phys) : 0ull;
+      cv[u] = phys < a.cell_hi ? __ldcg(accN + sb + phys) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int phys = t0 + u * kThreads + threadIdx.x;
-      if (phys < g.HW && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
+      if (phys < a.cell_hi && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
         const int prow = phys / g.W, pcol = phys - (phys / g.W) * g.W;
         int row = prow - f.r0, col = pcol - f.c0;
         row += row < 0 ? g.H : 0;
@@ -757,7 +757,9 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
   if (t >= g.HW) return;
   const int row = t / g.W, col = t - (t / g.W) * g.W;  // logical cell
   const int2 ring = a.ring[m];
-  const long long cell = (long long)m * g.HW + (long long)wrap(row + ring.x, g.H) * g.W + wrap(col + ring.y, g.W);
+  const int prow = wrap(row + ring.x, g.H);
+  if (prow < a.row_lo || prow >= a.row_hi) return;  // another rank's band (sharded map)
+  const long long cell = (long long)m * g.HW + (long long)prow * g.W + wrap(col + ring.y, g.W);
   if (!a.st.flags[(long long)kFlagValid * g.BHW + cell]) return;
   const MapFrame &f = a.frames ? a.frames[m] : a.f0;
   const float *vals = reinterpret_cast<const float *>(a.st.words);
@@ -959,6 +961,42 @@ __global__ void __launch_bounds__(kThreads) k_pca_project(const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------- k_merge (sharded map)
+// own band scratch op= the other ranks' partials, typed per record word (f64 sums, u64 sums,
+// u64 max), so the owner's k_cells sees the statistics of every rank's points.
+__global__ void __launch_bounds__(kThreads) k_merge(const __grid_constant__ MergeArgs a) {
+  const long long words = (long long)a.n * (1 + a.R);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < a.n) {  // counts: u64 n_in | n_out << 32
+      unsigned long long v = a.cnt[a.lo + i];
+      for (int p = 0; p < a.nsrc; ++p) v += a.src_cnt[(long long)p * a.n + i];
+      a.cnt[a.lo + i] = v;
+      continue;
+    }
+    const long long j = i - a.n;  // record word j of the band
+    const int w = (int)(j % a.R);
+    unsigned long long *dst = a.rec + (long long)a.lo * a.R + j;
+    const int ty = a.wtype[w];
+    if (ty == 0) {
+      double v = __longlong_as_double((long long)*dst);
+      for (int p = 0; p < a.nsrc; ++p) v += __longlong_as_double((long long)a.src_rec[(long long)p * a.n * a.R + j]);
+      *dst = (unsigned long long)__double_as_longlong(v);
+    } else if (ty == 1) {
+      unsigned long long v = *dst;
+      for (int p = 0; p < a.nsrc; ++p) v += a.src_rec[(long long)p * a.n * a.R + j];
+      *dst = v;
+    } else {
+      unsigned long long v = *dst;
+      for (int p = 0; p < a.nsrc; ++p) {
+        const unsigned long long x = a.src_rec[(long long)p * a.n * a.R + j];
+        v = x > v ? x : v;
+      }
+      *dst = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
@@ -1021,6 +1059,13 @@ cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
 
 cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s) {
   k_pca_project<<<cdiv(a.geo.HW, kThreads), kThreads, 0, s>>>(a, pass);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s) {
+  const long long words = (long long)a.n * (1 + a.R);
+  const long long blocks = (words + kThreads - 1) / kThreads;
+  k_merge<<<(unsigned)(blocks < 148LL * 16 ? blocks : 148LL * 16), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

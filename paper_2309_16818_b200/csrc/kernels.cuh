@@ -34,6 +34,7 @@ struct PassArgs {
   const int *pstart;           // device [n_maps+1] prefix sums of point warp-items (batched) or nullptr
   int p_single;                // point warp-items of the single map
   int m0, m1;                  // maps of this wave
+  int cell_lo, cell_hi;        // k_cells: physical cells [lo, hi) of each map (a row band when sharded)
   int p_uniform;               // > 0: every map of the wave has exactly this many point warp-items
   int slot0;                   // scratch map-slot of map m0 (map m -> slot slot0 + m - m0)
   int q_per_map;               // cell warp-items per map
@@ -60,6 +61,7 @@ struct PassArgs {
 };
 
 struct ImageArgs {
+  int row_lo, row_hi;          // physical rows fused (the owned band when sharded)
   const float *img;
   int C, IH, IW;
   long long map_stride;        // floats between consecutive maps' images
@@ -114,6 +116,16 @@ struct PcaArgs {
 };
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s);
 cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s);
+// sharded map: fold the partial scratch of the other ranks for this rank's band
+struct MergeArgs {
+  unsigned long long *cnt;           // own scratch counts (band cells [lo, lo + n))
+  unsigned long long *rec;           // own scratch records [HW][R]
+  const unsigned long long *src_cnt; // nsrc partial count bands, each n words, contiguous
+  const unsigned long long *src_rec; // nsrc partial record bands, each n * R words
+  int nsrc, lo, n, R;
+  const uint8_t *wtype;              // [R]: 0 f64 sum, 1 u64 sum, 2 u64 max
+};
+cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s);
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s);
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s);
 int points_blocks_per_sm(bool debug);

@@ -2,6 +2,7 @@
 // layer registry, device state allocation, per-call parameter staging and kernel launches.
 // No compute happens here: every step of the path runs in kernels.cu.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -102,6 +103,14 @@ struct mem_map {
   int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see PassArgs::ablate)
+  // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
+  int transport = 0, rank = 0, nranks = 1;
+  int band_lo = 0, band_n = 0;          // owned physical cells [band_lo, band_lo + band_n)
+  ncclComm_t comm = nullptr;
+  unsigned long long *recv = nullptr;   // (nranks-1) partial bands: counts then records
+  uint8_t *wtype = nullptr;             // [R] record word types (merge)
+  bool exchange_pending = false;        // local transport: accumulated, not yet fused
+  PassArgs shard_args{};                // the k_cells arguments of the frame being fused
   int l2_persist_mb = 0;    // DIAGNOSTICS: env MEM_L2_PERSIST_MB at create
   bool single_stream = false;  // DIAGNOSTICS: env MEM_SINGLE_STREAM=1: waves run P0 C0 P1 C1 ... in order
   std::vector<ShiftRec> pend;
@@ -391,6 +400,9 @@ void free_map(mem_map *m) {
   cudaFree(m->din);
   cudaFree(m->dout);
   cudaFree(m->pca_buf);
+  cudaFree(m->recv);
+  cudaFree(m->wtype);
+  if (m->comm) ncclCommDestroy(m->comm);
   cudaFree(m->ctl);
   cudaFree(m->dbg_cell);
   cudaFree(m->dbg_code);
@@ -609,6 +621,98 @@ mem_status mem_synchronize(mem_map *m) {
   return MEM_OK;
 }
 
+#define NC(expr)                                                                            \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess) return fail(MEM_ECOMM, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+// merge the received partial bands, clear the scratch outside the band, fuse the band
+static mem_status shard_merge_and_fuse(mem_map *m, const unsigned long long *src, int nsrc) {
+  const int HW = m->H * m->W, R = m->n_acc;
+  PassArgs &a = m->shard_args;
+  if (nsrc > 0) {
+    MergeArgs mg;
+    memset(&mg, 0, sizeof mg);
+    mg.cnt = a.cnt;
+    mg.rec = a.rec;
+    mg.src_cnt = src;
+    mg.src_rec = src + (size_t)nsrc * m->band_n;
+    mg.nsrc = nsrc;
+    mg.lo = m->band_lo;
+    mg.n = m->band_n;
+    mg.R = R;
+    mg.wtype = m->wtype;
+    TIMED(MEM_STAGE_CELL, launch_merge(mg, m->stream));
+  }
+  // the other bands' statistics were sent to their owners: zero them for the next frame
+  const size_t w8 = sizeof(unsigned long long);
+  if (m->band_lo > 0) {
+    CU(cudaMemsetAsync(a.cnt, 0, w8 * m->band_lo, m->stream));
+    CU(cudaMemsetAsync(a.rec, 0, w8 * (size_t)m->band_lo * R, m->stream));
+  }
+  const int hi = m->band_lo + m->band_n;
+  if (hi < HW) {
+    CU(cudaMemsetAsync(a.cnt + hi, 0, w8 * (size_t)(HW - hi), m->stream));
+    CU(cudaMemsetAsync(a.rec + (size_t)hi * R, 0, w8 * (size_t)(HW - hi) * R, m->stream));
+  }
+  const long long citems = (m->band_n + kWarpCells - 1) / kWarpCells;
+  const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
+  TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
+  return MEM_OK;
+}
+
+// NCCL transport: bands to their owners (grouped send/recv), merge + band fusion, all-gather of
+// elevation / variance / valid (every rank's next Mahalanobis test needs the whole map)
+static mem_status shard_fuse_nccl(mem_map *m) {
+  const int G = m->nranks, R = m->n_acc, bn = m->band_n;
+  PassArgs &a = m->shard_args;
+  if (G > 1) {
+    NC(ncclGroupStart());
+    int slot = 0;
+    for (int p = 0; p < G; ++p) {
+      if (p == m->rank) continue;
+      unsigned long long *rc = m->recv + (size_t)slot * bn;
+      unsigned long long *rr = m->recv + (size_t)(G - 1) * bn + (size_t)slot * bn * R;
+      NC(ncclSend(a.cnt + (size_t)p * bn, bn, ncclUint64, p, m->comm, m->stream));
+      NC(ncclSend(a.rec + (size_t)p * bn * R, (size_t)bn * R, ncclUint64, p, m->comm, m->stream));
+      NC(ncclRecv(rc, bn, ncclUint64, p, m->comm, m->stream));
+      NC(ncclRecv(rr, (size_t)bn * R, ncclUint64, p, m->comm, m->stream));
+      ++slot;
+    }
+    NC(ncclGroupEnd());
+  }
+  mem_status s = shard_merge_and_fuse(m, m->recv, G - 1);
+  if (s != MEM_OK) return s;
+  if (G > 1) {
+    float *vals = reinterpret_cast<float *>(m->st.words);
+    const int HW = m->H * m->W;
+    NC(ncclGroupStart());
+    NC(ncclAllGather(vals + (size_t)kWordElev * HW + m->band_lo, vals + (size_t)kWordElev * HW, bn, ncclFloat32,
+                     m->comm, m->stream));
+    NC(ncclAllGather(vals + (size_t)kWordVar * HW + m->band_lo, vals + (size_t)kWordVar * HW, bn, ncclFloat32,
+                     m->comm, m->stream));
+    NC(ncclAllGather(m->st.flags + m->band_lo, m->st.flags, bn, ncclUint8, m->comm, m->stream));
+    NC(ncclGroupEnd());
+  }
+  return MEM_OK;
+}
+
+// all-gather every stored layer (readout of a sharded NCCL map)
+static mem_status shard_gather_all(mem_map *m) {
+  if (m->transport != 1 || m->nranks == 1) return MEM_OK;
+  const int HW = m->H * m->W, bn = m->band_n;
+  NC(ncclGroupStart());
+  for (int w = 0; w < m->n_word; ++w)
+    NC(ncclAllGather(m->st.words + (size_t)w * HW + m->band_lo, m->st.words + (size_t)w * HW, bn, ncclUint32,
+                     m->comm, m->stream));
+  for (int f = 0; f < m->n_flag; ++f)
+    NC(ncclAllGather(m->st.flags + (size_t)f * HW + m->band_lo, m->st.flags + (size_t)f * HW, bn, ncclUint8,
+                     m->comm, m->stream));
+  NC(ncclGroupEnd());
+  return MEM_OK;
+}
+
 static mem_status input_points(mem_map *m, const float *pts, const int64_t *offsets, int64_t n_single, int stride,
                                const mem_binding *bind, int nb, const double *R, const double *t,
                                const mem_noise *np) {
@@ -660,10 +764,14 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     m->dbg_n = total;
   }
   CU(cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream));  // stats + work queue
-  if (total == 0) return flush_shift(m);  // legal; only a pending shift changes the map
+  // legal; only a pending shift changes the map -- except that a shard of a sharded map
+  // still takes part in the band exchange with its empty statistics
+  if (total == 0 && m->transport == 0) return flush_shift(m);
   const void *dpts = nullptr;
-  s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
-  if (s != MEM_OK) return s;
+  if (total > 0) {
+    s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
+    if (s != MEM_OK) return s;
+  }
   a.pts = (const float *)dpts;
   a.stride = stride;
   a.n_single = n_single;
@@ -676,6 +784,8 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.reset = m->reset_info();
   a.ablate = m->ablate;
   const int HW = m->H * m->W;
+  a.cell_lo = 0;
+  a.cell_hi = HW;
   a.q_per_map = (HW + kWarpCells - 1) / kWarpCells;
   if (m->flags & MEM_FLAG_DEBUG_POINTS) {
     a.dbg_cell = m->dbg_cell;
@@ -791,6 +901,18 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
     const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
+    if (m->transport != 0) {  // sharded map: accumulate this rank's shard, then the band protocol
+      TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
+      a.cell_lo = m->band_lo;
+      a.cell_hi = m->band_lo + m->band_n;
+      m->shard_args = a;
+      m->pending = false;
+      if (m->transport == 2) {
+        m->exchange_pending = true;
+        return MEM_OK;
+      }
+      return shard_fuse_nccl(m);
+    }
     if (n_waves == 1 || m->single_stream) {
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
       TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
@@ -849,6 +971,8 @@ static mem_status input_image(mem_map *m, const float *img, int C, int IH, int I
   s = stage_input(m, img, sizeof(float) * (size_t)per * B, &dimg);
   if (s != MEM_OK) return s;
   a.img = (const float *)dimg;
+  a.row_lo = m->transport ? m->band_lo / m->W : 0;  // sharded: fuse the owned band only
+  a.row_hi = m->transport ? (m->band_lo + m->band_n) / m->W : m->H;
   a.C = C;
   a.IH = IH;
   a.IW = IW;
@@ -966,6 +1090,8 @@ mem_status mem_get_layer(const mem_map *cm, const char *name, float *out) {
   if (set_device(m)) return MEM_ECUDA;
   {
     mem_status fs = flush_shift(m);
+    if (fs != MEM_OK) return fs;
+    fs = shard_gather_all(m);
     if (fs != MEM_OK) return fs;
   }
   ReadArgs a = read_args(m, *l);
@@ -1198,6 +1324,114 @@ mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   out->n_inlier = h[5];
   out->n_outlier = h[6];
   out->n_cells_touched = h[7];
+  return MEM_OK;
+}
+
+mem_status mem_nccl_unique_id(void *id128) {
+  if (!id128) return fail(MEM_EINVAL, "id is NULL");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  memcpy(id128, &id, sizeof id);
+  return MEM_OK;
+}
+
+mem_status mem_create_sharded(float resolution, int rows, int cols, const mem_layer_spec *groups, int n_groups,
+                              unsigned flags, mem_stream stream, const void *nccl_id128, int rank, int nranks,
+                              mem_map **out) {
+  if (!out) return fail(MEM_EINVAL, "out is NULL");
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks)
+    return fail(MEM_EINVAL, "rank %d / nranks %d invalid", rank, nranks);
+  if (rows % nranks != 0) return fail(MEM_EINVAL, "rows (%d) must be divisible by nranks (%d)", rows, nranks);
+  mem_map *m = nullptr;
+  mem_status s = mem_create_batch(1, resolution, rows, cols, groups, n_groups, flags, stream, &m);
+  if (s != MEM_OK) return s;
+  m->transport = nccl_id128 ? 1 : 2;
+  m->rank = rank;
+  m->nranks = nranks;
+  m->band_n = rows / nranks * cols;
+  m->band_lo = rank * m->band_n;
+  // record word types for the merge: P, S f64 sums; per group (see GroupDesc::acc0)
+  std::vector<uint8_t> wt(m->n_acc, 0);
+  for (int gi = 0; gi < m->ng; ++gi) {
+    const GroupDesc &g = m->g[gi];
+    if (g.rule == MEM_CLASS_MAX) {
+      wt[g.acc0] = 2;
+    } else if (g.rule == MEM_COLOR) {
+      wt[g.acc0] = wt[g.acc0 + 1] = 1;
+    } else {
+      wt[g.acc0] = 1;  // count, then f64 sums
+    }
+  }
+  const size_t recv_words = (size_t)(nranks - 1) * m->band_n * (1 + m->n_acc);
+  if (cudaMalloc((void **)&m->wtype, wt.size() + 1) != cudaSuccess ||
+      (recv_words && cudaMalloc((void **)&m->recv, recv_words * 8) != cudaSuccess)) {
+    cudaGetLastError();
+    free_map(m);
+    return fail(MEM_ENOMEM, "sharded buffers");
+  }
+  if (cudaMemcpy(m->wtype, wt.data(), wt.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    free_map(m);
+    return fail(MEM_ECUDA, "wtype upload");
+  }
+  if (m->transport == 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id128, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&m->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      free_map(m);
+      return fail(MEM_ECOMM, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = m;
+  return MEM_OK;
+}
+
+mem_status mem_shard_local_sync(mem_map **sh, int G) {
+  if (!sh || G < 1) return fail(MEM_EINVAL, "shards");
+  for (int r = 0; r < G; ++r) {
+    if (!sh[r] || sh[r]->transport != 2 || sh[r]->nranks != G || sh[r]->rank != r)
+      return fail(MEM_EINVAL, "shard %d is not local rank %d of %d", r, r, G);
+    if (sh[r]->stream != sh[0]->stream) return fail(MEM_EINVAL, "local shards must share one stream");
+  }
+  for (int r = 1; r < G; ++r)
+    if (sh[r]->exchange_pending != sh[0]->exchange_pending)
+      return fail(MEM_EINVAL, "shard %d did not take the same inputs as shard 0", r);
+  mem_map *m0 = sh[0];
+  if (set_device(m0)) return MEM_ECUDA;
+  const int R = m0->n_acc, bn = m0->band_n, HW = m0->H * m0->W;
+  const size_t w8 = sizeof(unsigned long long);
+  // exchange: rank r receives band r of every other shard (device copies)
+  for (int r = 0; r < G && m0->exchange_pending; ++r) {
+    int slot = 0;
+    for (int p = 0; p < G; ++p) {
+      if (p == r) continue;
+      unsigned long long *rc = sh[r]->recv + (size_t)slot * bn;
+      unsigned long long *rr = sh[r]->recv + (size_t)(G - 1) * bn + (size_t)slot * bn * R;
+      CU(cudaMemcpyAsync(rc, sh[p]->shard_args.cnt + (size_t)r * bn, w8 * bn, cudaMemcpyDeviceToDevice, m0->stream));
+      CU(cudaMemcpyAsync(rr, sh[p]->shard_args.rec + (size_t)r * bn * R, w8 * (size_t)bn * R, cudaMemcpyDeviceToDevice,
+                         m0->stream));
+      ++slot;
+    }
+  }
+  for (int r = 0; r < G && m0->exchange_pending; ++r) {
+    mem_status s = shard_merge_and_fuse(sh[r], sh[r]->recv, G - 1);
+    if (s != MEM_OK) return s;
+  }
+  for (int r = 0; r < G; ++r) sh[r]->exchange_pending = false;
+  // full replication (after point clouds and images alike): every layer's band r from shard r to all others
+  for (int r = 0; r < G; ++r)
+    for (int p = 0; p < G; ++p) {
+      if (p == r) continue;
+      for (int w = 0; w < m0->n_word; ++w)
+        CU(cudaMemcpyAsync(sh[p]->st.words + (size_t)w * HW + sh[r]->band_lo,
+                           sh[r]->st.words + (size_t)w * HW + sh[r]->band_lo, 4 * (size_t)bn,
+                           cudaMemcpyDeviceToDevice, m0->stream));
+      for (int f = 0; f < m0->n_flag; ++f)
+        CU(cudaMemcpyAsync(sh[p]->st.flags + (size_t)f * HW + sh[r]->band_lo,
+                           sh[r]->st.flags + (size_t)f * HW + sh[r]->band_lo, bn, cudaMemcpyDeviceToDevice,
+                           m0->stream));
+    }
   return MEM_OK;
 }
 

@@ -32,7 +32,8 @@ EXPORTS = ["mem_create", "mem_create_batch", "mem_destroy", "mem_set_stream", "m
            "mem_input_pointcloud", "mem_input_pointcloud_batch", "mem_input_image", "mem_input_image_batch",
            "mem_move_to", "mem_move_to_batch", "mem_get_layer", "mem_set_layer", "mem_get_layer_names",
            "mem_memory_footprint", "mem_get_info", "mem_get_center", "mem_frame_stats", "mem_debug_point_codes",
-           "mem_profile", "mem_profile_read", "mem_pca_readout", "mem_last_error", "mem_version"]
+           "mem_profile", "mem_profile_read", "mem_pca_readout", "mem_nccl_unique_id", "mem_create_sharded",
+           "mem_shard_local_sync", "mem_last_error", "mem_version"]
 STAGES = ["shift", "point", "cell", "image", "read", "write", "h2d", "d2h"]
 
 
@@ -92,6 +93,10 @@ _sig = {
     "mem_debug_point_codes": [_vp, _vp, _vp],
     "mem_profile": [_vp, C.c_int],
     "mem_pca_readout": [_vp, C.c_char_p, C.c_int, _vp],
+    "mem_nccl_unique_id": [_vp],
+    "mem_create_sharded": [C.c_float, C.c_int, C.c_int, _P(mem_layer_spec), C.c_int, C.c_uint, _vp, _vp, C.c_int,
+                           C.c_int, _P(_vp)],
+    "mem_shard_local_sync": [_P(_vp), C.c_int],
     "mem_profile_read": [_vp, _P(C.c_double), _P(C.c_uint64), C.c_int],
 }
 for _n, _a in _sig.items():
@@ -163,6 +168,37 @@ def _stream_ptr(stream):
 
 
 # ---------------------------------------------------------------- C-named functions
+def _specs(groups):
+    names = [g["name"].encode() for g in groups]
+    specs = (mem_layer_spec * max(1, len(groups)))()
+    for i, g in enumerate(groups):
+        rule = RULES[g["rule"]] if isinstance(g["rule"], str) else g["rule"]
+        specs[i] = mem_layer_spec(names[i], rule, g.get("n_channels", 3 if rule == MEM_COLOR else 1),
+                                  g.get("w", 1.0), g.get("sigma_f2", 1.0), g.get("mu0", 0.0),
+                                  g.get("sigma0_2", 1.0), g.get("alpha0", 1.0))
+    return specs, names
+
+
+def mem_nccl_unique_id():
+    buf = C.create_string_buffer(128)
+    _check(_lib.mem_nccl_unique_id(buf), "mem_nccl_unique_id")
+    return buf.raw
+
+
+def mem_create_sharded(resolution, rows, cols, groups, rank, nranks, nccl_id=None, flags=0, stream=None):
+    specs, names = _specs(groups)
+    h = _vp()
+    idb = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    _check(_lib.mem_create_sharded(resolution, rows, cols, specs, len(groups), flags, _stream_ptr(stream), idb, rank,
+                                   nranks, C.byref(h)), "mem_create_sharded")
+    return h.value
+
+
+def mem_shard_local_sync(handles):
+    arr = (_vp * len(handles))(*handles)
+    _check(_lib.mem_shard_local_sync(arr, len(handles)), "mem_shard_local_sync")
+
+
 def mem_create(resolution, rows, cols, groups=(), flags=0, stream=None, n_maps=1):
     names = [g["name"].encode() for g in groups]
     specs = (mem_layer_spec * max(1, len(groups)))()
@@ -317,11 +353,19 @@ def mem_set_stream(h, stream):
 class Map:
     """Owning wrapper of a mem_map handle (one map, or n_maps batched maps)."""
 
-    def __init__(self, resolution, rows, cols, groups=(), n_maps=1, debug_points=False, stream=None):
+    def __init__(self, resolution, rows, cols, groups=(), n_maps=1, debug_points=False, stream=None, _handle=None):
         self.rows, self.cols, self.res, self.n_maps = rows, cols, resolution, n_maps
-        self.h = mem_create(resolution, rows, cols, groups, MEM_FLAG_DEBUG_POINTS if debug_points else 0, stream,
-                            n_maps)
+        self.h = _handle if _handle is not None else mem_create(
+            resolution, rows, cols, groups, MEM_FLAG_DEBUG_POINTS if debug_points else 0, stream, n_maps)
         self._last_n = 0
+
+    @classmethod
+    def sharded(cls, resolution, rows, cols, groups, rank, nranks, nccl_id=None, debug_points=False, stream=None):
+        """rank `rank` of a big map sharded over `nranks` ranks (NCCL when nccl_id is given, else
+        a local shard for single-process emulation; see include/mem.h)."""
+        h = mem_create_sharded(resolution, rows, cols, groups, rank, nranks, nccl_id,
+                               MEM_FLAG_DEBUG_POINTS if debug_points else 0, stream)
+        return cls(resolution, rows, cols, groups, _handle=h)
 
     def close(self):
         if getattr(self, "h", None):
