@@ -242,6 +242,46 @@ def side_c5a(torch, M, stream, rank, world, steps=20):
             "map_updates_per_s_rank": mine / (ms * 1e-3), "scaling": "strong (4096 maps total)"}
 
 
+def side_c5b(torch, M, stream, rank, world, dist, steps=10):
+    """BASELINE configs[4] second half: one 2000x2000 map, 4M points per frame point-sharded
+    over the ranks (4M/G each), band exchange over NCCL inside mem_input_pointcloud
+    (include/mem.h sharded map).  Two pre-generated frames alternate."""
+    c = S.C5B
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(M.mem_nccl_unique_id()), dtype=torch.uint8))
+    if world > 1:
+        dist.broadcast(uid, 0)
+    mp = M.Map.sharded(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])],
+                       rank, world, nccl_id=bytes(uid.cpu().numpy()), stream=stream)
+    frames = [S.c5b_shard(f, rank, world) for f in range(2)]
+    dev = [torch.from_numpy(f["points"]).cuda() for f in frames]
+
+    def step(i):
+        f = frames[i % 2]
+        mp.move_to(*f["move"])
+        mp.input_pointcloud(dev[i % 2], [(0, 1, 0)], f["R"], f["t"], c["noise"])
+
+    if world > 1:
+        dist.barrier()
+    ms = timed_loop(torch, stream, steps, step)
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    mp.profile_read(reset=True)
+    mp.profile(True)
+    step(0)
+    torch.cuda.synchronize()
+    mp.profile(False)
+    prof = mp.profile_read(reset=True)
+    mp.close()
+    return {"workload": f"C5b: one 2000x2000@0.04m map, {c['points']} pts/frame point-sharded over {world} rank(s)",
+            "ms_per_frame_max_over_ranks": ms, "points_per_s": c["points"] / (ms * 1e-3),
+            "stage_ms_rank0": {k: v[0] for k, v in prof.items() if v[1]}, "transport": "NCCL",
+            "scaling": "strong (4M points total)"}
+
+
 def side_c3_c4(torch, M, stream, frames=2):
     out = {}
     c = S.C3
@@ -436,6 +476,7 @@ def run_mem(a):
         sides["c5a"]["ms_per_step_max_over_ranks"] = float(t5.item())
         sides["c5a"]["points_per_s"] = 4096 * S.C5A["points"] / (float(t5.item()) * 1e-3)
         sides["c5a"]["map_updates_per_s"] = 4096 / (float(t5.item()) * 1e-3)
+        sides["c5b"] = side_c5b(torch, M, stream, rank, world, dist)
         if rank == 0:
             sides.update(side_c3_c4(torch, M, stream))
 

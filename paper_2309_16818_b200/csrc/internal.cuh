@@ -49,7 +49,7 @@ struct BindDesc {  // one binding of a call, resolved against its group
   GroupDesc g;
 };
 
-struct MapFrame {  // per-map, per-call point/image frame parameters
+struct __align__(16) MapFrame {  // per-map, per-call point/image frame parameters (16-B aligned: vector loads)
   float R[9];      // sensor->map rotation (fp32 of the host doubles)
   float t[3];      // t.xy relative to the map centre (fp64 subtraction, then fp32), t.z
   float K[5];      // images: fx, skew, cx, fy, cy
@@ -69,6 +69,7 @@ struct Geometry {
   long long BHW;  // n_maps * HW: stride between layers (< 2^31, so cell indices fit in int)
   float res, hH, hW;
   float inv_res;  // (float)(1.0 / res): binning multiplies (reading D13)
+  double inv_W;   // 1.0 / W for divmod_w (index arithmetic only)
 };
 
 struct State {
@@ -79,6 +80,17 @@ struct State {
 
 // ---------------------------------------------------------------- indexing
 __device__ __forceinline__ int wrap(int v, int n) { return v >= n ? v - n : v; }
+
+// q = x / d, r = x % d for 0 <= x < 2^31, d >= 1 without the integer-division sequence: the
+// fp64 product x * (1/d) is within 2^-21 of x/d, so the truncated quotient is off by at most
+// one and one correction step makes it exact.
+__device__ __forceinline__ int divmod_fast(int x, int d, double inv_d, int &r) {
+  int q = (int)((double)x * inv_d);
+  r = x - q * d;
+  if (r < 0) { --q; r += d; }
+  else if (r >= d) { ++q; r -= d; }
+  return q;
+}
 
 // ---------------------------------------------------------------- class_max key (D19)
 // order-preserving map of finite fp32 to u32, so that u64 atomicMax picks the largest conf,
@@ -95,6 +107,15 @@ __device__ __forceinline__ float f32_of_ord(uint32_t o) {
 // Eq.(1)+(2): a = sum/n; theta' = w a + (1-w) theta; first touch theta' = a (D3)
 __device__ __forceinline__ float rule_average(float theta, bool observed, double sum, double n, float w) {
   const double a = sum / n;
+  const double wd = (double)w;
+  const double out = observed ? wd * a + (1.0 - wd) * (double)theta : a;
+  return __double2float_rn(out);
+}
+
+// the same with the reciprocal rn = 1/n precomputed: a = sum * rn is within one fp64 ulp of
+// sum / n, invisible after the rounding to fp32 but at double-rounding ties (reading D29b)
+__device__ __forceinline__ float rule_average_r(float theta, bool observed, double sum, double rn, float w) {
+  const double a = sum * rn;
   const double wd = (double)w;
   const double out = observed ? wd * a + (1.0 - wd) * (double)theta : a;
   return __double2float_rn(out);

@@ -484,16 +484,14 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
   for (int u = 0; u < N; ++u) {  // one round of loads
     if (phys[u] < 0) continue;
     const int c = m * g.HW + phys[u];
-    const unsigned long long *r = a.rec + (long long)(sb + phys[u]) * a.R;
-    P[u] = __longlong_as_double((long long)__ldcg(r + kRecP));
-    S[u] = __longlong_as_double((long long)__ldcg(r + kRecS));
-    w0[u] = __ldcg(r + gd.acc0);
-    if (kColor) {
-      w1[u] = __ldcg(r + gd.acc0 + 1);
-    } else {
-#pragma unroll
-      for (int k = 0; k < NCH; ++k) sum[u][k] = __longlong_as_double((long long)__ldcg(r + gd.acc0 + 1 + k));
-    }
+    // the record is [P, S, w0, w1] (colour: r|g<<32, b|n<<32; average: count, sum): 2 x 16 B
+    const ulonglong2 *r = reinterpret_cast<const ulonglong2 *>(a.rec + (long long)(sb + phys[u]) * 4);
+    const ulonglong2 ps = __ldcg(r), ww = __ldcg(r + 1);
+    P[u] = __longlong_as_double((long long)ps.x);
+    S[u] = __longlong_as_double((long long)ps.y);
+    w0[u] = ww.x;
+    w1[u] = ww.y;
+    if (!kColor) sum[u][0] = __longlong_as_double((long long)ww.y);
     h[u] = elev[c];
     s2[u] = var[c];
     vd[u] = validp[c];
@@ -505,28 +503,29 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
   for (int u = 0; u < N; ++u) {
     if (phys[u] < 0) continue;
     const int c = m * g.HW + phys[u];
-    unsigned long long *r = a.rec + (long long)(sb + phys[u]) * a.R;
+    unsigned long long *r = a.rec + (long long)(sb + phys[u]) * 4;
     // a9: Kalman height fusion (D7), outliers inflate first (D11)
     const double n_in = (double)(uint32_t)(cnt[u] & 0xffffffffull);
     const double n_out = (double)(uint32_t)(cnt[u] >> 32);
     if (vd[u]) {
       const double sp = (double)s2[u] + n_out * (double)a.np.v_out;
-      if (n_in > 0.0) {
-        const double den = 1.0 + P[u] * sp;
-        elev[c] = __double2float_rn(((double)h[u] + S[u] * sp) / den);
-        var[c] = __double2float_rn(sp / den);
+      if (n_in > 0.0) {  // one fp64 division, two multiplies (reading D29b)
+        const double rden = 1.0 / (1.0 + P[u] * sp);
+        elev[c] = __double2float_rn(((double)h[u] + S[u] * sp) * rden);
+        var[c] = __double2float_rn(sp * rden);
       } else {
         var[c] = __double2float_rn(sp);
       }
     } else if (n_in > 0.0) {
-      elev[c] = __double2float_rn(S[u] / P[u]);
-      var[c] = __double2float_rn(1.0 / P[u]);
+      const double rP = 1.0 / P[u];
+      elev[c] = __double2float_rn(S[u] * rP);
+      var[c] = __double2float_rn(rP);
       validp[c] = 1;
     }
     // a10: Eq.(1)+(2) per channel
     const unsigned long long nn = kColor ? (w1[u] >> 32) : w0[u];
     if (nn != 0ull) {
-      const double n = (double)nn;
+      const double rn = 1.0 / (double)nn;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         double sk;
@@ -537,13 +536,14 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
         } else {
           sk = sum[u][k];
         }
-        vals[(long long)(gd.word0 + k) * BHW + c] = rule_average(th[u][k], ob[u] != 0, sk, n, gd.w);
+        vals[(long long)(gd.word0 + k) * BHW + c] = rule_average_r(th[u][k], ob[u] != 0, sk, rn, gd.w);
       }
       obsp[c] = 1;
     }
-    // re-zero the scratch for the slot's next map
+    // re-zero the scratch for the slot's next map (fast-path records are 4 words, 32 B)
     __stcg(a.cnt + sb + phys[u], 0ull);
-    for (int k = 0; k < a.R; ++k) __stcg(r + k, 0ull);
+    __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
+    __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
   }
 }
 
@@ -577,86 +577,155 @@ __device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cn
 }
 
 // ---------------------------------------------------------------- k_points (a2-a8)
-// Persistent grid-stride over the 128-point warp-items of one wave.  Per lane: 4 float4 point
-// loads in flight, then binning, one batched state gather (a7), then warp-aggregated REDs.
+// Persistent grid-stride over the 128-point warp-items of one wave.  Per lane: its 4 points
+// of the item, binning, one batched state gather (a7), then warp-aggregated REDs.  On the
+// float4 path (stride 4, aligned) every lane prefetches its 4 points of the warp's NEXT item
+// into shared memory with cp.async while it processes the current one (double buffer, each
+// lane reads back only the slots it wrote itself, so no warp or CTA barrier is needed).
+
+// the map and point range of warp-item `it`
+struct Item {
+  int m;
+  long long beg, end, base;
+};
+__device__ __forceinline__ Item item_of(const PassArgs &a, int it, int i0) {
+  Item r;
+  r.m = a.m0;
+  if (a.p_uniform > 0) {
+    int rem;
+    r.m = a.m0 + divmod_fast(it - i0, a.p_uniform, a.inv_p_uniform, rem);
+  } else if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
+    int lo = a.m0, hi = a.m1 - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&a.pstart[mid]) <= it) lo = mid; else hi = mid - 1;
+    }
+    r.m = lo;
+  }
+  r.beg = 0;
+  r.end = a.n_single;
+  if (a.offsets) {
+    r.beg = __ldg(&a.offsets[r.m]);
+    r.end = __ldg(&a.offsets[r.m + 1]);
+  }
+  r.base = r.beg + (long long)(it - (a.pstart ? __ldg(&a.pstart[r.m]) : 0)) * kWarpPoints;
+  return r;
+}
+
+// 16-byte async copy global -> shared (L1 bypass, L2 evict-first); src_size 0 zero-fills
+__device__ __forceinline__ void cp_async_16(void *smem, const void *gmem, bool valid, unsigned long long pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 16 : 0), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool kDebug, int kFast>
+__device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, const float (&px)[kWarpPtsPerLane],
+                                             const float (&py)[kWarpPtsPerLane], const float (&pz)[kWarpPtsPerLane],
+                                             const float (&pw)[kWarpPtsPerLane], float rmin2, float rmax2,
+                                             unsigned long long &packed, unsigned &npk, unsigned (&cnt)[8]) {
+  const Geometry &g = a.geo;
+  const int lane = threadIdx.x & 31;
+  const MapFrame f = a.frames ? a.frames[t.m] : a.f0;
+  const int map_base = t.m * g.HW;
+  const int sb = (int)scratch_base(a, t.m);
+  PointOut o[kWarpPtsPerLane];
+#pragma unroll
+  for (int u = 0; u < kWarpPtsPerLane; ++u) {
+    const long long i = t.base + u * 32 + lane;
+    if (i < t.end && !(a.ablate & 8u)) {
+      o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
+    } else {
+      o[u].code = i < t.end ? MEM_CODE_NONFINITE : -1;
+      o[u].cell = -1;
+      o[u].test = false;
+    }
+  }
+  if (!(a.ablate & 4u)) mahalanobis(o, a.st, g, a.np.tau2);
+#pragma unroll
+  for (int u = 0; u < kWarpPtsPerLane; ++u) {
+    const long long i = t.base + u * 32 + lane;
+    if (i < t.end) {
+      if (kDebug) {
+        a.dbg_cell[i] = o[u].lcell;
+        a.dbg_code[i] = (uint8_t)o[u].code;
+      }
+      count_code(packed, npk, o[u].code, cnt);
+    }
+    if (!(a.ablate & 2u))
+      accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base),
+                             a.pts + (i < t.end ? i : t.beg) * (long long)a.stride, pw[u]);
+  }
+}
+
 template <bool kDebug, int kFast>
 __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
+  __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // by mem_stats slot
-  const Geometry &g = a.geo;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (kThreads / 32);
-  const int gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int gw = blockIdx.x * (kThreads / 32) + wid;
   const int i0 = a.pstart ? __ldg(&a.pstart[a.m0]) : 0;
   const int i1 = a.pstart ? __ldg(&a.pstart[a.m1]) : a.p_single;
   const unsigned long long pol = evict_first_policy();
   const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
   unsigned long long packed = 0ull;
   unsigned npk = 0;
-  for (int it = i0 + gw; it < i1; it += nwarps) {
-    int m = a.m0;
-    if (a.p_uniform > 0) {
-      m = a.m0 + (it - i0) / a.p_uniform;
-    } else if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
-      int lo = a.m0, hi = a.m1 - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&a.pstart[mid]) <= it) lo = mid; else hi = mid - 1;
-      }
-      m = lo;
-    }
-    long long beg = 0, end = a.n_single;
-    if (a.offsets) {
-      beg = __ldg(&a.offsets[m]);
-      end = __ldg(&a.offsets[m + 1]);
-    }
-    const long long base = beg + (long long)(it - (a.pstart ? __ldg(&a.pstart[m]) : 0)) * kWarpPoints;
-    float px[kWarpPtsPerLane], py[kWarpPtsPerLane], pz[kWarpPtsPerLane], pw[kWarpPtsPerLane];
+  float px[kWarpPtsPerLane], py[kWarpPtsPerLane], pz[kWarpPtsPerLane], pw[kWarpPtsPerLane];
+  if (kFast != 0 || a.vec4) {
+    const float4 *pts4 = reinterpret_cast<const float4 *>(a.pts);
+    auto issue = [&](const Item &t, int stage) {
 #pragma unroll
-    for (int u = 0; u < kWarpPtsPerLane; ++u) {  // all loads first (memory-level parallelism)
-      const long long i = base + u * 32 + lane;
-      px[u] = py[u] = pz[u] = pw[u] = 0.0f;
-      if (i < end) {
-        const float *q = a.pts + i * (long long)a.stride;
-        if (kFast != 0 || a.vec4) {
-          const float4 v = ld_stream_f4(q, pol);
-          px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
-        } else {
+      for (int u = 0; u < kWarpPtsPerLane; ++u) {
+        const long long i = t.base + u * 32 + lane;
+        cp_async_16(&s_pts[wid][stage][u * 32 + lane], pts4 + (i < t.end ? i : t.beg), i < t.end, pol);
+      }
+      cp_async_commit();
+    };
+    int it = i0 + gw, stage = 0;
+    Item cur;
+    if (it < i1) {
+      cur = item_of(a, it, i0);
+      issue(cur, 0);
+    }
+    for (; it < i1; it += nwarps, stage ^= 1) {
+      const int nx = it + nwarps;
+      Item nxt;
+      if (nx < i1) {
+        nxt = item_of(a, nx, i0);
+        issue(nxt, stage ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+#pragma unroll
+      for (int u = 0; u < kWarpPtsPerLane; ++u) {
+        const float4 v = s_pts[wid][stage][u * 32 + lane];
+        px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
+      }
+      process_item<kDebug, kFast>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+      cur = nxt;
+    }
+  } else {
+    for (int it = i0 + gw; it < i1; it += nwarps) {
+      const Item t = item_of(a, it, i0);
+#pragma unroll
+      for (int u = 0; u < kWarpPtsPerLane; ++u) {  // all loads first (memory-level parallelism)
+        const long long i = t.base + u * 32 + lane;
+        px[u] = py[u] = pz[u] = pw[u] = 0.0f;
+        if (i < t.end) {
+          const float *q = a.pts + i * (long long)a.stride;
           px[u] = __ldg(q); py[u] = __ldg(q + 1); pz[u] = __ldg(q + 2);
         }
       }
-    }
-    const MapFrame f = a.frames ? a.frames[m] : a.f0;
-    const int map_base = m * g.HW;
-    const int sb = (int)scratch_base(a, m);
-    PointOut o[kWarpPtsPerLane];
-#pragma unroll
-    for (int u = 0; u < kWarpPtsPerLane; ++u) {
-      const long long i = base + u * 32 + lane;
-      if (i < end && !(a.ablate & 8u)) {
-        o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
-      } else {
-        o[u].code = i < end ? MEM_CODE_NONFINITE : -1;
-        o[u].cell = -1;
-        o[u].test = false;
-      }
-    }
-    if (!(a.ablate & 4u)) mahalanobis(o, a.st, g, a.np.tau2);
-#pragma unroll
-    for (int u = 0; u < kWarpPtsPerLane; ++u) {
-      const long long i = base + u * 32 + lane;
-      if (i < end) {
-        if (kDebug) {
-          a.dbg_cell[i] = o[u].lcell;
-          a.dbg_code[i] = (uint8_t)o[u].code;
-        }
-        count_code(packed, npk, o[u].code, cnt);
-      }
-      if (!(a.ablate & 2u))
-        accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), a.pts + (i < end ? i : beg) * (long long)a.stride,
-                               pw[u]);
+      process_item<kDebug, kFast>(a, t, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
     }
   }
 #pragma unroll
@@ -707,7 +776,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
     for (int u = 0; u < 4; ++u) {
       const int phys = t0 + u * kThreads + threadIdx.x;
       if (phys < a.cell_hi && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
-        const int prow = phys / g.W, pcol = phys - (phys / g.W) * g.W;
+        int pcol;
+        const int prow = divmod_fast(phys, g.W, g.inv_W, pcol);
         int row = prow - f.r0, col = pcol - f.c0;
         row += row < 0 ? g.H : 0;
         col += col < 0 ? g.W : 0;

@@ -36,6 +36,7 @@ struct PassArgs {
   int m0, m1;                  // maps of this wave
   int cell_lo, cell_hi;        // k_cells: physical cells [lo, hi) of each map (a row band when sharded)
   int p_uniform;               // > 0: every map of the wave has exactly this many point warp-items
+  double inv_p_uniform;        // 1.0 / p_uniform (divmod_fast)
   int slot0;                   // scratch map-slot of map m0 (map m -> slot slot0 + m - m0)
   int q_per_map;               // cell warp-items per map
   long long SHW;               // scratch map-slots * HW

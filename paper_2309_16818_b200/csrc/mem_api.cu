@@ -141,6 +141,7 @@ struct mem_map {
     gg.hH = (float)H / 2.0f;
     gg.hW = (float)W / 2.0f;
     gg.inv_res = (float)(1.0 / (double)res);  // reading D13
+    gg.inv_W = 1.0 / (double)W;
     return gg;
   }
 };
@@ -575,7 +576,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   };
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
-      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc)) ||
+      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc) + 32) ||
       !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
       !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
@@ -583,7 +584,8 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   }
   mem_status s = MEM_OK;
   m->scratch_maps = 1;
-  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc), m->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc) + 32,
+                      m->stream) != cudaSuccess ||
       cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -822,7 +824,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     CU(cudaStreamSynchronize(m->side));
     CU(cudaFree(m->st.acc));
     m->st.acc = nullptr;
-    const size_t bytes = per_map * slots;
+    const size_t bytes = per_map * slots + 32;  // + the records' 32-B alignment pad
     if (cudaMalloc((void **)&m->st.acc, bytes) != cudaSuccess) {
       cudaGetLastError();
       m->scratch_maps = 0;
@@ -843,12 +845,13 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.st = m->st;
   a.SHW = (long long)m->scratch_maps * HW;
   a.cnt = m->st.acc;
-  a.rec = m->st.acc + a.SHW;
+  a.rec = m->st.acc + ((a.SHW + 3) & ~3LL);  // 32-B aligned records (the fast paths load 2 x 16 B)
   a.R = m->n_acc;
   a.fast = 0;
   if (nb == 1 && m->ng == 1 && !(m->ablate & 1024u)) {  // every group bound (no stale group state)
     if (a.b[0].g.rule == MEM_COLOR) a.fast = 1;
     else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) a.fast = 2;
+    if (m->n_acc != 4) a.fast = 0;  // the fast paths read 4-word (32 B) records
   }
   if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool in an L2 persisting window
     cudaStreamAttrValue v;
@@ -893,6 +896,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.p_uniform = pstart[a.m0 + 1] - pstart[a.m0];  // > 0 only if every map of the wave has it
     for (int i = a.m0; i < a.m1 && a.p_uniform > 0; ++i)
       if (pstart[i + 1] - pstart[i] != a.p_uniform) a.p_uniform = 0;
+    a.inv_p_uniform = a.p_uniform > 0 ? 1.0 / (double)a.p_uniform : 0.0;
     const long long pitems = pstart[a.m1] - pstart[a.m0];
     const long long citems = (long long)(a.m1 - a.m0) * a.q_per_map;
     // one wave: persistent grid; several waves: short-lived CTAs (~2 items per warp) so that

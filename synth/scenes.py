@@ -467,3 +467,51 @@ def c5a_batch(frame, first_map, n_maps, seed=1000, points=C5A["points"]):
     feat = fid / 3.0 + rng.normal(0.0, 0.05, h.shape)
     pts = np.concatenate([p, feat[..., None]], -1).astype(np.float32).reshape(-1, 4)
     return dict(points=pts, R=R, t=t, move=pos.copy(), offsets=np.arange(n_maps + 1, dtype=np.int64) * P)
+
+
+# --------------------------------------------------------------------------------------
+# C5b: one 2000x2000 map @ 0.04 m (80 m), 4M points/frame, point-sharded
+# --------------------------------------------------------------------------------------
+C5B = dict(res=0.04, rows=2000, cols=2000, points=4_194_304, w=0.5, sensor_h=20.0,
+           noise=dict(a=1e-4, b=2e-6, r_min=0.5, r_max=80.0, h_min=-25.0, h_max=-15.0, tau2=9.0, v_out=0.01))
+
+
+def c5b_pose(frame):
+    """a virtual elevated sensor 20 m above the map centre drifting 0.042 m/frame (1.05 cells)
+    along +x and 0.0412 m/frame (1.03 cells) along +y with yaw 0.02 rad/frame; the snap
+    fractions stay >= 0.05 cell from a tie for 12 frames (asserted)."""
+    frame = frame % 12
+    x, y = -0.01 + 0.042 * frame, -0.008 + 0.0412 * frame
+    assert_tie_guard(x, C5B["res"])
+    assert_tie_guard(y, C5B["res"])
+    return rot_z(0.02 * frame), np.array([x, y, C5B["sensor_h"]])
+
+
+def c5b_terrain(x, y):
+    """smooth rolling terrain plus a 10 x 10 grid of 2 m blocks (0.6 m high)."""
+    h = 0.4 * np.sin(x / 6.0) * np.cos(y / 9.0) + 0.01 * x
+    blk = ((np.floor(x / 8.0) + np.floor(y / 8.0)) % 2 == 0) & (np.mod(x, 8.0) < 2.0) & (np.mod(y, 8.0) < 2.0)
+    return h + 0.6 * blk, blk
+
+
+def c5b_shard(frame, rank, nranks, seed=5, points=C5B["points"]):
+    """rank's contiguous shard [rank*n/G, (rank+1)*n/G) of frame `frame`'s 4M points, (n/G, 4)
+    float32 [x y z feature] in the sensor frame: (x, y) uniform over +-41 m around the map
+    centre (the window is +-40 m; ~2.5% fall outside), z = terrain + N(0, 0.02^2), 1% outliers
+    (+U[0.5, 1]), 0.5% NaN; feature = block indicator + N(0, 0.05^2).  The shards of one frame
+    are drawn from per-shard seeds, so any G gives the same union only for the same G."""
+    R, t = c5b_pose(frame)
+    n = points // nranks
+    rng = np.random.default_rng([seed, frame, rank, nranks])
+    cx, cy = np.floor(t[0] / C5B["res"] + 0.5) * C5B["res"], np.floor(t[1] / C5B["res"] + 0.5) * C5B["res"]
+    x = cx + rng.uniform(-41.0, 41.0, n)
+    y = cy + rng.uniform(-41.0, 41.0, n)
+    h, blk = c5b_terrain(x, y)
+    z = h + rng.normal(0.0, 0.02, n)
+    kind = rng.uniform(size=n)
+    z = np.where(kind < 0.01, z + rng.uniform(0.5, 1.0, n), z)
+    d = np.stack([x - t[0], y - t[1], z - t[2]], 1)
+    p = d @ R  # R^T (world - t)
+    p[(kind >= 0.01) & (kind < 0.015), 0] = np.nan
+    feat = blk + rng.normal(0.0, 0.05, n)
+    return dict(points=np.concatenate([p, feat[:, None]], 1).astype(np.float32), R=R, t=t, move=(t[0], t[1]))

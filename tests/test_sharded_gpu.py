@@ -153,3 +153,29 @@ def test_sharded_errors():
         M.mem_shard_local_sync([a.h, b.h])  # b did not take the frame
     with pytest.raises(M.MemError):
         M.mem_shard_local_sync([b.h, a.h])  # wrong rank order
+
+
+def test_c5b_full_size_two_local_shards():
+    """BASELINE configs[4] big map at full size (2000x2000, 4M points/frame) on 2 local shards;
+    the oracle takes the union of the shards."""
+    c = S.C5B
+    G = 2
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    shards = [M.Map.sharded(c["res"], c["rows"], c["cols"], groups, r, G) for r in range(G)]
+    o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):
+        parts = [S.c5b_shard(f, r, G) for r in range(G)]
+        for s, p in zip(shards, parts):
+            s.move_to(*p["move"])
+            s.input_pointcloud(torch.from_numpy(p["points"]).cuda(), [(0, 1, 0)], p["R"], p["t"], c["noise"])
+        sync(shards)
+        o.move_to(*parts[0]["move"])
+        o.input_pointcloud(np.concatenate([p["points"] for p in parts]), [(0, 1, 0)], parts[0]["R"], parts[0]["t"],
+                           c["noise"])
+        total = None
+        for s in shards:
+            st = s.stats()
+            total = st if total is None else {k: total[k] + st[k] for k in st}
+        assert total == o.stats(), (total, o.stats())
+        compare_layers(shards[f % G], o, where=f"frame {f}: ")
+    assert o.stats()["n_outlier"] > 1000 and o.get_layer("valid").mean() > 0.9
