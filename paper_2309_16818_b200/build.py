@@ -49,7 +49,8 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *sources(), *LIBS]
+    extra = os.environ.get("MEM_NVCC_EXTRA", "").split()  # tuning experiments only (e.g. -DMEM_POINTS_MINB=4)
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", LIB + ".tmp", *sources(), *LIBS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

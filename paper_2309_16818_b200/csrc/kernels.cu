@@ -18,6 +18,13 @@
 
 #include "kernels.cuh"
 
+#ifndef MEM_POINTS_MINB
+#define MEM_POINTS_MINB 3  // resident CTAs per SM the register allocation of k_points targets
+#endif
+#ifndef MEM_CELLS_MINB
+#define MEM_CELLS_MINB 3
+#endif
+
 namespace memk {
 
 // ---------------------------------------------------------------- memory helpers
@@ -547,6 +554,49 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
   }
 }
 
+// a8, bucketed fast path: one 16-B record per in-window point, appended to the bucket of its
+// (map-slot, band): {local cell | outlier << 31, 1/v (fp32, 0 for outliers), z * (1/v) (fp32),
+// the channel word}.  These are exactly the fp32 terms the oracle sums in fp64,
+// so k_accum's sums equal the RED path's.  Lanes of the same bucket reserve their slots with one
+// atomicAdd (match_any).  A bucket that is full sends the point to the scratch with REDs instead
+// (accumulate_warp); k_accum merges the scratch of such a band.  All 32 lanes must call this.
+template <int kFast>
+__device__ __forceinline__ void bucket_warp(const PassArgs &a, const PointOut &o, int phys, int slot, int sc,
+                                            const float *p, float ch0) {
+  const bool act = o.cell >= 0;
+  if (!__any_sync(0xffffffffu, act)) return;
+  const int lane = threadIdx.x & 31;
+  int band = 0, local = 0;
+  if (act) band = divmod_fast(phys, a.band_cells, a.inv_band, local);
+  const int key = act ? slot * a.nbands + band : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int leader = __ffs(peers) - 1;
+  unsigned base = 0u;
+  if (act && lane == leader) base = atomicAdd(&a.bcnt[key], (unsigned)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  const unsigned pos = base + (unsigned)__popc(peers & lanemask_lt());
+  const bool spill = act && pos >= a.bcap;
+  if (act && !spill) {
+    const bool inl = o.code == MEM_CODE_INLIER;
+    float wf = 0.0f, zw = 0.0f;
+    if (inl) {
+      wf = 1.0f / o.v;
+      zw = o.z * wf;
+    }
+    uint4 r;
+    r.x = (unsigned)local | (inl ? 0u : 0x80000000u);
+    r.y = __float_as_uint(wf);
+    r.z = __float_as_uint(zw);
+    r.w = __float_as_uint(ch0);
+    __stcg(a.recs + (long long)key * a.bcap + pos, r);
+  }
+  if (__any_sync(0xffffffffu, spill)) {
+    PointOut q = o;
+    if (!spill) q.cell = -1;
+    accumulate_warp<kFast>(a, q, sc, p, ch0);
+  }
+}
+
 // scratch cell base of map m of this wave: its map-slot in the wave's half of the pool
 __device__ __forceinline__ long long scratch_base(const PassArgs &a, int m) {
   return (long long)(a.slot0 + m - a.m0) * a.geo.HW;
@@ -623,7 +673,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool kDebug, int kFast>
+template <bool kDebug, int kFast, bool kBucket>
 __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, const float (&px)[kWarpPtsPerLane],
                                              const float (&py)[kWarpPtsPerLane], const float (&pz)[kWarpPtsPerLane],
                                              const float (&pw)[kWarpPtsPerLane], float rmin2, float rmax2,
@@ -656,14 +706,18 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
       }
       count_code(packed, npk, o[u].code, cnt);
     }
-    if (!(a.ablate & 2u))
-      accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base),
-                             a.pts + (i < t.end ? i : t.beg) * (long long)a.stride, pw[u]);
+    if (a.ablate & 2u) continue;
+    const float *pp = a.pts + (i < t.end ? i : t.beg) * (long long)a.stride;
+    if constexpr (kBucket)
+      bucket_warp<kFast>(a, o[u], o[u].cell - map_base, a.slot0 + t.m - a.m0, sb + (o[u].cell - map_base), pp,
+                         pw[u]);
+    else
+      accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), pp, pw[u]);
   }
 }
 
-template <bool kDebug, int kFast>
-__global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ PassArgs a) {
+template <bool kDebug, int kFast, bool kBucket>
+__global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
@@ -710,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
         const float4 v = s_pts[wid][stage][u * 32 + lane];
         px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
       }
-      process_item<kDebug, kFast>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+      process_item<kDebug, kFast, kBucket>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
       cur = nxt;
     }
   } else {
@@ -725,7 +779,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
           px[u] = __ldg(q); py[u] = __ldg(q + 1); pz[u] = __ldg(q + 2);
         }
       }
-      process_item<kDebug, kFast>(a, t, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+      process_item<kDebug, kFast, kBucket>(a, t, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
     }
   }
 #pragma unroll
@@ -738,43 +792,47 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
 // (coalesced), applies the pending strip reset and compacts the touched cells into shared
 // memory; phase 2 fuses the touched cells densely (2 per lane in flight), so no lane idles on
 // untouched cells.
-constexpr int kCellTile = kThreads * 4;
+constexpr int kChunkPerLane = 4;                 // cells per lane per chunk
+constexpr int kChunk = 32 * kChunkPerLane;        // 128-cell chunk per warp
 
+// Warp-persistent grid-stride over 128-cell chunks of the wave's maps (newest map first: its
+// scratch was touched last by k_points and is still in L2).  Each warp, independently of the
+// others (no CTA barrier): 4 count loads per lane in flight, the pending shift strips reset,
+// its touched cells compacted in its own shared-memory slice, then fused 2 per lane per round.
 template <int kFast>
-__global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ PassArgs a) {
-  __shared__ int s_phys[kCellTile];
-  __shared__ unsigned long long s_cntv[kCellTile];
-  __shared__ int s_n;
+__global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid_constant__ PassArgs a) {
+  __shared__ int s_phys[kThreads / 32][kChunk];
+  __shared__ unsigned long long s_cntv[kThreads / 32][kChunk];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const Geometry &g = a.geo;
-  const int lane = threadIdx.x & 31;
-  const int tpm = (a.cell_hi - a.cell_lo + kCellTile - 1) / kCellTile;  // tiles per map (band)
-  const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * tpm;
-  const unsigned long long *accN = a.cnt;
-  for (int rt = blockIdx.x; rt < total; rt += gridDim.x) {
-    // newest-first: k_points walked the maps in order, so the last maps' scratch is the most
-    // recently touched (L2-resident); the next k_points starts with the lines zeroed last here
-    const int tile = (a.ablate & 32u) ? rt : total - 1 - rt;
-    const int m = a.m0 + tile / tpm;
-    const int t0 = a.cell_lo + (tile - (tile / tpm) * tpm) * kCellTile;
-    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = gridDim.x * (kThreads / 32);
+  const int gw = blockIdx.x * (kThreads / 32) + wid;
+  const int cpm = (a.cell_hi - a.cell_lo + kChunk - 1) / kChunk;  // chunks per map (band)
+  const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * cpm;
+  int *sp = s_phys[wid];
+  unsigned long long *sc = s_cntv[wid];
+  for (int rt = gw; rt < total; rt += nwarps) {
+    const int chunk = (a.ablate & 32u) ? rt : total - 1 - rt;
+    const int mi = chunk / cpm;
+    const int m = a.m0 + mi;
+    const int t0 = a.cell_lo + (chunk - mi * cpm) * kChunk;
     const int sb = (int)scratch_base(a, m);
-    if (threadIdx.x == 0) {
-      s_n = 0;
-      if (t0 == a.cell_lo) a.ring[m] = make_int2(f.r0, f.c0);
-    }
-    __syncthreads();
-    unsigned long long cv[4];
+    unsigned long long cv[kChunkPerLane];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // counts first (memory-level parallelism)
-      const int phys = t0 + u * kThreads + threadIdx.x;
-      cv[u] = phys < a.cell_hi ? __ldcg(accN + sb + phys) : 0ull;
+    for (int u = 0; u < kChunkPerLane; ++u) {  // counts first (memory-level parallelism)
+      const int phys = t0 + u * 32 + lane;
+      cv[u] = phys < a.cell_hi ? __ldcg(a.cnt + sb + phys) : 0ull;
     }
+    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    if (t0 == a.cell_lo && lane == 0) a.ring[m] = make_int2(f.r0, f.c0);
+    int n = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int phys = t0 + u * kThreads + threadIdx.x;
+    for (int u = 0; u < kChunkPerLane; ++u) {
+      const int phys = t0 + u * 32 + lane;
       if (phys < a.cell_hi && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
         int pcol;
         const int prow = divmod_fast(phys, g.W, g.inv_W, pcol);
@@ -785,26 +843,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
       }
       const bool t = cv[u] != 0ull;  // untouched cells stay bit-identical
       const unsigned b = __ballot_sync(0xffffffffu, t);
-      int base = 0;
-      if (lane == 0 && b) base = atomicAdd(&s_n, __popc(b));
-      base = __shfl_sync(0xffffffffu, base, 0);
       if (t) {
-        const int k = base + __popc(b & lanemask_lt());
-        s_phys[k] = phys;
-        s_cntv[k] = cv[u];
+        const int k = n + __popc(b & lanemask_lt());
+        sp[k] = phys;
+        sc[k] = cv[u];
       }
+      n += __popc(b);
     }
-    __syncthreads();
-    const int n = s_n;
-    cnt[7] += threadIdx.x == 0 ? (unsigned)n : 0u;
-    for (int k0 = 0; k0 < ((a.ablate & 512u) ? 0 : n); k0 += 2 * kThreads) {
+    __syncwarp();
+    cnt[7] += lane == 0 ? (unsigned)n : 0u;
+    for (int k0 = 0; k0 < ((a.ablate & 512u) ? 0 : n); k0 += 64) {
       int ph[2];
       unsigned long long cc[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int k = k0 + u * kThreads + threadIdx.x;
-        ph[u] = k < n ? s_phys[k] : -1;
-        cc[u] = k < n ? s_cntv[k] : 0ull;
+        const int k = k0 + u * 32 + lane;
+        ph[u] = k < n ? sp[k] : -1;
+        cc[u] = k < n ? sc[k] : 0ull;
       }
       if (kFast == 1)
         fuse_cells_avg<2, 3, true>(a, m, sb, ph, cc);
@@ -813,9 +868,273 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
       else
         fuse_cells<2>(a, m, sb, ph, cc);
     }
-    __syncthreads();  // s_phys / s_n are rewritten by the next tile
+    __syncwarp();  // this warp's slice is rewritten by its next chunk
   }
   __syncthreads();
+  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
+}
+
+// ---------------------------------------------------------------- k_accum (a8 end, a9-a10, lazy a13)
+// Bucketed fast path.  Grid-stride over the (map, band) units of the wave (band = 1024 cells,
+// 4 per thread).  Per unit: each thread issues the loads of its 4 cells' state (one round trip,
+// kept in registers); the band's records (<= kSortCap, the bucket capacity) are counting-sorted
+// by cell in shared memory (one native shared atomic per record for the histogram, one for the
+// scatter); then each thread sums its cells' records in registers (fp64, no atomics), merges the
+// scratch of a spilled band, resets its cells in a scrolled-in strip, fuses its touched cells
+// and stores the cells it changed.  The band's state is contiguous: loads and stores coalesce.
+constexpr int kAccumPerThread = 4;
+constexpr int kBand = kThreads * kAccumPerThread;  // 1024 cells
+constexpr int kSortCap = 4096;                     // records sorted per unit (= max bucket capacity)
+
+size_t accum_smem_bytes(int) { return (size_t)kSortCap * sizeof(uint4); }
+int accum_sort_cap() { return kSortCap; }
+
+// exclusive prefix sum of cnt[0, kBand) in place (256 threads, 4 consecutive cells each);
+// beg[c] receives the same offsets; returns the total
+__device__ __forceinline__ unsigned band_scan(unsigned *cnt, unsigned *beg, unsigned *wsum) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c0 = threadIdx.x * kAccumPerThread;
+  unsigned v[kAccumPerThread], t = 0;
+#pragma unroll
+  for (int j = 0; j < kAccumPerThread; ++j) {
+    v[j] = t;
+    t += cnt[c0 + j];
+  }
+  unsigned x = t;  // inclusive warp scan of the thread totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  unsigned wbase = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    const unsigned ws = wsum[w];
+    wbase += w < wid ? ws : 0u;
+    total += ws;
+  }
+  const unsigned base = wbase + x - t;
+#pragma unroll
+  for (int j = 0; j < kAccumPerThread; ++j) {
+    cnt[c0 + j] = base + v[j];
+    beg[c0 + j] = base + v[j];
+  }
+  return total;
+}
+
+template <int kFast>
+__global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ PassArgs a) {
+  constexpr int NCH = kFast == 1 ? 3 : 1;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint4 *s_rec = reinterpret_cast<uint4 *>(s_dyn);  // [kSortCap] records sorted by cell
+  __shared__ unsigned s_cur[kBand];                  // counts -> scatter cursors
+  __shared__ unsigned s_beg[kBand + 1];              // first sorted record of each cell
+  __shared__ unsigned s_wsum[kThreads / 32];
+  __shared__ unsigned s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const Geometry &g = a.geo;
+  const long long BHW = g.BHW;
+  const GroupDesc &gd = a.b[0].g;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
+  uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
+  uint8_t *obsp = a.st.flags + (long long)gd.flag * BHW;
+  const int units = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * a.nbands;
+  auto key_of = [&](int un) {
+    const int mi = un / a.nbands;
+    return (a.slot0 + mi) * a.nbands + (un - mi * a.nbands);
+  };
+  unsigned ntot_next = blockIdx.x < units ? __ldcg(a.bcnt + key_of(blockIdx.x)) : 0u;
+  for (int un = blockIdx.x; un < units; un += gridDim.x) {
+    const int mi = un / a.nbands, band = un - mi * a.nbands;
+    const int m = a.m0 + mi;
+    const int key = (a.slot0 + mi) * a.nbands + band;
+    const int lo = band * kBand;
+    const int ncell = min(kBand, g.HW - lo);
+    const long long cbase = (long long)m * g.HW + lo;
+    const unsigned ntot = ntot_next;
+    const unsigned nrec = min(ntot, a.bcap);  // bcap <= kSortCap (host)
+    const uint4 *rp = a.recs + (long long)key * a.bcap;
+    // (1) the frame, the next unit's record count; clear the histogram
+#pragma unroll
+    for (int u = 0; u < kAccumPerThread; ++u) s_cur[u * kThreads + threadIdx.x] = 0u;
+    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    ntot_next = un + (int)gridDim.x < units ? __ldcg(a.bcnt + key_of(un + gridDim.x)) : 0u;
+    __syncthreads();
+    // (2) histogram of the records' cells
+    for (unsigned r0 = threadIdx.x; r0 < nrec; r0 += 4 * kThreads) {
+      unsigned kx[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned r = r0 + u * kThreads;
+        kx[u] = r < nrec ? __ldcg(reinterpret_cast<const unsigned *>(rp + r)) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (kx[u] != 0xffffffffu) atomicAdd(&s_cur[kx[u] & 0x7fffffffu], 1u);
+    }
+    __syncthreads();
+    // (3) offsets, then the scatter into cell order
+    band_scan(s_cur, s_beg, s_wsum);
+    if (threadIdx.x == 0) s_beg[kBand] = nrec;
+    __syncthreads();
+    for (unsigned r0 = threadIdx.x; r0 < nrec; r0 += 4 * kThreads) {
+      uint4 rr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned r = r0 + u * kThreads;
+        if (r < nrec) rr[u] = __ldcg(rp + r);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r0 + u * kThreads < nrec) s_rec[atomicAdd(&s_cur[rr[u].x & 0x7fffffffu], 1u)] = rr[u];
+    }
+    if (threadIdx.x == 0) {
+      a.bcnt[key] = 0u;  // ready for the next frame
+      if (band == 0) a.ring[m] = make_int2(f.r0, f.c0);
+    }
+    __syncthreads();
+    // (4) per cell: sum the sorted records (+ the scratch of a spilled band); then, two cells
+    // at a time, one round of state loads for the cells that change (touched or scrolled in),
+    // strip reset, fusion, stores
+    const bool shift = f.sr != 0 || f.sc != 0;
+    const bool spilled = ntot > a.bcap;
+    const int sb = spilled ? (int)scratch_base(a, m) : 0;
+#pragma unroll
+    for (int u0 = 0; u0 < kAccumPerThread; u0 += 2) {
+      unsigned nin[2], nout[2], c0[2], c1[2], c2[2];
+      double P[2], S[2], X[2];
+      bool strip[2], dirty[2];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int c = (u0 + v) * kThreads + threadIdx.x;
+        nin[v] = nout[v] = c0[v] = c1[v] = c2[v] = 0u;
+        P[v] = S[v] = X[v] = 0.0;
+        strip[v] = dirty[v] = false;
+        if (c >= ncell) continue;
+        const unsigned e = s_beg[c + 1];
+        for (unsigned r = s_beg[c]; r < e; ++r) {
+          const uint4 q = s_rec[r];
+          if (q.x >> 31) {
+            ++nout[v];
+          } else {
+            ++nin[v];
+            P[v] += (double)__uint_as_float(q.y);
+            S[v] += (double)__uint_as_float(q.z);
+          }
+          if (kFast == 1) {  // D20: 0x00RRGGBB, exact integer sums
+            c0[v] += (q.w >> 16) & 255u;
+            c1[v] += (q.w >> 8) & 255u;
+            c2[v] += q.w & 255u;
+          } else {  // D31: a non-finite channel skips the group
+            const float x = __uint_as_float(q.w);
+            if (isfinite(x)) {
+              ++c0[v];
+              X[v] += (double)x;
+            }
+          }
+        }
+        if (spilled) {  // merge (and re-zero) the scratch of this cell
+          const unsigned long long cv = __ldcg(a.cnt + sb + lo + c);
+          if (cv != 0ull) {
+            ulonglong2 *rq = reinterpret_cast<ulonglong2 *>(a.rec + (long long)(sb + lo + c) * 4);
+            const ulonglong2 ps = __ldcg(rq), ww = __ldcg(rq + 1);
+            nin[v] += (unsigned)(cv & 0xffffffffull);
+            nout[v] += (unsigned)(cv >> 32);
+            P[v] += __longlong_as_double((long long)ps.x);
+            S[v] += __longlong_as_double((long long)ps.y);
+            if (kFast == 1) {
+              c0[v] += (unsigned)(ww.x & 0xffffffffull);
+              c1[v] += (unsigned)(ww.x >> 32);
+              c2[v] += (unsigned)(ww.y & 0xffffffffull);
+            } else {
+              c0[v] += (unsigned)ww.x;
+              X[v] += __longlong_as_double((long long)ww.y);
+            }
+            __stcg(a.cnt + sb + lo + c, 0ull);
+            __stcg(rq, make_ulonglong2(0ull, 0ull));
+            __stcg(rq + 1, make_ulonglong2(0ull, 0ull));
+          }
+        }
+        if (shift) {  // lazy ring shift: the scrolled-in cells start from the reset state (a13)
+          int pcol;
+          const int prow = divmod_fast(lo + c, g.W, g.inv_W, pcol);
+          int row = prow - f.r0, col = pcol - f.c0;
+          row += row < 0 ? g.H : 0;
+          col += col < 0 ? g.W : 0;
+          strip[v] = in_strip(row, col, f, g);
+        }
+        // untouched cells outside the strips stay bit-identical
+        dirty[v] = strip[v] || (nin[v] + nout[v] != 0u && !(a.ablate & 512u));
+      }
+      float h[2], s2[2], th[2][NCH];
+      uint8_t vd[2], ob[2];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {  // one round of loads
+        const long long cc = cbase + (u0 + v) * kThreads + threadIdx.x;
+        if (!dirty[v] || strip[v]) continue;
+        h[v] = elev[cc];
+        s2[v] = var[cc];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) th[v][k] = vals[(long long)(gd.word0 + k) * BHW + cc];
+        vd[v] = validp[cc];
+        ob[v] = obsp[cc];
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        if (!dirty[v]) continue;
+        const long long cc = cbase + (u0 + v) * kThreads + threadIdx.x;
+        if (strip[v]) {
+          h[v] = s2[v] = __int_as_float(0x7fc00000);
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) th[v][k] = 0.0f;
+          vd[v] = ob[v] = 0;
+        }
+        if (nin[v] + nout[v] != 0u && !(a.ablate & 512u)) {
+          ++cnt[7];
+          // a9: Kalman height fusion (D7), outliers inflate first (D11); reciprocals (D29b)
+          if (vd[v]) {
+            const double sp = (double)s2[v] + (double)nout[v] * (double)a.np.v_out;
+            if (nin[v] > 0u) {
+              const double rden = 1.0 / (1.0 + P[v] * sp);
+              h[v] = __double2float_rn(((double)h[v] + S[v] * sp) * rden);
+              s2[v] = __double2float_rn(sp * rden);
+            } else {
+              s2[v] = __double2float_rn(sp);
+            }
+          } else if (nin[v] > 0u) {
+            const double rP = 1.0 / P[v];
+            h[v] = __double2float_rn(S[v] * rP);
+            s2[v] = __double2float_rn(rP);
+            vd[v] = 1;
+          }
+          // a10: Eq.(1)+(2); colour n = every filtered in-bounds point (D20), average n = finite (D31)
+          const unsigned nn = kFast == 1 ? nin[v] + nout[v] : c0[v];
+          if (nn != 0u) {
+            const double rn = 1.0 / (double)nn;
+            if (kFast == 1) {
+              th[v][0] = rule_average_r(th[v][0], ob[v] != 0, (double)c0[v], rn, gd.w);
+              th[v][1 % NCH] = rule_average_r(th[v][1 % NCH], ob[v] != 0, (double)c1[v], rn, gd.w);
+              th[v][2 % NCH] = rule_average_r(th[v][2 % NCH], ob[v] != 0, (double)c2[v], rn, gd.w);
+            } else {
+              th[v][0] = rule_average_r(th[v][0], ob[v] != 0, X[v], rn, gd.w);
+            }
+            ob[v] = 1;
+          }
+        }
+        elev[cc] = h[v];
+        var[cc] = s2[v];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) vals[(long long)(gd.word0 + k) * BHW + cc] = th[v][k];
+        validp[cc] = vd[v];
+        obsp[cc] = ob[v];
+      }
+    }
+    __syncthreads();  // s_cur / s_beg / s_rec are rewritten by the next unit
+  }
   flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
 }
 
@@ -1073,9 +1392,9 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 int points_blocks_per_sm(bool debug) {
   int n = 0;
   if (debug)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0, false>, kThreads, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0, false>, kThreads, 0);
   return n > 0 ? n : 1;
 }
 
@@ -1089,13 +1408,17 @@ cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
   // the fast variants need the channel in the float4's w (vec4) and exactly one group bound
   const int f = a.vec4 ? a.fast : 0;
   if (a.dbg_cell) {
-    if (f == 1) k_points<true, 1><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2) k_points<true, 2><<<grid, kThreads, 0, s>>>(a);
-    else k_points<true, 0><<<grid, kThreads, 0, s>>>(a);
+    if (f == 1 && a.bucketed) k_points<true, 1, true><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2 && a.bucketed) k_points<true, 2, true><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 1) k_points<true, 1, false><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2) k_points<true, 2, false><<<grid, kThreads, 0, s>>>(a);
+    else k_points<true, 0, false><<<grid, kThreads, 0, s>>>(a);
   } else {
-    if (f == 1) k_points<false, 1><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2) k_points<false, 2><<<grid, kThreads, 0, s>>>(a);
-    else k_points<false, 0><<<grid, kThreads, 0, s>>>(a);
+    if (f == 1 && a.bucketed) k_points<false, 1, true><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2 && a.bucketed) k_points<false, 2, true><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 1) k_points<false, 1, false><<<grid, kThreads, 0, s>>>(a);
+    else if (f == 2) k_points<false, 2, false><<<grid, kThreads, 0, s>>>(a);
+    else k_points<false, 0, false><<<grid, kThreads, 0, s>>>(a);
   }
   return cudaGetLastError();
 }
@@ -1107,6 +1430,26 @@ cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
     k_cells<2><<<grid, kThreads, 0, s>>>(a);
   else
     k_cells<0><<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int accum_blocks_per_sm(int band_cells) {
+  const size_t smem = accum_smem_bytes(band_cells);
+  cudaFuncSetAttribute(k_accum<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_accum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_accum<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_accum<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_accum<1>, kThreads, smem);
+  return n > 0 ? n : 1;
+}
+
+cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s) {
+  const size_t smem = accum_smem_bytes(a.band_cells);
+  if (a.fast == 1)
+    k_accum<1><<<grid, kThreads, smem, s>>>(a);
+  else
+    k_accum<2><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,14 @@ struct mem_map {
   cudaStream_t side = nullptr;  // k_cells of wave w overlaps k_points of wave w+1
   std::vector<cudaEvent_t> ev_pts, ev_cells;
   int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
+  // bucketed fast path (records + k_accum)
+  int band_cells = 0, nbands = 0, accum_grid = 0;
+  unsigned *bk_cnt = nullptr;       // [slots][nbands]
+  size_t bk_cnt_n = 0;
+  uint4 *bk_recs = nullptr;         // [slots][nbands][bcap]
+  size_t bk_recs_n = 0;
+  unsigned bk_cap_override = 0;     // TESTING: env MEM_BUCKET_CAP (forces spills)
+  int bk_force = 0;                 // env MEM_BUCKETS=1 / 0 forces the bucketed / RED path
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see PassArgs::ablate)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
@@ -396,6 +404,8 @@ void free_map(mem_map *m) {
   cudaFree(m->st.words);
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
+  cudaFree(m->bk_cnt);
+  cudaFree(m->bk_recs);
   cudaFree(m->ring);
   cudaFree(m->dparam);
   cudaFree(m->din);
@@ -482,6 +492,9 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
     m->points_grid = points_blocks_per_sm((flags & MEM_FLAG_DEBUG_POINTS) != 0) * (sms > 0 ? sms : 1);
     m->cells_grid = cells_blocks_per_sm() * (sms > 0 ? sms : 1);
+    m->band_cells = 1024;  // k_accum's band (kBand)
+    m->nbands = (rows * cols + m->band_cells - 1) / m->band_cells;
+    m->accum_grid = accum_blocks_per_sm(m->band_cells) * (sms > 0 ? sms : 1);
     cudaGetLastError();
   }
   m->pend.assign(n_maps, ShiftRec{0, 0, 0, 0});
@@ -495,6 +508,8 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
   if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
   if (const char *ss = getenv("MEM_SINGLE_STREAM")) m->single_stream = atoi(ss) != 0;
+  if (const char *bc = getenv("MEM_BUCKET_CAP")) m->bk_cap_override = (unsigned)strtoul(bc, nullptr, 0);
+  if (const char *bo = getenv("MEM_BUCKETS")) m->bk_force = atoi(bo) != 0 ? 1 : -1;
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -812,7 +827,23 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     if (pi > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
     pstart[i + 1] = (int)pi;
   }
-  const size_t per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
+  // bucketed fast path: one colour or 1-channel average group, float4 points, unsharded map
+  int fast = 0;
+  if (nb == 1 && m->ng == 1 && !(m->ablate & 1024u) && m->n_acc == 4) {
+    if (a.b[0].g.rule == MEM_COLOR) fast = 1;
+    else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) fast = 2;
+  }
+  // opt-in (env MEM_BUCKETS=1): measured slower than the REDs + k_cells on C2x64 and C5a
+  // (DESIGN.md §4.3), kept as a tested alternative
+  const bool bucketed = fast != 0 && a.vec4 && m->transport == 0 && m->bk_force > 0;
+  unsigned bcap = 0;
+  if (bucketed) {  // generous: all of a map's points spread evenly over its bands, + slack
+    bcap = m->bk_cap_override ? m->bk_cap_override
+                              : (unsigned)std::min<long long>((max_n + m->nbands - 1) / m->nbands + 256, 1LL << 30);
+    bcap = std::min((bcap + 31u) & ~31u, (unsigned)accum_sort_cap());
+  }
+  const size_t scratch_per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
+  const size_t per_map = scratch_per_map + (bucketed ? (size_t)m->nbands * bcap * sizeof(uint4) : 0);
   long long wm = (long long)(kScratchBudget / 2 / per_map);
   if (wm < 1) wm = 1;
   if (wm > B) wm = B;
@@ -824,7 +855,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     CU(cudaStreamSynchronize(m->side));
     CU(cudaFree(m->st.acc));
     m->st.acc = nullptr;
-    const size_t bytes = per_map * slots + 32;  // + the records' 32-B alignment pad
+    const size_t bytes = scratch_per_map * slots + 32;  // + the records' 32-B alignment pad
     if (cudaMalloc((void **)&m->st.acc, bytes) != cudaSuccess) {
       cudaGetLastError();
       m->scratch_maps = 0;
@@ -847,16 +878,46 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.cnt = m->st.acc;
   a.rec = m->st.acc + ((a.SHW + 3) & ~3LL);  // 32-B aligned records (the fast paths load 2 x 16 B)
   a.R = m->n_acc;
-  a.fast = 0;
-  if (nb == 1 && m->ng == 1 && !(m->ablate & 1024u)) {  // every group bound (no stale group state)
-    if (a.b[0].g.rule == MEM_COLOR) a.fast = 1;
-    else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) a.fast = 2;
-    if (m->n_acc != 4) a.fast = 0;  // the fast paths read 4-word (32 B) records
+  a.fast = fast;  // every group bound (no stale group state); 4-word (32 B) records
+  a.bucketed = bucketed ? 1 : 0;
+  if (bucketed) {
+    const size_t ncnt = (size_t)m->scratch_maps * m->nbands, nrec = ncnt * bcap;
+    if (ncnt > m->bk_cnt_n || nrec > m->bk_recs_n) {
+      CU(cudaStreamSynchronize(m->stream));
+      CU(cudaStreamSynchronize(m->side));
+      if (ncnt > m->bk_cnt_n) {
+        CU(cudaFree(m->bk_cnt));
+        m->bk_cnt = nullptr;
+        m->bk_cnt_n = 0;
+        if (cudaMalloc((void **)&m->bk_cnt, ncnt * sizeof(unsigned)) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(MEM_ENOMEM, "bucket counters (%zu)", ncnt);
+        }
+        CU(cudaMemsetAsync(m->bk_cnt, 0, ncnt * sizeof(unsigned), m->stream));
+        m->bk_cnt_n = ncnt;
+      }
+      if (nrec > m->bk_recs_n) {
+        CU(cudaFree(m->bk_recs));
+        m->bk_recs = nullptr;
+        m->bk_recs_n = 0;
+        if (cudaMalloc((void **)&m->bk_recs, nrec * sizeof(uint4)) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(MEM_ENOMEM, "bucket records (%zu bytes)", nrec * sizeof(uint4));
+        }
+        m->bk_recs_n = nrec;
+      }
+    }
+    a.band_cells = m->band_cells;
+    a.inv_band = 1.0 / (double)m->band_cells;
+    a.nbands = m->nbands;
+    a.bcap = bcap;
+    a.bcnt = m->bk_cnt;
+    a.recs = m->bk_recs;
   }
   if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool in an L2 persisting window
     cudaStreamAttrValue v;
     memset(&v, 0, sizeof v);
-    const size_t win = per_map * m->scratch_maps;
+    const size_t win = scratch_per_map * m->scratch_maps;
     const size_t setaside = (size_t)m->l2_persist_mb << 20;
     v.accessPolicyWindow.base_ptr = m->st.acc;
     v.accessPolicyWindow.num_bytes = win;
@@ -905,6 +966,8 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
     const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
+    const int ga = (int)std::max(1LL, std::min<long long>(m->accum_grid, (long long)(a.m1 - a.m0) * m->nbands));
+    auto launch_fuse = [&](cudaStream_t st) { return bucketed ? launch_accum(a, ga, st) : launch_cells(a, gc, st); };
     if (m->transport != 0) {  // sharded map: accumulate this rank's shard, then the band protocol
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
       a.cell_lo = m->band_lo;
@@ -919,7 +982,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     }
     if (n_waves == 1 || m->single_stream) {
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
-      TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
+      TIMED(MEM_STAGE_CELL, launch_fuse(m->stream));
       if (n_waves == 1) break;
       continue;
     }
@@ -927,7 +990,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
     CU(cudaEventRecord(m->ev_pts[w], m->stream));
     CU(cudaStreamWaitEvent(m->side, m->ev_pts[w], 0));
-    TIMED_ON(m->side, MEM_STAGE_CELL, launch_cells(a, gc, m->side));
+    TIMED_ON(m->side, MEM_STAGE_CELL, launch_fuse(m->side));
     CU(cudaEventRecord(m->ev_cells[w], m->side));
   }
   if (n_waves > 1 && !m->single_stream) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));

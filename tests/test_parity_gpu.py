@@ -449,3 +449,29 @@ def test_c5a_batched_maps_subset():
             else:
                 assert np.all(np.abs(g[fin].astype(np.float64) - o[fin]) <= 1e-6 + 1e-5 * np.abs(o[fin])), (b, nm)
         assert (gb.get_layer("valid")[b] > 0).sum() > 8000
+
+
+@pytest.mark.parametrize("cap", ["32", "1000", None])
+def test_bucketed_path(monkeypatch, cap):
+    """the bucketed fast path (records + k_accum), forced on, also with tiny buckets so that
+    most records spill to the scratch REDs and k_accum merges both; results must not change
+    (C2 colour and C1 average, vs the oracle)."""
+    monkeypatch.setenv("MEM_BUCKETS", "1")
+    if cap is not None:
+        monkeypatch.setenv("MEM_BUCKET_CAP", cap)
+    c = S.C2
+    g, o = make_pair(c["res"], c["rows"], c["cols"], [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])])
+    for f in range(4):
+        fr = S.c2_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        compare_layers(g, o, where=f"C2 frame {f}: ")
+    c = S.C1
+    g, o = make_pair(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])])
+    for f in range(4):
+        fr = S.c1_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        compare_layers(g, o, where=f"C1 frame {f}: ")
