@@ -49,6 +49,13 @@ struct BindDesc {  // one binding of a call, resolved against its group
   GroupDesc g;
 };
 
+struct __align__(16) PointFrame {  // per-map frame of a point input (64 B)
+  float R[9];      // sensor->map rotation (fp32 of the host doubles)
+  float t[3];      // t.xy relative to the map centre (fp64 subtraction, then fp32), t.z
+  int sr, sc;      // pending (lazy) shift of the preceding mem_move_to: strips to reset first
+  int r0, c0;      // ring offsets after that shift
+};
+
 struct __align__(16) MapFrame {  // per-map, per-call point/image frame parameters (16-B aligned: vector loads)
   float R[9];      // sensor->map rotation (fp32 of the host doubles)
   float t[3];      // t.xy relative to the map centre (fp64 subtraction, then fp32), t.z

@@ -27,6 +27,10 @@
 
 namespace memk {
 
+// ---------------------------------------------------------------- programmatic dependent launch
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- memory helpers
 __device__ __forceinline__ unsigned long long evict_first_policy() {
   unsigned long long pol;
@@ -50,7 +54,8 @@ __device__ __forceinline__ int stat_slot(int code) {
 }
 
 // is logical cell (row, col) in the strips that scrolled in with the pending shift (D14)?
-__device__ __forceinline__ bool in_strip(int row, int col, const MapFrame &f, const Geometry &g) {
+template <class F>
+__device__ __forceinline__ bool in_strip(int row, int col, const F &f, const Geometry &g) {
   if (f.sr == 0 && f.sc == 0) return false;
   const int ar = f.sr < 0 ? -f.sr : f.sr, ac = f.sc < 0 ? -f.sc : f.sc;
   if (ar >= g.H || ac >= g.W) return true;
@@ -79,7 +84,7 @@ struct PointOut {
 };
 
 // a2-a6 for one point: no memory access (the state gather of a7 is batched by the caller)
-__device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const MapFrame &f, const Geometry &g,
+__device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const PointFrame &f, const Geometry &g,
                                               const mem_noise &np, float rmin2, float rmax2, int map_base) {
   PointOut o;
   o.code = MEM_CODE_NONFINITE;
@@ -633,6 +638,15 @@ __device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cn
 // into shared memory with cp.async while it processes the current one (double buffer, each
 // lane reads back only the slots it wrote itself, so no warp or CTA barrier is needed).
 
+// per-map call parameters: inline (kernel parameter space) or staged
+__device__ __forceinline__ const PointFrame &frame_of(const PassArgs &a, int m) {
+  return a.frames ? a.frames[m] : a.fi[m];
+}
+__device__ __forceinline__ long long off_of(const PassArgs &a, int m) {
+  return a.offsets ? __ldg(&a.offsets[m]) : a.offi[m];
+}
+__device__ __forceinline__ int ps_of(const PassArgs &a, int m) { return a.pstart ? __ldg(&a.pstart[m]) : a.psi[m]; }
+
 // the map and point range of warp-item `it`
 struct Item {
   int m;
@@ -644,21 +658,17 @@ __device__ __forceinline__ Item item_of(const PassArgs &a, int it, int i0) {
   if (a.p_uniform > 0) {
     int rem;
     r.m = a.m0 + divmod_fast(it - i0, a.p_uniform, a.inv_p_uniform, rem);
-  } else if (a.pstart) {  // last map m in [m0, m1) with pstart[m] <= it
+  } else if (a.m1 - a.m0 > 1) {  // last map m in [m0, m1) with pstart[m] <= it
     int lo = a.m0, hi = a.m1 - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&a.pstart[mid]) <= it) lo = mid; else hi = mid - 1;
+      if (ps_of(a, mid) <= it) lo = mid; else hi = mid - 1;
     }
     r.m = lo;
   }
-  r.beg = 0;
-  r.end = a.n_single;
-  if (a.offsets) {
-    r.beg = __ldg(&a.offsets[r.m]);
-    r.end = __ldg(&a.offsets[r.m + 1]);
-  }
-  r.base = r.beg + (long long)(it - (a.pstart ? __ldg(&a.pstart[r.m]) : 0)) * kWarpPoints;
+  r.beg = off_of(a, r.m);
+  r.end = off_of(a, r.m + 1);
+  r.base = r.beg + (long long)(it - ps_of(a, r.m)) * kWarpPoints;
   return r;
 }
 
@@ -680,7 +690,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
                                              unsigned long long &packed, unsigned &npk, unsigned (&cnt)[8]) {
   const Geometry &g = a.geo;
   const int lane = threadIdx.x & 31;
-  const MapFrame f = a.frames ? a.frames[t.m] : a.f0;
+  const PointFrame f = frame_of(a, t.m);
   const int map_base = t.m * g.HW;
   const int sb = (int)scratch_base(a, t.m);
   PointOut o[kWarpPtsPerLane];
@@ -721,13 +731,17 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
   __shared__ unsigned s_cnt[8];
   __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0)  // the other epoch is the next point input's (no memset per call)
+    for (int i = threadIdx.x; i < kStatSlots * 8; i += kThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;
   __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // by mem_stats slot
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (kThreads / 32);
   const int gw = blockIdx.x * (kThreads / 32) + wid;
-  const int i0 = a.pstart ? __ldg(&a.pstart[a.m0]) : 0;
-  const int i1 = a.pstart ? __ldg(&a.pstart[a.m1]) : a.p_single;
+  const int i0 = ps_of(a, a.m0);
+  const int i1 = ps_of(a, a.m1);
   const unsigned long long pol = evict_first_policy();
   const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
   unsigned long long packed = 0ull;
@@ -784,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
   }
 #pragma unroll
   for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
-  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
+  flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
 // ---------------------------------------------------------------- k_cells (a9-a10, lazy a13)
@@ -805,6 +819,8 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
   __shared__ unsigned long long s_cntv[kThreads / 32][kChunk];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const Geometry &g = a.geo;
@@ -827,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
       const int phys = t0 + u * 32 + lane;
       cv[u] = phys < a.cell_hi ? __ldcg(a.cnt + sb + phys) : 0ull;
     }
-    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    const PointFrame f = frame_of(a, m);
     if (t0 == a.cell_lo && lane == 0) a.ring[m] = make_int2(f.r0, f.c0);
     int n = 0;
 #pragma unroll
@@ -871,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
     __syncwarp();  // this warp's slice is rewritten by its next chunk
   }
   __syncthreads();
-  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
+  flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
 // ---------------------------------------------------------------- k_accum (a8 end, a9-a10, lazy a13)
@@ -934,6 +950,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
   __shared__ unsigned s_wsum[kThreads / 32];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  pdl_wait();
+  pdl_trigger();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const Geometry &g = a.geo;
   const long long BHW = g.BHW;
@@ -961,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
     // (1) the frame, the next unit's record count; clear the histogram
 #pragma unroll
     for (int u = 0; u < kAccumPerThread; ++u) s_cur[u * kThreads + threadIdx.x] = 0u;
-    const MapFrame f = a.frames ? a.frames[m] : a.f0;
+    const PointFrame f = frame_of(a, m);
     ntot_next = un + (int)gridDim.x < units ? __ldcg(a.bcnt + key_of(un + gridDim.x)) : 0u;
     __syncthreads();
     // (2) histogram of the records' cells
@@ -1135,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
     }
     __syncthreads();  // s_cur / s_beg / s_rec are rewritten by the next unit
   }
-  flush_stats(s_cnt, cnt, &a.ctl->stats[0][0]);
+  flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)
@@ -1404,33 +1422,49 @@ int cells_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
+// Programmatic dependent launch: k_points, k_cells and k_accum may be scheduled while the
+// kernel before them on the stream drains (its CTAs retire); each waits on griddepcontrol.wait
+// before it reads anything the previous kernel wrote, and lets its own dependent launch early.
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, const PassArgs &a) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
   // the fast variants need the channel in the float4's w (vec4) and exactly one group bound
   const int f = a.vec4 ? a.fast : 0;
   if (a.dbg_cell) {
-    if (f == 1 && a.bucketed) k_points<true, 1, true><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2 && a.bucketed) k_points<true, 2, true><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 1) k_points<true, 1, false><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2) k_points<true, 2, false><<<grid, kThreads, 0, s>>>(a);
-    else k_points<true, 0, false><<<grid, kThreads, 0, s>>>(a);
+    if (f == 1 && a.bucketed) return launch_pdl(k_points<true, 1, true>, grid, 0, s, a);
+    else if (f == 2 && a.bucketed) return launch_pdl(k_points<true, 2, true>, grid, 0, s, a);
+    else if (f == 1) return launch_pdl(k_points<true, 1, false>, grid, 0, s, a);
+    else if (f == 2) return launch_pdl(k_points<true, 2, false>, grid, 0, s, a);
+    else return launch_pdl(k_points<true, 0, false>, grid, 0, s, a);
   } else {
-    if (f == 1 && a.bucketed) k_points<false, 1, true><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2 && a.bucketed) k_points<false, 2, true><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 1) k_points<false, 1, false><<<grid, kThreads, 0, s>>>(a);
-    else if (f == 2) k_points<false, 2, false><<<grid, kThreads, 0, s>>>(a);
-    else k_points<false, 0, false><<<grid, kThreads, 0, s>>>(a);
+    if (f == 1 && a.bucketed) return launch_pdl(k_points<false, 1, true>, grid, 0, s, a);
+    else if (f == 2 && a.bucketed) return launch_pdl(k_points<false, 2, true>, grid, 0, s, a);
+    else if (f == 1) return launch_pdl(k_points<false, 1, false>, grid, 0, s, a);
+    else if (f == 2) return launch_pdl(k_points<false, 2, false>, grid, 0, s, a);
+    else return launch_pdl(k_points<false, 0, false>, grid, 0, s, a);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
   if (a.fast == 1)
-    k_cells<1><<<grid, kThreads, 0, s>>>(a);
-  else if (a.fast == 2)
-    k_cells<2><<<grid, kThreads, 0, s>>>(a);
-  else
-    k_cells<0><<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+    return launch_pdl(k_cells<1>, grid, 0, s, a);
+  if (a.fast == 2) return launch_pdl(k_cells<2>, grid, 0, s, a);
+  return launch_pdl(k_cells<0>, grid, 0, s, a);
 }
 
 int accum_blocks_per_sm(int band_cells) {
@@ -1447,10 +1481,8 @@ int accum_blocks_per_sm(int band_cells) {
 cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s) {
   const size_t smem = accum_smem_bytes(a.band_cells);
   if (a.fast == 1)
-    k_accum<1><<<grid, kThreads, smem, s>>>(a);
-  else
-    k_accum<2><<<grid, kThreads, smem, s>>>(a);
-  return cudaGetLastError();
+    return launch_pdl(k_accum<1>, grid, smem, s, a);
+  return launch_pdl(k_accum<2>, grid, smem, s, a);
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {

@@ -9,11 +9,12 @@ constexpr int kWarpPtsPerLane = 4;      // point warp-item = 128 points (4 float
 constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
 constexpr int kWarpCellsPerLane = 4;    // cell warp-item = 128 physical cells
 constexpr int kWarpCells = 32 * kWarpCellsPerLane;
+constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 
 // Control block of one point input (zeroed by one cudaMemsetAsync per call).
 constexpr int kStatSlots = 64;  // CTAs add their counters to slot blockIdx % 64 (no hot address)
-struct Control {
-  unsigned long long stats[kStatSlots][8];  // mem_stats order (n_input is derived on the host)
+struct Control {  // two epochs: a point input adds to stats[epoch] and clears stats[epoch ^ 1]
+  unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
 };
 
 // reset description shared by k_cells (lazy strips) and k_shift
@@ -29,10 +30,12 @@ struct PassArgs {
   const float *pts;
   int stride;
   int vec4;                    // stride == 4 and 16-B aligned: one float4 per point
-  const long long *offsets;    // device [n_maps+1] (batched) or nullptr (single map: [0, n_single))
-  long long n_single;
-  const int *pstart;           // device [n_maps+1] prefix sums of point warp-items (batched) or nullptr
-  int p_single;                // point warp-items of the single map
+  // per-map frames, point offsets [n_maps+1] and prefix sums of point warp-items [n_maps+1]:
+  // inline in the kernel parameters (fi, offi, psi) for n_maps <= kInlineMaps (no copy per
+  // call), else in a staged device buffer (frames, offsets, pstart non-null)
+  const PointFrame *frames;
+  const long long *offsets;
+  const int *pstart;
   int m0, m1;                  // maps of this wave
   int cell_lo, cell_hi;        // k_cells: physical cells [lo, hi) of each map (a row band when sharded)
   int p_uniform;               // > 0: every map of the wave has exactly this many point warp-items
@@ -44,8 +47,6 @@ struct PassArgs {
   unsigned long long *rec;     // scratch records [SHW][R]
   int R;                       // record words per cell
   int fast;                    // k_cells fast path: 1 = one colour group, 2 = one 1-channel average group
-  const MapFrame *frames;      // device [n_maps] (batched) or nullptr (single map: f0)
-  MapFrame f0;
   int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)
   Geometry geo;
   State st;                    // st.acc: [n_acc][map-slots][HW]
@@ -53,6 +54,8 @@ struct PassArgs {
   int nb;
   BindDesc b[kMaxBind];
   Control *ctl;
+  int epoch;                   // stats epoch of this call (0/1)
+  int pdl;                     // launch with programmatic stream serialization (see launch_pdl)
   ResetInfo reset;
   int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;
@@ -66,6 +69,9 @@ struct PassArgs {
                                // rest of its points to the scratch with REDs (merged by k_accum)
   unsigned *bcnt;              // [map-slots][nbands] records appended (k_accum resets them to 0)
   uint4 *recs;                 // [map-slots][nbands][bcap]
+  PointFrame fi[kInlineMaps];
+  long long offi[kInlineMaps + 1];
+  int psi[kInlineMaps + 1];
   unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE; results are wrong when != 0):
                                // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math,
                                // 32 forward (not newest-first) cell tile order, 64 no warp aggregation,

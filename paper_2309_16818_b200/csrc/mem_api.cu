@@ -96,6 +96,9 @@ struct mem_map {
   size_t pca_cap = 0;
   Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
   size_t ctl_bytes = 0;
+  int pdl = 1;               // programmatic dependent launch (env MEM_PDL=0 disables)
+  int epoch = 1;             // stats epoch of the last point input (the first one uses 0)
+  bool stats_empty = true;   // the last point input had no points (all counters 0)
   int points_grid = 0;      // resident CTAs of k_points (persistent grid)
   int cells_grid = 0;       // resident CTAs of k_cells
   cudaStream_t side = nullptr;  // k_cells of wave w overlaps k_points of wave w+1
@@ -246,6 +249,13 @@ mem_status stage_params(mem_map *m, const void *src, size_t bytes, void **dptr) 
   p.next = (p.next + 1) % PinnedRing::kSlots;
   CU(cudaEventSynchronize(p.ev[k]));
   memcpy(p.host[k], src, bytes);
+  if (getenv("MEM_ZEROCOPY")) {  // EXPERIMENT: kernels read the pinned slot directly
+    CU(cudaEventRecord(p.ev[k], m->stream));
+    void *d = nullptr;
+    CU(cudaHostGetDevicePointer(&d, p.host[k], 0));
+    *dptr = d;
+    return MEM_OK;
+  }
   CU(cudaMemcpyAsync(m->dparam, p.host[k], bytes, cudaMemcpyHostToDevice, m->stream));
   CU(cudaEventRecord(p.ev[k], m->stream));
   *dptr = m->dparam;
@@ -508,6 +518,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
   if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
   if (const char *ss = getenv("MEM_SINGLE_STREAM")) m->single_stream = atoi(ss) != 0;
+  if (const char *pd = getenv("MEM_PDL")) m->pdl = atoi(pd) != 0;
   if (const char *bc = getenv("MEM_BUCKET_CAP")) m->bk_cap_override = (unsigned)strtoul(bc, nullptr, 0);
   if (const char *bo = getenv("MEM_BUCKETS")) m->bk_force = atoi(bo) != 0 ? 1 : -1;
   m->kx.assign(n_maps, 0);
@@ -780,10 +791,15 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     }
     m->dbg_n = total;
   }
-  CU(cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream));  // stats + work queue
   // legal; only a pending shift changes the map -- except that a shard of a sharded map
   // still takes part in the band exchange with its empty statistics
-  if (total == 0 && m->transport == 0) return flush_shift(m);
+  if (total == 0 && m->transport == 0) {
+    m->stats_empty = true;
+    return flush_shift(m);
+  }
+  // counters: this call adds to stats[epoch], its k_points clears the other epoch for the next
+  m->epoch ^= 1;
+  m->stats_empty = false;
   const void *dpts = nullptr;
   if (total > 0) {
     s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
@@ -791,13 +807,14 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   }
   a.pts = (const float *)dpts;
   a.stride = stride;
-  a.n_single = n_single;
   a.ring = m->ring;
   a.geo = m->geo();
   a.st = m->st;
   a.np = *np;
   a.nb = nb;
   a.ctl = m->ctl;
+  a.epoch = m->epoch;
+  a.pdl = m->pdl;
   a.reset = m->reset_info();
   a.ablate = m->ablate;
   const int HW = m->H * m->W;
@@ -809,7 +826,10 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.dbg_code = m->dbg_code;
   }
   auto frame = [&](int i) {
-    MapFrame f = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
+    const MapFrame mf = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
+    PointFrame f;
+    memcpy(f.R, mf.R, sizeof f.R);
+    memcpy(f.t, mf.t, sizeof f.t);
     // fold the pending shift of the preceding mem_move_to into this launch (lazy a13)
     f.sr = m->pending ? m->pend[i].sr : 0;
     f.sc = m->pending ? m->pend[i].sc : 0;
@@ -929,22 +949,25 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     cudaStreamSetAttribute(m->side, cudaStreamAttributeAccessPolicyWindow, &v);
     cudaGetLastError();
   }
-  if (B == 1 && !offsets) {
-    a.f0 = frame(0);
-    a.p_single = pstart[1];
+  if (B <= kInlineMaps) {  // frames, offsets and item prefix sums ride in the kernel parameters
+    for (int i = 0; i < B; ++i) a.fi[i] = frame(i);
+    for (int i = 0; i <= B; ++i) {
+      a.offi[i] = offsets ? offsets[i] : (i == 0 ? 0 : total);
+      a.psi[i] = pstart[i];
+    }
   } else {
     // parameter blob: frames [B] | offsets [B+1] (i64) | pstart [B+1] (i32)
-    const size_t off_at = (sizeof(MapFrame) * B + 15) & ~(size_t)15;  // int64 alignment
+    const size_t off_at = (sizeof(PointFrame) * B + 15) & ~(size_t)15;  // int64 alignment
     const size_t ps_at = off_at + sizeof(long long) * (B + 1);
     std::vector<unsigned char> blob(ps_at + sizeof(int) * (B + 1));
-    MapFrame *fr = reinterpret_cast<MapFrame *>(blob.data());
+    PointFrame *fr = reinterpret_cast<PointFrame *>(blob.data());
     for (int i = 0; i < B; ++i) fr[i] = frame(i);
     memcpy(blob.data() + off_at, offsets, sizeof(long long) * (B + 1));
     memcpy(blob.data() + ps_at, pstart.data(), sizeof(int) * (B + 1));
     void *d = nullptr;
     s = stage_params(m, blob.data(), blob.size(), &d);
     if (s != MEM_OK) return s;
-    a.frames = reinterpret_cast<const MapFrame *>(d);
+    a.frames = reinterpret_cast<const PointFrame *>(d);
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
     a.pstart = reinterpret_cast<const int *>((char *)d + ps_at);
   }
@@ -1378,8 +1401,9 @@ mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   if (!m || !out) return fail(MEM_EINVAL, "NULL argument");
   if (set_device(m)) return MEM_ECUDA;
   unsigned long long hs[kStatSlots][8], h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  CU(cudaMemcpyAsync(hs, m->ctl->stats, sizeof hs, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaMemcpyAsync(hs, m->ctl->stats[m->epoch], sizeof hs, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
+  if (m->stats_empty) memset(hs, 0, sizeof hs);
   for (int i = 0; i < kStatSlots; ++i)
     for (int k = 0; k < 8; ++k) h[k] += hs[i][k];
   h[0] = h[1] + h[2] + h[3] + h[4] + h[5] + h[6];
