@@ -173,7 +173,8 @@ MEM_API mem_status mem_shard_local_sync(mem_map **shards, int nranks);
  * sensor frame, then channels), AoS, host or device.  R (row-major 3x3, sensor->map) and
  * t (sensor position in the map/world frame) are host doubles.  n == 0 is legal and leaves
  * the map unchanged.  Atomic per call: on error nothing is enqueued.
- * Errors: EINVAL (n < 0, stride < 3, bad binding), EPOSE, ECUDA. */
+ * Errors: EINVAL (n < 0, stride < 3, bad binding, a <= 0, b < 0, a + b r_max^2 not finite), EPOSE,
+ * ECUDA. */
 MEM_API mem_status mem_input_pointcloud(mem_map *map, const float *pts, int64_t n, int stride, const mem_binding *bind,
                                 int n_bind, const double R[9], const double t[3], const mem_noise *noise);
 

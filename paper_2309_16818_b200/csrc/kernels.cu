@@ -231,6 +231,32 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     w = reduce_peers(peers, w, OpAdd());
     zw = reduce_peers(peers, zw, OpAdd());
   }
+  if constexpr (kFast == 1) {
+    // colour fast path, 4 REDs per inlier instead of 5: count word
+    // b | n << 32 (n = every filtered in-bounds point, D20; n > 0 marks the cell touched),
+    // record [P, S, r | g << 32, n_out]; n_in > 0 iff P > 0 (every 1/v > 0)
+    unsigned rg = 0u, bb = 0u;
+    if (act) {
+      const uint32_t bits = __float_as_uint(ch0);
+      rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
+      bb = bits & 255u;
+    }
+    if (!single) {
+      rg = reduce_peers(peers, rg, OpAdd());
+      bb = reduce_peers(peers, bb, OpAdd());
+    }
+    if (leader) {
+      const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+      red_add_u64(&a.cnt[sc], (unsigned long long)bb | ((unsigned long long)n_all << 32));
+      if (n_in) {
+        red_add_f64(rec + kRecP, w);
+        red_add_f64(rec + kRecS, zw);
+      }
+      red_add_u64(rec + 2, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
+      if (n_all != n_in) red_add_u64(rec + 3, (unsigned long long)(n_all - n_in));
+    }
+    return;
+  }
   if (leader) {
     const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
     red_add_u64(&a.cnt[sc], (unsigned long long)n_in | ((unsigned long long)(n_all - n_in) << 32));
@@ -241,22 +267,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
   }
   if constexpr (kFast != 0) {  // one group, channel in ch0 (the float4's w)
     unsigned long long *ga = rec + a.b[0].g.acc0;
-    if (kFast == 1) {  // D20 colour: exact integer sums
-      unsigned rg = 0u, bb = 0u;
-      if (act) {
-        const uint32_t bits = __float_as_uint(ch0);
-        rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
-        bb = bits & 255u;
-      }
-      if (!single) {
-        rg = reduce_peers(peers, rg, OpAdd());
-        bb = reduce_peers(peers, bb, OpAdd());
-      }
-      if (leader) {
-        red_add_u64(ga, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
-        red_add_u64(ga + 1, (unsigned long long)bb | ((unsigned long long)__popc(peers) << 32));
-      }
-    } else {  // Eq.(1) sums of one channel; non-finite values skip the group (D31)
+    {  // Eq.(1) sums of one channel; non-finite values skip the group (D31)
       const bool fin = act && isfinite(ch0);
       double v = fin ? (double)ch0 : 0.0;
       unsigned ng = fin ? 1u : 0u;
@@ -516,9 +527,10 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
     if (phys[u] < 0) continue;
     const int c = m * g.HW + phys[u];
     unsigned long long *r = a.rec + (long long)(sb + phys[u]) * 4;
-    // a9: Kalman height fusion (D7), outliers inflate first (D11)
-    const double n_in = (double)(uint32_t)(cnt[u] & 0xffffffffull);
-    const double n_out = (double)(uint32_t)(cnt[u] >> 32);
+    // a9: Kalman height fusion (D7), outliers inflate first (D11).  Colour layout: count word
+    // b | n << 32, record [P, S, r | g << 32, n_out] (n_in > 0 iff P > 0)
+    const double n_in = kColor ? (P[u] > 0.0 ? 1.0 : 0.0) : (double)(uint32_t)(cnt[u] & 0xffffffffull);
+    const double n_out = kColor ? (double)w1[u] : (double)(uint32_t)(cnt[u] >> 32);
     if (vd[u]) {
       const double sp = (double)s2[u] + n_out * (double)a.np.v_out;
       if (n_in > 0.0) {  // one fp64 division, two multiplies (reading D29b)
@@ -535,7 +547,7 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
       validp[c] = 1;
     }
     // a10: Eq.(1)+(2) per channel
-    const unsigned long long nn = kColor ? (w1[u] >> 32) : w0[u];
+    const unsigned long long nn = kColor ? (cnt[u] >> 32) : w0[u];
     if (nn != 0ull) {
       const double rn = 1.0 / (double)nn;
 #pragma unroll
@@ -543,7 +555,7 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
         double sk;
         if (kColor) {
           const uint32_t v = k == 0 ? (uint32_t)(w0[u] & 0xffffffffull)
-                                    : k == 1 ? (uint32_t)(w0[u] >> 32) : (uint32_t)(w1[u] & 0xffffffffull);
+                                    : k == 1 ? (uint32_t)(w0[u] >> 32) : (uint32_t)(cnt[u] & 0xffffffffull);
           sk = (double)v;  // exact integer colour sums (D20)
         } else {
           sk = sum[u][k];
@@ -1060,15 +1072,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
           if (cv != 0ull) {
             ulonglong2 *rq = reinterpret_cast<ulonglong2 *>(a.rec + (long long)(sb + lo + c) * 4);
             const ulonglong2 ps = __ldcg(rq), ww = __ldcg(rq + 1);
-            nin[v] += (unsigned)(cv & 0xffffffffull);
-            nout[v] += (unsigned)(cv >> 32);
             P[v] += __longlong_as_double((long long)ps.x);
             S[v] += __longlong_as_double((long long)ps.y);
-            if (kFast == 1) {
+            if (kFast == 1) {  // colour layout: b | n << 32, [P, S, r | g << 32, n_out]
+              nout[v] += (unsigned)ww.y;
+              nin[v] += (unsigned)(cv >> 32) - (unsigned)ww.y;
               c0[v] += (unsigned)(ww.x & 0xffffffffull);
               c1[v] += (unsigned)(ww.x >> 32);
-              c2[v] += (unsigned)(ww.y & 0xffffffffull);
+              c2[v] += (unsigned)(cv & 0xffffffffull);
             } else {
+              nin[v] += (unsigned)(cv & 0xffffffffull);
+              nout[v] += (unsigned)(cv >> 32);
               c0[v] += (unsigned)ww.x;
               X[v] += __longlong_as_double((long long)ww.y);
             }

@@ -749,6 +749,8 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   if (!R || !t || !np) return fail(MEM_EINVAL, "R, t and noise must be non-NULL");
   if (!(np->a > 0.0f) || !(np->b >= 0.0f))
     return fail(MEM_EINVAL, "noise: need a > 0 and b >= 0 (v = a + b r^2 > 0)");
+  if (np->b > 0.0f && std::isfinite(np->r_max) && !std::isfinite(np->a + np->b * (np->r_max * np->r_max)))
+    return fail(MEM_EINVAL, "noise: v = a + b r_max^2 overflows fp32");  // every 1/v must be > 0
   const int B = m->B;
   long long total = 0, max_n = 0;
   if (offsets) {
