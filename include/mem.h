@@ -211,7 +211,10 @@ MEM_API mem_status mem_get_layer(const mem_map *map, const char *name, float *ou
 
 /* Overwrites a stored layer from logical row-major float32 (host or device); flags take
  * value != 0; labels are truncated to int.  Derived layers (class_bayesian theta) give
- * EINVAL.  Used for single-step parity and resume. */
+ * EINVAL.  Used for single-step parity and resume.
+ * The variance of a cell with valid = 0 is not stored (it reads as NaN anyway): writing
+ * "variance" stores NaN there, writing 0 to "valid" clears the variance.  To restore a
+ * state, write "valid" before "variance". */
 MEM_API mem_status mem_set_layer(mem_map *map, const char *name, const float *src);
 
 /* PCA readout of a feature group (BASELINE configs[3]):

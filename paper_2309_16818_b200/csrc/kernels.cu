@@ -124,30 +124,29 @@ __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, cons
   return o;
 }
 
-// a7 for a batch of points: issue every state gather first (one round trip), then decide
+// a7 for a batch of points: issue every state gather first (one round trip), then decide.
+// The valid flag is not read: an invalid cell always holds a NaN variance (reset_cell, and
+// k_write keeps it so for state written through mem_set_layer), and a NaN h or s2 makes the
+// comparison false -- exactly the oracle's "no test on an invalid cell" (D10); a valid cell
+// whose h or s2 was set to NaN compares false in the oracle too.
 template <int N>
 __device__ __forceinline__ void mahalanobis(PointOut (&o)[N], const State &st, const Geometry &g, float tau2) {
   const float *elev = reinterpret_cast<const float *>(st.words) + (long long)kWordElev * g.BHW;
   const float *var = reinterpret_cast<const float *>(st.words) + (long long)kWordVar * g.BHW;
-  const uint8_t *valid = st.flags + (long long)kFlagValid * g.BHW;
-  uint8_t vl[N];
   float hv[N], sv[N];
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    vl[u] = 0;
-    hv[u] = sv[u] = 0.0f;
+    hv[u] = sv[u] = __int_as_float(0x7fc00000);
     if (o[u].test) {
-      vl[u] = valid[o[u].cell];
       hv[u] = elev[o[u].cell];
       sv[u] = var[o[u].cell];
     }
   }
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    if (o[u].test && vl[u]) {  // outlier iff valid and (z - h)^2 > tau^2 (sigma^2 + v) (D10)
-      const float d = o[u].z - hv[u];
-      if (d * d > tau2 * (sv[u] + o[u].v)) o[u].code = MEM_CODE_OUTLIER;
-    }
+    // outlier iff valid and (z - h)^2 > tau^2 (sigma^2 + v) (D10); NaN state compares false
+    const float d = o[u].z - hv[u];
+    if (d * d > tau2 * (sv[u] + o[u].v)) o[u].code = MEM_CODE_OUTLIER;
   }
 }
 
@@ -1292,13 +1291,21 @@ __global__ void __launch_bounds__(kThreads) k_write(const __grid_constant__ Read
   const int row = t / g.W, col = t - (t / g.W) * g.W;
   const int2 ring = a.ring[m];
   const long long cell = (long long)m * g.HW + (long long)wrap(row + ring.x, g.H) * g.W + wrap(col + ring.y, g.W);
-  const float v = a.src[(long long)m * g.HW + t];
+  float v = a.src[(long long)m * g.HW + t];
+  float *var = reinterpret_cast<float *>(a.st.words) + (long long)kWordVar * g.BHW;
+  const uint8_t *validp = a.st.flags + (long long)kFlagValid * g.BHW;
   switch (a.kind) {
+    case RK_VAR:  // invariant: an invalid cell holds a NaN variance (see mahalanobis)
+      if (!validp[cell]) v = __int_as_float(0x7fc00000);
+      var[cell] = v;
+      break;
     case RK_ELEV:
-    case RK_VAR:
     case RK_WORD: reinterpret_cast<float *>(a.st.words)[(long long)a.idx * g.BHW + cell] = v; break;
     case RK_LABEL: reinterpret_cast<int *>(a.st.words)[(long long)a.idx * g.BHW + cell] = (int)v; break;
-    case RK_FLAG: a.st.flags[(long long)a.idx * g.BHW + cell] = v != 0.0f; break;
+    case RK_FLAG:
+      a.st.flags[(long long)a.idx * g.BHW + cell] = v != 0.0f;
+      if (a.idx == kFlagValid && v == 0.0f) var[cell] = __int_as_float(0x7fc00000);
+      break;
     default: break;
   }
 }

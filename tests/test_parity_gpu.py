@@ -475,3 +475,34 @@ def test_bucketed_path(monkeypatch, cap):
         o.move_to(*fr["move"])
         step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
         compare_layers(g, o, where=f"C1 frame {f}: ")
+
+
+def test_injected_state_then_fusion():
+    """state written through mem_set_layer (valid first, as mem.h asks) then one fused frame:
+    per-point codes (the Mahalanobis gate reads the injected h / s2) and every layer must match
+    the oracle; variance written on invalid cells reads back as NaN."""
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):  # the oracle alone builds a state
+        fr = S.c2_frame(f)
+        o.move_to(*fr["move"])
+        o.input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+    g.move_to(*S.c2_frame(2)["move"])
+    assert tuple(g.center()[0]) == o.center()
+    names = g.layer_names()
+    for nm in ["valid"] + [n for n in names if n != "valid"]:
+        g.set_layer(nm, o.get_layer(nm))
+    compare_layers(g, o, where="injected: ")
+    var = np.full((c["rows"], c["cols"]), 0.5, np.float32)
+    h = g.get_layer("valid")
+    g2 = M.Map(c["res"], c["rows"], c["cols"], groups)
+    g2.set_layer("valid", h)
+    g2.set_layer("variance", var)
+    v2 = np.asarray(g2.get_layer("variance"))
+    assert np.isnan(v2[h == 0]).all() and (v2[h == 1] == 0.5).all()
+    fr = S.c2_frame(3)
+    g.move_to(*fr["move"])
+    o.move_to(*fr["move"])
+    step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+    compare_layers(g, o, where="after one frame: ")
