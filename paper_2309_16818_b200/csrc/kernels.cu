@@ -21,6 +21,9 @@
 #ifndef MEM_POINTS_MINB
 #define MEM_POINTS_MINB 3  // resident CTAs per SM the register allocation of k_points targets
 #endif
+#ifndef MEM_PAIR_MIN
+#define MEM_PAIR_MIN 4  // colour fast path: pair lanes of the same cell when >= this many repeat
+#endif
 #ifndef MEM_CELLS_MINB
 #define MEM_CELLS_MINB 3
 #endif
@@ -240,12 +243,32 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
       bb = bits & 255u;
     }
+    unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+    bool lead = leader;
     if (!single) {
       rg = reduce_peers(peers, rg, OpAdd());
       bb = reduce_peers(peers, bb, OpAdd());
+    } else if (__popc(dup) >= MEM_PAIR_MIN && !(a.ablate & 64u)) {
+      // a LiDAR scan line puts ~30% of its in-window points in the cell of the previous
+      // lane: the head of each run absorbs its successor (one shuffle per value), so such
+      // a pair costs one set of REDs
+      const bool fol = dup >> lane & 1u;
+      const bool prev_fol = lane > 0 && (dup >> (lane - 1) & 1u);
+      const bool absorbed = fol && !prev_fol;
+      const bool absorbs = !fol && lane < 31 && (dup >> (lane + 1) & 1u);
+      const double w2 = __shfl_down_sync(0xffffffffu, w, 1), zw2 = __shfl_down_sync(0xffffffffu, zw, 1);
+      const unsigned rg2 = __shfl_down_sync(0xffffffffu, rg, 1), bb2 = __shfl_down_sync(0xffffffffu, bb, 1);
+      if (absorbs) {
+        w += w2;
+        zw += zw2;
+        rg += rg2;
+        bb += bb2;
+        n_all = 2;
+        n_in += in_b >> (lane + 1) & 1u;
+      }
+      lead = act && !absorbed;
     }
-    if (leader) {
-      const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+    if (lead) {
       red_add_u64(&a.cnt[sc], (unsigned long long)bb | ((unsigned long long)n_all << 32));
       if (n_in) {
         red_add_f64(rec + kRecP, w);
