@@ -97,6 +97,8 @@ typedef struct om_map {
   int ng;
   om_group g[32];
   unsigned long long stats[8];
+  int occlusion;   /* image association with the Bresenham occlusion test (NEXT-1) */
+  float eps_occ;   /* occlusion tolerance, default 1e-4 m */
 } om_map;
 
 static int nval_of(int rule, int nch) {
@@ -151,6 +153,7 @@ om_map *om_create(float res, int rows, int cols, const om_group_spec *gs, int ng
   om_map *m = (om_map *)calloc(1, sizeof(om_map));
   if (!m) { *status = OM_ENOMEM; return NULL; }
   m->res = res; m->rows = rows; m->cols = cols; m->kx = 0; m->ky = 0;
+  m->occlusion = 0; m->eps_occ = 1e-4f;
   long n = ncells(m);
   m->h = (float *)malloc(sizeof(float) * n);
   m->s2 = (float *)malloc(sizeof(float) * n);
@@ -498,6 +501,62 @@ int om_input_pointcloud(om_map *m, const float *pts, long n, int stride, const o
   return status;
 }
 
+/* ---- Bresenham line ("computed using Bresenham's algorithm").
+ * The intermediate cells (both endpoints excluded) of the 8-connected line between integer
+ * cells a and b, written to out (capacity cap), returns their count.  Standard all-octant
+ * integer form (err = dx + dy with dy = -|y1-y0|; step x when 2 err >= dy, y when 2 err <= dx),
+ * always walked from the lexicographically smaller endpoint so that (a, b) and (b, a) give the
+ * same cell set (reading D33). ---- */
+int om_bresenham(int r0, int c0, int r1, int c1, int *out_r, int *out_c, int cap) {
+  if (r1 < r0 || (r1 == r0 && c1 < c0)) { int t = r0; r0 = r1; r1 = t; t = c0; c0 = c1; c1 = t; }
+  const int dx = abs(r1 - r0), dy = -abs(c1 - c0);
+  const int sx = r0 < r1 ? 1 : -1, sy = c0 < c1 ? 1 : -1;
+  int err = dx + dy, x = r0, y = c0, n = 0;
+  for (;;) {
+    if (x == r1 && y == c1) break;
+    const int e2 = 2 * err;
+    if (e2 >= dy) { err += dy; x += sx; }
+    if (e2 <= dx) { err += dx; y += sy; }
+    if (x == r1 && y == c1) break;
+    if (n < cap) { out_r[n] = x; out_c[n] = y; }
+    ++n;
+  }
+  return n;
+}
+
+void om_set_occlusion(om_map *m, int enable, float eps_occ) {
+  m->occlusion = enable != 0;
+  m->eps_occ = eps_occ;
+}
+
+/* the occlusion test of one target cell (readings
+ * D32-D34): every valid in-map intermediate cell on the line from the camera's footprint cell
+ * to the target must have elevation <= the ray height + eps_occ, the ray height interpolated
+ * linearly between the camera height and the target elevation by 2D distance fraction */
+static int om_visible(const om_map *m, int row, int col, float tx, float ty, float tz, float hb) {
+  const int H = m->rows, W = m->cols;
+  const float hH = (float)H / 2.0f, hW = (float)W / 2.0f;
+  const float inv_res = (float)(1.0 / (double)m->res);
+  const int rc = (int)floorf(tx * inv_res + hH), cc = (int)floorf(ty * inv_res + hW);
+  const float xb = ((float)row + 0.5f - hH) * m->res, yb = ((float)col + 0.5f - hW) * m->res;
+  const float dxb = xb - tx, dyb = yb - ty;
+  const float db = sqrtf(dxb * dxb + dyb * dyb);
+  static int rr[1 << 16], cr[1 << 16];
+  const int n = om_bresenham(rc, cc, row, col, rr, cr, 1 << 16);
+  for (int k = 0; k < n && k < (1 << 16); ++k) {
+    const int i = rr[k], jj = cr[k];
+    if (i < 0 || i >= H || jj < 0 || jj >= W) continue; /* outside the map: no occluder */
+    const long j = (long)i * W + jj;
+    if (!m->valid[j]) continue;                          /* unknown terrain does not occlude */
+    const float xi = ((float)i + 0.5f - hH) * m->res, yi = ((float)jj + 0.5f - hW) * m->res;
+    const float dxi = xi - tx, dyi = yi - ty;
+    const float di = sqrtf(dxi * dxi + dyi * dyi);
+    const float ray = tz + (di / db) * (hb - tz);
+    if (m->h[j] > ray + m->eps_occ) return 0;
+  }
+  return 1;
+}
+
 /* ---- image input: SURVEY §8(c) N2 step 4 (a11 + a12), PAPER.md:232-239 ---- */
 int om_input_image(om_map *m, const float *img, int C, int IH, int IW, const om_binding *bind, int nb,
                    const double K[9], const double R[9], const double t[3]) {
@@ -539,6 +598,7 @@ int om_input_image(om_map *m, const float *img, int C, int IH, int IW, const om_
       const float v = fy * uy + ccy;
       const float fu = floorf(u + 0.5f), fv = floorf(v + 0.5f); /* nearest pixel (D16) */
       if (!(0.0f <= fu && fu < (float)IW && 0.0f <= fv && fv < (float)IH)) continue; /* frustum */
+      if (m->occlusion && !om_visible(m, row, col, tx, ty, tz, m->h[j])) continue; /* NEXT-1 */
       const long pix = (long)(int)fv * IW + (long)(int)fu;
       /* a12: sample the bound channels and fuse with N_j = 1 (D21) */
       for (int b = 0; b < nb; ++b) {

@@ -66,6 +66,8 @@ def lib():
         L.om_get_stats.argtypes = [vp, vp]
         L.om_get_center.argtypes = [vp, vp]
         L.om_pca_readout.argtypes = [vp, C.c_char_p, C.c_int, vp]
+        L.om_bresenham.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int]
+        L.om_set_occlusion.argtypes = [vp, C.c_int, C.c_float]
         L.om_accumulate.restype = vp
         L.om_accumulate.argtypes = L.om_input_pointcloud.argtypes + [C.POINTER(C.c_int)]
         L.om_fuse_rows.argtypes = [vp, vp, C.c_int, C.c_int]
@@ -93,6 +95,14 @@ def make_binds(bindings):
     for i, (off, n, g) in enumerate(bindings):
         arr[i] = _Bind(off, n, g)
     return arr
+
+
+def bresenham(a, b):
+    """intermediate cells (exclusive of both endpoints) of the 8-connected line a -> b."""
+    cap = 4 * (abs(a[0] - b[0]) + abs(a[1] - b[1])) + 8
+    rr, cc = np.empty(cap, np.int32), np.empty(cap, np.int32)
+    n = lib().om_bresenham(int(a[0]), int(a[1]), int(b[0]), int(b[1]), rr.ctypes.data, cc.ctypes.data, cap)
+    return list(zip(rr[:n].tolist(), cc[:n].tolist()))
 
 
 class OracleFrame:
@@ -192,6 +202,9 @@ class OracleMap:
         st = lib().om_fuse_rows(self._h, frame._h, row_lo, row_hi)
         if st != 0:
             raise OracleError(st, "om_fuse_rows")
+
+    def set_occlusion(self, enable=True, eps_occ=1e-4):
+        lib().om_set_occlusion(self._h, int(enable), C.c_float(eps_occ))
 
     def input_image(self, img, bindings, K, R, t):
         img = np.ascontiguousarray(img, np.float32)
