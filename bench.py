@@ -321,6 +321,18 @@ def side_c3_c4(torch, M, stream, frames=2):
     mp.profile(False)
     prof = mp.profile_read(reset=True)
     out["c3"]["stage_ms"] = {k: v[0] for k, v in prof.items() if v[1]}
+    # NEXT-1: the same frames with the Bresenham occlusion test in the image association
+    mp.set_image_occlusion(True, 1e-4)
+    ms_occ = timed_loop(torch, stream, 20, c3_step)
+    mp.profile_read(reset=True)
+    mp.profile(True)
+    c3_step(0)
+    torch.cuda.synchronize()
+    mp.profile(False)
+    prof = mp.profile_read(reset=True)
+    out["c3_occlusion"] = {"workload": "C3 with the Bresenham occlusion test (PAPER.md:234-236) on the image",
+                           "ms_per_frame": ms_occ, "frames_per_s": 1e3 / ms_occ,
+                           "image_stage_ms": prof.get("image", (None,))[0]}
     mp.close()
     c4 = S.C4
     m4 = M.Map(c4["res"], c4["rows"], c4["cols"], [dict(name="feat", rule=0, n_channels=c4["d"], w=c4["w"])])

@@ -195,6 +195,16 @@ MEM_API mem_status mem_input_image(mem_map *map, const float *img, int C, int H,
 MEM_API mem_status mem_input_image_batch(mem_map *map, const float *img, int C, int H, int W, const mem_binding *bind,
                                  int n_bind, const double *K, const double *R, const double *t);
 
+/* Image association with the occlusion test of PAPER.md:234-236, for
+ * the following mem_input_image[_batch] calls of this map (default off: frustum only, D18).
+ * A valid in-frustum cell is fused only if every intermediate cell of the Bresenham line from
+ * the camera's footprint cell to it (8-connected, endpoints excluded; cells outside the map
+ * and cells with valid = 0 do not occlude) has elevation <= ray height + eps_occ, the ray
+ * height linear in the 2D distance between the camera height and the cell's elevation
+ * (readings D32-D34).  eps_occ: metres, >= 0 (1e-4 in SPEC).
+ * Errors: EINVAL (eps_occ negative or not finite). */
+MEM_API mem_status mem_set_image_occlusion(mem_map *map, int enable, float eps_occ);
+
 /* Recentres on (x, y) snapped to the lattice, k = floor(x/res + 1/2) (D14); scrolled-in
  * cells are reset to the create state.  Errors: EINVAL (non-finite), ECUDA. */
 MEM_API mem_status mem_move_to(mem_map *map, double x, double y);

@@ -1192,6 +1192,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
   flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
+// ---------------------------------------------------------------- occlusion (NEXT-1)
+// Is logical cell (row, col) of map m seen from the camera at (tx, ty, tz) (map-centred, fp32)?
+// every intermediate cell of the Bresenham line from the camera's footprint
+// cell to the target must lie below the ray; readings D32-D34: the line is walked
+// from the lexicographically smaller endpoint (all-octant integer form), cells outside the map
+// and unknown cells do not occlude, the ray height is linear in the 2D distance between the
+// camera height and the target elevation, tolerance eps_occ.  fp32 in the oracle's order.
+__device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row, int col, float tx, float ty,
+                                             float tz, float hb, int2 ring) {
+  const Geometry &g = a.geo;
+  const float *elev = reinterpret_cast<const float *>(a.st.words) + (long long)kWordElev * g.BHW;
+  const uint8_t *validp = a.st.flags + (long long)kFlagValid * g.BHW;
+  const int rc = (int)floorf(tx * g.inv_res + g.hH), cc = (int)floorf(ty * g.inv_res + g.hW);
+  const float xb = ((float)row + 0.5f - g.hH) * g.res, yb = ((float)col + 0.5f - g.hW) * g.res;
+  const float dxb = xb - tx, dyb = yb - ty;
+  const float db = sqrtf(dxb * dxb + dyb * dyb);
+  int r0 = rc, c0 = cc, r1 = row, c1 = col;
+  if (r1 < r0 || (r1 == r0 && c1 < c0)) {
+    r0 = row; c0 = col; r1 = rc; c1 = cc;
+  }
+  const int dx = abs(r1 - r0), dy = -abs(c1 - c0);
+  const int sx = r0 < r1 ? 1 : -1, sy = c0 < c1 ? 1 : -1;
+  int err = dx + dy, x = r0, y = c0;
+  const long long mbase = (long long)m * g.HW;
+  for (;;) {
+    if (x == r1 && y == c1) break;
+    const int e2 = 2 * err;
+    if (e2 >= dy) { err += dy; x += sx; }
+    if (e2 <= dx) { err += dx; y += sy; }
+    if (x == r1 && y == c1) break;
+    if (x < 0 || x >= g.H || y < 0 || y >= g.W) continue;  // outside the map: no occluder
+    const long long j = mbase + (long long)wrap(x + ring.x, g.H) * g.W + wrap(y + ring.y, g.W);
+    if (!validp[j]) continue;                                // unknown terrain does not occlude
+    const float xi = ((float)x + 0.5f - g.hH) * g.res, yi = ((float)y + 0.5f - g.hW) * g.res;
+    const float dxi = xi - tx, dyi = yi - ty;
+    const float di = sqrtf(dxi * dxi + dyi * dyi);
+    const float ray = tz + (di / db) * (hb - tz);
+    if (elev[j] > ray + a.eps_occ) return false;
+  }
+  return true;
+}
+
 // ---------------------------------------------------------------- k_image (a11-a12)
 __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ ImageArgs a) {
   const Geometry &g = a.geo;
@@ -1210,7 +1252,8 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
   const float xc = ((float)row + 0.5f - g.hH) * g.res;
   const float yc = ((float)col + 0.5f - g.hW) * g.res;
   const float dx = xc - f.t[0], dy = yc - f.t[1];
-  const float dz = vals[(long long)kWordElev * g.BHW + cell] - f.t[2];
+  const float hcell = vals[(long long)kWordElev * g.BHW + cell];
+  const float dz = hcell - f.t[2];
   const float pcx = (f.R[0] * dx + f.R[3] * dy) + f.R[6] * dz;
   const float pcy = (f.R[1] * dx + f.R[4] * dy) + f.R[7] * dz;
   const float pcz = (f.R[2] * dx + f.R[5] * dy) + f.R[8] * dz;
@@ -1220,6 +1263,7 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
   const float v = f.K[3] * uy + f.K[4];
   const float fu = floorf(u + 0.5f), fv = floorf(v + 0.5f);  // nearest pixel (D16)
   if (!(0.0f <= fu && fu < (float)a.IW && 0.0f <= fv && fv < (float)a.IH)) return;  // frustum
+  if (a.occlusion && !cell_visible(a, m, row, col, f.t[0], f.t[1], f.t[2], hcell, ring)) return;
   const long long plane = (long long)a.IH * a.IW;
   const float *pix = a.img + (long long)m * a.map_stride + (long long)(int)fv * a.IW + (int)fu;
   // a12: sample and fuse with N_j = 1

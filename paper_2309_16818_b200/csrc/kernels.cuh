@@ -80,6 +80,8 @@ struct PassArgs {
 
 struct ImageArgs {
   int row_lo, row_hi;          // physical rows fused (the owned band when sharded)
+  int occlusion;               // NEXT-1: Bresenham occlusion test of every in-frustum cell
+  float eps_occ;
   const float *img;
   int C, IH, IW;
   long long map_stride;        // floats between consecutive maps' images

@@ -97,6 +97,8 @@ struct mem_map {
   Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
   size_t ctl_bytes = 0;
   int pdl = 1;               // programmatic dependent launch (env MEM_PDL=0 disables)
+  int occlusion = 0;         // image association with the Bresenham occlusion test (NEXT-1)
+  float eps_occ = 1e-4f;
   int epoch = 1;             // stats epoch of the last point input (the first one uses 0)
   bool stats_empty = true;   // the last point input had no points (all counters 0)
   int points_grid = 0;      // resident CTAs of k_points (persistent grid)
@@ -1063,6 +1065,8 @@ static mem_status input_image(mem_map *m, const float *img, int C, int IH, int I
   s = stage_input(m, img, sizeof(float) * (size_t)per * B, &dimg);
   if (s != MEM_OK) return s;
   a.img = (const float *)dimg;
+  a.occlusion = m->occlusion;
+  a.eps_occ = m->eps_occ;
   a.row_lo = m->transport ? m->band_lo / m->W : 0;  // sharded: fuse the owned band only
   a.row_hi = m->transport ? (m->band_lo + m->band_n) / m->W : m->H;
   a.C = C;
@@ -1417,6 +1421,14 @@ mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   out->n_inlier = h[5];
   out->n_outlier = h[6];
   out->n_cells_touched = h[7];
+  return MEM_OK;
+}
+
+mem_status mem_set_image_occlusion(mem_map *m, int enable, float eps_occ) {
+  if (check_map(m)) return MEM_EINVAL;
+  if (!(eps_occ >= 0.0f) || !std::isfinite(eps_occ)) return fail(MEM_EINVAL, "eps_occ must be finite and >= 0");
+  m->occlusion = enable != 0;
+  m->eps_occ = eps_occ;
   return MEM_OK;
 }
 

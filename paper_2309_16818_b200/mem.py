@@ -33,7 +33,7 @@ EXPORTS = ["mem_create", "mem_create_batch", "mem_destroy", "mem_set_stream", "m
            "mem_move_to", "mem_move_to_batch", "mem_get_layer", "mem_set_layer", "mem_get_layer_names",
            "mem_memory_footprint", "mem_get_info", "mem_get_center", "mem_frame_stats", "mem_debug_point_codes",
            "mem_profile", "mem_profile_read", "mem_pca_readout", "mem_nccl_unique_id", "mem_create_sharded",
-           "mem_shard_local_sync", "mem_last_error", "mem_version"]
+           "mem_shard_local_sync", "mem_set_image_occlusion", "mem_last_error", "mem_version"]
 STAGES = ["shift", "point", "cell", "image", "read", "write", "h2d", "d2h"]
 
 
@@ -97,6 +97,7 @@ _sig = {
     "mem_create_sharded": [C.c_float, C.c_int, C.c_int, _P(mem_layer_spec), C.c_int, C.c_uint, _vp, _vp, C.c_int,
                            C.c_int, _P(_vp)],
     "mem_shard_local_sync": [_P(_vp), C.c_int],
+    "mem_set_image_occlusion": [_vp, C.c_int, C.c_float],
     "mem_profile_read": [_vp, _P(C.c_double), _P(C.c_uint64), C.c_int],
 }
 for _n, _a in _sig.items():
@@ -358,6 +359,10 @@ class Map:
         self.h = _handle if _handle is not None else mem_create(
             resolution, rows, cols, groups, MEM_FLAG_DEBUG_POINTS if debug_points else 0, stream, n_maps)
         self._last_n = 0
+
+    def set_image_occlusion(self, enable=True, eps_occ=1e-4):
+        """NEXT-1: Bresenham occlusion test for the following image inputs (include/mem.h)."""
+        _check(_lib.mem_set_image_occlusion(self.h, int(enable), eps_occ), "mem_set_image_occlusion")
 
     @classmethod
     def sharded(cls, resolution, rows, cols, groups, rank, nranks, nccl_id=None, debug_points=False, stream=None):

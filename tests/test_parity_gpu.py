@@ -506,3 +506,64 @@ def test_injected_state_then_fusion():
     o.move_to(*fr["move"])
     step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
     compare_layers(g, o, where="after one frame: ")
+
+
+# ---------------------------------------------------------------- NEXT-1 occlusion
+def test_image_occlusion_random_terrain():
+    """Bresenham occlusion on blocky + sloped terrain with unknown cells,
+    several cameras (inside and outside the map), all rules: every layer vs the oracle, and
+    the occlusion must actually remove cells the frustum alone would fuse."""
+    rows, cols, res = 90, 70, 0.05
+    g, o = make_pair(res, rows, cols, IMG_GROUPS)
+    g.set_image_occlusion(True, 1e-4)
+    o.set_occlusion(True, 1e-4)
+    ref = O.OracleMap(res, rows, cols, IMG_GROUPS)  # same inputs, frustum only
+    rng = np.random.default_rng(123)
+    x = (np.arange(rows) + 0.5 - rows / 2) * res
+    y = (np.arange(cols) + 0.5 - cols / 2) * res
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    elev = 0.1 * np.sin(2 * X) * np.cos(3 * Y)
+    for _ in range(8):
+        r, c = rng.integers(5, rows - 12), rng.integers(5, cols - 12)
+        elev[r:r + rng.integers(2, 8), c:c + rng.integers(2, 10)] += rng.uniform(0.3, 1.2)
+    valid = (rng.uniform(size=(rows, cols)) > 0.05).astype(np.float32)
+    for m in (g, o, ref):
+        m.set_layer("valid", valid)
+        m.set_layer("elevation", np.where(valid > 0, elev, np.nan).astype(np.float32))
+        m.set_layer("variance", np.where(valid > 0, 0.01, np.nan).astype(np.float32))
+    K = np.array([[150.0, 0.3, 79.5], [0, 148.0, 59.5], [0, 0, 1.0]])
+    eyes = [(-1.9, 0.1, 1.2), (-3.0, -0.4, 1.6), (0.2, -2.2, 1.0), (1.9, 1.5, 2.0), (0.03, 0.02, 1.5)]
+    for f, eye in enumerate(eyes):
+        eye = np.array(eye)
+        R = camera_looking_at(eye, [rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), 0.0]) if f < 4 else \
+            camera_looking_at(eye, [0.8, 0.3, 0.0])
+        img = np.concatenate([S.softmax_image(rng.integers(0, 5, (120, 160)), 5, rng),
+                              rng.normal(0, 1, (5, 120, 160)).astype(np.float32),
+                              rng.uniform(0, 255, (3, 120, 160)).astype(np.float32)])
+        g.input_image(torch.from_numpy(img).cuda(), IMG_BINDS, K, R, eye)
+        o.input_image(img, IMG_BINDS, K, R, eye)
+        ref.input_image(img, IMG_BINDS, K, R, eye)
+        compare_layers(g, o, where=f"camera {f}: ")
+    seen, seen_ref = g.get_layer("sem_observed"), ref.get_layer("sem_observed")
+    assert (seen <= seen_ref).all() and (seen_ref - seen).sum() > 200 and seen.sum() > 1000
+
+
+def test_c3_with_occlusion_full_size():
+    c = S.C3
+    groups = [dict(name="sem", rule=M.MEM_CLASS_BAYESIAN, n_channels=c["n_classes"], alpha0=1.0),
+              dict(name="top", rule=M.MEM_CLASS_MAX, n_channels=c["n_classes"])]
+    binds = [(0, c["n_classes"], 0), (0, c["n_classes"], 1)]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    g.set_image_occlusion(True)
+    o.set_occlusion(True)
+    for f in range(2):
+        fr = S.c3_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        for cl in fr["clouds"]:
+            step_points(g, o, cl["points"], [], cl["R"], cl["t"], c["noise"])
+        im = fr["image"]
+        g.input_image(torch.from_numpy(im["img"]).cuda(), binds, im["K"], im["R"], im["t"])
+        o.input_image(im["img"], binds, im["K"], im["R"], im["t"])
+        compare_layers(g, o, where=f"C3+occlusion frame {f}: ")
+    assert (g.get_layer("top_label") >= 0).sum() > 5000
