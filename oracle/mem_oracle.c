@@ -850,3 +850,104 @@ int om_pca_readout(const om_map *m, const char *group, int k, float *out) {
   free(mu); free(C); free(A); free(v); free(w); free(comp);
   return OM_OK;
 }
+
+/* ---- NEXT-3 post-processing plugins on the fused map (Table II
+ * rows "normal calculation", "traversability"; readings D35-D37) ---- */
+
+/* gradient of the elevation along one axis at a valid cell: central difference when both
+ * neighbours are valid, one-sided with the valid one otherwise; 0 = no valid neighbour */
+static int om_grad(const om_map *m, int i, int j, int di, int dj, float *g) {
+  const int H = m->rows, W = m->cols;
+  const long c = (long)i * W + j;
+  const int ip = i + di, jp = j + dj, im = i - di, jm = j - dj;
+  const int vp = ip >= 0 && ip < H && jp >= 0 && jp < W && m->valid[(long)ip * W + jp];
+  const int vm = im >= 0 && im < H && jm >= 0 && jm < W && m->valid[(long)im * W + jm];
+  if (vp && vm) *g = (m->h[(long)ip * W + jp] - m->h[(long)im * W + jm]) / (2.0f * m->res);
+  else if (vp) *g = (m->h[(long)ip * W + jp] - m->h[c]) / m->res;
+  else if (vm) *g = (m->h[c] - m->h[(long)im * W + jm]) / m->res;
+  else return 0;
+  return 1;
+}
+
+/* unit normal (-gx, -gy, 1)/|.| of a cell (x = rows, y = cols, D13); 0 = invalid output */
+static int om_normal(const om_map *m, int i, int j, float n[3]) {
+  const long c = (long)i * m->cols + j;
+  float gx, gy;
+  if (!m->valid[c] || !om_grad(m, i, j, 1, 0, &gx) || !om_grad(m, i, j, 0, 1, &gy)) return 0;
+  const float norm = sqrtf((gx * gx + gy * gy) + 1.0f);
+  n[0] = -gx / norm;
+  n[1] = -gy / norm;
+  n[2] = 1.0f / norm;
+  return 1;
+}
+
+/* out: 3 x rows x cols (normal_x, normal_y, normal_z), NaN where invalid */
+int om_plugin_normals(const om_map *m, float *out) {
+  const long cells = ncells(m);
+  for (int i = 0; i < m->rows; ++i)
+    for (int j = 0; j < m->cols; ++j) {
+      const long c = (long)i * m->cols + j;
+      float n[3];
+      if (!om_normal(m, i, j, n)) n[0] = n[1] = n[2] = NAN;
+      for (int k = 0; k < 3; ++k) out[(long)k * cells + c] = n[k];
+    }
+  return OM_OK;
+}
+
+/* score = clamp(min(slope, step), 0, 1), slope = (n_z - cos_max) / (1 - cos_max),
+ * step = 1 - max |h_nb - h| / step_max over the valid 8-neighbours (D36); NaN where invalid.
+ * cos_max = cos(slope_max) rounded once to fp32 by the caller. */
+int om_plugin_traversability(const om_map *m, float cos_max, float step_max, float *out) {
+  if (!(step_max > 0.0f) || !(cos_max < 1.0f)) return OM_EINVAL;
+  const int H = m->rows, W = m->cols;
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < W; ++j) {
+      const long c = (long)i * W + j;
+      float n[3];
+      if (!om_normal(m, i, j, n)) { out[c] = NAN; continue; }
+      const float slope = (n[2] - cos_max) / (1.0f - cos_max);
+      float mx = 0.0f;
+      for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj) {
+          const int a = i + di, b = j + dj;
+          if ((di == 0 && dj == 0) || a < 0 || a >= H || b < 0 || b >= W || !m->valid[(long)a * W + b]) continue;
+          const float d = fabsf(m->h[(long)a * W + b] - m->h[c]);
+          if (d > mx) mx = d;
+        }
+      const float step = 1.0f - mx / step_max;
+      float s = slope < step ? slope : step;
+      s = s < 0.0f ? 0.0f : s;
+      out[c] = s > 1.0f ? 1.0f : s;
+    }
+  return OM_OK;
+}
+
+/* per cell argmax of the group's class probabilities theta (class_bayesian: alpha / sum alpha
+ * as read out; class_average: the stored values; class_max: its label/conf), ties to the
+ * lowest class (D37); out: 2 x rows x cols (class_id, confidence), -1 / 0 where unobserved */
+int om_plugin_semantic_argmax(const om_map *m, const char *group, float *out) {
+  int gi = -1;
+  for (int k = 0; k < m->ng; ++k) if (!strcmp(m->g[k].name, group)) gi = k;
+  if (gi < 0) return OM_ENOTFOUND;
+  const om_group *g = &m->g[gi];
+  if (g->rule != OM_CLASS_BAYESIAN && g->rule != OM_CLASS_AVERAGE && g->rule != OM_CLASS_MAX) return OM_ERULE;
+  const long cells = ncells(m);
+  for (long c = 0; c < cells; ++c) {
+    float id = -1.0f, conf = 0.0f;
+    if (g->rule == OM_CLASS_MAX) {
+      if (g->label[c] >= 0) { id = (float)g->label[c]; conf = g->val[c]; }
+    } else if (g->observed[c]) {
+      double tot = 0.0;
+      if (g->rule == OM_CLASS_BAYESIAN)
+        for (int k = 0; k < g->nch; ++k) tot += (double)g->val[(long)k * cells + c];
+      for (int k = 0; k < g->nch; ++k) {
+        const float th = g->rule == OM_CLASS_BAYESIAN ? (float)((double)g->val[(long)k * cells + c] / tot)
+                                                      : g->val[(long)k * cells + c];
+        if (k == 0 || th > conf) { conf = th; id = (float)k; }
+      }
+    }
+    out[c] = id;
+    out[cells + c] = conf;
+  }
+  return OM_OK;
+}

@@ -68,6 +68,9 @@ def lib():
         L.om_pca_readout.argtypes = [vp, C.c_char_p, C.c_int, vp]
         L.om_bresenham.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int]
         L.om_set_occlusion.argtypes = [vp, C.c_int, C.c_float]
+        L.om_plugin_normals.argtypes = [vp, vp]
+        L.om_plugin_traversability.argtypes = [vp, C.c_float, C.c_float, vp]
+        L.om_plugin_semantic_argmax.argtypes = [vp, C.c_char_p, vp]
         L.om_accumulate.restype = vp
         L.om_accumulate.argtypes = L.om_input_pointcloud.argtypes + [C.POINTER(C.c_int)]
         L.om_fuse_rows.argtypes = [vp, vp, C.c_int, C.c_int]
@@ -202,6 +205,27 @@ class OracleMap:
         st = lib().om_fuse_rows(self._h, frame._h, row_lo, row_hi)
         if st != 0:
             raise OracleError(st, "om_fuse_rows")
+
+    def normals(self):
+        out = np.empty((3, self.rows, self.cols), np.float32)
+        lib().om_plugin_normals(self._h, out.ctypes.data)
+        return out
+
+    def traversability(self, slope_max, step_max):
+        """slope_max (rad): cos(slope_max) is rounded once to fp32 (reading D36)."""
+        out = np.empty((self.rows, self.cols), np.float32)
+        st = lib().om_plugin_traversability(self._h, C.c_float(float(np.float32(np.cos(slope_max)))),
+                                            C.c_float(step_max), out.ctypes.data)
+        if st != 0:
+            raise OracleError(st, "om_plugin_traversability")
+        return out
+
+    def semantic_argmax(self, group):
+        out = np.empty((2, self.rows, self.cols), np.float32)
+        st = lib().om_plugin_semantic_argmax(self._h, group.encode(), out.ctypes.data)
+        if st != 0:
+            raise OracleError(st, "om_plugin_semantic_argmax")
+        return out
 
     def set_occlusion(self, enable=True, eps_occ=1e-4):
         lib().om_set_occlusion(self._h, int(enable), C.c_float(eps_occ))

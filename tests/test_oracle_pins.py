@@ -726,3 +726,83 @@ def test_visibility_random_terrain_vs_dense_sampling():
         occluded += sum(not d for d in dense.values())
     assert total > 20000 and occluded > 1000
     assert agree / total >= 0.98, agree / total
+
+
+# ---------------------------------------------------------------- NEXT-3 plugins
+def flat_map(n0, n1, res, elev, valid=None, groups=()):
+    m = OracleMap(res, n0, n1, list(groups))
+    m.set_layer("elevation", np.asarray(elev, np.float32))
+    m.set_layer("valid", np.ones((n0, n1), np.float32) if valid is None else np.asarray(valid, np.float32))
+    return m
+
+
+def test_normals_spec_and_planes(golden):
+    res, n0, n1 = 0.1, 12, 9
+    x = (np.arange(n0) + 0.5 - n0 / 2) * res
+    y = (np.arange(n1) + 0.5 - n1 / 2) * res
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    nrm = flat_map(n0, n1, res, np.zeros((n0, n1))).normals()
+    assert (nrm[2] == 1.0).all() and (nrm[:2] == 0.0).all()  # flat map -> (0, 0, 1)
+    nrm = flat_map(n0, n1, res, X).normals()  # plane z = x (45 deg) -> (-sqrt2/2, 0, sqrt2/2)
+    want = np.array(golden["plugins"]["normal_plane_z_eq_x"])
+    assert np.abs(nrm.reshape(3, -1).T - want).max() < 1e-6
+    rng = np.random.default_rng(5)
+    for _ in range(5):  # any plane: the analytic unit normal, one-sided differences included
+        a, b, c0 = rng.uniform(-2, 2, 3)
+        nrm = flat_map(n0, n1, res, a * X + b * Y + c0).normals()
+        want = np.array([-a, -b, 1.0]) / math.sqrt(a * a + b * b + 1.0)
+        assert np.abs(nrm.reshape(3, -1).T - want).max() < 2e-5
+    valid = np.zeros((n0, n1))
+    valid[5, 4] = 1  # isolated valid cell -> invalid output
+    valid[8, 2:5] = 1  # a row strip: no neighbour along x -> invalid
+    nrm = flat_map(n0, n1, res, np.zeros((n0, n1)), valid).normals()
+    assert np.isnan(nrm).all()
+
+
+def test_traversability_spec():
+    res, n = 0.1, 16
+    x = (np.arange(n) + 0.5 - n / 2) * res
+    X = np.repeat(x[:, None], n, 1)
+    flat = flat_map(n, n, res, np.zeros((n, n)))
+    assert (flat.traversability(math.radians(45), 0.3) == 1.0).all()
+    wall = np.zeros((n, n))
+    wall[8:, :] = 2.0
+    t = flat_map(n, n, res, wall).traversability(math.radians(45), 0.3)
+    assert (t[7:9] == 0.0).all() and (t[:6] == 1.0).all() and (t[10:] == 1.0).all()
+    scores = []
+    for deg in (10, 20, 30, 40):  # ramps under slope_max = 45 deg: interior in (0, 1), monotone
+        s = flat_map(n, n, res, np.tan(math.radians(deg)) * X).traversability(math.radians(45), 10.0)
+        inner = s[2:-2, 2:-2]
+        assert ((inner > 0) & (inner < 1)).all()
+        expect = (math.cos(math.radians(deg)) - math.cos(math.radians(45))) / (1 - math.cos(math.radians(45)))
+        assert abs(float(inner.mean()) - expect) < 1e-5
+        scores.append(float(inner.mean()))
+    assert scores == sorted(scores, reverse=True)
+
+
+def test_semantic_argmax_spec_and_brute_force(golden):
+    res, n0, n1 = 0.1, 6, 5
+    for case in golden["plugins"]["argmax_cases"]:
+        K = len(case["theta"])
+        m = flat_map(n0, n1, res, np.zeros((n0, n1)), groups=[dict(name="c", rule=CLASS_AVERAGE, n_channels=K, w=1.0)])
+        for k, v in enumerate(case["theta"]):
+            m.set_layer(f"c_{k}", v)
+        m.set_layer("c_observed", 1)
+        out = m.semantic_argmax("c")
+        assert (out[0] == case["id"]).all() and np.allclose(out[1], case["conf"])
+    rng = np.random.default_rng(9)
+    K = 7
+    m = flat_map(n0, n1, res, np.zeros((n0, n1)), groups=[dict(name="d", rule=CLASS_BAYESIAN, n_channels=K, alpha0=1.0)])
+    alpha = rng.integers(1, 5, (K, n0, n1)).astype(np.float32)  # integer alphas: many exact ties
+    for k in range(K):
+        m.set_layer(f"d_alpha_{k}", alpha[k])
+    obs = (rng.uniform(size=(n0, n1)) > 0.2).astype(np.float32)
+    m.set_layer("d_observed", obs)
+    out = m.semantic_argmax("d")
+    theta = np.stack([m.get_layer(f"d_{k}") for k in range(K)])
+    brute = np.argmax(theta, 0)  # numpy: first maximal index
+    assert (out[0][obs > 0] == brute[obs > 0]).all()
+    assert (out[1][obs > 0] == theta.max(0)[obs > 0]).all()
+    assert (out[0][obs == 0] == -1).all() and (out[1][obs == 0] == 0).all()
+    with pytest.raises(OracleError):
+        flat_map(n0, n1, res, np.zeros((n0, n1)), groups=[dict(name="f", rule=AVERAGE, n_channels=1)]).semantic_argmax("f")
