@@ -321,6 +321,15 @@ def side_c3_c4(torch, M, stream, frames=2):
     mp.profile(False)
     prof = mp.profile_read(reset=True)
     out["c3"]["stage_ms"] = {k: v[0] for k, v in prof.items() if v[1]}
+    # NEXT-3 plugins on the fused C3 map (device outputs)
+    o3 = torch.empty((3, c["rows"], c["cols"]), device="cuda")
+    t1 = torch.empty((1, c["rows"], c["cols"]), device="cuda")
+    o2 = torch.empty((2, c["rows"], c["cols"]), device="cuda")
+    out["plugins_c3_map"] = {
+        "workload": "NEXT-3 plugins on the 250x250 C3 map",
+        "normals_us": 1e3 * timed_loop(torch, stream, 50, lambda i: mp.normals(out=o3)),
+        "traversability_us": 1e3 * timed_loop(torch, stream, 50, lambda i: mp.traversability(0.6, 0.1, out=t1)),
+        "semantic_argmax_us": 1e3 * timed_loop(torch, stream, 50, lambda i: mp.semantic_argmax("sem", out=o2))}
     # NEXT-1: the same frames with the Bresenham occlusion test in the image association
     mp.set_image_occlusion(True, 1e-4)
     ms_occ = timed_loop(torch, stream, 20, c3_step)

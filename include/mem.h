@@ -195,6 +195,27 @@ MEM_API mem_status mem_input_image(mem_map *map, const float *img, int C, int H,
 MEM_API mem_status mem_input_image_batch(mem_map *map, const float *img, int C, int H, int W, const mem_binding *bind,
                                  int n_bind, const double *K, const double *R, const double *t);
 
+/* ---- post-processing plugins on the fused map (PAPER.md:379-385,
+ * Table II rows "normal calculation", "traversability"; DESIGN.md readings
+ * D35-D37).  Outputs are logical row-major float32 planes [k][n_maps][rows][cols] into `out`
+ * (host or device, like mem_get_layer); no stored layer changes. ---- */
+
+/* 3 planes normal_x, normal_y, normal_z: unit (-gx, -gy, 1)/|.| with gx (rows, +x) and gy
+ * (cols, +y) the central difference of the valid neighbours, one-sided when only one is
+ * valid; NaN for invalid cells and cells without a valid neighbour along either axis. */
+MEM_API mem_status mem_plugin_normals(const mem_map *map, float *out);
+
+/* 1 plane in [0, 1]: clamp(min(slope, step), 0, 1), slope = (n_z - cos(slope_max)) /
+ * (1 - cos(slope_max)) with cos rounded once to fp32, step = 1 - max |h_nb - h| / step_max over
+ * the valid 8-neighbours; NaN where the normal is invalid.  slope_max in radians.
+ * Errors: EINVAL (step_max <= 0, cos(slope_max) >= 1). */
+MEM_API mem_status mem_plugin_traversability(const mem_map *map, float slope_max, float step_max, float *out);
+
+/* 2 planes class_id, confidence: argmax_k theta_k of a class group (class_bayesian: alpha /
+ * sum alpha as read out; class_average: its values; class_max: its label and conf), ties to
+ * the lowest class; -1 and 0 where unobserved.  Errors: ENOTFOUND, ERULE (not a class rule). */
+MEM_API mem_status mem_plugin_semantic_argmax(const mem_map *map, const char *group, float *out);
+
 /* Image association with the occlusion test of PAPER.md:234-236, for
  * the following mem_input_image[_batch] calls of this map (default off: frustum only, D18).
  * A valid in-frustum cell is fused only if every intermediate cell of the Bresenham line from

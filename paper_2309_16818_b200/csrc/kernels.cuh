@@ -116,6 +116,18 @@ struct ReadArgs {
   const float *src;            // write
 };
 
+// NEXT-3 post-processing plugins: one thread per logical cell
+struct PostArgs {
+  Geometry geo;
+  State st;
+  const int2 *ring;
+  int op;                      // 0 normals (3 layers), 1 traversability, 2 semantic argmax (2 layers)
+  float cos_max, step_max;     // traversability
+  int rule, first, K, flag, label;  // argmax: group rule, first value word, classes, observed flag, label word
+  float *out;                  // [n_layers][n_maps][H][W] logical row-major
+};
+cudaError_t launch_post(const PostArgs &a, cudaStream_t s);
+
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s);

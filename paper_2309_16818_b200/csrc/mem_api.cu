@@ -1424,6 +1424,78 @@ mem_status mem_frame_stats(const mem_map *m, mem_stats *out) {
   return MEM_OK;
 }
 
+// NEXT-3 plugins: one k_post launch into `layers` output planes (host or device `out`)
+static mem_status run_post(mem_map *m, PostArgs &a, int layers, float *out) {
+  if (!out) return fail(MEM_EINVAL, "out is NULL");
+  if (set_device(m)) return MEM_ECUDA;
+  mem_status fs = flush_shift(m);
+  if (fs == MEM_OK) fs = shard_gather_all(m);
+  if (fs != MEM_OK) return fs;
+  a.geo = m->geo();
+  a.st = m->st;
+  a.ring = m->ring;
+  const size_t bytes = sizeof(float) * (size_t)layers * m->B * m->H * m->W;
+  const bool dev = is_device_ptr(out);
+  if (dev) {
+    a.out = out;
+  } else {
+    mem_status s = grow((void **)&m->dout, &m->dout_cap, bytes, m->stream);
+    if (s != MEM_OK) return s;
+    a.out = m->dout;
+  }
+  TIMED(MEM_STAGE_READ, launch_post(a, m->stream));
+  if (!dev) {
+    TIMED(MEM_STAGE_D2H, cudaMemcpyAsync(out, m->dout, bytes, cudaMemcpyDeviceToHost, m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+  }
+  return MEM_OK;
+}
+
+mem_status mem_plugin_normals(const mem_map *cm, float *out) {
+  mem_map *m = const_cast<mem_map *>(cm);
+  if (check_map(m)) return MEM_EINVAL;
+  PostArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = 0;
+  return run_post(m, a, 3, out);
+}
+
+mem_status mem_plugin_traversability(const mem_map *cm, float slope_max, float step_max, float *out) {
+  mem_map *m = const_cast<mem_map *>(cm);
+  if (check_map(m)) return MEM_EINVAL;
+  const float cos_max = (float)std::cos((double)slope_max);  // rounded once to fp32 (D36)
+  if (!(step_max > 0.0f) || !std::isfinite(step_max) || !(cos_max < 1.0f))
+    return fail(MEM_EINVAL, "traversability: need step_max > 0 and cos(slope_max) < 1");
+  PostArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = 1;
+  a.cos_max = cos_max;
+  a.step_max = step_max;
+  return run_post(m, a, 1, out);
+}
+
+mem_status mem_plugin_semantic_argmax(const mem_map *cm, const char *group, float *out) {
+  mem_map *m = const_cast<mem_map *>(cm);
+  if (check_map(m)) return MEM_EINVAL;
+  if (!group) return fail(MEM_EINVAL, "group is NULL");
+  int gi = -1;
+  for (int k = 0; k < m->ng; ++k)
+    if (m->gname[k] == group) gi = k;
+  if (gi < 0) return fail(MEM_ENOTFOUND, "no group named '%s'", group);
+  const GroupDesc &gd = m->g[gi];
+  if (gd.rule != MEM_CLASS_BAYESIAN && gd.rule != MEM_CLASS_AVERAGE && gd.rule != MEM_CLASS_MAX)
+    return fail(MEM_ERULE, "semantic argmax needs a class rule (group '%s')", group);
+  PostArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = 2;
+  a.rule = gd.rule;
+  a.first = gd.word0;
+  a.K = gd.nch;
+  a.flag = gd.flag;
+  a.label = gd.label;
+  return run_post(m, a, 2, out);
+}
+
 mem_status mem_set_image_occlusion(mem_map *m, int enable, float eps_occ) {
   if (check_map(m)) return MEM_EINVAL;
   if (!(eps_occ >= 0.0f) || !std::isfinite(eps_occ)) return fail(MEM_EINVAL, "eps_occ must be finite and >= 0");

@@ -33,7 +33,8 @@ EXPORTS = ["mem_create", "mem_create_batch", "mem_destroy", "mem_set_stream", "m
            "mem_move_to", "mem_move_to_batch", "mem_get_layer", "mem_set_layer", "mem_get_layer_names",
            "mem_memory_footprint", "mem_get_info", "mem_get_center", "mem_frame_stats", "mem_debug_point_codes",
            "mem_profile", "mem_profile_read", "mem_pca_readout", "mem_nccl_unique_id", "mem_create_sharded",
-           "mem_shard_local_sync", "mem_set_image_occlusion", "mem_last_error", "mem_version"]
+           "mem_shard_local_sync", "mem_set_image_occlusion", "mem_plugin_normals",
+           "mem_plugin_traversability", "mem_plugin_semantic_argmax", "mem_last_error", "mem_version"]
 STAGES = ["shift", "point", "cell", "image", "read", "write", "h2d", "d2h"]
 
 
@@ -98,6 +99,9 @@ _sig = {
                            C.c_int, _P(_vp)],
     "mem_shard_local_sync": [_P(_vp), C.c_int],
     "mem_set_image_occlusion": [_vp, C.c_int, C.c_float],
+    "mem_plugin_normals": [_vp, _vp],
+    "mem_plugin_traversability": [_vp, C.c_float, C.c_float, _vp],
+    "mem_plugin_semantic_argmax": [_vp, C.c_char_p, _vp],
     "mem_profile_read": [_vp, _P(C.c_double), _P(C.c_uint64), C.c_int],
 }
 for _n, _a in _sig.items():
@@ -359,6 +363,26 @@ class Map:
         self.h = _handle if _handle is not None else mem_create(
             resolution, rows, cols, groups, MEM_FLAG_DEBUG_POINTS if debug_points else 0, stream, n_maps)
         self._last_n = 0
+
+    def _plugin(self, planes, call, *args, out=None):
+        shape = (planes, self.n_maps, self.rows, self.cols) if self.n_maps > 1 else (planes, self.rows, self.cols)
+        if out is None:
+            out = np.empty(shape, np.float32)
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        _check(call(self.h, *args, C.c_void_p(ptr)), call.__name__)
+        return out
+
+    def normals(self, out=None):
+        """NEXT-3: normal_x, normal_y, normal_z planes (include/mem.h)."""
+        return self._plugin(3, _lib.mem_plugin_normals, out=out)
+
+    def traversability(self, slope_max, step_max, out=None):
+        r = self._plugin(1, _lib.mem_plugin_traversability, C.c_float(slope_max), C.c_float(step_max), out=out)
+        return r[0] if out is None else r
+
+    def semantic_argmax(self, group, out=None):
+        """NEXT-3: class_id, confidence planes of a class group."""
+        return self._plugin(2, _lib.mem_plugin_semantic_argmax, group.encode(), out=out)
 
     def set_image_occlusion(self, enable=True, eps_occ=1e-4):
         """NEXT-1: Bresenham occlusion test for the following image inputs (include/mem.h)."""

@@ -567,3 +567,32 @@ def test_c3_with_occlusion_full_size():
         o.input_image(im["img"], binds, im["K"], im["R"], im["t"])
         compare_layers(g, o, where=f"C3+occlusion frame {f}: ")
     assert (g.get_layer("top_label") >= 0).sum() > 5000
+
+
+# ---------------------------------------------------------------- NEXT-3 plugins
+def test_plugins_vs_oracle():
+    """normals, traversability and semantic argmax (include/mem.h NEXT-3) on a fused random
+    map with holes, after shifts (the ring is unrolled): bit-exact labels, fp32 tolerance."""
+    rows, cols, res = 64, 48, 0.05
+    g, o = make_pair(res, rows, cols, ALL_GROUPS)
+    for f, (x, y) in enumerate([(0.0, 0.0), (0.12, -0.07), (0.31, 0.2)]):
+        g.move_to(x, y)
+        o.move_to(x, y)
+        pts = random_all_channels(700 + f, 9000, rows, cols, res)
+        step_points(g, o, pts, ALL_BINDS, S.rot_z(0.2 * f), np.array([x, y, 1.0]), NOISE_R)
+    tol = lambda a, b: np.array_equal(np.isnan(a), np.isnan(b)) and np.all(
+        np.abs(a[~np.isnan(b)] - b[~np.isnan(b)]) <= 1e-6 + 1e-5 * np.abs(b[~np.isnan(b)]))
+    gn, on = np.asarray(g.normals()), o.normals()
+    assert tol(gn, on) and (~np.isnan(on[2])).sum() > 1000
+    for smax, stepmax in ((0.7, 0.2), (1.2, 0.05)):
+        assert tol(np.asarray(g.traversability(smax, stepmax)), o.traversability(smax, stepmax))
+    for grp in ("cavg", "sem", "top"):
+        ga, oa = np.asarray(g.semantic_argmax(grp)), o.semantic_argmax(grp)
+        assert np.array_equal(ga[0], oa[0]), grp
+        assert tol(ga[1], oa[1]), grp
+        assert (oa[0] >= 0).sum() > 1000
+    with pytest.raises(M.MemError):
+        g.semantic_argmax("feat")
+    d = torch.empty((3, rows, cols), device="cuda")
+    g.normals(out=d)
+    assert tol(d.cpu().numpy(), on)
