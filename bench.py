@@ -291,6 +291,48 @@ def side_c5b(torch, M, stream, rank, world, dist, steps=10):
             "scaling": "strong (4M points total)"}
 
 
+def side_paper_sweep(torch, M, stream, iters=300):
+    """SURVEY §8(f) NEXT-4, the paper's performance setup (Table II, Fig. 6):
+    250x250 @ 4 cm, a 230,400-point semantic cloud per frame, the multi-modal update swept over
+    L in {1, 2, 4, 8, 16, 20} layers for exponential averaging and Bayesian inference; 300
+    iterations per point (CUDA events).  Reports ms per frame, the multi-modal share (frame
+    time minus the height-only frame) and a least-squares line with its R^2."""
+    c = S.PAPER
+    out = {"workload": "PAPER: 250x250@0.04m, 230400-pt semantic cloud (ZED 2i 360x640), layer sweep",
+           "iterations": iters}
+
+    def frame_ms(groups, binds, n_layers):
+        clouds = [S.paper_cloud(max(n_layers, 1), f) for f in range(2)]
+        dev = [torch.from_numpy(np.ascontiguousarray(cl["points"][:, :3 + n_layers])).cuda() for cl in clouds]
+        mp = M.Map(c["res"], c["rows"], c["cols"], groups)
+
+        def step(i):
+            cl = clouds[i % 2]
+            mp.move_to(*cl["move"])
+            mp.input_pointcloud(dev[i % 2], binds, cl["R"], cl["t"], c["noise"])
+
+        ms = timed_loop(torch, stream, iters, step)
+        mp.close()
+        return ms
+
+    base = frame_ms([], [], 0)
+    out["height_only_ms"] = base
+    for name, rule in (("exponential_averaging", 0), ("bayesian", 3)):
+        xs, ys = [], []
+        for L in c["layers"]:
+            if rule == 3 and L < 2:
+                continue
+            ms = frame_ms([dict(name="sem", rule=rule, n_channels=L, w=0.5, alpha0=1.0)], [(0, L, 0)], L)
+            xs.append(L)
+            ys.append(ms)
+        x, y = np.array(xs, float), np.array(ys)
+        slope, icpt = np.polyfit(x, y, 1)
+        r2 = 1.0 - ((y - (slope * x + icpt)) ** 2).sum() / max(((y - y.mean()) ** 2).sum(), 1e-30)
+        out[name] = {"layers": xs, "ms_per_frame": ys, "multimodal_ms": [v - base for v in ys],
+                     "fit_ms_per_layer": slope, "fit_intercept_ms": icpt, "r2": r2}
+    return out
+
+
 def side_c3_c4(torch, M, stream, frames=2):
     out = {}
     c = S.C3
@@ -513,6 +555,7 @@ def run_mem(a):
             sides["c5b"] = side_c5b(torch, M, stream, rank, world, dist)
         if rank == 0:
             sides.update(side_c3_c4(torch, M, stream))
+            sides["paper_sweep"] = side_paper_sweep(torch, M, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:

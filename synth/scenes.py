@@ -515,3 +515,32 @@ def c5b_shard(frame, rank, nranks, seed=5, points=C5B["points"]):
     p[(kind >= 0.01) & (kind < 0.015), 0] = np.nan
     feat = blk + rng.normal(0.0, 0.05, n)
     return dict(points=np.concatenate([p, feat[:, None]], 1).astype(np.float32), R=R, t=t, move=(t[0], t[1]))
+
+
+# --------------------------------------------------------------------------------------
+# PAPER: the performance setup of PAPER.md:404-408 / Table II / Fig. 6:
+# 250x250 @ 0.04 m map, one ZED-2i-like 360x640 RGB-D camera -> a 230,400-point semantic cloud
+# whose channels are L class probabilities (softmax of 4 onehot + N(0,1) over L classes)
+# --------------------------------------------------------------------------------------
+PAPER = dict(res=0.04, rows=250, cols=250, W=640, H=360, f=340.0, cam_h=0.7, pitch=math.radians(25.0),
+             layers=(1, 2, 4, 8, 16, 20), noise=C3["noise"])
+
+
+def paper_cloud(n_layers, frame=0, seed=6):
+    """(230400, 3 + L) float32 [x y z p_0..p_{L-1}] in the camera frame (no-return pixels NaN),
+    R, t, move.  The class of a point is the scene's object id modulo L."""
+    c = PAPER
+    rng = np.random.default_rng([seed, frame, n_layers])
+    scene = c3_scene(3)
+    x0, y0 = 0.009 + 0.029 * frame, 0.009 - 0.013 * frame
+    assert_tie_guard(x0, c["res"])
+    assert_tie_guard(y0, c["res"])
+    eye = np.array([x0, y0, c["cam_h"]])
+    R = camera_yaw_pitch(eye, 0.05 * frame, c["pitch"])
+    pts, hit, pw = depth_frame(scene, R, eye, rng, c["W"], c["H"], c["f"], c["noise"]["a"], c["noise"]["b"])
+    cls, _ = scene.attributes(pw[:, 0], pw[:, 1], pw[:, 2])
+    cls = np.where(hit, cls, 0) % n_layers
+    logits = 4.0 * np.eye(n_layers)[cls] + rng.normal(0.0, 1.0, (len(cls), n_layers))
+    p = np.exp(logits - logits.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    return dict(points=np.concatenate([pts, p.astype(np.float32)], 1), R=R, t=eye, move=(x0, y0))

@@ -596,3 +596,19 @@ def test_plugins_vs_oracle():
     d = torch.empty((3, rows, cols), device="cuda")
     g.normals(out=d)
     assert tol(d.cpu().numpy(), on)
+
+
+# ---------------------------------------------------------------- NEXT-4 paper-shaped workload
+@pytest.mark.parametrize("rule,L", [(M.MEM_AVERAGE, 4), (M.MEM_CLASS_BAYESIAN, 20)])
+def test_paper_cloud_full_size(rule, L):
+    """the 230,400-point semantic cloud of the paper's performance setup."""
+    c = S.PAPER
+    groups = [dict(name="sem", rule=rule, n_channels=L, w=0.5, alpha0=1.0)]
+    g, o = make_pair(c["res"], c["rows"], c["cols"], groups)
+    for f in range(2):
+        cl = S.paper_cloud(L, f)
+        g.move_to(*cl["move"])
+        o.move_to(*cl["move"])
+        step_points(g, o, cl["points"], [(0, L, 0)], cl["R"], cl["t"], c["noise"])
+        compare_layers(g, o, where=f"paper cloud L={L} frame {f}: ")
+    assert g.get_layer("sem_observed").sum() > 5000
