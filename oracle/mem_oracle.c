@@ -68,6 +68,7 @@ typedef struct {
   int ch_offset; /* point clouds: channel index counted from float 3; images: from channel 0 */
   int n_ch;
   int group;
+  int topk;      /* > 0: n_ch = 2 topk channels (class id, probability) pairs (NEXT-2, D38) */
 } om_binding;
 
 typedef struct {
@@ -185,6 +186,31 @@ static int pose_ok(const double R[9]) {
   double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
                R[2] * (R[3] * R[7] - R[4] * R[6]);
   return fabs(det - 1.0) <= 1e-6;
+}
+
+/* top-k class input ("inputting the top k classes", SPEC.md:144-147,
+ * 168-176 expand_topk; reading D38): the group's last class (index K = nch - 1) is the
+ * reserved "other" class.  dense[id_j] += p_j, dense[K] = 1 - sum_j p_j (fp32, pair order);
+ * returns 0 (the group skips this point / pixel, like a non-finite channel, D31) if a value is
+ * non-finite or an id is not an integer in [0, K). */
+static int expand_topk(const float *ch, long step, int k, int nch, float *dense) {
+  const int K = nch - 1;
+  for (int c = 0; c < nch; ++c) dense[c] = 0.0f;
+  float sp = 0.0f;
+  for (int j = 0; j < k; ++j) {
+    const float id = ch[(long)(2 * j) * step], pj = ch[(long)(2 * j + 1) * step];
+    if (!isfinite(id) || !isfinite(pj) || id != floorf(id) || id < 0.0f || id >= (float)K) return 0;
+    dense[(int)id] += pj;
+    sp += pj;
+  }
+  dense[K] = 1.0f - sp;
+  return 1;
+}
+
+static int topk_binding_ok(const om_group *g, const om_binding *b) {
+  if (b->topk <= 0) return 1;
+  return (g->rule == OM_CLASS_AVERAGE || g->rule == OM_CLASS_BAYESIAN || g->rule == OM_CLASS_MAX) &&
+         b->n_ch == 2 * b->topk;
 }
 
 static int binding_width_ok(const om_group *g, int n_ch, int is_image) {
@@ -316,7 +342,8 @@ om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const o
   for (int b = 0; b < nb; ++b) {
     if (bind[b].group < 0 || bind[b].group >= m->ng) return NULL;
     if (bind[b].ch_offset < 0 || 3 + bind[b].ch_offset + bind[b].n_ch > stride) return NULL;
-    if (!binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 0)) return NULL;
+    if (bind[b].topk > 0 ? !topk_binding_ok(&m->g[bind[b].group], &bind[b])
+                         : !binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 0)) return NULL;
     for (int c = 0; c < b; ++c) if (bind[c].group == bind[b].group) return NULL;
   }
   const long cells = ncells(m);
@@ -423,13 +450,19 @@ om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const o
         gsum[b][(long)2 * cells + j] += (double)(bits & 255u);
         continue;
       }
+      float dense[257];
+      const float *src = ch;
+      if (bind[b].topk > 0) { /* NEXT-2: expand the top-k pairs first (D38) */
+        if (!expand_topk(ch, 1, bind[b].topk, g->nch, dense)) continue;
+        src = dense;
+      }
       int finite = 1;
-      for (int k = 0; k < g->nch; ++k) finite &= isfinite(ch[k]) ? 1 : 0;
+      for (int k = 0; k < g->nch; ++k) finite &= isfinite(src[k]) ? 1 : 0;
       if (!finite) continue; /* D31 */
       ng[b][j]++;
-      for (int k = 0; k < g->nch; ++k) gsum[b][(long)k * cells + j] += (double)ch[k];
+      for (int k = 0; k < g->nch; ++k) gsum[b][(long)k * cells + j] += (double)src[k];
       if (g->rule == OM_CLASS_MAX) {
-        uint64_t key = class_max_key(ch, g->nch, 1);
+        uint64_t key = class_max_key(src, g->nch, 1);
         if (key > gkey[b][j]) gkey[b][j] = key;
       }
     }
@@ -567,7 +600,8 @@ int om_input_image(om_map *m, const float *img, int C, int IH, int IW, const om_
   for (int b = 0; b < nb; ++b) {
     if (bind[b].group < 0 || bind[b].group >= m->ng) return OM_EINVAL;
     if (bind[b].ch_offset < 0 || bind[b].ch_offset + bind[b].n_ch > C) return OM_EINVAL;
-    if (!binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 1)) return OM_EINVAL;
+    if (bind[b].topk > 0 ? !topk_binding_ok(&m->g[bind[b].group], &bind[b])
+                         : !binding_width_ok(&m->g[bind[b].group], bind[b].n_ch, 1)) return OM_EINVAL;
     for (int c = 0; c < b; ++c) if (bind[c].group == bind[b].group) return OM_EINVAL;
   }
   const long cells = ncells(m);
@@ -604,17 +638,25 @@ int om_input_image(om_map *m, const float *img, int C, int IH, int IW, const om_
       for (int b = 0; b < nb; ++b) {
         om_group *g = &m->g[bind[b].group];
         const float *ch = img + (long)bind[b].ch_offset * plane + pix;
+        float dense[257];
+        long step = plane;
+        if (bind[b].topk > 0) { /* NEXT-2: expand the top-k pairs first (D38) */
+          if (!expand_topk(ch, plane, bind[b].topk, g->nch, dense)) continue;
+          ch = dense;
+          step = 1;
+        }
+        const int width = bind[b].topk > 0 ? g->nch : bind[b].n_ch;
         int finite = 1;
-        for (int k = 0; k < bind[b].n_ch; ++k) finite &= isfinite(ch[(long)k * plane]) ? 1 : 0;
+        for (int k = 0; k < width; ++k) finite &= isfinite(ch[(long)k * step]) ? 1 : 0;
         if (!finite) continue;
-        for (int k = 0; k < bind[b].n_ch; ++k) sums[k] = (double)ch[(long)k * plane];
+        for (int k = 0; k < width; ++k) sums[k] = (double)ch[(long)k * step];
         switch (g->rule) {
           case OM_AVERAGE:
           case OM_CLASS_AVERAGE:
           case OM_COLOR: fuse_average(g, j, cells, 1, sums); break;
           case OM_GAUSSIAN: fuse_gaussian(g, j, cells, 1, sums); break;
           case OM_CLASS_BAYESIAN: fuse_dirichlet(g, j, cells, sums); break;
-          case OM_CLASS_MAX: store_class_max(g, j, class_max_key(ch, g->nch, plane)); break;
+          case OM_CLASS_MAX: store_class_max(g, j, class_max_key(ch, g->nch, step)); break;
         }
       }
     }

@@ -30,7 +30,7 @@ class _Spec(C.Structure):
 
 
 class _Bind(C.Structure):
-    _fields_ = [("ch_offset", C.c_int), ("n_ch", C.c_int), ("group", C.c_int)]
+    _fields_ = [("ch_offset", C.c_int), ("n_ch", C.c_int), ("group", C.c_int), ("topk", C.c_int)]
 
 
 class _Noise(C.Structure):
@@ -95,8 +95,8 @@ class OracleError(RuntimeError):
 
 def make_binds(bindings):
     arr = (_Bind * max(1, len(bindings)))()
-    for i, (off, n, g) in enumerate(bindings):
-        arr[i] = _Bind(off, n, g)
+    for i, b in enumerate(bindings):  # (ch_offset, n_ch, group[, topk])
+        arr[i] = _Bind(*b)
     return arr
 
 

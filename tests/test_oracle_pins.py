@@ -806,3 +806,53 @@ def test_semantic_argmax_spec_and_brute_force(golden):
     assert (out[0][obs == 0] == -1).all() and (out[1][obs == 0] == 0).all()
     with pytest.raises(OracleError):
         flat_map(n0, n1, res, np.zeros((n0, n1)), groups=[dict(name="f", rule=AVERAGE, n_channels=1)]).semantic_argmax("f")
+
+
+# ---------------------------------------------------------------- NEXT-2 top-k class input
+def topk_point(pairs, stride_pad=0):
+    ch = [v for pr in pairs for v in pr]
+    return put([[0.05, 0.05, 0.0]], ch=[ch + [0.0] * stride_pad])
+
+
+def test_topk_spec_examples(golden):
+    """expand_topk seen through a class_average group with w = 1 (theta = the
+    frame mean = the expanded vector of the single point) and class_max."""
+    for case in golden["topk"]["cases"]:
+        K, pairs, dense = case["K"], case["pairs"], case["dense"]
+        m = OracleMap(0.1, 4, 4, [dict(name="c", rule=CLASS_AVERAGE, n_channels=K + 1, w=1.0),
+                                   dict(name="x", rule=CLASS_MAX, n_channels=K + 1)])
+        k = len(pairs)
+        m.input_pointcloud(topk_point(pairs), [(0, 2 * k, 0, k), (0, 2 * k, 1, k)], EYE, [0, 0, 0], NOISE)
+        got = [float(m.get_layer(f"c_{c}")[2, 2]) for c in range(K + 1)]
+        assert np.allclose(got, dense, atol=1e-7), (got, dense)
+        assert abs(sum(got) - 1.0) < 1e-6  # SPEC.md:183
+        assert m.get_layer("x_label")[2, 2] == int(np.argmax(dense))
+    bad = golden["topk"]["bad_id"]  # an id outside the vocabulary: the group skips the point (D38)
+    m = OracleMap(0.1, 4, 4, [dict(name="c", rule=CLASS_BAYESIAN, n_channels=bad["K"] + 1, alpha0=1.0)])
+    m.input_pointcloud(topk_point(bad["pairs"]), [(0, 2, 0, 1)], EYE, [0, 0, 0], NOISE)
+    assert m.get_layer("c_observed").sum() == 0 and m.get_layer("valid").sum() == 1
+
+
+def test_topk_equals_dense_input():
+    """a top-k point cloud fuses exactly like the dense (K + 1)-vector it expands to, built here
+    independently with numpy (Dirichlet, class average and class max, many points and cells)."""
+    rng = np.random.default_rng(21)
+    K, k, n, res = 6, 3, 4000, 0.1
+    ids = np.stack([rng.choice(K, k, replace=False) for _ in range(n)]).astype(np.float32)
+    p = rng.dirichlet(np.ones(k + 1), n)[:, :k].astype(np.float32)
+    dense = np.zeros((n, K + 1), np.float32)
+    for j in range(k):
+        dense[np.arange(n), ids[:, j].astype(int)] += p[:, j]
+    dense[:, K] = np.float32(1.0) - ((p[:, 0] + p[:, 1]) + p[:, 2])  # 1 - sum, the sum fp32 in pair order
+    xy = rng.uniform(-0.75, 0.75, (n, 2))
+    xyz = np.concatenate([xy, rng.normal(0, 0.01, (n, 1))], 1)
+    pairs = np.stack([ids, p], 2).reshape(n, 2 * k)
+    groups = [dict(name="d", rule=CLASS_BAYESIAN, n_channels=K + 1, alpha0=0.5),
+              dict(name="a", rule=CLASS_AVERAGE, n_channels=K + 1, w=0.7),
+              dict(name="x", rule=CLASS_MAX, n_channels=K + 1)]
+    mt, md = OracleMap(res, 16, 16, groups), OracleMap(res, 16, 16, groups)
+    for f in range(2):
+        mt.input_pointcloud(put(xyz, ch=pairs), [(0, 2 * k, g, k) for g in range(3)], EYE, [0, 0, 0], NOISE)
+        md.input_pointcloud(put(xyz, ch=dense), [(0, K + 1, g) for g in range(3)], EYE, [0, 0, 0], NOISE)
+    for nm in [f"d_alpha_{c}" for c in range(K + 1)] + [f"a_{c}" for c in range(K + 1)] + ["x_label", "x_conf"]:
+        assert np.array_equal(mt.get_layer(nm), md.get_layer(nm)), nm
