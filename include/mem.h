@@ -93,11 +93,19 @@ typedef struct {
 /* Binds an input channel range to a group.  Point clouds: ch_offset counts from float 3 of a
  * point (the first channel after xyz); images: from channel 0.  n_ch must equal the group's
  * input width (color: 1 packed channel for points, 3 for images).  A group may be bound at
- * most once per call; one channel range may feed several groups. */
+ * most once per call; one channel range may feed several groups.
+ * Top-k class input ("inputting the top k classes";
+ * SPEC.md:144-147, 168-176; reading D38): topk = k > 0 binds n_ch = 2k channels
+ * holding (class id, probability) pairs to a class rule group of n_channels = K + 1, whose last
+ * class K is the reserved "other" class: the pairs expand to the dense vector
+ * dense[id_j] += p_j, dense[K] = 1 - sum_j p_j (fp32, pair order), which is then fused like
+ * dense input.  A point/pixel with a non-finite value or an id that is not an integer in
+ * [0, K) skips the group (like a non-finite channel, D31).  topk = 0: dense channels. */
 typedef struct {
   int ch_offset;
   int n_ch;
   int group; /* index into the mem_layer_spec array given at create */
+  int topk;  /* 0 = dense channels; k > 0 = k (id, probability) pairs (see above) */
 } mem_binding;
 
 /* Point noise model and filters (readings D8-D11, D30). */

@@ -46,6 +46,7 @@ struct GroupDesc {
 
 struct BindDesc {  // one binding of a call, resolved against its group
   int ch_offset, nch, group;
+  int topk;  // > 0: nch = 2 topk (id, p) pairs expanding to the group's K + 1 classes (D38)
   GroupDesc g;
 };
 

@@ -198,6 +198,50 @@ struct OpMax {
   __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a > b ? a : b; }
 };
 
+// NEXT-2 (reading D38): the k (id, p) pairs of one point / pixel, `step` floats apart, seen as
+// the dense K + 1 class vector dense[id_j] += p_j, dense[K] = 1 - sum p_j (fp32, pair order)
+struct TopK {
+  const float *ch;
+  long long step;
+  int k, K;
+  __device__ float id(int j) const { return __ldg(ch + (long long)(2 * j) * step); }
+  __device__ float p(int j) const { return __ldg(ch + (long long)(2 * j + 1) * step); }
+  __device__ bool ok() const {  // every value finite, every id an integer in [0, K)
+    for (int j = 0; j < k; ++j) {
+      const float i = id(j), q = p(j);
+      if (!isfinite(i) || !isfinite(q) || i != floorf(i) || i < 0.0f || i >= (float)K) return false;
+    }
+    return true;
+  }
+  __device__ float value(int c) const {
+    float v = 0.0f;
+    if (c == K) {
+      for (int j = 0; j < k; ++j) v += p(j);
+      return 1.0f - v;
+    }
+    for (int j = 0; j < k; ++j)
+      if ((int)id(j) == c) v += p(j);
+    return v;
+  }
+  __device__ bool first(int j) const {  // id(j) does not occur among the earlier pairs
+    for (int i = 0; i < j; ++i)
+      if (id(i) == id(j)) return false;
+    return true;
+  }
+  __device__ unsigned long long key() const {  // D19 class_max key of the dense vector
+    int best = 0;
+    float bv = value(0);
+    for (int c = 1; c <= K; ++c) {
+      const float v = value(c);
+      if (v > bv) {
+        bv = v;
+        best = c;
+      }
+    }
+    return ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(K - best);
+  }
+};
+
 // a8: scatter-accumulate the sufficient statistics of the warp's current points (one per lane,
 // `o.cell < 0` = dropped) into their scratch cells `sc`.  Lanes hitting the same cell are
 // combined first (__match_any_sync + reduce_peers) so that one lane issues the REDs of the
@@ -307,6 +351,19 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     const BindDesc &b = a.b[bi];
     unsigned long long *ga = rec + b.g.acc0;
     const float *ch = p + 3 + b.ch_offset;
+    if (b.topk > 0) {  // top-k pairs (D38): per-lane REDs of the expanded vector's non-zero classes
+      const TopK tk{ch, 1, b.topk, b.g.nch - 1};
+      if (!act || !tk.ok()) continue;
+      if (b.g.rule == MEM_CLASS_MAX) {
+        red_max_u64(ga, tk.key());
+        continue;
+      }
+      red_add_u64(ga, 1ull);
+      for (int j = 0; j < tk.k; ++j)
+        if (tk.first(j)) red_add_f64(ga + 1 + (int)tk.id(j), (double)tk.value((int)tk.id(j)));
+      red_add_f64(ga + 1 + tk.K, (double)tk.value(tk.K));
+      continue;
+    }
     if (b.g.rule == MEM_COLOR) {  // D20: packed 0x00RRGGBB; exact integer sums
       unsigned rg = 0u, bb = 0u;  // r | g << 16 (a warp sums <= 32 * 255 per channel)
       if (act) {
@@ -1370,6 +1427,13 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
   for (int bi = 0; bi < a.nb; ++bi) {
     const BindDesc &b = a.b[bi];
     const float *ch = pix + (long long)b.ch_offset * plane;
+    if (b.topk > 0) {  // top-k pairs (D38)
+      const TopK tk{ch, plane, b.topk, b.g.nch - 1};
+      if (!tk.ok()) continue;
+      const unsigned long long key = b.g.rule == MEM_CLASS_MAX ? tk.key() : 0ull;
+      apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)tk.value(k); }, key);
+      continue;
+    }
     bool fin = true;
     for (int k = 0; k < b.nch; ++k) fin &= (bool)isfinite(__ldg(ch + k * plane));
     if (!fin) continue;  // D21

@@ -321,15 +321,25 @@ mem_status resolve_bindings(const mem_map *m, const mem_binding *bind, int nb, b
     if (b.ch_offset < 0 || b.n_ch < 1 || b.ch_offset + b.n_ch > avail)
       return fail(MEM_EINVAL, "binding %d: channels [%d, %d) outside the %d input channels", i, b.ch_offset,
                   b.ch_offset + b.n_ch, avail);
-    const int want = g.rule == MEM_COLOR ? (image ? 3 : 1) : g.nch;
-    if (b.n_ch != want)
-      return fail(MEM_EINVAL, "binding %d: group '%s' takes %d channel(s), got %d", i, m->gname[b.group].c_str(),
-                  want, b.n_ch);
+    if (b.topk < 0) return fail(MEM_EINVAL, "binding %d: topk %d < 0", i, b.topk);
+    if (b.topk > 0) {  // top-k class input (D38)
+      if (g.rule != MEM_CLASS_AVERAGE && g.rule != MEM_CLASS_BAYESIAN && g.rule != MEM_CLASS_MAX)
+        return fail(MEM_ERULE, "binding %d: top-k input needs a class rule (group '%s')", i,
+                    m->gname[b.group].c_str());
+      if (b.n_ch != 2 * b.topk)
+        return fail(MEM_EINVAL, "binding %d: top-%d input takes %d channels, got %d", i, b.topk, 2 * b.topk, b.n_ch);
+    } else {
+      const int want = g.rule == MEM_COLOR ? (image ? 3 : 1) : g.nch;
+      if (b.n_ch != want)
+        return fail(MEM_EINVAL, "binding %d: group '%s' takes %d channel(s), got %d", i,
+                    m->gname[b.group].c_str(), want, b.n_ch);
+    }
     for (int j = 0; j < i; ++j)
       if (bind[j].group == b.group) return fail(MEM_EINVAL, "group '%s' bound twice", m->gname[b.group].c_str());
     out[i].ch_offset = b.ch_offset;
     out[i].nch = b.n_ch;
     out[i].group = b.group;
+    out[i].topk = b.topk;
     out[i].g = g;
   }
   return MEM_OK;

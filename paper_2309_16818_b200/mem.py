@@ -43,8 +43,8 @@ class mem_layer_spec(C.Structure):
                 ("sigma_f2", C.c_float), ("mu0", C.c_float), ("sigma0_2", C.c_float), ("alpha0", C.c_float)]
 
 
-class mem_binding(C.Structure):
-    _fields_ = [("ch_offset", C.c_int), ("n_ch", C.c_int), ("group", C.c_int)]
+class mem_binding(C.Structure):  # bindings are given as (ch_offset, n_ch, group[, topk]) tuples
+    _fields_ = [("ch_offset", C.c_int), ("n_ch", C.c_int), ("group", C.c_int), ("topk", C.c_int)]
 
 
 class mem_noise(C.Structure):

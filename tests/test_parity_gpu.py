@@ -612,3 +612,48 @@ def test_paper_cloud_full_size(rule, L):
         step_points(g, o, cl["points"], [(0, L, 0)], cl["R"], cl["t"], c["noise"])
         compare_layers(g, o, where=f"paper cloud L={L} frame {f}: ")
     assert g.get_layer("sem_observed").sum() > 5000
+
+
+# ---------------------------------------------------------------- NEXT-2 top-k class input
+def topk_channels(rng, n, K, k, bad_frac=0.02):
+    """(n, 2k) pairs: distinct ids mostly, some repeated ids, some invalid ids / NaN."""
+    ids = np.stack([rng.choice(K, k, replace=False) for _ in range(n)]).astype(np.float32)
+    rep = rng.uniform(size=n) < 0.05
+    ids[rep, 1] = ids[rep, 0]  # a repeated id: its probabilities add up
+    p = rng.dirichlet(np.ones(k + 1), n)[:, :k].astype(np.float32)
+    tie = rng.uniform(size=n) < 0.1
+    p[tie] = np.round(p[tie] * 4) / 4  # exact ties exercise the lowest-index rule of class_max
+    bad = rng.uniform(size=n) < bad_frac
+    ids[bad, 0] = np.where(rng.uniform(size=bad.sum()) < 0.5, K + 2, 1.5)  # out of range / not integer
+    nanm = rng.uniform(size=n) < bad_frac
+    p[nanm, -1] = np.nan
+    return np.stack([ids, p], 2).reshape(n, 2 * k)
+
+
+TOPK_GROUPS = [dict(name="d", rule=M.MEM_CLASS_BAYESIAN, n_channels=9, alpha0=0.5),
+               dict(name="a", rule=M.MEM_CLASS_AVERAGE, n_channels=9, w=0.4),
+               dict(name="x", rule=M.MEM_CLASS_MAX, n_channels=9)]
+
+
+def test_topk_points_and_images_vs_oracle():
+    rows, cols, res, K, k = 50, 44, 0.05, 8, 3
+    g, o = make_pair(res, rows, cols, TOPK_GROUPS)
+    rng = np.random.default_rng(61)
+    noise = dict(a=1e-3, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=9.0, v_out=0.01)
+    binds = [(0, 2 * k, gi, k) for gi in range(3)]
+    Kimg = np.array([[120.0, 0.0, 79.5], [0, 118.0, 59.5], [0, 0, 1.0]])
+    for f in range(4):
+        pts = S.random_cloud(900 + f, 15000, 3, rows, cols, res)
+        pts = np.concatenate([pts, topk_channels(rng, len(pts), K, k)], 1).astype(np.float32)
+        step_points(g, o, pts, binds, np.eye(3), [0.0, 0.0, 1.0], noise)
+        compare_layers(g, o, where=f"top-k points frame {f}: ")
+        eye = np.array([rng.uniform(-3, -2), rng.uniform(-1, 1), rng.uniform(1.0, 2.0)])
+        R = camera_looking_at(eye, [rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), 0.0])
+        img = np.ascontiguousarray(topk_channels(rng, 120 * 160, K, k).T.reshape(2 * k, 120, 160))
+        g.input_image(torch.from_numpy(img).cuda(), binds, Kimg, R, eye)
+        o.input_image(img, binds, Kimg, R, eye)
+        compare_layers(g, o, where=f"top-k image frame {f}: ")
+    assert (g.get_layer("x_label") >= 0).sum() > 1000
+    with pytest.raises(M.MemError):  # top-k needs a class rule
+        M.Map(res, rows, cols, [dict(name="f", rule=M.MEM_AVERAGE, n_channels=9)]).input_pointcloud(
+            pts, [(0, 2 * k, 0, k)], np.eye(3), [0.0, 0.0, 1.0], noise)
