@@ -948,12 +948,13 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.bcnt = m->bk_cnt;
     a.recs = m->bk_recs;
   }
-  if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool in an L2 persisting window
+  if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool (or the state) in an L2 persisting window
     cudaStreamAttrValue v;
     memset(&v, 0, sizeof v);
-    const size_t win = scratch_per_map * m->scratch_maps;
+    const bool state = getenv("MEM_L2_STATE") != nullptr;
+    const size_t win = state ? sizeof(uint32_t) * (size_t)B * HW * m->n_word : scratch_per_map * m->scratch_maps;
     const size_t setaside = (size_t)m->l2_persist_mb << 20;
-    v.accessPolicyWindow.base_ptr = m->st.acc;
+    v.accessPolicyWindow.base_ptr = state ? (void *)m->st.words : (void *)m->st.acc;
     v.accessPolicyWindow.num_bytes = win;
     v.accessPolicyWindow.hitRatio = win <= setaside ? 1.0f : (float)setaside / (float)win;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
