@@ -24,6 +24,9 @@
 #ifndef MEM_PAIR_MIN
 #define MEM_PAIR_MIN 4  // colour fast path: pair lanes of the same cell when >= this many repeat
 #endif
+#ifndef MEM_OCC_BATCH
+#define MEM_OCC_BATCH 4  // occlusion walk: intermediate cells whose loads are issued together
+#endif
 #ifndef MEM_CELLS_MINB
 #define MEM_CELLS_MINB 3
 #endif
@@ -1373,20 +1376,46 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
   const int sx = r0 < r1 ? 1 : -1, sy = c0 < c1 ? 1 : -1;
   int err = dx + dy, x = r0, y = c0;
   const long long mbase = (long long)m * g.HW;
-  for (;;) {
-    if (x == r1 && y == c1) break;
-    const int e2 = 2 * err;
-    if (e2 >= dy) { err += dy; x += sx; }
-    if (e2 <= dx) { err += dx; y += sy; }
-    if (x == r1 && y == c1) break;
-    if (x < 0 || x >= g.H || y < 0 || y >= g.W) continue;  // outside the map: no occluder
-    const long long j = mbase + (long long)wrap(x + ring.x, g.H) * g.W + wrap(y + ring.y, g.W);
-    if (!validp[j]) continue;                                // unknown terrain does not occlude
-    const float xi = ((float)x + 0.5f - g.hH) * g.res, yi = ((float)y + 0.5f - g.hW) * g.res;
-    const float dxi = xi - tx, dyi = yi - ty;
-    const float di = sqrtf(dxi * dxi + dyi * dyi);
-    const float ray = tz + (di / db) * (hb - tz);
-    if (elev[j] > ray + a.eps_occ) return false;
+  // the line has max(dx, -dy) - 1 intermediate cells; they are generated kOccBatch at a time
+  // and all their (valid, h) loads issued before any test (one round trip per batch)
+  constexpr int kOccBatch = MEM_OCC_BATCH;
+  int left = max(dx, -dy) - 1;
+  while (left > 0) {
+    int bx[kOccBatch], by[kOccBatch];
+    long long bj[kOccBatch];
+    uint8_t bv[kOccBatch];
+    float bh[kOccBatch];
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      bj[k] = -1;
+      if (k < left) {
+        const int e2 = 2 * err;
+        if (e2 >= dy) { err += dy; x += sx; }
+        if (e2 <= dx) { err += dx; y += sy; }
+        bx[k] = x;
+        by[k] = y;
+        if (x >= 0 && x < g.H && y >= 0 && y < g.W)  // outside the map: no occluder
+          bj[k] = mbase + (long long)wrap(x + ring.x, g.H) * g.W + wrap(y + ring.y, g.W);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      bv[k] = 0;
+      if (bj[k] >= 0) {
+        bv[k] = validp[bj[k]];
+        bh[k] = elev[bj[k]];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      if (!bv[k]) continue;  // unknown terrain does not occlude
+      const float xi = ((float)bx[k] + 0.5f - g.hH) * g.res, yi = ((float)by[k] + 0.5f - g.hW) * g.res;
+      const float dxi = xi - tx, dyi = yi - ty;
+      const float di = sqrtf(dxi * dxi + dyi * dyi);
+      const float ray = tz + (di / db) * (hb - tz);
+      if (bh[k] > ray + a.eps_occ) return false;
+    }
+    left -= kOccBatch;
   }
   return true;
 }
