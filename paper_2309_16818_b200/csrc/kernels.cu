@@ -787,14 +787,16 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   const PointFrame f = frame_of(a, t.m);
   const int map_base = t.m * g.HW;
   const int sb = (int)scratch_base(a, t.m);
+  // points of the item present: [0, nv) (32-bit indices within the item)
+  const int nv = t.end - t.base < kWarpPoints ? (int)(t.end - t.base) : kWarpPoints;
   PointOut o[kWarpPtsPerLane];
 #pragma unroll
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
-    const long long i = t.base + u * 32 + lane;
-    if (i < t.end && !(a.ablate & 8u)) {
+    const bool in = u * 32 + lane < nv;
+    if (in && !(a.ablate & 8u)) {
       o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
     } else {
-      o[u].code = i < t.end ? MEM_CODE_NONFINITE : -1;
+      o[u].code = in ? MEM_CODE_NONFINITE : -1;
       o[u].cell = -1;
       o[u].test = false;
     }
@@ -802,16 +804,16 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   if (!(a.ablate & 4u)) mahalanobis(o, a.st, g, a.np.tau2);
 #pragma unroll
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
-    const long long i = t.base + u * 32 + lane;
-    if (i < t.end) {
+    const int k = u * 32 + lane;
+    if (k < nv) {
       if (kDebug) {
-        a.dbg_cell[i] = o[u].lcell;
-        a.dbg_code[i] = (uint8_t)o[u].code;
+        a.dbg_cell[t.base + k] = o[u].lcell;
+        a.dbg_code[t.base + k] = (uint8_t)o[u].code;
       }
       count_code(packed, npk, o[u].code, cnt);
     }
     if (a.ablate & 2u) continue;
-    const float *pp = a.pts + (i < t.end ? i : t.beg) * (long long)a.stride;
+    const float *pp = kFast != 0 ? nullptr : a.pts + (k < nv ? t.base + k : t.beg) * (long long)a.stride;
     if constexpr (kBucket)
       bucket_warp<kFast>(a, o[u], o[u].cell - map_base, a.slot0 + t.m - a.m0, sb + (o[u].cell - map_base), pp,
                          pw[u]);
