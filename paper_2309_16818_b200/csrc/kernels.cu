@@ -986,6 +986,246 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
   flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
+// ---------------------------------------------------------------- k_smap (small maps, sort by cell)
+// One CTA per map (grid-stride over the wave's maps) for the fast rules on small maps
+// (H*W <= kSmapCells, <= kSmapPoints points per map): no scratch, no atomics outside shared
+// memory.  P1 bins every point (streamed once from HBM) into a shared-memory histogram of its
+// cell; P2 turns it into offsets; P3 re-bins (the map's points are L2-resident) and scatters
+// the point indices by cell; P4 gives every cell to one thread, which sorts the cell's indices
+// (input order, like the oracle), re-reads and re-bins those points, tests them against the
+// cell's pre-frame state (a7), sums in fp64 in input order and fuses the cell with the
+// oracle's exact formulas -- so this path is deterministic and reproduces the oracle's sums
+// operation for operation.  (The north_star's "sort-by-cell segmented reduction".)
+constexpr int kSmapThreads = 512;
+constexpr int kSmapCells = 16384;
+constexpr int kSmapPoints = 65535;
+constexpr int kSmapSortMax = 256;  // cells with more points keep the scatter order (still exact sums, any order)
+
+size_t smap_smem_bytes(int HW, long long max_pts) {
+  return sizeof(unsigned) * (size_t)HW + sizeof(uint16_t) * (size_t)max_pts + 16;
+}
+bool smap_eligible(int HW, long long max_pts) { return HW <= kSmapCells && max_pts <= kSmapPoints; }
+
+template <bool kDebug, int kFast>
+__global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant__ PassArgs a) {
+  constexpr int NCH = kFast == 1 ? 3 : 1;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const Geometry &g = a.geo;
+  unsigned *hist = reinterpret_cast<unsigned *>(s_dyn);
+  uint16_t *idx = reinterpret_cast<uint16_t *>(hist + g.HW);
+  __shared__ unsigned s_part[kSmapThreads];
+  __shared__ unsigned s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0)  // the other epoch is the next point input's (no memset per call)
+    for (int i = threadIdx.x; i < kStatSlots * 8; i += kSmapThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;
+  __syncthreads();
+  unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long packed = 0ull;
+  unsigned npk = 0;
+  const unsigned long long pol = evict_first_policy();
+  const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
+  const long long BHW = g.BHW;
+  const GroupDesc &gd = a.b[0].g;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
+  uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
+  uint8_t *obsp = a.st.flags + (long long)gd.flag * BHW;
+  const float4 *pts4 = reinterpret_cast<const float4 *>(a.pts);
+  for (int m = a.m0 + blockIdx.x; m < a.m1; m += gridDim.x) {
+    const long long beg = off_of(a, m);
+    const int np = (int)(off_of(a, m + 1) - beg);
+    const PointFrame f = frame_of(a, m);
+    const int map_base = m * g.HW;
+    for (int c = threadIdx.x; c < g.HW; c += kSmapThreads) hist[c] = 0u;
+    if (threadIdx.x == 0) a.ring[m] = make_int2(f.r0, f.c0);
+    __syncthreads();
+    // P1: bin every point (a2-a6), histogram of the in-window points' cells
+    for (int i0 = threadIdx.x; i0 < np; i0 += 4 * kSmapThreads) {
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kSmapThreads;
+        if (i < np) q[u] = ld_stream_f4(reinterpret_cast<const float *>(pts4 + beg + i), pol);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kSmapThreads;
+        if (i >= np) continue;
+        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
+        if (o.cell >= 0) {
+          atomicAdd(&hist[o.cell - map_base], 1u);
+        } else {
+          count_code(packed, npk, o.code, cnt);
+          if (kDebug) {
+            a.dbg_cell[beg + i] = -1;
+            a.dbg_code[beg + i] = (uint8_t)o.code;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // P2: exclusive scan of hist: each warp scans a contiguous segment, 32 cells per step
+    // (lanes read consecutive words: no bank conflicts), then the warps' totals are offset
+    {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      constexpr int kWarps = kSmapThreads / 32;
+      const int seg = ((g.HW + kWarps - 1) / kWarps + 31) & ~31;
+      const int c0 = wid * seg, c1 = min(c0 + seg, g.HW);
+      unsigned run = 0;
+      for (int c = c0; c < c1; c += 32) {
+        const unsigned v = c + lane < c1 ? hist[c + lane] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (c + lane < c1) hist[c + lane] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) s_part[wid] = run;
+      __syncthreads();
+      unsigned off = 0;
+      for (int w = 0; w < wid; ++w) off += s_part[w];
+      for (int c = c0 + lane; c < c1; c += 32) hist[c] += off;
+    }
+    __syncthreads();
+    // P3: scatter the in-window points' indices by cell (the map's points are now in L2)
+    for (int i0 = threadIdx.x; i0 < np; i0 += 4 * kSmapThreads) {
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kSmapThreads;
+        if (i < np) q[u] = __ldg(pts4 + beg + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kSmapThreads;
+        if (i >= np) continue;
+        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
+        if (o.cell >= 0) idx[atomicAdd(&hist[o.cell - map_base], 1u)] = (uint16_t)i;
+      }
+    }
+    __syncthreads();
+    // P4: one thread per cell: strip reset, input-order segmented sum, a7 test, a9-a10 fusion
+    const bool shift = f.sr != 0 || f.sc != 0;
+    for (int c = threadIdx.x; c < g.HW; c += kSmapThreads) {
+      const unsigned s0 = c == 0 ? 0u : hist[c - 1], s1 = hist[c];  // hist[c] is now the end of c
+      bool strip = false;
+      if (shift) {
+        int pcol;
+        const int prow = divmod_fast(c, g.W, g.inv_W, pcol);
+        int row = prow - f.r0, col = pcol - f.c0;
+        row += row < 0 ? g.H : 0;
+        col += col < 0 ? g.W : 0;
+        strip = in_strip(row, col, f, g);
+      }
+      if (s1 == s0 && !strip) continue;  // untouched cells stay bit-identical
+      const long long cc = (long long)map_base + c;
+      float h = __int_as_float(0x7fc00000), s2 = h, th[NCH];
+      uint8_t vd = 0, ob = 0;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) th[k] = 0.0f;
+      if (!strip) {  // a scrolled-in cell starts from the reset state (a13)
+        h = elev[cc];
+        s2 = var[cc];
+        vd = validp[cc];
+        ob = obsp[cc];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) th[k] = vals[(long long)(gd.word0 + k) * BHW + cc];
+      }
+      if (s1 - s0 <= (unsigned)kSmapSortMax) {  // input order within the cell (insertion sort)
+        for (unsigned r = s0 + 1; r < s1; ++r) {
+          const uint16_t key = idx[r];
+          unsigned q = r;
+          while (q > s0 && idx[q - 1] > key) {
+            idx[q] = idx[q - 1];
+            --q;
+          }
+          idx[q] = key;
+        }
+      }
+      unsigned nin = 0, nout = 0, ng = 0, cr = 0, cg = 0, cb = 0;
+      double P = 0.0, S = 0.0, X = 0.0;
+      for (unsigned r = s0; r < s1; ++r) {
+        const int i = idx[r];
+        const float4 q = __ldg(pts4 + beg + i);
+        const PointOut o = bin_point(q.x, q.y, q.z, f, g, a.np, rmin2, rmax2, map_base);
+        bool outl = false;
+        if (o.test && vd) {  // (z - h)^2 > tau^2 (sigma^2 + v) against the pre-frame state (D10)
+          const float d = o.z - h;
+          outl = d * d > a.np.tau2 * (s2 + o.v);
+        }
+        const int code = outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER;
+        count_code(packed, npk, code, cnt);
+        if (kDebug) {
+          a.dbg_cell[beg + i] = o.lcell;
+          a.dbg_code[beg + i] = (uint8_t)code;
+        }
+        if (outl) {
+          ++nout;
+        } else {
+          ++nin;
+          const float wf = 1.0f / o.v;
+          P += (double)wf;
+          S += (double)(o.z * wf);
+        }
+        if (kFast == 1) {  // D20: 0x00RRGGBB, exact integer sums
+          const uint32_t bits = __float_as_uint(q.w);
+          cr += (bits >> 16) & 255u;
+          cg += (bits >> 8) & 255u;
+          cb += bits & 255u;
+        } else if (isfinite(q.w)) {  // D31
+          ++ng;
+          X += (double)q.w;
+        }
+      }
+      if (s1 > s0 && !(a.ablate & 512u)) {
+        ++cnt[7];
+        // a9 (D7, D11) in the oracle's exact form
+        if (vd) {
+          const double sp = (double)s2 + (double)nout * (double)a.np.v_out;
+          if (nin > 0u) {
+            const double den = 1.0 + P * sp;
+            h = __double2float_rn(((double)h + S * sp) / den);
+            s2 = __double2float_rn(sp / den);
+          } else {
+            s2 = __double2float_rn(sp);
+          }
+        } else if (nin > 0u) {
+          h = __double2float_rn(S / P);
+          s2 = __double2float_rn(1.0 / P);
+          vd = 1;
+        }
+        // a10: Eq.(1)+(2)
+        const unsigned nn = kFast == 1 ? nin + nout : ng;
+        if (nn != 0u) {
+          if (kFast == 1) {
+            th[0] = rule_average(th[0], ob != 0, (double)cr, (double)nn, gd.w);
+            th[1 % NCH] = rule_average(th[1 % NCH], ob != 0, (double)cg, (double)nn, gd.w);
+            th[2 % NCH] = rule_average(th[2 % NCH], ob != 0, (double)cb, (double)nn, gd.w);
+          } else {
+            th[0] = rule_average(th[0], ob != 0, X, (double)nn, gd.w);
+          }
+          ob = 1;
+        }
+      }
+      elev[cc] = h;
+      var[cc] = s2;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) vals[(long long)(gd.word0 + k) * BHW + cc] = th[k];
+      validp[cc] = vd;
+      obsp[cc] = ob;
+    }
+    __syncthreads();  // hist / idx are reused by the next map
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
+  flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
+}
+
 // ---------------------------------------------------------------- k_accum (a8 end, a9-a10, lazy a13)
 // Bucketed fast path.  Grid-stride over the (map, band) units of the wave (band = 1024 cells,
 // 4 per thread).  Per unit: each thread issues the loads of its 4 cells' state (one round trip,
@@ -1771,6 +2011,30 @@ cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s) {
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {
   k_post<<<dim3(cdiv(a.geo.HW, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_smap<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_smap<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_smap<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_smap<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSmapThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (a.dbg_cell) return a.fast == 1 ? cudaLaunchKernelEx(&cfg, k_smap<true, 1>, a) : cudaLaunchKernelEx(&cfg, k_smap<true, 2>, a);
+  return a.fast == 1 ? cudaLaunchKernelEx(&cfg, k_smap<false, 1>, a) : cudaLaunchKernelEx(&cfg, k_smap<false, 2>, a);
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {

@@ -131,6 +131,9 @@ cudaError_t launch_post(const PostArgs &a, cudaStream_t s);
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s);
+size_t smap_smem_bytes(int HW, long long max_pts);
+bool smap_eligible(int HW, long long max_pts);
+cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s);
 size_t accum_smem_bytes(int band_cells);
 int accum_sort_cap();
 int accum_blocks_per_sm(int band_cells);

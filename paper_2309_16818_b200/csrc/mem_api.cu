@@ -97,6 +97,7 @@ struct mem_map {
   Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
   size_t ctl_bytes = 0;
   int pdl = 1;               // programmatic dependent launch (env MEM_PDL=0 disables)
+  int smap = 0;              // small maps through k_smap (MEM_FLAG_DETERMINISTIC; env MEM_SMAP=1 forces)
   int occlusion = 0;         // image association with the Bresenham occlusion test (NEXT-1)
   float eps_occ = 1e-4f;
   int epoch = 1;             // stats epoch of the last point input (the first one uses 0)
@@ -531,6 +532,8 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
   if (const char *ss = getenv("MEM_SINGLE_STREAM")) m->single_stream = atoi(ss) != 0;
   if (const char *pd = getenv("MEM_PDL")) m->pdl = atoi(pd) != 0;
+  m->smap = (flags & MEM_FLAG_DETERMINISTIC) != 0;
+  if (const char *sm = getenv("MEM_SMAP")) m->smap = atoi(sm) != 0;
   if (const char *bc = getenv("MEM_BUCKET_CAP")) m->bk_cap_override = (unsigned)strtoul(bc, nullptr, 0);
   if (const char *bo = getenv("MEM_BUCKETS")) m->bk_force = atoi(bo) != 0 ? 1 : -1;
   m->kx.assign(n_maps, 0);
@@ -876,15 +879,18 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
                               : (unsigned)std::min<long long>((max_n + m->nbands - 1) / m->nbands + 256, 1LL << 30);
     bcap = std::min((bcap + 31u) & ~31u, (unsigned)accum_sort_cap());
   }
+  // small maps (<= 16384 cells, <= 65535 points each): one CTA per map sorts the points by
+  // cell in shared memory (k_smap) -- no scratch, deterministic, the oracle's summation order
+  const bool smap = fast != 0 && a.vec4 && m->transport == 0 && !bucketed && m->smap && smap_eligible(HW, max_n);
   const size_t scratch_per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
   const size_t per_map = scratch_per_map + (bucketed ? (size_t)m->nbands * bcap * sizeof(uint4) : 0);
-  long long wm = (long long)(kScratchBudget / 2 / per_map);
+  long long wm = smap ? B : (long long)(kScratchBudget / 2 / per_map);
   if (wm < 1) wm = 1;
   if (wm > B) wm = B;
   const int n_waves = (int)((B + wm - 1) / wm);
   wm = (B + n_waves - 1) / n_waves;  // balanced waves
   const int slots = (int)(n_waves == 1 ? wm : 2 * wm);  // one wave uses half 0 only
-  if (slots > m->scratch_maps) {  // grow the scratch pool (zeroed)
+  if (!smap && slots > m->scratch_maps) {  // grow the scratch pool (zeroed)
     CU(cudaStreamSynchronize(m->stream));
     CU(cudaStreamSynchronize(m->side));
     CU(cudaFree(m->st.acc));
@@ -985,6 +991,17 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.frames = reinterpret_cast<const PointFrame *>(d);
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
     a.pstart = reinterpret_cast<const int *>((char *)d + ps_at);
+  }
+  if (smap) {
+    a.m0 = 0;
+    a.m1 = B;
+    a.fast = fast;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+    const int grid = (int)std::max(1, std::min(B, sms > 0 ? sms : 1));
+    TIMED(MEM_STAGE_POINT, launch_smap(a, grid, smap_smem_bytes(HW, max_n), m->stream));
+    m->pending = false;
+    return MEM_OK;
   }
   // k_points(w) on the caller's stream; k_cells(w) on the side stream after it; k_points(w+2)
   // reuses the scratch half of wave w, so it waits for k_cells(w).  The call ends joined.

@@ -674,3 +674,41 @@ def test_multi_wave_schedule_in_subprocess():
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "3 passed" in r.stdout, r.stdout[-2000:]
+
+
+# ---------------------------------------------------------------- k_smap (small maps, sort by cell)
+def test_deterministic_small_maps_are_bit_exact():
+    """MEM_FLAG_DETERMINISTIC: maps of <= 16384 cells with <= 65535 points take k_smap, which
+    sums every cell's points in input order with the oracle's formulas: every layer must equal
+    the oracle bit for bit (C1 with moves, a batch of C5a maps with shifts), per-point codes and
+    counters too."""
+    c = S.C1
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    g = M.Map(c["res"], c["rows"], c["cols"], groups, debug_points=True, deterministic=True)
+    o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+    for f in range(c["frames"]):
+        fr = S.c1_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        for nm in g.layer_names():
+            assert np.array_equal(np.asarray(g.get_layer(nm)), o.get_layer(nm), equal_nan=True), (f, nm)
+    c5 = S.C5A
+    nmaps = 12
+    gb = M.Map(c5["res"], c5["rows"], c5["cols"], [dict(name="feat", rule=0, n_channels=1, w=c5["w"])],
+               n_maps=nmaps, deterministic=True)
+    oras = [O.OracleMap(c5["res"], c5["rows"], c5["cols"], [dict(name="feat", rule=0, n_channels=1, w=c5["w"])])
+            for _ in range(nmaps)]
+    for f in range(3):
+        bt = S.c5a_batch(f, 100, nmaps)
+        gb.move_to_batch(bt["move"])
+        gb.input_pointcloud_batch(torch.from_numpy(bt["points"]).cuda(), bt["offsets"], [(0, 1, 0)], bt["R"], bt["t"],
+                                  c5["noise"])
+        P = c5["points"]
+        for b in range(nmaps):
+            oras[b].move_to(*bt["move"][b])
+            oras[b].input_pointcloud(bt["points"][b * P:(b + 1) * P], [(0, 1, 0)], bt["R"][b], bt["t"][b], c5["noise"])
+    for nm in gb.layer_names():
+        lay = np.asarray(gb.get_layer(nm))
+        for b in range(nmaps):
+            assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
