@@ -996,23 +996,32 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
 // cell's pre-frame state (a7), sums in fp64 in input order and fuses the cell with the
 // oracle's exact formulas -- so this path is deterministic and reproduces the oracle's sums
 // operation for operation.  (The north_star's "sort-by-cell segmented reduction".)
-constexpr int kSmapThreads = 512;
+#ifndef MEM_SMAP_THREADS
+#define MEM_SMAP_THREADS 1024  // P4 walks the cells one per thread: more threads, shorter chains
+#endif
+#ifndef MEM_SMAP_MINB
+#define MEM_SMAP_MINB 1
+#endif
+constexpr int kSmapThreads = MEM_SMAP_THREADS;
 constexpr int kSmapCells = 16384;
 constexpr int kSmapPoints = 65535;
 constexpr int kSmapSortMax = 256;  // cells with more points keep the scatter order (still exact sums, any order)
 
+// shared memory: the per-cell counts / offsets as packed u16 pairs (a map has < 65536 points)
+// and the u16 point indices
 size_t smap_smem_bytes(int HW, long long max_pts) {
-  return sizeof(unsigned) * (size_t)HW + sizeof(uint16_t) * (size_t)max_pts + 16;
+  return sizeof(unsigned) * (size_t)((HW + 1) / 2) + sizeof(uint16_t) * (size_t)max_pts + 16;
 }
 bool smap_eligible(int HW, long long max_pts) { return HW <= kSmapCells && max_pts <= kSmapPoints; }
 
 template <bool kDebug, int kFast>
-__global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __grid_constant__ PassArgs a) {
   constexpr int NCH = kFast == 1 ? 3 : 1;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   const Geometry &g = a.geo;
-  unsigned *hist = reinterpret_cast<unsigned *>(s_dyn);
-  uint16_t *idx = reinterpret_cast<uint16_t *>(hist + g.HW);
+  unsigned *hist = reinterpret_cast<unsigned *>(s_dyn);  // cell c: 16-bit half (c & 1) of word c >> 1
+  uint16_t *idx = reinterpret_cast<uint16_t *>(hist + (g.HW + 1) / 2);
+  auto h16 = [&](int c) { return (hist[c >> 1] >> (16 * (c & 1))) & 0xffffu; };
   __shared__ unsigned s_part[kSmapThreads];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
@@ -1038,7 +1047,7 @@ __global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant_
     const int np = (int)(off_of(a, m + 1) - beg);
     const PointFrame f = frame_of(a, m);
     const int map_base = m * g.HW;
-    for (int c = threadIdx.x; c < g.HW; c += kSmapThreads) hist[c] = 0u;
+    for (int c = threadIdx.x; c < (g.HW + 1) / 2; c += kSmapThreads) hist[c] = 0u;
     if (threadIdx.x == 0) a.ring[m] = make_int2(f.r0, f.c0);
     __syncthreads();
     // P1: bin every point (a2-a6), histogram of the in-window points' cells
@@ -1055,7 +1064,8 @@ __global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant_
         if (i >= np) continue;
         const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
         if (o.cell >= 0) {
-          atomicAdd(&hist[o.cell - map_base], 1u);
+          const int c = o.cell - map_base;
+          atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1)));
         } else {
           count_code(packed, npk, o.code, cnt);
           if (kDebug) {
@@ -1066,30 +1076,33 @@ __global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant_
       }
     }
     __syncthreads();
-    // P2: exclusive scan of hist: each warp scans a contiguous segment, 32 cells per step
-    // (lanes read consecutive words: no bank conflicts), then the warps' totals are offset
+    // P2: exclusive scan of the counts: each warp scans a contiguous run of words (2 cells each,
+    // lanes on consecutive words), then the warps' totals are offset
     {
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
       constexpr int kWarps = kSmapThreads / 32;
-      const int seg = ((g.HW + kWarps - 1) / kWarps + 31) & ~31;
-      const int c0 = wid * seg, c1 = min(c0 + seg, g.HW);
+      const int nw = (g.HW + 1) / 2;
+      const int seg = ((nw + kWarps - 1) / kWarps + 31) & ~31;
+      const int w0 = wid * seg, w1 = min(w0 + seg, nw);
       unsigned run = 0;
-      for (int c = c0; c < c1; c += 32) {
-        const unsigned v = c + lane < c1 ? hist[c + lane] : 0u;
-        unsigned x = v;
+      for (int w = w0; w < w1; w += 32) {
+        const unsigned word = w + lane < w1 ? hist[w + lane] : 0u;
+        const unsigned lo = word & 0xffffu, pair = lo + (word >> 16);
+        unsigned x = pair;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
           if (lane >= o) x += y;
         }
-        if (c + lane < c1) hist[c + lane] = run + x - v;
+        const unsigned off = run + x - pair;
+        if (w + lane < w1) hist[w + lane] = off | ((off + lo) << 16);
         run += __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) s_part[wid] = run;
       __syncthreads();
       unsigned off = 0;
       for (int w = 0; w < wid; ++w) off += s_part[w];
-      for (int c = c0 + lane; c < c1; c += 32) hist[c] += off;
+      for (int w = w0 + lane; w < w1; w += 32) hist[w] += off | (off << 16);
     }
     __syncthreads();
     // P3: scatter the in-window points' indices by cell (the map's points are now in L2)
@@ -1105,14 +1118,17 @@ __global__ void __launch_bounds__(kSmapThreads, 1) k_smap(const __grid_constant_
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
         const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
-        if (o.cell >= 0) idx[atomicAdd(&hist[o.cell - map_base], 1u)] = (uint16_t)i;
+        if (o.cell >= 0) {
+          const int c = o.cell - map_base;
+          idx[(atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1))) >> (16 * (c & 1))) & 0xffffu] = (uint16_t)i;
+        }
       }
     }
     __syncthreads();
     // P4: one thread per cell: strip reset, input-order segmented sum, a7 test, a9-a10 fusion
     const bool shift = f.sr != 0 || f.sc != 0;
     for (int c = threadIdx.x; c < g.HW; c += kSmapThreads) {
-      const unsigned s0 = c == 0 ? 0u : hist[c - 1], s1 = hist[c];  // hist[c] is now the end of c
+      const unsigned s0 = c == 0 ? 0u : h16(c - 1), s1 = h16(c);  // the count of c is now its end
       bool strip = false;
       if (shift) {
         int pcol;
