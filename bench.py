@@ -312,9 +312,18 @@ def side_paper_sweep(torch, M, stream, iters=300):
             mp.input_pointcloud(dev[i % 2], binds, cl["R"], cl["t"], c["noise"])
 
         ms = timed_loop(torch, stream, iters, step)
+        if n_layers == max(c["layers"]):  # Table II-style stage split of the largest case
+            mp.profile_read(reset=True)
+            mp.profile(True)
+            step(0)
+            torch.cuda.synchronize()
+            mp.profile(False)
+            prof = mp.profile_read(reset=True)
+            stages[groups[0]["rule"] if groups else -1] = {k: v[0] for k, v in prof.items() if v[1]}
         mp.close()
         return ms
 
+    stages = {}
     base = frame_ms([], [], 0)
     out["height_only_ms"] = base
     for name, rule in (("exponential_averaging", 0), ("bayesian", 3)):
@@ -329,7 +338,8 @@ def side_paper_sweep(torch, M, stream, iters=300):
         slope, icpt = np.polyfit(x, y, 1)
         r2 = 1.0 - ((y - (slope * x + icpt)) ** 2).sum() / max(((y - y.mean()) ** 2).sum(), 1e-30)
         out[name] = {"layers": xs, "ms_per_frame": ys, "multimodal_ms": [v - base for v in ys],
-                     "fit_ms_per_layer": slope, "fit_intercept_ms": icpt, "r2": r2}
+                     "fit_ms_per_layer": slope, "fit_intercept_ms": icpt, "r2": r2,
+                     "stage_ms_at_max_layers": stages.get(rule)}
     return out
 
 

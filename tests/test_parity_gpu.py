@@ -712,3 +712,20 @@ def test_deterministic_small_maps_are_bit_exact():
         lay = np.asarray(gb.get_layer(nm))
         for b in range(nmaps):
             assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
+
+
+def test_deterministic_flag_falls_back_beyond_limits():
+    """MEM_FLAG_DETERMINISTIC on inputs k_smap does not take (too many points per map, a
+    multi-group map) fuses through the default path, still within the parity bar."""
+    rows, cols, res = 40, 36, 0.1
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)]
+    g = M.Map(res, rows, cols, groups, deterministic=True)
+    o = O.OracleMap(res, rows, cols, groups)
+    pts = S.random_cloud(4242, 70000, 4, rows, cols, res)  # > 65535 points
+    step_points(g, o, pts, [(0, 1, 0)], np.eye(3), [0.0, 0.0, 1.0], NOISE_R, check_codes=False)
+    compare_layers(g, o, where="70k points: ")
+    g2 = M.Map(res, rows, cols, ALL_GROUPS, deterministic=True)
+    o2 = O.OracleMap(res, rows, cols, ALL_GROUPS)
+    step_points(g2, o2, random_all_channels(77, 5000, rows, cols, res), ALL_BINDS, np.eye(3), [0.0, 0.0, 1.0],
+                NOISE_R, check_codes=False)
+    compare_layers(g2, o2, where="all rules: ")
