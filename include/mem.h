@@ -158,12 +158,19 @@ MEM_API mem_status mem_set_stream(mem_map *map, mem_stream stream);
 MEM_API mem_status mem_synchronize(mem_map *map);
 
 /* ---- one big map sharded across ranks ----------------------------
- * Every rank holds the full map state and fuses its own shard of each frame's points; the
- * per-cell statistics are moved to the owner of each physical row band (rows divisible by
- * nranks; band r = physical rows [r*rows/nranks, (r+1)*rows/nranks)), folded there by a typed
- * merge kernel (f64 sums, u64 sums, u64 max) and fused for the band only; elevation,
- * variance and valid are then all-gathered so that every rank's next Mahalanobis test sees
- * the whole pre-frame map.  Transport:
+ * Rank r owns the physical row band [r*rows/nranks, (r+1)*rows/nranks) (rows divisible by
+ * nranks) and every rank takes its own shard of each frame's points.  Two protocols:
+ *  - point routing (default for nranks > 1): each rank filters and bins its shard, counts its dropped
+ *    points, and sends every in-window point to the owner of its cell's band; the owner tests,
+ *    accumulates and fuses what it received (in source-rank order) for its band only.  A rank
+ *    keeps only its own band current (the readout all-gathers; an image input with occlusion
+ *    all-gathers elevation and valid first).
+ *  - statistics exchange (maps created with MEM_FLAG_DEBUG_POINTS, whose per-point codes need
+ *    the test on the routing rank, or env MEM_ROUTE=0): every rank accumulates its shard into
+ *    full-map per-cell statistics, which are moved to the band owners, folded by a typed merge
+ *    kernel (f64 sums, u64 sums, u64 max) and fused for the band; elevation, variance and
+ *    valid are then all-gathered for the next frame's Mahalanobis test.
+ * Counters (mem_frame_stats) are per rank and add up to the unsharded counters.  Transport:
  *  - NCCL (nccl_id != NULL, one process per GPU): grouped ncclSend/ncclRecv of the bands and
  *    ncclAllGather, stream-ordered on the map's stream.  Every call on a sharded map is
  *    collective (all ranks, same order); mem_get_layer all-gathers every layer first.

@@ -186,19 +186,24 @@ class OracleMap:
             raise OracleError(st, "om_input_pointcloud")
         return (cell, code) if debug else None
 
-    def accumulate(self, pts, bindings, R, t, noise):
-        """steps 1-2 only (per-point filtering and binning against the current state)."""
+    def accumulate(self, pts, bindings, R, t, noise, cells=False):
+        """steps 1-2 only (per-point filtering and binning against the current state); with
+        cells=True also returns every point's logical cell (-1 = dropped) and code."""
         pts = np.ascontiguousarray(pts, np.float32)
         n, stride = pts.shape
         Rr, Rp = _dbl(R, 9)
         tt, tp = _dbl(t, 3)
         nz = _Noise(**noise)
         st = C.c_int(0)
+        cell = np.empty(max(n, 1), np.int32) if cells else None
+        code = np.empty(max(n, 1), np.uint8) if cells else None
         h = lib().om_accumulate(self._h, pts.ctypes.data, n, stride, make_binds(bindings), len(bindings), Rp, tp,
-                                C.byref(nz), None, None, C.byref(st))
+                                C.byref(nz), cell.ctypes.data if cells else None, code.ctypes.data if cells else None,
+                                C.byref(st))
         if not h:
             raise OracleError(st.value, "om_accumulate")
-        return OracleFrame(h, len(bindings))
+        fr = OracleFrame(h, len(bindings))
+        return (fr, cell[:n], code[:n]) if cells else fr
 
     def fuse_rows(self, frame, row_lo, row_hi):
         """step 3 on rows [row_lo, row_hi)."""

@@ -128,6 +128,16 @@ struct PostArgs {
 };
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s);
 
+// sharded big map, point routing: every in-window point of this rank's shard is
+// copied (stride floats) into the bucket of the rank that owns its cell's row band
+struct RouteArgs {
+  float *buf;                  // [nranks][cap][stride]
+  unsigned *cnt;               // [nranks] points appended per destination (zeroed before)
+  long long cap;               // points per bucket (= the shard's point count)
+  int band_n;                  // cells per band
+};
+cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, int grid, cudaStream_t s);
+
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s);

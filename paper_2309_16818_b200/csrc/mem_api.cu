@@ -125,6 +125,16 @@ struct mem_map {
   uint8_t *wtype = nullptr;             // [R] record word types (merge)
   bool exchange_pending = false;        // local transport: accumulated, not yet fused
   PassArgs shard_args{};                // the k_cells arguments of the frame being fused
+  // point routing (default for sharded maps without MEM_FLAG_DEBUG_POINTS; env MEM_ROUTE=0: off)
+  bool route = false;
+  float *rbuf = nullptr;                // [nranks][cap][stride] outgoing points by owner band
+  size_t rbuf_cap = 0;                  // bytes
+  unsigned *rcnt = nullptr;             // [nranks] outgoing counts (device)
+  unsigned *rall = nullptr;             // [nranks][nranks] all ranks' counts (device, NCCL)
+  float *rin = nullptr;                 // incoming points of this rank's band
+  size_t rin_cap = 0;                   // bytes
+  long long route_cap = 0;              // points per outgoing bucket of the last frame
+  int route_stride = 0;
   int l2_persist_mb = 0;    // DIAGNOSTICS: env MEM_L2_PERSIST_MB at create
   bool single_stream = false;  // DIAGNOSTICS: env MEM_SINGLE_STREAM=1: waves run P0 C0 P1 C1 ... in order
   std::vector<ShiftRec> pend;
@@ -435,6 +445,10 @@ void free_map(mem_map *m) {
   cudaFree(m->dout);
   cudaFree(m->pca_buf);
   cudaFree(m->recv);
+  cudaFree(m->rbuf);
+  cudaFree(m->rcnt);
+  cudaFree(m->rall);
+  cudaFree(m->rin);
   cudaFree(m->wtype);
   if (m->comm) ncclCommDestroy(m->comm);
   cudaFree(m->ctl);
@@ -756,6 +770,103 @@ static mem_status shard_gather_all(mem_map *m) {
   return MEM_OK;
 }
 
+// point routing: the owner of a band fuses the in-window points it received (all in its band)
+static mem_status owner_pass(mem_map *m, const float *pts, long long n) {
+  PassArgs b = m->shard_args;
+  b.pts = pts;
+  b.vec4 = (b.stride == 4 && ((uintptr_t)pts & 15) == 0) ? 1 : 0;
+  if (!b.vec4) b.fast = 0;
+  b.frames = nullptr;
+  b.offsets = nullptr;
+  b.pstart = nullptr;
+  b.m0 = 0;
+  b.m1 = 1;
+  b.slot0 = 0;
+  const long long items = (n + kWarpPoints - 1) / kWarpPoints;
+  if (items > 0x7fffffffLL) return fail(MEM_EINVAL, "too many routed points");
+  b.offi[0] = 0;
+  b.offi[1] = n;
+  b.psi[0] = 0;
+  b.psi[1] = (int)items;
+  b.p_uniform = (int)items;
+  b.inv_p_uniform = items > 0 ? 1.0 / (double)items : 0.0;
+  b.dbg_cell = nullptr;
+  b.dbg_code = nullptr;
+  if (items > 0) {
+    const int gp = (int)std::max(1LL, std::min<long long>(m->points_grid, (items + 7) / 8));
+    TIMED(MEM_STAGE_POINT, launch_points(b, gp, m->stream));
+  }
+  const long long citems = (m->band_n + kWarpCells - 1) / kWarpCells;
+  const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
+  TIMED(MEM_STAGE_CELL, launch_cells(b, gc, m->stream));
+  return MEM_OK;
+}
+
+static mem_status grow_floats(float **buf, size_t *cap_bytes, size_t need_floats, cudaStream_t s) {
+  return grow((void **)buf, cap_bytes, need_floats * sizeof(float), s);
+}
+
+// NCCL transport of the routed points: counts all-gathered (one host sync), grouped send/recv
+// of the buckets into one contiguous buffer ordered by source rank, then the owner pass
+static mem_status shard_route_nccl(mem_map *m) {
+  const int G = m->nranks, st = m->route_stride;
+  std::vector<unsigned> all((size_t)G * G, 0u);
+  if (G > 1) {
+    NC(ncclAllGather(m->rcnt, m->rall, G, ncclUint32, m->comm, m->stream));
+    CU(cudaMemcpyAsync(all.data(), m->rall, sizeof(unsigned) * G * G, cudaMemcpyDeviceToHost, m->stream));
+  } else {
+    CU(cudaMemcpyAsync(all.data(), m->rcnt, sizeof(unsigned) * G, cudaMemcpyDeviceToHost, m->stream));
+  }
+  CU(cudaStreamSynchronize(m->stream));
+  std::vector<long long> off(G + 1, 0);
+  for (int p = 0; p < G; ++p) off[p + 1] = off[p] + all[(size_t)p * G + m->rank];
+  if (grow_floats(&m->rin, &m->rin_cap, (size_t)std::max(1LL, off[G]) * st, m->stream) != MEM_OK)
+    return fail(MEM_ENOMEM, "routed points (%lld)", off[G]);
+  const size_t own = all[(size_t)m->rank * G + m->rank];
+  if (own)
+    CU(cudaMemcpyAsync(m->rin + (size_t)off[m->rank] * st, m->rbuf + (size_t)m->rank * m->route_cap * st,
+                       sizeof(float) * own * st, cudaMemcpyDeviceToDevice, m->stream));
+  if (G > 1) {
+    NC(ncclGroupStart());
+    for (int p = 0; p < G; ++p) {
+      if (p == m->rank) continue;
+      const size_t ns = all[(size_t)m->rank * G + p], nr = all[(size_t)p * G + m->rank];
+      if (ns) NC(ncclSend(m->rbuf + (size_t)p * m->route_cap * st, ns * st, ncclFloat32, p, m->comm, m->stream));
+      if (nr) NC(ncclRecv(m->rin + (size_t)off[p] * st, nr * st, ncclFloat32, p, m->comm, m->stream));
+    }
+    NC(ncclGroupEnd());
+  }
+  return owner_pass(m, m->rin, off[G]);
+}
+
+// this rank's shard: drop / count / route (k_route)
+static mem_status route_points(mem_map *m, PassArgs &a, long long n, int stride) {
+  const int G = m->nranks;
+  if (grow_floats(&m->rbuf, &m->rbuf_cap, (size_t)G * std::max(1LL, n) * stride, m->stream) != MEM_OK)
+    return fail(MEM_ENOMEM, "route buckets");
+  CU(cudaMemsetAsync(m->rcnt, 0, sizeof(unsigned) * G, m->stream));
+  RouteArgs r;
+  r.buf = m->rbuf;
+  r.cnt = m->rcnt;
+  r.cap = std::max(1LL, n);
+  r.band_n = m->band_n;
+  m->route_cap = r.cap;
+  m->route_stride = stride;
+  if (n > 0) {
+    const int grid = (int)std::max(1LL, std::min<long long>(4LL * m->points_grid, (n + kThreads - 1) / kThreads));
+    TIMED(MEM_STAGE_POINT, launch_route(a, r, grid, m->stream));
+  }
+  a.cell_lo = m->band_lo;
+  a.cell_hi = m->band_lo + m->band_n;
+  m->shard_args = a;
+  m->pending = false;
+  if (m->transport == 2) {
+    m->exchange_pending = true;
+    return MEM_OK;
+  }
+  return shard_route_nccl(m);
+}
+
 static mem_status input_points(mem_map *m, const float *pts, const int64_t *offsets, int64_t n_single, int stride,
                                const mem_binding *bind, int nb, const double *R, const double *t,
                                const mem_noise *np) {
@@ -1026,6 +1137,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
     const int ga = (int)std::max(1LL, std::min<long long>(m->accum_grid, (long long)(a.m1 - a.m0) * m->nbands));
     auto launch_fuse = [&](cudaStream_t st) { return bucketed ? launch_accum(a, ga, st) : launch_cells(a, gc, st); };
+    if (m->transport != 0 && m->route) return route_points(m, a, total, stride);  // point routing
     if (m->transport != 0) {  // sharded map: accumulate this rank's shard, then the band protocol
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
       a.cell_lo = m->band_lo;
@@ -1098,6 +1210,16 @@ static mem_status input_image(mem_map *m, const float *img, int C, int IH, int I
   a.img = (const float *)dimg;
   a.occlusion = m->occlusion;
   a.eps_occ = m->eps_occ;
+  if (m->transport == 1 && m->route && m->occlusion && m->nranks > 1) {
+    // routed NCCL shards only keep their own band current: the occlusion walk needs the rest
+    const int HW = m->H * m->W, bn = m->band_n;
+    float *vals = reinterpret_cast<float *>(m->st.words);
+    NC(ncclGroupStart());
+    NC(ncclAllGather(vals + (size_t)kWordElev * HW + m->band_lo, vals + (size_t)kWordElev * HW, bn, ncclFloat32,
+                     m->comm, m->stream));
+    NC(ncclAllGather(m->st.flags + m->band_lo, m->st.flags, bn, ncclUint8, m->comm, m->stream));
+    NC(ncclGroupEnd());
+  }
   a.row_lo = m->transport ? m->band_lo / m->W : 0;  // sharded: fuse the owned band only
   a.row_hi = m->transport ? (m->band_lo + m->band_n) / m->W : m->H;
   a.C = C;
@@ -1559,6 +1681,18 @@ mem_status mem_create_sharded(float resolution, int rows, int cols, const mem_la
   m->nranks = nranks;
   m->band_n = rows / nranks * cols;
   m->band_lo = rank * m->band_n;
+  // point routing unless per-point debug codes are wanted (their outlier decision would be taken
+  // on another rank); env MEM_ROUTE=0 selects the statistics exchange
+  // (one rank has nothing to exchange: the statistics path is then the plain fused path;
+  // env MEM_ROUTE=1 forces routing, MEM_ROUTE=0 disables it)
+  m->route = nranks > 1 && !(flags & MEM_FLAG_DEBUG_POINTS);
+  if (const char *rt = getenv("MEM_ROUTE")) m->route = !(flags & MEM_FLAG_DEBUG_POINTS) && atoi(rt) != 0;
+  if (cudaMalloc((void **)&m->rcnt, sizeof(unsigned) * nranks) != cudaSuccess ||
+      cudaMalloc((void **)&m->rall, sizeof(unsigned) * nranks * nranks) != cudaSuccess) {
+    cudaGetLastError();
+    free_map(m);
+    return fail(MEM_ENOMEM, "route counters");
+  }
   // record word types for the merge: P, S f64 sums; per group (see GroupDesc::acc0)
   std::vector<uint8_t> wt(m->n_acc, 0);
   for (int gi = 0; gi < m->ng; ++gi) {
@@ -1609,6 +1743,33 @@ mem_status mem_shard_local_sync(mem_map **sh, int G) {
   if (set_device(m0)) return MEM_ECUDA;
   const int R = m0->n_acc, bn = m0->band_n, HW = m0->H * m0->W;
   const size_t w8 = sizeof(unsigned long long);
+  for (int r = 1; r < G; ++r)
+    if (sh[r]->route != m0->route) return fail(MEM_EINVAL, "shards disagree on point routing");
+  if (m0->route && m0->exchange_pending) {  // point routing: buckets to their owners, owner passes
+    const int st = m0->route_stride;
+    std::vector<unsigned> cnt((size_t)G * G);
+    for (int p = 0; p < G; ++p)
+      CU(cudaMemcpyAsync(cnt.data() + (size_t)p * G, sh[p]->rcnt, sizeof(unsigned) * G, cudaMemcpyDeviceToHost,
+                         m0->stream));
+    CU(cudaStreamSynchronize(m0->stream));
+    for (int r = 0; r < G; ++r) {
+      long long n_in = 0;
+      for (int p = 0; p < G; ++p) n_in += cnt[(size_t)p * G + r];
+      if (grow_floats(&sh[r]->rin, &sh[r]->rin_cap, (size_t)std::max(1LL, n_in) * st, m0->stream) != MEM_OK)
+        return fail(MEM_ENOMEM, "routed points");
+      long long off = 0;
+      for (int p = 0; p < G; ++p) {
+        const size_t k = cnt[(size_t)p * G + r];
+        if (k)
+          CU(cudaMemcpyAsync(sh[r]->rin + (size_t)off * st, sh[p]->rbuf + (size_t)r * sh[p]->route_cap * st,
+                             sizeof(float) * k * st, cudaMemcpyDeviceToDevice, m0->stream));
+        off += (long long)k;
+      }
+      mem_status s = owner_pass(sh[r], sh[r]->rin, n_in);
+      if (s != MEM_OK) return s;
+    }
+    for (int r = 0; r < G; ++r) sh[r]->exchange_pending = false;
+  }
   // exchange: rank r receives band r of every other shard (device copies)
   for (int r = 0; r < G && m0->exchange_pending; ++r) {
     int slot = 0;

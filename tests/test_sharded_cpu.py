@@ -8,6 +8,10 @@ the library's k_merge does on the band each rank owns), each rank fuses its own 
 (om_fuse_rows = step 3) and the bands are all-gathered.  After every frame each rank's map
 must equal one unsharded oracle fed all the points: integer layers and counters exactly,
 fp32 layers within the north_star tolerance (the f64 sums are re-associated).
+
+The second protocol (point routing, the library's default for sharded maps) is checked the
+same way: points are sent to the owner of their cell's band and fused there, in global input
+order, so the maps must equal the unsharded oracle bit for bit.
 """
 import os
 import socket
@@ -142,3 +146,70 @@ def test_band_decomposition_equals_unsharded(world):
     bad = [r for r in results if r[1] != "ok"]
     assert not bad, bad
     assert all(p.exitcode == 0 for p in procs)
+
+
+def worker_route(rank, world, port, q):
+    """point routing: each rank bins its shard, sends every in-window point to the owner of its
+    cell's row band (all_gather_object), the owner accumulates what it received -- in rank order,
+    i.e. the global input order -- and fuses its band; bands all-gathered.  Because every cell's
+    points are summed in input order, the maps equal the unsharded oracle bit for bit."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        shard = O.OracleMap(RES, ROWS, COLS, GROUPS)
+        full = O.OracleMap(RES, ROWS, COLS, GROUPS)
+        band = ROWS // world
+        lo, hi = rank * band, (rank + 1) * band
+        moves = [(0.0, 0.0), (0.15, -0.1), (0.4, 0.2), (-1.0, 0.5)]
+        for f, (x, y) in enumerate(moves):
+            shard.move_to(x, y)
+            full.move_to(x, y)
+            pts = cloud(f)
+            cuts = np.linspace(0, len(pts), world + 1).astype(int)
+            R, t = S.rot_z(0.4 * f), np.array([x + 0.02, y - 0.01, 1.0])
+            mine = pts[cuts[rank]:cuts[rank + 1]]
+            fr, cell, code = shard.accumulate(mine, BINDS, R, t, NOISE, cells=True)
+            drops = np.array([int(fr.counters[k]) for k in range(8)], np.int64)  # codes 1-4: this rank's drops
+            owner = np.where(cell >= 0, (cell // COLS) // band, -1)
+            out = [mine[owner == d] for d in range(world)]
+            got = [None] * world
+            dist.all_gather_object(got, out)
+            recv = np.concatenate([got[p][rank] for p in range(world)])
+            fo = shard.accumulate(recv, BINDS, R, t, NOISE)
+            shard.fuse_rows(fo, lo, hi)
+            for nm in LAYERS:
+                part = torch.from_numpy(np.ascontiguousarray(shard.get_layer(nm)[lo:hi]))
+                parts = [torch.empty_like(part) for _ in range(world)]
+                dist.all_gather(parts, part)
+                shard.set_layer(nm, torch.cat(parts).numpy())
+            full.input_pointcloud(pts, BINDS, R, t, NOISE)
+            st = shard.stats()
+            mix = torch.tensor([drops[1], drops[2], drops[3], drops[4], st["n_inlier"], st["n_outlier"],
+                                st["n_cells_touched"]], dtype=torch.int64)
+            dist.all_reduce(mix)
+            fs = full.stats()
+            assert mix.tolist() == [fs["n_nonfinite"], fs["n_range"], fs["n_height"], fs["n_oob"], fs["n_inlier"],
+                                    fs["n_outlier"], fs["n_cells_touched"]], (f, mix.tolist(), fs)
+            for nm in LAYERS:
+                a, b = shard.get_layer(nm), full.get_layer(nm)
+                assert np.array_equal(a, b, equal_nan=True), (f, nm)
+        dist.destroy_process_group()
+        q.put((rank, "ok", 0.0))
+    except Exception as e:
+        q.put((rank, f"{type(e).__name__}: {e}", None))
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_point_routing_equals_unsharded_bit_for_bit(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker_route, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    bad = [r for r in results if r[1] != "ok"]
+    assert not bad, bad

@@ -179,3 +179,101 @@ def test_c5b_full_size_two_local_shards():
         assert total == o.stats(), (total, o.stats())
         compare_layers(shards[f % G], o, where=f"frame {f}: ")
     assert o.stats()["n_outlier"] > 1000 and o.get_layer("valid").mean() > 0.9
+
+
+# ---------------------------------------------------------------- point routing (default protocol)
+def make_route_shards(res, rows, cols, groups, G):
+    return [M.Map.sharded(res, rows, cols, groups, r, G) for r in range(G)]  # no debug codes: routing
+
+
+def step_routed(shards, o, pts, binds, R, t, noise, rng, empty=None):
+    G = len(shards)
+    b = split_points(len(pts), G, rng, empty)
+    for r, s in enumerate(shards):
+        s.input_pointcloud(torch.from_numpy(np.ascontiguousarray(pts[b[r]:b[r + 1]])).cuda(), binds, R, t, noise)
+    sync(shards)
+    o.input_pointcloud(pts, binds, R, t, noise)
+    total = None
+    for s in shards:
+        st = s.stats()
+        total = st if total is None else {k: total[k] + st[k] for k in st}
+    assert total == o.stats(), (total, o.stats())
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_routed_shards_all_rules_with_shifts(G):
+    """point routing: every shard sends its in-window points to their band owner, which tests,
+    accumulates and fuses them; counters summed over shards and every shard's layers equal the
+    oracle fed all the points."""
+    rows, cols, res = 60, 48, 0.05
+    shards = make_route_shards(res, rows, cols, ALL_GROUPS, G)
+    o = O.OracleMap(res, rows, cols, ALL_GROUPS)
+    rng = np.random.default_rng(17 + G)
+    moves = [(0.0, 0.0), (0.12, 0.0), (0.31, -0.22), (-0.4, 0.05), (3.0, 2.0), (2.95, 2.1), (2.7, 2.3)]
+    for f, (x, y) in enumerate(moves):
+        for s in shards:
+            s.move_to(x, y)
+        o.move_to(x, y)
+        pts = random_all_channels(800 + f, 7000 + 131 * f, rows, cols, res)
+        step_routed(shards, o, pts, ALL_BINDS, S.rot_z(0.3 * f), np.array([x + 0.01, y - 0.02, 1.0]), NOISE_R, rng,
+                    empty=f % G if f % 3 == 0 else None)
+        for r, s in enumerate(shards):
+            compare_layers(s, o, where=f"routed frame {f} shard {r}: ")
+
+
+def test_routed_shards_c5b_and_images():
+    c = S.C5B
+    G = 4
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    shards = make_route_shards(c["res"], c["rows"], c["cols"], groups, G)
+    o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+    for f in range(2):
+        parts = [S.c5b_shard(f, r, G) for r in range(G)]
+        for s, p in zip(shards, parts):
+            s.move_to(*p["move"])
+            s.input_pointcloud(torch.from_numpy(p["points"]).cuda(), [(0, 1, 0)], p["R"], p["t"], c["noise"])
+        sync(shards)
+        o.move_to(*parts[0]["move"])
+        o.input_pointcloud(np.concatenate([p["points"] for p in parts]), [(0, 1, 0)], parts[0]["R"], parts[0]["t"],
+                           c["noise"])
+        compare_layers(shards[f], o, where=f"routed C5b frame {f}: ")
+    # images with occlusion on routed shards (every shard fuses its band)
+    rows, cols, res = 60, 70, 0.05
+    im_sh = make_route_shards(res, rows, cols, IMG_GROUPS, 3)
+    oi = O.OracleMap(res, rows, cols, IMG_GROUPS)
+    for s in im_sh:
+        s.set_image_occlusion(True)
+    oi.set_occlusion(True)
+    rng = np.random.default_rng(5)
+    noise = dict(a=1e-3, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=9.0, v_out=0.01)
+    K = np.array([[120.0, 0.5, 79.5], [0, 118.0, 59.5], [0, 0, 1.0]])
+    for f in range(3):
+        pts = S.random_cloud(600 + f, 20000, 3, rows, cols, res)
+        step_routed(im_sh, oi, pts, [], np.eye(3), [0.0, 0.0, 1.0], noise, rng)
+        eye = np.array([rng.uniform(-3, -2), rng.uniform(-1, 1), rng.uniform(1.0, 2.0)])
+        R = camera_looking_at(eye, [rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), 0.0])
+        img = np.concatenate([S.softmax_image(rng.integers(0, 5, (120, 160)), 5, rng),
+                              rng.normal(0, 1, (5, 120, 160)).astype(np.float32),
+                              rng.uniform(0, 255, (3, 120, 160)).astype(np.float32)])
+        for s in im_sh:
+            s.input_image(torch.from_numpy(img).cuda(), IMG_BINDS, K, R, eye)
+        sync(im_sh)
+        oi.input_image(img, IMG_BINDS, K, R, eye)
+        for r, s in enumerate(im_sh):
+            compare_layers(s, oi, where=f"routed image frame {f} shard {r}: ")
+
+
+def test_nccl_single_rank_routed(monkeypatch):
+    monkeypatch.setenv("MEM_ROUTE", "1")  # one rank takes the statistics path unless forced
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    g = M.Map.sharded(c["res"], c["rows"], c["cols"], groups, 0, 1, nccl_id=M.mem_nccl_unique_id())
+    o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):
+        fr = S.c2_frame(f)
+        g.move_to(*fr["move"])
+        o.move_to(*fr["move"])
+        g.input_pointcloud(torch.from_numpy(fr["points"]).cuda(), [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        o.input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        assert g.stats() == o.stats()
+        compare_layers(g, o, where=f"NCCL routed frame {f}: ")
