@@ -729,3 +729,40 @@ def test_deterministic_flag_falls_back_beyond_limits():
     step_points(g2, o2, random_all_channels(77, 5000, rows, cols, res), ALL_BINDS, np.eye(3), [0.0, 0.0, 1.0],
                 NOISE_R, check_codes=False)
     compare_layers(g2, o2, where="all rules: ")
+
+
+def test_c2x64_bench_configuration_sampled():
+    """the headline step exactly as bench.py times it: 64 C2 maps batched in one call (one
+    wave, colour fast path, frames rotating through the 16-frame pool with map m at frame
+    (step + m) % 16); 3 steps; 6 sampled maps compared against their own oracle maps
+    (counters of the sampled maps via per-map oracle sums, every layer)."""
+    c = S.C2
+    pool = [S.c2_frame(f) for f in range(16)]
+    maps, npts = 64, pool[0]["points"].shape[0]
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    gb = M.Map(c["res"], c["rows"], c["cols"], groups, n_maps=maps)
+    sample = [0, 1, 17, 31, 50, 63]
+    oras = {b: O.OracleMap(c["res"], c["rows"], c["cols"], groups) for b in sample}
+    dev = [torch.from_numpy(fr["points"]).cuda() for fr in pool]
+    offsets = np.arange(maps + 1, dtype=np.int64) * npts
+    for step in range(3):
+        idx = [(step + m) % 16 for m in range(maps)]
+        gb.move_to_batch(np.stack([pool[i]["move"] for i in idx]))
+        gb.input_pointcloud_batch(torch.cat([dev[i] for i in idx]), offsets, [(0, 1, 0)],
+                                  np.stack([pool[i]["R"] for i in idx]), np.stack([pool[i]["t"] for i in idx]),
+                                  c["noise"])
+        for b in sample:
+            fr = pool[idx[b]]
+            oras[b].move_to(*fr["move"])
+            oras[b].input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+    for nm in gb.layer_names():
+        lay = np.asarray(gb.get_layer(nm))
+        for b in sample:
+            o = oras[b].get_layer(nm)
+            g = lay[b]
+            assert np.array_equal(np.isnan(g), np.isnan(o)), (b, nm)
+            fin = ~np.isnan(o)
+            if nm.endswith("_observed") or nm == "valid":
+                assert np.array_equal(g, o), (b, nm)
+            else:
+                assert np.all(np.abs(g[fin].astype(np.float64) - o[fin]) <= 1e-6 + 1e-5 * np.abs(o[fin])), (b, nm)
