@@ -56,6 +56,7 @@ struct PassArgs {
   Control *ctl;
   int epoch;                   // stats epoch of this call (0/1)
   int pdl;                     // launch with programmatic stream serialization (see launch_pdl)
+  int smap_maxpts;             // k_smap: points of the largest map of the call (shared memory layout)
   ResetInfo reset;
   int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;

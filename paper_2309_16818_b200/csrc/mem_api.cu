@@ -1113,6 +1113,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
     const int grid = (int)std::max(1, std::min(B, sms > 0 ? sms : 1));
+    a.smap_maxpts = (int)max_n;
     TIMED(MEM_STAGE_POINT, launch_smap(a, grid, smap_smem_bytes(HW, max_n), m->stream));
     m->pending = false;
     return MEM_OK;
