@@ -2132,14 +2132,14 @@ cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_smap<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_smap<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_smap<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_smap<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  // the opt-in shared-memory size is a per-device function attribute: set it for the current
+  // device on every launch (a host-side call; maps may live on different devices)
+  if (a.dbg_cell)
+    cudaFuncSetAttribute(a.fast == 1 ? k_smap<true, 1> : k_smap<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  else
+    cudaFuncSetAttribute(a.fast == 1 ? k_smap<false, 1> : k_smap<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3(grid);
