@@ -1,0 +1,50 @@
+// dev_common.cuh -- device helpers shared by the kernels: PDL, streaming loads, strip test, cell reset.
+// Part of the single translation unit kernels.cu (included inside namespace memk, in order).
+#pragma once
+
+// ---------------------------------------------------------------- programmatic dependent launch
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------- memory helpers
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// read-once point data: no L1 allocation, evict-first in L2 so the scratch of the maps in
+// flight keeps its L2 residency
+__device__ __forceinline__ float4 ld_stream_f4(const float *p, unsigned long long pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ bool finite3(float a, float b, float c) { return isfinite(a) && isfinite(b) && isfinite(c); }
+
+__device__ __forceinline__ int stat_slot(int code) {
+  // mem_stats order: n_input, nonfinite, range, height, oob, inlier, outlier, touched
+  return code == MEM_CODE_INLIER ? 5 : code == MEM_CODE_OUTLIER ? 6 : code - 1;
+}
+
+// is logical cell (row, col) in the strips that scrolled in with the pending shift (D14)?
+template <class F>
+__device__ __forceinline__ bool in_strip(int row, int col, const F &f, const Geometry &g) {
+  if (f.sr == 0 && f.sc == 0) return false;
+  const int ar = f.sr < 0 ? -f.sr : f.sr, ac = f.sc < 0 ? -f.sc : f.sc;
+  if (ar >= g.H || ac >= g.W) return true;
+  const bool rs = f.sr > 0 ? row >= g.H - f.sr : row < -f.sr;
+  const bool cs = f.sc > 0 ? col >= g.W - f.sc : col < -f.sc;
+  return rs || cs;
+}
+
+// the state of a never-observed cell (D15)
+__device__ __forceinline__ void reset_cell(const State &st, long long BHW, long long cell, const ResetInfo &r) {
+  float *vals = reinterpret_cast<float *>(st.words);
+  vals[(long long)kWordElev * BHW + cell] = __int_as_float(0x7fc00000);
+  vals[(long long)kWordVar * BHW + cell] = __int_as_float(0x7fc00000);
+  for (int w = 2; w < r.n_word; ++w) st.words[(long long)w * BHW + cell] = 0u;
+  for (int l = 0; l < r.n_label; ++l) reinterpret_cast<int *>(st.words)[(long long)r.label_word[l] * BHW + cell] = -1;
+  for (int fl = 0; fl < r.n_flag; ++fl) st.flags[(long long)fl * BHW + cell] = 0;
+}

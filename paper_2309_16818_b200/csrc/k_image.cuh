@@ -1,0 +1,134 @@
+// k_image.cuh -- occlusion walk (NEXT-1) and k_image (a11-a12).
+// Part of the single translation unit kernels.cu (included inside namespace memk, in order).
+#pragma once
+
+// ---------------------------------------------------------------- occlusion (NEXT-1)
+// Is logical cell (row, col) of map m seen from the camera at (tx, ty, tz) (map-centred, fp32)?
+// every intermediate cell of the Bresenham line from the camera's footprint
+// cell to the target must lie below the ray; readings D32-D34: the line is walked
+// from the lexicographically smaller endpoint (all-octant integer form), cells outside the map
+// and unknown cells do not occlude, the ray height is linear in the 2D distance between the
+// camera height and the target elevation, tolerance eps_occ.  fp32 in the oracle's order.
+__device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row, int col, float tx, float ty,
+                                             float tz, float hb, int2 ring) {
+  const Geometry &g = a.geo;
+  const float *elev = reinterpret_cast<const float *>(a.st.words) + (long long)kWordElev * g.BHW;
+  const uint8_t *validp = a.st.flags + (long long)kFlagValid * g.BHW;
+  const int rc = (int)floorf(tx * g.inv_res + g.hH), cc = (int)floorf(ty * g.inv_res + g.hW);
+  const float xb = ((float)row + 0.5f - g.hH) * g.res, yb = ((float)col + 0.5f - g.hW) * g.res;
+  const float dxb = xb - tx, dyb = yb - ty;
+  const float db = sqrtf(dxb * dxb + dyb * dyb);
+  int r0 = rc, c0 = cc, r1 = row, c1 = col;
+  if (r1 < r0 || (r1 == r0 && c1 < c0)) {
+    r0 = row; c0 = col; r1 = rc; c1 = cc;
+  }
+  const int dx = abs(r1 - r0), dy = -abs(c1 - c0);
+  const int sx = r0 < r1 ? 1 : -1, sy = c0 < c1 ? 1 : -1;
+  int err = dx + dy, x = r0, y = c0;
+  const long long mbase = (long long)m * g.HW;
+  // the line has max(dx, -dy) - 1 intermediate cells; they are generated kOccBatch at a time
+  // and all their (valid, h) loads issued before any test (one round trip per batch)
+  constexpr int kOccBatch = MEM_OCC_BATCH;
+  int left = max(dx, -dy) - 1;
+  while (left > 0) {
+    int bx[kOccBatch], by[kOccBatch];
+    long long bj[kOccBatch];
+    uint8_t bv[kOccBatch];
+    float bh[kOccBatch];
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      bj[k] = -1;
+      if (k < left) {
+        const int e2 = 2 * err;
+        if (e2 >= dy) { err += dy; x += sx; }
+        if (e2 <= dx) { err += dx; y += sy; }
+        bx[k] = x;
+        by[k] = y;
+        if (x >= 0 && x < g.H && y >= 0 && y < g.W)  // outside the map: no occluder
+          bj[k] = mbase + (long long)wrap(x + ring.x, g.H) * g.W + wrap(y + ring.y, g.W);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      bv[k] = 0;
+      if (bj[k] >= 0) {
+        bv[k] = validp[bj[k]];
+        bh[k] = elev[bj[k]];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kOccBatch; ++k) {
+      if (!bv[k]) continue;  // unknown terrain does not occlude
+      const float xi = ((float)bx[k] + 0.5f - g.hH) * g.res, yi = ((float)by[k] + 0.5f - g.hW) * g.res;
+      const float dxi = xi - tx, dyi = yi - ty;
+      const float di = sqrtf(dxi * dxi + dyi * dyi);
+      const float ray = tz + (di / db) * (hb - tz);
+      if (bh[k] > ray + a.eps_occ) return false;
+    }
+    left -= kOccBatch;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- k_image (a11-a12)
+__global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ ImageArgs a) {
+  const Geometry &g = a.geo;
+  const int m = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.HW) return;
+  const int row = t / g.W, col = t - (t / g.W) * g.W;  // logical cell
+  const int2 ring = a.ring[m];
+  const int prow = wrap(row + ring.x, g.H);
+  if (prow < a.row_lo || prow >= a.row_hi) return;  // another rank's band (sharded map)
+  const long long cell = (long long)m * g.HW + (long long)prow * g.W + wrap(col + ring.y, g.W);
+  if (!a.st.flags[(long long)kFlagValid * g.BHW + cell]) return;
+  const MapFrame &f = a.frames ? a.frames[m] : a.f0;
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  // a11: cell centre at its elevation, relative to the map centre (D13), into the camera (D17)
+  const float xc = ((float)row + 0.5f - g.hH) * g.res;
+  const float yc = ((float)col + 0.5f - g.hW) * g.res;
+  const float dx = xc - f.t[0], dy = yc - f.t[1];
+  const float hcell = vals[(long long)kWordElev * g.BHW + cell];
+  const float dz = hcell - f.t[2];
+  const float pcx = (f.R[0] * dx + f.R[3] * dy) + f.R[6] * dz;
+  const float pcy = (f.R[1] * dx + f.R[4] * dy) + f.R[7] * dz;
+  const float pcz = (f.R[2] * dx + f.R[5] * dy) + f.R[8] * dz;
+  if (!(pcz > 1e-6f)) return;
+  const float ux = pcx / pcz, uy = pcy / pcz;
+  const float u = (f.K[0] * ux + f.K[1] * uy) + f.K[2];  // pinhole
+  const float v = f.K[3] * uy + f.K[4];
+  const float fu = floorf(u + 0.5f), fv = floorf(v + 0.5f);  // nearest pixel (D16)
+  if (!(0.0f <= fu && fu < (float)a.IW && 0.0f <= fv && fv < (float)a.IH)) return;  // frustum
+  if (a.occlusion && !cell_visible(a, m, row, col, f.t[0], f.t[1], f.t[2], hcell, ring)) return;
+  const long long plane = (long long)a.IH * a.IW;
+  const float *pix = a.img + (long long)m * a.map_stride + (long long)(int)fv * a.IW + (int)fu;
+  // a12: sample and fuse with N_j = 1
+  for (int bi = 0; bi < a.nb; ++bi) {
+    const BindDesc &b = a.b[bi];
+    const float *ch = pix + (long long)b.ch_offset * plane;
+    if (b.topk > 0) {  // top-k pairs (D38)
+      const TopK tk{ch, plane, b.topk, b.g.nch - 1};
+      if (!tk.ok()) continue;
+      const unsigned long long key = b.g.rule == MEM_CLASS_MAX ? tk.key() : 0ull;
+      apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)tk.value(k); }, key);
+      continue;
+    }
+    bool fin = true;
+    for (int k = 0; k < b.nch; ++k) fin &= (bool)isfinite(__ldg(ch + k * plane));
+    if (!fin) continue;  // D21
+    unsigned long long key = 0ull;
+    if (b.g.rule == MEM_CLASS_MAX) {
+      int best = 0;
+      float bv = __ldg(ch);
+      for (int k = 1; k < b.nch; ++k) {
+        const float c = __ldg(ch + k * plane);
+        if (c > bv) {
+          bv = c;
+          best = k;
+        }
+      }
+      key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
+    }
+    apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)__ldg(ch + k * plane); }, key);
+  }
+}
