@@ -28,6 +28,10 @@ import time
 
 import numpy as np
 
+# stdout carries exactly one JSON line: NCCL's own log lines (the version banner of the C5b
+# communicator, NCCL_DEBUG output) go to stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -676,6 +676,24 @@ def test_multi_wave_schedule_in_subprocess():
     assert "3 passed" in r.stdout, r.stdout[-2000:]
 
 
+def test_tma_cell_pass_in_subprocess():
+    """the opt-in bulk-copy cell pass k_cells_tma (env MEM_CELLS_TMA=1, read when libmem loads)
+    runs the fast paths (C1: one average channel, C2 / C2x64: colour) including shifts and a
+    ragged last tile (40000 = 78 x 512 + 64 cells); the parity tests must pass under it."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MEM_CELLS_TMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        "tests/test_parity_gpu.py::test_c1_chained_10_frames",
+                        "tests/test_parity_gpu.py::test_c2_lidar_10_frames",
+                        "tests/test_parity_gpu.py::test_batched_equals_single_and_oracle",
+                        "tests/test_parity_gpu.py::test_c2x64_bench_configuration_sampled"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "4 passed" in r.stdout, r.stdout[-2000:]
+
+
 # ---------------------------------------------------------------- k_smap (small maps, sort by cell)
 def test_deterministic_small_maps_are_bit_exact():
     """MEM_FLAG_DETERMINISTIC: maps of <= 16384 cells with <= 65535 points take k_smap, which
