@@ -530,9 +530,12 @@ def run_mem(a):
         te = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_step = float(te.item()) * 1e-3 / e_steps
         e2e = {"value": npts * M_ * e_steps * world / (float(te.item()) * 1e-3), "unit": "points/s",
                "h2d_bytes_per_step": int(host[0].numel() * 4), "d2h_bytes_per_step": int(out.numel() * 4),
-               "steps": e_steps}
+               "steps": e_steps,
+               # host<->device bytes per step over the step time: the PCIe link is the bound here
+               "pcie_gbs": (host[0].numel() + out.numel()) * 4 / t_step / 1e9}
 
     # ---- single-map C2 latency (context: below launch latency)
     single = None
