@@ -26,14 +26,26 @@ constexpr int kSmapSortMax = 256;  // cells with more points keep the scatter or
 // shared memory: the per-cell counts / offsets as packed u16 pairs (a map has < 65536 points)
 // and the u16 point indices
 constexpr int kSmapChunk = 64;  // P4: points per warp step
+// The P4 slices share their space with the u16 cell of every point that P1 records for P3
+// (P3 then scatters from shared memory instead of re-reading and re-binning the points).
+#ifndef MEM_SMAP_CACHE
+#define MEM_SMAP_CACHE 1
+#endif
 __host__ __device__ inline size_t smap_tmp_offset(int HW, long long max_pts) {
   return (sizeof(unsigned) * (size_t)((HW + 1) / 2) + sizeof(uint16_t) * (size_t)max_pts + 15) & ~(size_t)15;
 }
+constexpr size_t kSmapTmpBytes = sizeof(float4) * (size_t)kSmapChunk * (kSmapThreads / 32);
+constexpr size_t kSmapMaxSmem = 220 * 1024;
+__host__ __device__ inline bool smap_cached(int HW, long long max_pts) {
+  const size_t pc = sizeof(uint16_t) * (size_t)max_pts;
+  return MEM_SMAP_CACHE && smap_tmp_offset(HW, max_pts) + (pc > kSmapTmpBytes ? pc : kSmapTmpBytes) <= kSmapMaxSmem;
+}
 size_t smap_smem_bytes(int HW, long long max_pts) {
-  return smap_tmp_offset(HW, max_pts) + sizeof(float4) * (size_t)kSmapChunk * (kSmapThreads / 32);
+  const size_t pc = smap_cached(HW, max_pts) ? sizeof(uint16_t) * (size_t)max_pts : 0;
+  return smap_tmp_offset(HW, max_pts) + (pc > kSmapTmpBytes ? pc : kSmapTmpBytes);
 }
 bool smap_eligible(int HW, long long max_pts) {
-  return HW <= kSmapCells && max_pts <= kSmapPoints && smap_smem_bytes(HW, max_pts) <= 220 * 1024;
+  return HW <= kSmapCells && max_pts <= kSmapPoints && smap_smem_bytes(HW, max_pts) <= kSmapMaxSmem;
 }
 
 template <bool kDebug, int kFast>
@@ -45,6 +57,8 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
   uint16_t *idx = reinterpret_cast<uint16_t *>(hist + (g.HW + 1) / 2);
   auto h16 = [&](int c) { return (hist[c >> 1] >> (16 * (c & 1))) & 0xffffu; };
   float4 *s_tmp = reinterpret_cast<float4 *>(s_dyn + smap_tmp_offset(g.HW, a.smap_maxpts));  // P4 slices
+  uint16_t *pcell = reinterpret_cast<uint16_t *>(s_tmp);  // P1 -> P3: cell of every point (0xffff: dropped)
+  const bool cached = smap_cached(g.HW, a.smap_maxpts);
   __shared__ unsigned s_part[kSmapThreads];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
@@ -86,6 +100,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
         const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
+        if (cached) pcell[i] = o.cell >= 0 ? (uint16_t)(o.cell - map_base) : (uint16_t)0xffffu;
         if (o.cell >= 0) {
           const int c = o.cell - map_base;
           atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1)));
@@ -128,8 +143,14 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
       for (int w = w0 + lane; w < w1; w += 32) hist[w] += off | (off << 16);
     }
     __syncthreads();
-    // P3: scatter the in-window points' indices by cell (the map's points are now in L2)
-    for (int i0 = threadIdx.x; i0 < np; i0 += 4 * kSmapThreads) {
+    // P3: scatter the in-window points' indices by cell
+    if (cached) {
+      for (int i = threadIdx.x; i < np; i += kSmapThreads) {
+        const unsigned c = pcell[i];
+        if (c != 0xffffu) idx[(atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1))) >> (16 * (c & 1))) & 0xffffu] = (uint16_t)i;
+      }
+    }
+    for (int i0 = threadIdx.x; i0 < (cached ? 0 : np); i0 += 4 * kSmapThreads) {  // re-binned (points in L2)
       float4 q[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
