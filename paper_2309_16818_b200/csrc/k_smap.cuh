@@ -6,10 +6,11 @@
 // One CTA per map (grid-stride over the wave's maps) for the fast rules on small maps
 // (H*W <= kSmapCells, <= kSmapPoints points per map): no scratch, no atomics outside shared
 // memory.  P1 bins every point (streamed once from HBM) into a shared-memory histogram of its
-// cell; P2 turns it into offsets; P3 re-bins (the map's points are L2-resident) and scatters
-// the point indices by cell; P4 gives every cell to one thread, which sorts the cell's indices
-// (input order, like the oracle), re-reads and re-bins those points, tests them against the
-// cell's pre-frame state (a7), sums in fp64 in input order and fuses the cell with the
+// cell (and records the cell of every point when shared memory allows); P2 turns it into
+// offsets; P3 scatters the point indices by cell (from the recorded cells, else re-binned
+// from L2); P4 gives every cell to one lane, which sorts the cell's indices (input order,
+// like the oracle); the warp re-reads those points, recomputes z and v and tests them
+// against the cell's pre-frame state (a7); the lane sums in fp64 in input order and fuses the cell with the
 // oracle's exact formulas -- so this path is deterministic and reproduces the oracle's sums
 // operation for operation.  (The north_star's "sort-by-cell segmented reduction".)
 #ifndef MEM_SMAP_THREADS
@@ -171,8 +172,9 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
     __syncthreads();
     // P4: warps take groups of 32 consecutive cells (lane = cell).  Each lane sorts its cell's
     // point indices into input order and loads its cell's pre-frame state; the warp then walks
-    // the group's points (contiguous in idx) 64 at a time, lane-parallel: re-read, re-bin,
-    // outlier test against the owner lane's state (shuffle), contributions staged in the
+    // the group's points (contiguous in idx) 64 at a time, lane-parallel: re-read, recompute
+    // z and v, find the owner lane (the segment holding the position), outlier test against
+    // the owner lane's state (shuffle), contributions staged in the
     // warp's shared slice; each lane then adds its own cell's contributions in input order --
     // the oracle's sequential fp64 sums -- and finally fuses and stores its cell.
     const bool shift = f.sr != 0 || f.sc != 0;
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
         }
         const unsigned last = __reduce_max_sync(0xffffffffu, inmap ? (unsigned)lane : 0u);
         const unsigned R0 = __shfl_sync(0xffffffffu, s0, 0), R1 = __shfl_sync(0xffffffffu, s1, last);
+        const unsigned e = inmap ? s1 : 0xffffffffu;  // segment ends, non-decreasing over the lanes
         __syncwarp();  // every lane's sorted segment is visible
         unsigned nin = 0, nout = 0, ng = 0, cr = 0, cg = 0, cbl = 0;
         double P = 0.0, S = 0.0, X = 0.0;
@@ -240,8 +243,30 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
             o.test = false;
             o.z = o.v = 0.0f;
             o.lcell = -1;
-            if (act) o = bin_point(q.x, q.y, q.z, f, g, a.np, rmin2, rmax2, map_base);
-            const int owner = act ? o.cell - map_base - gbase : lane;  // the lane holding its cell
+            int owner = lane;  // the lane holding the point's cell
+            if (kDebug) {
+              if (act) o = bin_point(q.x, q.y, q.z, f, g, a.np, rmin2, rmax2, map_base);
+              if (act) owner = o.cell - map_base - gbase;
+            } else {
+              // the point is known to be in the window: only z and v are recomputed (bin_point's
+              // expressions, same rounding), and its cell is the segment that holds position r
+              // (binary search over the lanes' segment ends).  A scrolled-in strip cell has
+              // vd = 0 (reset state), so the test flag of bin_point is not needed.
+              if (act) {
+                const float r2 = (q.x * q.x + q.y * q.y) + q.z * q.z;
+                const float qz = (f.R[6] * q.x + f.R[7] * q.y) + f.R[8] * q.z;
+                o.z = qz + f.t[2];
+                o.v = a.np.a + a.np.b * r2;
+                o.test = true;
+              }
+              int lo = 0;
+#pragma unroll
+              for (int st = 16; st > 0; st >>= 1) {
+                const unsigned eo = __shfl_sync(0xffffffffu, e, lo + st - 1);
+                lo += eo <= r ? st : 0;
+              }
+              if (act) owner = lo;
+            }
             const float ho = __shfl_sync(0xffffffffu, h, owner), so = __shfl_sync(0xffffffffu, s2, owner);
             const int vo = __shfl_sync(0xffffffffu, (int)vd, owner);
             if (act) {
@@ -251,7 +276,8 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
                 outl = d * d > a.np.tau2 * (so + o.v);
               }
               const int code = outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER;
-              count_code(packed, npk, code, cnt);
+              cnt[5] += outl ? 0u : 1u;  // stat_slot(INLIER), stat_slot(OUTLIER)
+              cnt[6] += outl ? 1u : 0u;
               if (kDebug) {
                 a.dbg_cell[beg + i] = o.lcell;
                 a.dbg_code[beg + i] = (uint8_t)code;

@@ -732,6 +732,51 @@ def test_deterministic_small_maps_are_bit_exact():
             assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
 
 
+@pytest.mark.parametrize("rule", ["color", "average"])
+def test_deterministic_batch_without_debug_outputs_is_bit_exact(rule):
+    """k_smap without per-point debug outputs (its production variant: the point's cell comes
+    from its sorted position, z and v are recomputed) on a batch of 64 maps of 64x64 cells with
+    up to 60,000 points each, dense and sparse maps, colour or average (with NaN features),
+    moves every frame: every layer bit-identical to the oracle, counters equal."""
+    rows, cols, res, B = 64, 64, 0.1, 64
+    if rule == "color":
+        groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.4)]
+    else:
+        groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.4)]
+    gb = M.Map(res, rows, cols, groups, n_maps=B, deterministic=True)
+    oras = [O.OracleMap(res, rows, cols, groups) for _ in range(B)]
+    rng = np.random.default_rng(31)
+    for f in range(3):
+        sizes = rng.integers(0, 60000, B)
+        sizes[0], sizes[1] = 0, 60000
+        clouds = []
+        for b in range(B):
+            p = S.random_cloud(1000 * f + b, int(sizes[b]), 4, rows, cols, res)
+            if rule == "color":
+                p[:, 3] = S.pack_rgb(rng.integers(0, 256, (len(p), 3)).astype(np.uint8))
+            else:
+                p[rng.uniform(size=len(p)) < 0.03, 3] = np.nan
+            p[rng.uniform(size=len(p)) < 0.02, 2] += 2.0  # outliers
+            clouds.append(p)
+        offs = np.concatenate([[0], np.cumsum([len(p) for p in clouds])]).astype(np.int64)
+        moves = rng.uniform(-0.3, 0.3, (B, 2)) * f
+        Rs = np.stack([S.rot_z(0.1 * f + 0.01 * b) for b in range(B)])
+        ts = np.stack([[moves[b, 0] + 0.01, moves[b, 1] - 0.02, 1.0] for b in range(B)])
+        gb.move_to_batch(moves)
+        gb.input_pointcloud_batch(torch.from_numpy(np.concatenate(clouds)).cuda(), offs, [(0, 1, 0)], Rs, ts, NOISE_R)
+        for b in range(B):
+            oras[b].move_to(*moves[b])
+            oras[b].input_pointcloud(clouds[b], [(0, 1, 0)], Rs[b], ts[b], NOISE_R)
+        st = gb.stats()
+        for k in O.STAT_NAMES:
+            assert st[k] == sum(o.stats()[k] for o in oras), (f, k)
+    for nm in gb.layer_names():
+        lay = np.asarray(gb.get_layer(nm))
+        for b in range(B):
+            assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (rule, b, nm)
+    assert sum((np.asarray(gb.get_layer("valid"))[b] > 0).sum() for b in range(B)) > 100000
+
+
 def test_deterministic_flag_falls_back_beyond_limits():
     """MEM_FLAG_DETERMINISTIC on inputs k_smap does not take (too many points per map, a
     multi-group map) fuses through the default path, still within the parity bar."""
