@@ -28,9 +28,22 @@ import time
 
 import numpy as np
 
-# stdout carries exactly one JSON line: NCCL's own log lines (the version banner of the C5b
-# communicator, NCCL_DEBUG output) go to stderr
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# stdout carries exactly one JSON line: file descriptor 1 is pointed at stderr for the whole
+# run (native libraries print there too, e.g. NCCL's version banner when the C5b communicator
+# is created) and the line is written to the saved original stdout
+_JSON_FD = None
+
+
+def claim_stdout():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line):
+    sys.stdout.flush()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -203,7 +216,7 @@ def run_reference(a):
                                    f"{a.steps} steps"},
         "e2e": {"value": pts, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -606,7 +619,7 @@ def run_mem(a):
             "side_lines": sides,
             "frame_stats_last_step": stats,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -616,6 +629,7 @@ def run_mem(a):
 
 def main():
     a = parse()
+    claim_stdout()
     if a.impl == "reference":
         return run_reference(a)
     return run_mem(a)
