@@ -13,6 +13,7 @@
 __device__ __forceinline__ const PointFrame &frame_of(const PassArgs &a, int m) {
   return a.frames ? a.frames[m] : a.fi[m];
 }
+
 __device__ __forceinline__ long long off_of(const PassArgs &a, int m) {
   return a.offsets ? __ldg(&a.offsets[m]) : a.offi[m];
 }
@@ -87,7 +88,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
         a.dbg_cell[t.base + k] = o[u].lcell;
         a.dbg_code[t.base + k] = (uint8_t)o[u].code;
       }
-      count_code(packed, npk, o[u].code, cnt);
+      if (o[u].code >= 0) packed += 1ull << (10 * o[u].code);  // flushed once per item, below
     }
     if (a.ablate & 2u) continue;
     const float *pp = kFast != 0 ? nullptr : a.pts + (k < nv ? t.base + k : t.beg) * (long long)a.stride;
@@ -96,6 +97,13 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
                          pw[u]);
     else
       accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), pp, pw[u]);
+  }
+  npk += kWarpPtsPerLane;  // the 10-bit code fields are flushed before they can wrap
+  if (npk > 1023u - kWarpPtsPerLane) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
+    packed = 0ull;
+    npk = 0;
   }
 }
 

@@ -98,18 +98,19 @@ static cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, c
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
   // the fast variants need the channel in the float4's w (vec4) and exactly one group bound
   const int f = a.vec4 ? a.fast : 0;
+  const size_t fs = 0;  // no dynamic shared memory
   if (a.dbg_cell) {
-    if (f == 1 && a.bucketed) return launch_pdl(k_points<true, 1, true>, grid, 0, s, a);
-    else if (f == 2 && a.bucketed) return launch_pdl(k_points<true, 2, true>, grid, 0, s, a);
-    else if (f == 1) return launch_pdl(k_points<true, 1, false>, grid, 0, s, a);
-    else if (f == 2) return launch_pdl(k_points<true, 2, false>, grid, 0, s, a);
-    else return launch_pdl(k_points<true, 0, false>, grid, 0, s, a);
+    if (f == 1 && a.bucketed) return launch_pdl(k_points<true, 1, true>, grid, fs, s, a);
+    else if (f == 2 && a.bucketed) return launch_pdl(k_points<true, 2, true>, grid, fs, s, a);
+    else if (f == 1) return launch_pdl(k_points<true, 1, false>, grid, fs, s, a);
+    else if (f == 2) return launch_pdl(k_points<true, 2, false>, grid, fs, s, a);
+    else return launch_pdl(k_points<true, 0, false>, grid, fs, s, a);
   } else {
-    if (f == 1 && a.bucketed) return launch_pdl(k_points<false, 1, true>, grid, 0, s, a);
-    else if (f == 2 && a.bucketed) return launch_pdl(k_points<false, 2, true>, grid, 0, s, a);
-    else if (f == 1) return launch_pdl(k_points<false, 1, false>, grid, 0, s, a);
-    else if (f == 2) return launch_pdl(k_points<false, 2, false>, grid, 0, s, a);
-    else return launch_pdl(k_points<false, 0, false>, grid, 0, s, a);
+    if (f == 1 && a.bucketed) return launch_pdl(k_points<false, 1, true>, grid, fs, s, a);
+    else if (f == 2 && a.bucketed) return launch_pdl(k_points<false, 2, true>, grid, fs, s, a);
+    else if (f == 1) return launch_pdl(k_points<false, 1, false>, grid, fs, s, a);
+    else if (f == 2) return launch_pdl(k_points<false, 2, false>, grid, fs, s, a);
+    else return launch_pdl(k_points<false, 0, false>, grid, fs, s, a);
   }
   return cudaGetLastError();
 }
