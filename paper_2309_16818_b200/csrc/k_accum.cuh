@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
   float *elev = vals + (long long)kWordElev * BHW, *var = vals + (long long)kWordVar * BHW;
   uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
   uint8_t *obsp = a.st.flags + (long long)gd.flag * BHW;
-  const int units = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * a.nbands;
+  const int units = ABLATE(a, 1u) ? 0 : (a.m1 - a.m0) * a.nbands;
   auto key_of = [&](int un) {
     const int mi = un / a.nbands;
     return (a.slot0 + mi) * a.nbands + (un - mi * a.nbands);
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
           strip[v] = in_strip(row, col, f, g);
         }
         // untouched cells outside the strips stay bit-identical
-        dirty[v] = strip[v] || (nin[v] + nout[v] != 0u && !(a.ablate & 512u));
+        dirty[v] = strip[v] || (nin[v] + nout[v] != 0u && !ABLATE(a, 512u));
       }
       float h[2], s2[2], th[2][NCH];
       uint8_t vd[2], ob[2];
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_accum(const __grid_constant__ P
           for (int k = 0; k < NCH; ++k) th[v][k] = 0.0f;
           vd[v] = ob[v] = 0;
         }
-        if (nin[v] + nout[v] != 0u && !(a.ablate & 512u)) {
+        if (nin[v] + nout[v] != 0u && !ABLATE(a, 512u)) {
           ++cnt[7];
           // a9: Kalman height fusion (D7), outliers inflate first (D11); reciprocals (D29b)
           if (vd[v]) {

@@ -25,11 +25,11 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
   const int nwarps = gridDim.x * (kThreads / 32);
   const int gw = blockIdx.x * (kThreads / 32) + wid;
   const int cpm = (a.cell_hi - a.cell_lo + kChunk - 1) / kChunk;  // chunks per map (band)
-  const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * cpm;
+  const int total = ABLATE(a, 1u) ? 0 : (a.m1 - a.m0) * cpm;
   int *sp = s_phys[wid];
   unsigned long long *sc = s_cntv[wid];
   for (int rt = gw; rt < total; rt += nwarps) {
-    const int chunk = (a.ablate & 32u) ? rt : total - 1 - rt;
+    const int chunk = ABLATE(a, 32u) ? rt : total - 1 - rt;
     const int mi = chunk / cpm;
     const int m = a.m0 + mi;
     const int t0 = a.cell_lo + (chunk - mi * cpm) * kChunk;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
     }
     __syncwarp();
     cnt[7] += lane == 0 ? (unsigned)n : 0u;
-    for (int k0 = 0; k0 < ((a.ablate & 512u) ? 0 : n); k0 += 64) {
+    for (int k0 = 0; k0 < (ABLATE(a, 512u) ? 0 : n); k0 += 64) {
       int ph[2];
       unsigned long long cc[2];
 #pragma unroll

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kTmaThreads, MEM_TMA_MINB) k_cells_tma(const _
   const long long BHW = g.BHW;
   float *vals = reinterpret_cast<float *>(a.st.words);
   const int tpm = (a.cell_hi - a.cell_lo + kTT - 1) / kTT;  // tiles per map (band)
-  const int total = (a.ablate & 1u) ? 0 : (a.m1 - a.m0) * tpm;
+  const int total = ABLATE(a, 1u) ? 0 : (a.m1 - a.m0) * tpm;
   const int ntile = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   // this CTA's j-th tile: map and first physical cell (newest map first, as k_cells)
   auto tile_of = [&](int j, int &m, int &t0, int &n) {

@@ -71,7 +71,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
 #pragma unroll
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
     const bool in = u * 32 + lane < nv;
-    if (in && !(a.ablate & 8u)) {
+    if (in && !ABLATE(a, 8u)) {
       o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
     } else {
       o[u].code = in ? MEM_CODE_NONFINITE : -1;
@@ -79,7 +79,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
       o[u].test = false;
     }
   }
-  if (!(a.ablate & 4u)) mahalanobis(o, a.st, g, a.np.tau2);
+  if (!ABLATE(a, 4u)) mahalanobis(o, a.st, g, a.np.tau2);
 #pragma unroll
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
     const int k = u * 32 + lane;
@@ -90,7 +90,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
       }
       if (o[u].code >= 0) packed += 1ull << (10 * o[u].code);  // flushed once per item, below
     }
-    if (a.ablate & 2u) continue;
+    if (ABLATE(a, 2u)) continue;
     const float *pp = kFast != 0 ? nullptr : a.pts + (k < nv ? t.base + k : t.beg) * (long long)a.stride;
     if constexpr (kBucket)
       bucket_warp<kFast>(a, o[u], o[u].cell - map_base, a.slot0 + t.m - a.m0, sb + (o[u].cell - map_base), pp,

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
           __syncwarp();  // the slice is refilled by the next chunk
         }
         if (!live) continue;
-        if (s1 > s0 && !(a.ablate & 512u)) {
+        if (s1 > s0 && !ABLATE(a, 512u)) {
           ++cnt[7];
           // a9 (D7, D11) in the oracle's exact form
           if (vd) {

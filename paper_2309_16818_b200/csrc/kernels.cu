@@ -37,6 +37,12 @@
 #ifndef MEM_OCC_BATCH
 #define MEM_OCC_BATCH 4  // occlusion walk: intermediate cells whose loads are issued together
 #endif
+// DIAGNOSTICS ONLY: env MEM_ABLATE switches parts of the kernels off (PassArgs::ablate) in a
+// build with -DMEM_ABLATION=1; production builds compile the checks out
+#ifndef MEM_ABLATION
+#define MEM_ABLATION 0
+#endif
+#define ABLATE(a, bit) (MEM_ABLATION && ((a).ablate & (bit)))
 #ifndef MEM_CELLS_MINB
 #define MEM_CELLS_MINB 3
 #endif

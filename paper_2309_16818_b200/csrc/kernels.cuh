@@ -73,7 +73,8 @@ struct PassArgs {
   PointFrame fi[kInlineMaps];
   long long offi[kInlineMaps + 1];
   int psi[kInlineMaps + 1];
-  unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE; results are wrong when != 0):
+  unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE, honoured by builds with -DMEM_ABLATION=1;
+                               // results are wrong when != 0):
                                // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math,
                                // 32 forward (not newest-first) cell tile order, 64 no warp aggregation,
                                // 4096 k_accum: no fp64 shared atomics, 8192 k_accum: no channel atomics

@@ -185,7 +185,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
   // LiDAR scan line has ~1.5 points per cell and is faster with one RED set per lane)
   const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
   const unsigned dup = __ballot_sync(0xffffffffu, act && lane > 0 && prev == key);
-  const bool agg = __popc(dup) >= 16 && !(a.ablate & 64u);
+  const bool agg = __popc(dup) >= 16 && !ABLATE(a, 64u);
   const unsigned peers = agg ? __match_any_sync(0xffffffffu, key) : (1u << lane);
   const bool single = !agg;
   const bool leader = act && (__ffs(peers) - 1 == lane);
@@ -217,7 +217,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     if (!single) {
       rg = reduce_peers(peers, rg, OpAdd());
       bb = reduce_peers(peers, bb, OpAdd());
-    } else if (__popc(dup) >= MEM_PAIR_MIN && !(a.ablate & 64u)) {
+    } else if (__popc(dup) >= MEM_PAIR_MIN && !ABLATE(a, 64u)) {
       // a LiDAR scan line puts ~30% of its in-window points in the cell of the previous
       // lane: the head of each run absorbs its successor (one shuffle per value), so such
       // a pair costs one set of REDs
