@@ -140,15 +140,34 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
     };
     int it = i0 + gw, stage = 0;
     Item cur;
+    // uniform maps: the (map, item-in-map) of the warp's next item follows from the current
+    // one by an add and one carry (no division per item)
+    int um = 0, ur = 0;
+    const int ustep_m = a.p_uniform > 0 ? nwarps / a.p_uniform : 0;
+    const int ustep_r = a.p_uniform > 0 ? nwarps - ustep_m * a.p_uniform : 0;
     if (it < i1) {
       cur = item_of(a, it, i0);
+      if (a.p_uniform > 0) um = divmod_fast(it - i0, a.p_uniform, a.inv_p_uniform, ur);
       issue(cur, 0);
     }
     for (; it < i1; it += nwarps, stage ^= 1) {
       const int nx = it + nwarps;
       Item nxt;
       if (nx < i1) {
-        nxt = item_of(a, nx, i0);
+        if (a.p_uniform > 0) {
+          um += ustep_m;
+          ur += ustep_r;
+          if (ur >= a.p_uniform) {
+            ur -= a.p_uniform;
+            ++um;
+          }
+          nxt.m = a.m0 + um;
+          nxt.beg = off_of(a, nxt.m);
+          nxt.end = off_of(a, nxt.m + 1);
+          nxt.base = nxt.beg + (long long)ur * kWarpPoints;
+        } else {
+          nxt = item_of(a, nx, i0);
+        }
         issue(nxt, stage ^ 1);
         cp_async_wait<1>();
       } else {

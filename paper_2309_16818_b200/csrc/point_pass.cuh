@@ -175,7 +175,8 @@ struct TopK {
 template <int kFast>
 __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, const float *p,
                                                 float ch0) {
-  unsigned long long *rec = a.rec + (long long)sc * a.R;
+  // the fast paths' records are 4 words (mem_api selects them only then)
+  unsigned long long *rec = a.rec + (long long)sc * (kFast != 0 ? 4 : a.R);
   const bool act = o.cell >= 0;
   const unsigned act_b = __ballot_sync(0xffffffffu, act);
   if (act_b == 0u) return;
