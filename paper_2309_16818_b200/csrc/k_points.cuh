@@ -55,7 +55,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool kDebug, int kFast, bool kBucket>
+template <bool kDebug, int kFast, bool kBucket, bool kFull = false>
 __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, const float (&px)[kWarpPtsPerLane],
                                              const float (&py)[kWarpPtsPerLane], const float (&pz)[kWarpPtsPerLane],
                                              const float (&pw)[kWarpPtsPerLane], float rmin2, float rmax2,
@@ -66,7 +66,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   const int map_base = t.m * g.HW;
   const int sb = (int)scratch_base(a, t.m);
   // points of the item present: [0, nv) (32-bit indices within the item)
-  const int nv = t.end - t.base < kWarpPoints ? (int)(t.end - t.base) : kWarpPoints;
+  const int nv = kFull ? kWarpPoints : t.end - t.base < kWarpPoints ? (int)(t.end - t.base) : kWarpPoints;
   PointOut o[kWarpPtsPerLane];
 #pragma unroll
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
@@ -131,10 +131,16 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
   if (kFast != 0 || a.vec4) {
     const float4 *pts4 = reinterpret_cast<const float4 *>(a.pts);
     auto issue = [&](const Item &t, int stage) {
+      if (t.end - t.base >= kWarpPoints) {  // a full item (all but a map's last): no per-lane bounds
+        const float4 *src = pts4 + t.base + lane;
 #pragma unroll
-      for (int u = 0; u < kWarpPtsPerLane; ++u) {
-        const long long i = t.base + u * 32 + lane;
-        cp_async_16(&s_pts[wid][stage][u * 32 + lane], pts4 + (i < t.end ? i : t.beg), i < t.end, pol);
+        for (int u = 0; u < kWarpPtsPerLane; ++u) cp_async_16(&s_pts[wid][stage][u * 32 + lane], src + u * 32, true, pol);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kWarpPtsPerLane; ++u) {
+          const long long i = t.base + u * 32 + lane;
+          cp_async_16(&s_pts[wid][stage][u * 32 + lane], pts4 + (i < t.end ? i : t.beg), i < t.end, pol);
+        }
       }
       cp_async_commit();
     };
@@ -178,7 +184,12 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
         const float4 v = s_pts[wid][stage][u * 32 + lane];
         px[u] = v.x; py[u] = v.y; pz[u] = v.z; pw[u] = v.w;
       }
-      process_item<kDebug, kFast, kBucket>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+#if MEM_FULL_ITEMS
+      if (cur.end - cur.base >= kWarpPoints)  // every lane holds 4 points: no bounds checks
+        process_item<kDebug, kFast, kBucket, true>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+      else
+#endif
+        process_item<kDebug, kFast, kBucket>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
       cur = nxt;
     }
   } else {

@@ -43,6 +43,9 @@
 #define MEM_ABLATION 0
 #endif
 #define ABLATE(a, bit) (MEM_ABLATION && ((a).ablate & (bit)))
+#ifndef MEM_FULL_ITEMS
+#define MEM_FULL_ITEMS 1  // k_points: a variant of the item body without per-lane bounds for full items
+#endif
 #ifndef MEM_CELLS_MINB
 #define MEM_CELLS_MINB 3
 #endif
