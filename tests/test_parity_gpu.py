@@ -777,6 +777,36 @@ def test_deterministic_batch_without_debug_outputs_is_bit_exact(rule):
     assert sum((np.asarray(gb.get_layer("valid"))[b] > 0).sum() for b in range(B)) > 100000
 
 
+def test_c5a_bench_configuration_sampled():
+    """C5a exactly as bench.py's side line runs it: 4096 maps (256 generated maps tiled) in one
+    batched call per step, k_smap with its full grid (one CTA per SM, each CTA walking ~28
+    maps with its shared memory reused), frames alternating with moves; 3 steps.  Sampled maps
+    (first and later maps of a CTA, the last map) are bit-identical to their own oracle."""
+    c = S.C5A
+    total, P = 4096, c["points"]
+    pool = [S.c5a_batch(f, 0, 256) for f in range(2)]
+    idx = np.arange(total) % 256
+    dev = [torch.from_numpy(fr["points"].reshape(256, P, 4)[idx].reshape(-1, 4)).cuda() for fr in pool]
+    offsets = np.arange(total + 1, dtype=np.int64) * P
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])]
+    gb = M.Map(c["res"], c["rows"], c["cols"], groups, n_maps=total)
+    sample = [0, 147, 148, 296, 2049, 4095]
+    oras = {b: O.OracleMap(c["res"], c["rows"], c["cols"], groups) for b in sample}
+    for step in range(3):
+        fr = pool[step % 2]
+        gb.move_to_batch(fr["move"][idx])
+        gb.input_pointcloud_batch(dev[step % 2], offsets, [(0, 1, 0)], fr["R"][idx], fr["t"][idx], c["noise"])
+        for b in sample:
+            g = idx[b]
+            oras[b].move_to(*fr["move"][g])
+            oras[b].input_pointcloud(fr["points"][g * P:(g + 1) * P], [(0, 1, 0)], fr["R"][g], fr["t"][g], c["noise"])
+    for nm in gb.layer_names():
+        lay = np.asarray(gb.get_layer(nm))
+        for b in sample:
+            assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
+    assert all((np.asarray(gb.get_layer("valid"))[b] > 0).sum() > 8000 for b in sample)
+
+
 def test_deterministic_flag_falls_back_beyond_limits():
     """MEM_FLAG_DETERMINISTIC on inputs k_smap does not take (too many points per map, a
     multi-group map) fuses through the default path, still within the parity bar."""
