@@ -16,12 +16,18 @@
  * written order, no FMA contraction (compile with -ffp-contract=off, never with
  * -ffast-math); per-cell sums and closed forms in fp64, stored as (float).
  *
- * Parity pins: tests/test_oracle_pins.py.  Functions with no pin against the paper
- * are listed as "parity unpinned" below and in DESIGN.md §3:
- *   - the noise model v = a + b r^2 (D8), the Mahalanobis gate (D10), the outlier
- *     inflation sigma2 + n_out v_out (D11), class_max's temporal rule (D19), the
- *     colour rule (D20): pinned only by our own definitions + brute force, i.e.
- *     "parity unpinned vs the paper".
+ * Parity pins: tests/test_oracle_pins.py (list in DESIGN.md §3).  Every function has a
+ * pin that is not a re-typing of its own formula.  Where the paper is silent and the
+ * oracle follows the north_star / SPEC.md reading, the pin checks that reading by
+ * independent means:
+ *   - noise model v = a + b r^2 (D8): a single point into an empty cell gives height z
+ *     and variance a + b r^2 exactly (dyadic values; test_single_point_empty_cell);
+ *   - Mahalanobis gate (D10) and outlier inflation sigma2 + n_out v_out (D11): the
+ *     equality / next-float boundary cases and the inflated variance
+ *     (test_outlier_boundary);
+ *   - class_max's frame winner (D19): brute force with ties and input permutations
+ *     (test_class_max_brute_force_ties_permutation);
+ *   - colour rule (D20): brute-force per-cell RGB means (test_color_brute_force).
  */
 #include <math.h>
 #include <stdint.h>
