@@ -262,13 +262,6 @@ mem_status stage_params(mem_map *m, const void *src, size_t bytes, void **dptr) 
   p.next = (p.next + 1) % PinnedRing::kSlots;
   CU(cudaEventSynchronize(p.ev[k]));
   memcpy(p.host[k], src, bytes);
-  if (getenv("MEM_ZEROCOPY")) {  // EXPERIMENT: kernels read the pinned slot directly
-    CU(cudaEventRecord(p.ev[k], m->stream));
-    void *d = nullptr;
-    CU(cudaHostGetDevicePointer(&d, p.host[k], 0));
-    *dptr = d;
-    return MEM_OK;
-  }
   CU(cudaMemcpyAsync(m->dparam, p.host[k], bytes, cudaMemcpyHostToDevice, m->stream));
   CU(cudaEventRecord(p.ev[k], m->stream));
   *dptr = m->dparam;
