@@ -5,7 +5,10 @@
 namespace memk {
 
 constexpr int kThreads = 256;           // 8 warps per CTA
-constexpr int kWarpPtsPerLane = 4;      // point warp-item = 128 points (4 float4 loads in flight per lane)
+#ifndef MEM_WARP_PTS
+#define MEM_WARP_PTS 4
+#endif
+constexpr int kWarpPtsPerLane = MEM_WARP_PTS;  // point warp-item = 128 points (4 float4 loads in flight per lane)
 constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
 constexpr int kWarpCellsPerLane = 4;    // cell warp-item = 128 physical cells
 constexpr int kWarpCells = 32 * kWarpCellsPerLane;
