@@ -57,6 +57,9 @@ __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, cons
 // k_write keeps it so for state written through mem_set_layer), and a NaN h or s2 makes the
 // comparison false -- exactly the oracle's "no test on an invalid cell" (D10); a valid cell
 // whose h or s2 was set to NaN compares false in the oracle too.
+#ifndef MEM_STATE_LD
+#define MEM_STATE_LD 2  // state gathers: 0 plain LDG, 1 __ldg (.nc), 2 __ldcg (L2 only)
+#endif
 template <int N>
 __device__ __forceinline__ void mahalanobis(PointOut (&o)[N], const State &st, const Geometry &g, float tau2) {
   const float *elev = reinterpret_cast<const float *>(st.words) + (long long)kWordElev * g.BHW;
@@ -66,8 +69,16 @@ __device__ __forceinline__ void mahalanobis(PointOut (&o)[N], const State &st, c
   for (int u = 0; u < N; ++u) {
     hv[u] = sv[u] = __int_as_float(0x7fc00000);
     if (o[u].test) {
+#if MEM_STATE_LD == 1
+      hv[u] = __ldg(elev + o[u].cell);
+      sv[u] = __ldg(var + o[u].cell);
+#elif MEM_STATE_LD == 2
+      hv[u] = __ldcg(elev + o[u].cell);
+      sv[u] = __ldcg(var + o[u].cell);
+#else
       hv[u] = elev[o[u].cell];
       sv[u] = var[o[u].cell];
+#endif
     }
   }
 #pragma unroll
