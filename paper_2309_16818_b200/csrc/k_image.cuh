@@ -71,6 +71,40 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)
+// One-word-per-channel rules (average, class_average, color, class_bayesian) with N_j = 1,
+// kImgBatch channels at a time: the pixel and state loads of a batch are all issued before its
+// math and stores (apply_group's per-channel load -> store chain is one L2 round trip per
+// channel, since the compiler cannot move a load over a store to a possibly aliasing layer).
+// Same rule calls, same operands, same order: results are identical to apply_group's.
+#ifndef MEM_IMG_BATCH
+#define MEM_IMG_BATCH 8
+#endif
+constexpr int kImgBatch = MEM_IMG_BATCH;
+__device__ __forceinline__ void image_fuse_words(const State &st, long long BHW, long long cell, const GroupDesc &g,
+                                                 const float *ch, long long plane) {
+  float *vals = reinterpret_cast<float *>(st.words);
+  uint8_t *obs = st.flags + (long long)g.flag * BHW + cell;
+  const bool observed = *obs != 0;
+  const bool dir = g.rule == MEM_CLASS_BAYESIAN;
+  for (int k0 = 0; k0 < g.nch; k0 += kImgBatch) {
+    float p[kImgBatch], th[kImgBatch];
+#pragma unroll
+    for (int u = 0; u < kImgBatch; ++u) {
+      if (k0 + u < g.nch) {
+        p[u] = __ldg(ch + (long long)(k0 + u) * plane);
+        th[u] = vals[(long long)(g.word0 + k0 + u) * BHW + cell];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kImgBatch; ++u) {
+      if (k0 + u < g.nch)
+        vals[(long long)(g.word0 + k0 + u) * BHW + cell] =
+            dir ? rule_dirichlet(th[u], observed, (double)p[u], g.a0) : rule_average(th[u], observed, (double)p[u], 1.0, g.w);
+    }
+  }
+  *obs = 1;
+}
+
 __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ ImageArgs a) {
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
@@ -114,20 +148,36 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
       continue;
     }
     bool fin = true;
-    for (int k = 0; k < b.nch; ++k) fin &= (bool)isfinite(__ldg(ch + k * plane));
+    for (int k0 = 0; k0 < b.nch; k0 += kImgBatch) {  // loads of a batch in flight together
+      float c[kImgBatch];
+#pragma unroll
+      for (int u = 0; u < kImgBatch; ++u) c[u] = k0 + u < b.nch ? __ldg(ch + (long long)(k0 + u) * plane) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < kImgBatch; ++u) fin &= (bool)isfinite(c[u]);
+    }
     if (!fin) continue;  // D21
     unsigned long long key = 0ull;
     if (b.g.rule == MEM_CLASS_MAX) {
       int best = 0;
       float bv = __ldg(ch);
-      for (int k = 1; k < b.nch; ++k) {
-        const float c = __ldg(ch + k * plane);
-        if (c > bv) {
-          bv = c;
-          best = k;
+      for (int k0 = 1; k0 < b.nch; k0 += kImgBatch) {  // first maximum in channel order wins
+        float c[kImgBatch];
+#pragma unroll
+        for (int u = 0; u < kImgBatch; ++u) c[u] = k0 + u < b.nch ? __ldg(ch + (long long)(k0 + u) * plane) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < kImgBatch; ++u) {
+          if (k0 + u < b.nch && c[u] > bv) {
+            bv = c[u];
+            best = k0 + u;
+          }
         }
       }
       key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
+    }
+    if (b.g.rule == MEM_AVERAGE || b.g.rule == MEM_CLASS_AVERAGE || b.g.rule == MEM_COLOR ||
+        b.g.rule == MEM_CLASS_BAYESIAN) {
+      image_fuse_words(a.st, g.BHW, cell, b.g, ch, plane);
+      continue;
     }
     apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)__ldg(ch + k * plane); }, key);
   }
