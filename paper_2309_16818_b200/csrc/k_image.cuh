@@ -77,7 +77,7 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 // channel, since the compiler cannot move a load over a store to a possibly aliasing layer).
 // Same rule calls, same operands, same order: results are identical to apply_group's.
 #ifndef MEM_IMG_BATCH
-#define MEM_IMG_BATCH 8
+#define MEM_IMG_BATCH 16
 #endif
 constexpr int kImgBatch = MEM_IMG_BATCH;
 __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW, long long cell, const GroupDesc &g,

@@ -40,3 +40,22 @@ for kw in (dict(), dict(image=False), dict(clouds=False)):
     print(kw, f"{e0.elapsed_time(e1) / n * 1e3:.1f} us per frame")
 st = mp.stats() if hasattr(mp, "stats") else None
 print("stats", st)
+
+# C4: 64-channel feature image, average-fused (as bench.py side_c3_c4)
+c4 = S.C4
+m4 = M.Map(c4["res"], c4["rows"], c4["cols"], [dict(name="feat", rule=0, n_channels=c4["d"], w=c4["w"])])
+m4.move_to(*fr[0]["move"])
+for cl, dp in zip(fr[0]["clouds"], dev[0]["clouds"]):
+    m4.input_pointcloud(dp, [], cl["R"], cl["t"], c["noise"])
+ims = [S.c4_image(f) for f in range(2)]
+dims = [torch.from_numpy(im["img"]).cuda() for im in ims]
+for i in range(5):
+    m4.input_image(dims[i % 2], [(0, c4["d"], 0)], ims[i % 2]["K"], ims[i % 2]["R"], ims[i % 2]["t"])
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for i in range(n):
+    m4.input_image(dims[i % 2], [(0, c4["d"], 0)], ims[i % 2]["K"], ims[i % 2]["R"], ims[i % 2]["t"])
+e1.record()
+torch.cuda.synchronize()
+print(f"C4 {e0.elapsed_time(e1) / n * 1e3:.1f} us per image")
