@@ -71,7 +71,7 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)
-// One-word-per-channel rules (average, class_average, color, class_bayesian) with N_j = 1,
+// The per-channel rules (average, class_average, color, class_bayesian, gaussian) with N_j = 1,
 // kImgBatch channels at a time: the pixel and state loads of a batch are all issued before its
 // math and stores (apply_group's per-channel load -> store chain is one L2 round trip per
 // channel, since the compiler cannot move a load over a store to a possibly aliasing layer).
@@ -86,6 +86,29 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
   uint8_t *obs = st.flags + (long long)g.flag * BHW + cell;
   const bool observed = *obs != 0;
   const bool dir = g.rule == MEM_CLASS_BAYESIAN;
+  if (g.rule == MEM_GAUSSIAN) {  // two words per channel: mean at word0 + k, variance at word0 + nch + k
+    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch) {
+      float p[kImgBatch], mu[kImgBatch], var[kImgBatch];
+#pragma unroll
+      for (int u = 0; u < kImgBatch; ++u) {
+        if (k0 + u < g.nch) {
+          p[u] = __ldg(ch + (long long)(k0 + u) * plane);
+          mu[u] = vals[(long long)(g.word0 + k0 + u) * BHW + cell];
+          var[u] = vals[(long long)(g.word0 + g.nch + k0 + u) * BHW + cell];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kImgBatch; ++u) {
+        if (k0 + u < g.nch) {
+          rule_gaussian(mu[u], var[u], observed, (double)p[u], 1.0, g);
+          vals[(long long)(g.word0 + k0 + u) * BHW + cell] = mu[u];
+          vals[(long long)(g.word0 + g.nch + k0 + u) * BHW + cell] = var[u];
+        }
+      }
+    }
+    *obs = 1;
+    return;
+  }
   for (int k0 = 0; k0 < g.nch; k0 += kImgBatch) {
     float p[kImgBatch], th[kImgBatch];
 #pragma unroll
@@ -174,8 +197,7 @@ __global__ void __launch_bounds__(kThreads) k_image(const __grid_constant__ Imag
       }
       key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
     }
-    if (b.g.rule == MEM_AVERAGE || b.g.rule == MEM_CLASS_AVERAGE || b.g.rule == MEM_COLOR ||
-        b.g.rule == MEM_CLASS_BAYESIAN) {
+    if (b.g.rule != MEM_CLASS_MAX) {
       image_fuse_words(a.st, g.BHW, cell, b.g, ch, plane);
       continue;
     }

@@ -176,6 +176,35 @@ def test_image_fusion_chained():
     assert (g.get_layer("top_label") >= 0).sum() > 500
 
 
+
+@pytest.mark.gpu
+def test_image_fusion_wide_groups():
+    """Groups wider than k_image's 16-channel load batch (ragged last batch), every per-channel
+    rule, a NaN in the second batch (D21 skips the whole group), class_max ties across batches."""
+    rows, cols, res = 40, 50, 0.05
+    groups = [dict(name="gw", rule=M.MEM_GAUSSIAN, n_channels=19, sigma_f2=0.3, mu0=0.0, sigma0_2=1.0),
+              dict(name="ca", rule=M.MEM_CLASS_AVERAGE, n_channels=21, w=0.4),
+              dict(name="av", rule=M.MEM_AVERAGE, n_channels=17, w=0.5),
+              dict(name="db", rule=M.MEM_CLASS_BAYESIAN, n_channels=33, alpha0=1.0),
+              dict(name="mx", rule=M.MEM_CLASS_MAX, n_channels=33)]
+    binds = [(0, 19, 0), (19, 21, 1), (40, 17, 2), (57, 33, 3), (57, 33, 4)]
+    g, o = make_pair(res, rows, cols, groups)
+    rng = np.random.default_rng(77)
+    noise = dict(a=1e-3, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=9.0, v_out=0.01)
+    K = np.array([[120.0, 0.0, 79.5], [0, 120.0, 59.5], [0, 0, 1.0]])
+    for f in range(4):
+        step_points(g, o, S.random_cloud(300 + f, 15000, 3, rows, cols, res), [], np.eye(3), [0.0, 0.0, 1.0], noise)
+        eye = np.array([rng.uniform(-3, -2), rng.uniform(-1, 1), rng.uniform(1.0, 2.0)])
+        R = camera_looking_at(eye, [rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), 0.0])
+        img = rng.normal(0, 1, (90, 120, 160)).astype(np.float32)
+        img[57:90] = np.round(rng.uniform(0, 3, (33, 120, 160))).astype(np.float32)  # many ties
+        img[17, rng.integers(0, 120, 40), rng.integers(0, 160, 40)] = np.nan  # gaussian, 2nd batch
+        img[75, rng.integers(0, 120, 40), rng.integers(0, 160, 40)] = np.inf  # class groups
+        g.input_image(torch.from_numpy(img).cuda(), binds, K, R, eye)
+        o.input_image(img, binds, K, R, eye)
+        compare_layers(g, o, where=f"frame {f}: ")
+
+
 # ---------------------------------------------------------------- batched maps
 def test_batched_equals_single_and_oracle():
     rows, cols, res = 48, 40, 0.1
