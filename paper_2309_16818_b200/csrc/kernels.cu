@@ -220,7 +220,7 @@ cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, int grid, cudaSt
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
-  k_image<<<dim3(cdiv(a.geo.HW, kThreads), a.geo.n_maps), kThreads, 0, s>>>(a);
+  k_image<<<dim3(cdiv(a.geo.HW, kImgThreads), a.geo.n_maps), kImgThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
