@@ -360,9 +360,7 @@ om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const o
   const double cx = (double)m->kx * (double)m->res, cy = (double)m->ky * (double)m->res;
   const float tx = (float)(t[0] - cx), ty = (float)(t[1] - cy), tz = (float)t[2];
   const float hH = (float)H / 2.0f, hW = (float)W / 2.0f;
-  /* binning multiplies by 1/res rounded once to fp32 (reading D13) */
-  const float inv_res = (float)(1.0 / (double)m->res);
-  const float rmin2 = np->r_min * np->r_min, rmax2 = np->r_max * np->r_max;
+  const float res = m->res;
 
   /* per-cell, per-frame sufficient statistics */
   om_frame *f = (om_frame *)calloc(1, sizeof(om_frame));
@@ -395,10 +393,10 @@ om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const o
     if (!isfinite(px) || !isfinite(py) || !isfinite(pz)) {
       code = OM_NONFINITE; /* 2.1 */
     } else {
-      /* 2.2: range filter r_min <= |p| <= r_max, tested on the square (reading D9):
-         r_min^2 <= r2 <= r_max^2 with the squares rounded once to fp32 */
+      /* 2.2: range filter r_min <= r <= r_max on the sensor-frame range (reading D9) */
       const float r2 = (px * px + py * py) + pz * pz;
-      if (!(rmin2 <= r2 && r2 <= rmax2)) {
+      const float r = sqrtf(r2);
+      if (!(np->r_min <= r && r <= np->r_max)) {
         code = OM_RANGE;
       } else {
         /* 2.3: q = R p ("point trsf.") */
@@ -412,7 +410,7 @@ om_frame *om_accumulate(om_map *m, const float *pts, long n, int stride, const o
           const float x = qx + tx, y = qy + ty;
           z = qz + tz;
           /* 2.5: bin by horizontal coordinates, half-open cells */
-          const float fr = x * inv_res + hH, fc = y * inv_res + hW; /* reading D13 */
+          const float fr = x / res + hH, fc = y / res + hW; /* reading D13 */
           if (!(0.0f <= fr && fr < (float)H && 0.0f <= fc && fc < (float)W)) {
             code = OM_OOB;
           } else {
@@ -497,11 +495,10 @@ int om_fuse_rows(om_map *m, om_frame *f, int row_lo, int row_hi) {
     if (m->valid[j]) {
       const double sp = (double)m->s2[j] + (double)n_out[j] * (double)np->v_out;
       if (n_in[j] > 0) {
-        /* information form h' = (h/sp + S)/(1/sp + P), sigma2' = 1/(1/sp + P), written with
-           numerator and denominator multiplied by sp (reading D7): */
-        const double den = 1.0 + P[j] * sp;
-        m->h[j] = (float)(((double)m->h[j] + S[j] * sp) / den);
-        m->s2[j] = (float)(sp / den);
+        /* information form h' = (h/sp + S)/(1/sp + P), sigma2' = 1/(1/sp + P) (reading D7) */
+        const double den = 1.0 / sp + P[j];
+        m->h[j] = (float)(((double)m->h[j] / sp + S[j]) / den);
+        m->s2[j] = (float)(1.0 / den);
       } else {
         m->s2[j] = (float)sp;
       }
@@ -575,8 +572,7 @@ void om_set_occlusion(om_map *m, int enable, float eps_occ) {
 static int om_visible(const om_map *m, int row, int col, float tx, float ty, float tz, float hb) {
   const int H = m->rows, W = m->cols;
   const float hH = (float)H / 2.0f, hW = (float)W / 2.0f;
-  const float inv_res = (float)(1.0 / (double)m->res);
-  const int rc = (int)floorf(tx * inv_res + hH), cc = (int)floorf(ty * inv_res + hW);
+  const int rc = (int)floorf(tx / m->res + hH), cc = (int)floorf(ty / m->res + hW); /* binned like a point (D13) */
   const float xb = ((float)row + 0.5f - hH) * m->res, yb = ((float)col + 0.5f - hW) * m->res;
   const float dxb = xb - tx, dyb = yb - ty;
   const float db = sqrtf(dxb * dxb + dyb * dyb);

@@ -64,6 +64,92 @@ def test_cell_centre_round_trip(rows, cols, res):
     assert list(code) == [OOB, OOB, OOB]
 
 
+def _exact_fr(x, res_f, n):
+    """x / res + n/2 in exact rational arithmetic (x and res are the fp32 values as given)."""
+    from fractions import Fraction as F
+    return F(float(x)) / F(float(res_f)) + F(n, 2)
+
+
+@pytest.mark.parametrize("rows,cols,res", [(200, 200, 0.04), (64, 64, 0.1), (250, 250, 0.04), (37, 53, 0.1)])
+def test_binning_non_dyadic_vs_exact_footprint(rows, cols, res):
+    """SPEC.md:62 / PAPER.md:229: a point belongs to the cell whose square footprint
+    [(i - H/2) res, (i + 1 - H/2) res) contains it.  At the non-dyadic resolutions every
+    benchmark config uses (0.04, 0.1 m) the cell edges are not fp32 numbers, so the oracle's
+    fp32 binning is checked against exact rational footprint containment (Python
+    fractions): every point agrees, except points whose exact x/res + H/2 lies within the
+    fp32 rounding of the binning expression (<= 2 ulp at magnitude max(|x/res|, H)) of an
+    integer -- and the test makes sure such near-edge points are actually exercised, both
+    sides of every edge of one row and one column."""
+    import math as _m
+    res_f = np.float32(res)
+    m = OracleMap(float(res_f), rows, cols)
+    rng = np.random.default_rng(rows * 1000 + cols)
+    # random points over 1.2x the window, plus the fp32 neighbours of every cell edge
+    xs = list(rng.uniform(-0.6 * rows * res, 0.6 * rows * res, 3000))
+    ys = list(rng.uniform(-0.6 * cols * res, 0.6 * cols * res, 3000))
+    for k in range(rows + 1):
+        e = np.float32((k - rows / 2) * float(res_f))
+        for v in (np.nextafter(e, np.float32(-1e9)), e, np.nextafter(e, np.float32(1e9))):
+            xs.append(float(v))
+            ys.append(float(rng.uniform(-0.4 * cols * res, 0.4 * cols * res)))
+    for k in range(cols + 1):
+        e = np.float32((k - cols / 2) * float(res_f))
+        for v in (np.nextafter(e, np.float32(-1e9)), e, np.nextafter(e, np.float32(1e9))):
+            ys.append(float(v))
+            xs.append(float(rng.uniform(-0.4 * rows * res, 0.4 * rows * res)))
+    pts = np.stack([np.array(xs, np.float32), np.array(ys, np.float32), np.zeros(len(xs), np.float32)], 1)
+    # R = I and t = (0, 0, 1): the map-frame x, y are the sensor-frame coordinates exactly
+    cell, code = m.input_pointcloud(pts - np.float32([0, 0, 1]), [], EYE, [0, 0, 1], NOISE, debug=True)
+    n_near = n_disagree = 0
+    for (x, y), ci, co in zip(pts[:, :2], cell, code):
+        frs = [_exact_fr(x, res_f, rows), _exact_fr(y, res_f, cols)]
+        inside = all(0 <= f < n for f, n in zip(frs, (rows, cols)))
+        exp = _m.floor(frs[0]) * cols + _m.floor(frs[1]) if inside else -1
+        tols = [2.0 ** -22 * max(abs(float(x) / float(res_f)), rows), 2.0 ** -22 * max(abs(float(y) / float(res_f)), cols)]
+        near = any(abs(float(f) - round(float(f))) <= t for f, t in zip(frs, tols))
+        n_near += near
+        got = int(ci) if co == INLIER else -1
+        if got != exp:
+            n_disagree += 1
+            assert near, (x, y, got, exp)
+    assert n_near >= rows + cols  # the edge neighbours were exercised
+    # the reading is measured, not assumed: report how often fp32 binning differs from exact
+    print(f"binning {rows}x{cols}@{res}: {n_disagree} of {len(pts)} points differ from exact footprint "
+          f"containment, all within fp32 rounding of a cell edge ({n_near} near-edge points)")
+
+
+@pytest.mark.parametrize("r_min,r_max", [(0.1, 0.3), (0.3, 59.9), (1.7, 20.0), (0.0, 0.7)])
+def test_range_filter_non_representable_bounds_vs_exact(r_min, r_max):
+    """D9 / north_star: keep a point iff r_min <= |p| <= r_max, |p| the Euclidean norm of its
+    fp32 sensor-frame coordinates.  With bounds fp32 cannot represent (0.1, 0.3, 0.7, 59.9)
+    the oracle's fp32 test (r = sqrtf(r2)) must equal the exact test |p|^2 vs bound^2 in
+    rational arithmetic, except within the rounding of r2 and sqrt (relative 2^-21) of a
+    bound; points on and beside both spheres are exercised."""
+    from fractions import Fraction as F
+    rmn, rmx = np.float32(r_min), np.float32(r_max)
+    rng = np.random.default_rng(int(r_max * 100))
+    d = rng.normal(size=(4000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rad = np.concatenate([rng.uniform(0, 1.2 * r_max, 2000),
+                          float(rmx) * (1 + rng.uniform(-3e-7, 3e-7, 1000)),
+                          float(rmn) * (1 + rng.uniform(-3e-7, 3e-7, 1000))])
+    pts = (d * rad[:, None]).astype(np.float32)
+    m = OracleMap(1.0, 2, 2)
+    nz = dict(NOISE, r_min=float(rmn), r_max=float(rmx))
+    _, code = m.input_pointcloud(pts, [], EYE, [0, 0, 0], nz, debug=True)
+    n_near = n_disagree = 0
+    for p, co in zip(pts, code):
+        n2 = sum(F(float(c)) ** 2 for c in p)
+        keep = F(float(rmn)) ** 2 <= n2 <= F(float(rmx)) ** 2
+        near = any(abs(float(n2) - float(b) ** 2) <= 2.0 ** -20 * float(b) ** 2 for b in (rmn, rmx) if b > 0)
+        n_near += near
+        if (co != RANGE) != keep:
+            n_disagree += 1
+            assert near, (p, co, keep)
+    assert n_near >= 500
+    print(f"range [{r_min}, {r_max}]: {n_disagree} of {len(pts)} points differ from the exact test (all near a bound)")
+
+
 def test_transform_spec_examples(golden):
     """SPEC.md:156-158 through the binning: the transformed point lands in the cell of q."""
     res, n = 0.25, 16
