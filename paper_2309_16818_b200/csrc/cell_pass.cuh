@@ -1,4 +1,4 @@
-// cell_pass.cuh -- a9-a10 device functions: batched per-cell fusion (generic and fast), bucket records.
+// cell_pass.cuh -- a9-a10 device functions: batched per-cell fusion (generic and fast).
 // Part of the single translation unit kernels.cu (included inside namespace memk, in order).
 #pragma once
 
@@ -22,7 +22,7 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
     sc[u] = sb + phys[u];
     hit |= phys[u] >= 0 ? (1u << u) : 0u;
   }
-  // ---- a9: Kalman height fusion (D7: h' = (h + S sp)/(1 + P sp), s2' = sp/(1 + P sp))
+  // ---- a9: Kalman height fusion (D7, kalman_height)
   {
     double P[N], S[N];
     float h[N], s2[N];
@@ -42,19 +42,15 @@ __device__ __forceinline__ void fuse_cells(const PassArgs &a, int m, int sb, con
       if (!(hit >> u & 1u)) continue;
       const double n_in = (double)(uint32_t)(cnt[u] & 0xffffffffull);
       const double n_out = (double)(uint32_t)(cnt[u] >> 32);
-      if (vd[u]) {
-        const double sp = (double)s2[u] + n_out * (double)a.np.v_out;  // outliers inflate first (D11)
-        if (n_in > 0.0) {
-          const double den = 1.0 + P[u] * sp;
-          elev[c[u]] = __double2float_rn(((double)h[u] + S[u] * sp) / den);
-          var[c[u]] = __double2float_rn(sp / den);
-        } else {
-          var[c[u]] = __double2float_rn(sp);
+      {
+        float hh = h[u], ss = s2[u];
+        uint8_t vv = vd[u];
+        kalman_height(hh, ss, vv, n_in, n_out, P[u], S[u], a.np.v_out);
+        if (vv) {
+          elev[c[u]] = hh;
+          var[c[u]] = ss;
+          if (!vd[u]) validp[c[u]] = 1;
         }
-      } else if (n_in > 0.0) {  // first touch: h = S/P, s2 = 1/P
-        elev[c[u]] = __double2float_rn(S[u] / P[u]);
-        var[c[u]] = __double2float_rn(1.0 / P[u]);
-        validp[c[u]] = 1;
       }
       unsigned long long *r = a.rec + (long long)sc[u] * a.R;  // re-zero for the slot's next map
       __stcg(a.cnt + sc[u], 0ull);
@@ -192,25 +188,19 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
     // b | n << 32, record [P, S, r | g << 32, n_out] (n_in > 0 iff P > 0)
     const double n_in = kColor ? (P[u] > 0.0 ? 1.0 : 0.0) : (double)(uint32_t)(cnt[u] & 0xffffffffull);
     const double n_out = kColor ? (double)w1[u] : (double)(uint32_t)(cnt[u] >> 32);
-    if (vd[u]) {
-      const double sp = (double)s2[u] + n_out * (double)a.np.v_out;
-      if (n_in > 0.0) {  // one fp64 division, two multiplies (reading D29b)
-        const double rden = 1.0 / (1.0 + P[u] * sp);
-        elev[c] = __double2float_rn(((double)h[u] + S[u] * sp) * rden);
-        var[c] = __double2float_rn(sp * rden);
-      } else {
-        var[c] = __double2float_rn(sp);
+    {
+      float hh = h[u], ss = s2[u];
+      uint8_t vv = vd[u];
+      kalman_height(hh, ss, vv, n_in, n_out, P[u], S[u], a.np.v_out);
+      if (vv) {
+        elev[c] = hh;
+        var[c] = ss;
+        if (!vd[u]) validp[c] = 1;
       }
-    } else if (n_in > 0.0) {
-      const double rP = 1.0 / P[u];
-      elev[c] = __double2float_rn(S[u] * rP);
-      var[c] = __double2float_rn(rP);
-      validp[c] = 1;
     }
     // a10: Eq.(1)+(2) per channel
     const unsigned long long nn = kColor ? (cnt[u] >> 32) : w0[u];
     if (nn != 0ull) {
-      const double rn = 1.0 / (double)nn;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         double sk;
@@ -221,7 +211,7 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
         } else {
           sk = sum[u][k];
         }
-        vals[(long long)(gd.word0 + k) * BHW + c] = rule_average_r(th[u][k], ob[u] != 0, sk, rn, gd.w);
+        vals[(long long)(gd.word0 + k) * BHW + c] = rule_average(th[u][k], ob[u] != 0, sk, (double)nn, gd.w);
       }
       obsp[c] = 1;
     }
@@ -229,49 +219,6 @@ __device__ __forceinline__ void fuse_cells_avg(const PassArgs &a, int m, int sb,
     __stcg(a.cnt + sb + phys[u], 0ull);
     __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
     __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
-  }
-}
-
-// a8, bucketed fast path: one 16-B record per in-window point, appended to the bucket of its
-// (map-slot, band): {local cell | outlier << 31, 1/v (fp32, 0 for outliers), z * (1/v) (fp32),
-// the channel word}.  These are exactly the fp32 terms the oracle sums in fp64,
-// so k_accum's sums equal the RED path's.  Lanes of the same bucket reserve their slots with one
-// atomicAdd (match_any).  A bucket that is full sends the point to the scratch with REDs instead
-// (accumulate_warp); k_accum merges the scratch of such a band.  All 32 lanes must call this.
-template <int kFast>
-__device__ __forceinline__ void bucket_warp(const PassArgs &a, const PointOut &o, int phys, int slot, int sc,
-                                            const float *p, float ch0) {
-  const bool act = o.cell >= 0;
-  if (!__any_sync(0xffffffffu, act)) return;
-  const int lane = threadIdx.x & 31;
-  int band = 0, local = 0;
-  if (act) band = divmod_fast(phys, a.band_cells, a.inv_band, local);
-  const int key = act ? slot * a.nbands + band : -1;
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  const int leader = __ffs(peers) - 1;
-  unsigned base = 0u;
-  if (act && lane == leader) base = atomicAdd(&a.bcnt[key], (unsigned)__popc(peers));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  const unsigned pos = base + (unsigned)__popc(peers & lanemask_lt());
-  const bool spill = act && pos >= a.bcap;
-  if (act && !spill) {
-    const bool inl = o.code == MEM_CODE_INLIER;
-    float wf = 0.0f, zw = 0.0f;
-    if (inl) {
-      wf = 1.0f / o.v;
-      zw = o.z * wf;
-    }
-    uint4 r;
-    r.x = (unsigned)local | (inl ? 0u : 0x80000000u);
-    r.y = __float_as_uint(wf);
-    r.z = __float_as_uint(zw);
-    r.w = __float_as_uint(ch0);
-    __stcg(a.recs + (long long)key * a.bcap + pos, r);
-  }
-  if (__any_sync(0xffffffffu, spill)) {
-    PointOut q = o;
-    if (!spill) q.cell = -1;
-    accumulate_warp<kFast>(a, q, sc, p, ch0);
   }
 }
 

@@ -76,7 +76,6 @@ struct Geometry {
   int n_maps;
   long long BHW;  // n_maps * HW: stride between layers (< 2^31, so cell indices fit in int)
   float res, hH, hW;
-  float inv_res;  // (float)(1.0 / res): binning multiplies (reading D13)
   double inv_W;   // 1.0 / W for divmod_w (index arithmetic only)
 };
 
@@ -111,19 +110,33 @@ __device__ __forceinline__ float f32_of_ord(uint32_t o) {
   return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
+// ---------------------------------------------------------------- a9: Kalman height (fp64)
+// Information form of SURVEY §8(c) a9 / reading D7, in the oracle's exact expressions: prior
+// variance inflated by the outliers first (D11), sp = s2 + n_out v_out; valid cell with
+// inliers: den = 1/sp + P, h' = (h/sp + S)/den, s2' = 1/den; first touch h = S/P, s2 = 1/P.
+// Returns true when the cell becomes valid.
+__device__ __forceinline__ void kalman_height(float &h, float &s2, uint8_t &valid, double n_in, double n_out,
+                                              double P, double S, float v_out) {
+  if (valid) {
+    const double sp = (double)s2 + n_out * (double)v_out;
+    if (n_in > 0.0) {
+      const double den = 1.0 / sp + P;
+      h = __double2float_rn(((double)h / sp + S) / den);
+      s2 = __double2float_rn(1.0 / den);
+    } else {
+      s2 = __double2float_rn(sp);
+    }
+  } else if (n_in > 0.0) {
+    h = __double2float_rn(S / P);
+    s2 = __double2float_rn(1.0 / P);
+    valid = 1;
+  }
+}
+
 // ---------------------------------------------------------------- per-cell rules (fp64)
 // Eq.(1)+(2): a = sum/n; theta' = w a + (1-w) theta; first touch theta' = a (D3)
 __device__ __forceinline__ float rule_average(float theta, bool observed, double sum, double n, float w) {
   const double a = sum / n;
-  const double wd = (double)w;
-  const double out = observed ? wd * a + (1.0 - wd) * (double)theta : a;
-  return __double2float_rn(out);
-}
-
-// the same with the reciprocal rn = 1/n precomputed: a = sum * rn is within one fp64 ulp of
-// sum / n, invisible after the rounding to fp32 but at double-rounding ties (reading D29b)
-__device__ __forceinline__ float rule_average_r(float theta, bool observed, double sum, double rn, float w) {
-  const double a = sum * rn;
   const double wd = (double)w;
   const double out = observed ? wd * a + (1.0 - wd) * (double)theta : a;
   return __double2float_rn(out);

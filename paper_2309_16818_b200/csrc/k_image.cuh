@@ -14,7 +14,7 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
   const Geometry &g = a.geo;
   const float *elev = reinterpret_cast<const float *>(a.st.words) + (long long)kWordElev * g.BHW;
   const uint8_t *validp = a.st.flags + (long long)kFlagValid * g.BHW;
-  const int rc = (int)floorf(tx * g.inv_res + g.hH), cc = (int)floorf(ty * g.inv_res + g.hW);
+  const int rc = (int)floorf(__fdiv_rn(tx, g.res) + g.hH), cc = (int)floorf(__fdiv_rn(ty, g.res) + g.hW);
   const float xb = ((float)row + 0.5f - g.hH) * g.res, yb = ((float)col + 0.5f - g.hW) * g.res;
   const float dxb = xb - tx, dyb = yb - ty;
   const float db = sqrtf(dxb * dxb + dyb * dyb);

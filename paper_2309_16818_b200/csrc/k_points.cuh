@@ -55,10 +55,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool kDebug, int kFast, bool kBucket, bool kFull = false>
+template <bool kDebug, int kFast, bool kFull = false>
 __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, const float (&px)[kWarpPtsPerLane],
                                              const float (&py)[kWarpPtsPerLane], const float (&pz)[kWarpPtsPerLane],
-                                             const float (&pw)[kWarpPtsPerLane], float rmin2, float rmax2,
+                                             const float (&pw)[kWarpPtsPerLane],
                                              unsigned long long &packed, unsigned &npk, unsigned (&cnt)[8]) {
   const Geometry &g = a.geo;
   const int lane = threadIdx.x & 31;
@@ -72,7 +72,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   for (int u = 0; u < kWarpPtsPerLane; ++u) {
     const bool in = u * 32 + lane < nv;
     if (in && !ABLATE(a, 8u)) {
-      o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, rmin2, rmax2, map_base);
+      o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, map_base);
     } else {
       o[u].code = in ? MEM_CODE_NONFINITE : -1;
       o[u].cell = -1;
@@ -92,11 +92,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
     }
     if (ABLATE(a, 2u)) continue;
     const float *pp = kFast != 0 ? nullptr : a.pts + (k < nv ? t.base + k : t.beg) * (long long)a.stride;
-    if constexpr (kBucket)
-      bucket_warp<kFast>(a, o[u], o[u].cell - map_base, a.slot0 + t.m - a.m0, sb + (o[u].cell - map_base), pp,
-                         pw[u]);
-    else
-      accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), pp, pw[u]);
+    accumulate_warp<kFast>(a, o[u], sb + (o[u].cell - map_base), pp, pw[u]);
   }
   npk += kWarpPtsPerLane;  // the 10-bit code fields are flushed before they can wrap
   if (npk > 1023u - kWarpPtsPerLane) {
@@ -107,7 +103,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   }
 }
 
-template <bool kDebug, int kFast, bool kBucket>
+template <bool kDebug, int kFast>
 __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
@@ -124,7 +120,6 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
   const int i0 = ps_of(a, a.m0);
   const int i1 = ps_of(a, a.m1);
   const unsigned long long pol = evict_first_policy();
-  const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
   unsigned long long packed = 0ull;
   unsigned npk = 0;
   float px[kWarpPtsPerLane], py[kWarpPtsPerLane], pz[kWarpPtsPerLane], pw[kWarpPtsPerLane];
@@ -186,10 +181,10 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
       }
 #if MEM_FULL_ITEMS
       if (cur.end - cur.base >= kWarpPoints)  // every lane holds 4 points: no bounds checks
-        process_item<kDebug, kFast, kBucket, true>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+        process_item<kDebug, kFast, true>(a, cur, px, py, pz, pw, packed, npk, cnt);
       else
 #endif
-        process_item<kDebug, kFast, kBucket>(a, cur, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+        process_item<kDebug, kFast>(a, cur, px, py, pz, pw, packed, npk, cnt);
       cur = nxt;
     }
   } else {
@@ -204,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
           px[u] = __ldg(q); py[u] = __ldg(q + 1); pz[u] = __ldg(q + 2);
         }
       }
-      process_item<kDebug, kFast, kBucket>(a, t, px, py, pz, pw, rmin2, rmax2, packed, npk, cnt);
+      process_item<kDebug, kFast>(a, t, px, py, pz, pw, packed, npk, cnt);
     }
   }
 #pragma unroll

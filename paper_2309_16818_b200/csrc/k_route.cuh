@@ -22,7 +22,6 @@ __global__ void __launch_bounds__(kThreads) k_route(const __grid_constant__ Pass
   const int lane = threadIdx.x & 31;
   const long long n = off_of(a, 1);
   const PointFrame f = frame_of(a, 0);
-  const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
   const long long nthreads = (long long)gridDim.x * kThreads;
   for (long long i0 = (long long)blockIdx.x * kThreads; i0 < n; i0 += nthreads) {  // warp-uniform trip count
     const long long i = i0 + threadIdx.x;
@@ -31,7 +30,7 @@ __global__ void __launch_bounds__(kThreads) k_route(const __grid_constant__ Pass
     PointOut o;
     o.cell = -1;
     o.code = -1;
-    if (in) o = bin_point(__ldg(q), __ldg(q + 1), __ldg(q + 2), f, g, a.np, rmin2, rmax2, 0);
+    if (in) o = bin_point(__ldg(q), __ldg(q + 1), __ldg(q + 2), f, g, a.np, 0);
     if (in && o.cell < 0) count_code(packed, npk, o.code, cnt);
     const int dest = o.cell >= 0 ? o.cell / r.band_n : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, dest);

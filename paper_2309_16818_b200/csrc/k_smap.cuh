@@ -22,7 +22,6 @@
 constexpr int kSmapThreads = MEM_SMAP_THREADS;
 constexpr int kSmapCells = 16384;
 constexpr int kSmapPoints = 65535;
-constexpr int kSmapSortMax = 256;  // cells with more points keep the scatter order (still exact sums, any order)
 
 // shared memory: the per-cell counts / offsets as packed u16 pairs (a map has < 65536 points)
 // and the u16 point indices
@@ -72,7 +71,6 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
   unsigned long long packed = 0ull;
   unsigned npk = 0;
   const unsigned long long pol = evict_first_policy();
-  const float rmin2 = a.np.r_min * a.np.r_min, rmax2 = a.np.r_max * a.np.r_max;  // D9
   const long long BHW = g.BHW;
   const GroupDesc &gd = a.b[0].g;
   float *vals = reinterpret_cast<float *>(a.st.words);
@@ -100,7 +98,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
-        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
+        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, map_base);
         if (cached) pcell[i] = o.cell >= 0 ? (uint16_t)(o.cell - map_base) : (uint16_t)0xffffu;
         if (o.cell >= 0) {
           const int c = o.cell - map_base;
@@ -162,7 +160,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
-        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, rmin2, rmax2, map_base);
+        const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, map_base);
         if (o.cell >= 0) {
           const int c = o.cell - map_base;
           idx[(atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1))) >> (16 * (c & 1))) & 0xffffu] = (uint16_t)i;
@@ -197,7 +195,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
             col += col < 0 ? g.W : 0;
             strip = in_strip(row, col, f, g);
           }
-          if (s1 - s0 > 1u && s1 - s0 <= (unsigned)kSmapSortMax) {  // input order (insertion sort)
+          if (s1 - s0 > 1u) {  // input order (insertion sort; every cell)
             for (unsigned r = s0 + 1; r < s1; ++r) {
               const uint16_t key = idx[r];
               unsigned q = r;
@@ -245,7 +243,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
             o.lcell = -1;
             int owner = lane;  // the lane holding the point's cell
             if (kDebug) {
-              if (act) o = bin_point(q.x, q.y, q.z, f, g, a.np, rmin2, rmax2, map_base);
+              if (act) o = bin_point(q.x, q.y, q.z, f, g, a.np, map_base);
               if (act) owner = o.cell - map_base - gbase;
             } else {
               // the point is known to be in the window: only z and v are recomputed (bin_point's
@@ -317,20 +315,7 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
         if (s1 > s0 && !ABLATE(a, 512u)) {
           ++cnt[7];
           // a9 (D7, D11) in the oracle's exact form
-          if (vd) {
-            const double sp = (double)s2 + (double)nout * (double)a.np.v_out;
-            if (nin > 0u) {
-              const double den = 1.0 + P * sp;
-              h = __double2float_rn(((double)h + S * sp) / den);
-              s2 = __double2float_rn(sp / den);
-            } else {
-              s2 = __double2float_rn(sp);
-            }
-          } else if (nin > 0u) {
-            h = __double2float_rn(S / P);
-            s2 = __double2float_rn(1.0 / P);
-            vd = 1;
-          }
+          kalman_height(h, s2, vd, (double)nin, (double)nout, P, S, a.np.v_out);
           // a10: Eq.(1)+(2)
           const unsigned nn = kFast == 1 ? nin + nout : ng;
           if (nn != 0u) {

@@ -7,13 +7,9 @@
 //                   per-cell scratch
 //   cell_pass / k_cells  a9-a10 + lazy a13: warp-persistent over 128-cell chunks: strip reset,
 //                   Kalman height fusion, per-group rules (fp64), scratch re-zeroed
-//   k_cells_tma     the same for the fast paths (one average / colour group): persistent CTAs
-//                   stream whole cell tiles through a bulk-copy (TMA) + mbarrier shared-memory
-//                   ring, fuse in shared memory and write the tiles back with bulk stores
 //   k_smap          batches of small maps: one CTA per map sorts its points by cell in shared
 //                   memory and fuses every cell in input order (deterministic, oracle order)
 //   k_route         sharded big map: route in-window points to their band owner
-//   k_accum         opt-in bucketed fast path (records instead of REDs)
 //   k_image         a11-a12 (+ NEXT-1 occlusion walk): project, frustum, gather, fuse (N_j = 1)
 //   k_post          NEXT-3 plugins: normals, traversability, semantic argmax
 //   k_readout       k_shift (eager a13), k_read / k_write (a14), PCA readout (C4)
@@ -57,10 +53,8 @@ namespace memk {
 #include "cell_pass.cuh"
 #include "k_points.cuh"
 #include "k_cells.cuh"
-#include "k_cells_tma.cuh"
 #include "k_smap.cuh"
 #include "k_route.cuh"
-#include "k_accum.cuh"
 #include "k_post.cuh"
 #include "k_image.cuh"
 #include "k_readout.cuh"
@@ -72,9 +66,9 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 int points_blocks_per_sm(bool debug) {
   int n = 0;
   if (debug)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0>, kThreads, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0>, kThreads, 0);
   return n > 0 ? n : 1;
 }
 
@@ -84,7 +78,7 @@ int cells_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
-// Programmatic dependent launch: k_points, k_cells and k_accum may be scheduled while the
+// Programmatic dependent launch: k_points and k_cells may be scheduled while the
 // kernel before them on the stream drains (its CTAs retire); each waits on griddepcontrol.wait
 // before it reads anything the previous kernel wrote, and lets its own dependent launch early.
 template <class K>
@@ -109,80 +103,22 @@ cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
   const int f = a.vec4 ? a.fast : 0;
   const size_t fs = 0;  // no dynamic shared memory
   if (a.dbg_cell) {
-    if (f == 1 && a.bucketed) return launch_pdl(k_points<true, 1, true>, grid, fs, s, a);
-    else if (f == 2 && a.bucketed) return launch_pdl(k_points<true, 2, true>, grid, fs, s, a);
-    else if (f == 1) return launch_pdl(k_points<true, 1, false>, grid, fs, s, a);
-    else if (f == 2) return launch_pdl(k_points<true, 2, false>, grid, fs, s, a);
-    else return launch_pdl(k_points<true, 0, false>, grid, fs, s, a);
+    if (f == 1) return launch_pdl(k_points<true, 1>, grid, fs, s, a);
+    else if (f == 2) return launch_pdl(k_points<true, 2>, grid, fs, s, a);
+    else return launch_pdl(k_points<true, 0>, grid, fs, s, a);
   } else {
-    if (f == 1 && a.bucketed) return launch_pdl(k_points<false, 1, true>, grid, fs, s, a);
-    else if (f == 2 && a.bucketed) return launch_pdl(k_points<false, 2, true>, grid, fs, s, a);
-    else if (f == 1) return launch_pdl(k_points<false, 1, false>, grid, fs, s, a);
-    else if (f == 2) return launch_pdl(k_points<false, 2, false>, grid, fs, s, a);
-    else return launch_pdl(k_points<false, 0, false>, grid, fs, s, a);
+    if (f == 1) return launch_pdl(k_points<false, 1>, grid, fs, s, a);
+    else if (f == 2) return launch_pdl(k_points<false, 2>, grid, fs, s, a);
+    else return launch_pdl(k_points<false, 0>, grid, fs, s, a);
   }
   return cudaGetLastError();
 }
 
-// k_cells_tma (bulk-copy tiles) for the fast paths when every copy is 16-B aligned, opt-in
-// with env MEM_CELLS_TMA=1: on C2x64 it measures 41.5 us against k_cells' 40.2 us (DESIGN.md
-// §4.3), so k_cells stays the default
-static bool cells_tma_ok(const PassArgs &a) {
-  static int env = -2;
-  if (env == -2) {
-    const char *e = getenv("MEM_CELLS_TMA");
-    env = e ? atoi(e) : 0;
-  }
-  if (!env || (a.fast != 1 && a.fast != 2)) return false;
-  auto al = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
-  return a.geo.HW % 16 == 0 && a.cell_lo % 16 == 0 && a.cell_hi % 16 == 0 && a.cell_hi > a.cell_lo &&
-         al(a.st.words) && al(a.st.flags) && al(a.cnt) && al(a.rec);
-}
-
-static cudaError_t launch_cells_tma(const PassArgs &a, cudaStream_t s) {
-  static int grid_per_dev[64];  // resident CTAs (occupancy x SMs) per device, 0 = unknown
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const size_t smem = cells_tma_smem_bytes(a.fast);
-  auto k = a.fast == 1 ? k_cells_tma<1> : k_cells_tma<2>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int &gd = grid_per_dev[dev & 63];
-  if (gd == 0) {
-    int sms = 0, per = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kTmaThreads, smem);
-    gd = std::max(1, per) * std::max(1, sms);
-  }
-  const long long tiles = (long long)(a.m1 - a.m0) * ((a.cell_hi - a.cell_lo + kTT - 1) / kTT);
-  const int grid = (int)std::max(1LL, std::min<long long>(gd, tiles));
-  return launch_pdl(k, grid, smem, s, a, kTmaThreads);
-}
-
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
-  if (cells_tma_ok(a)) return launch_cells_tma(a, s);
   if (a.fast == 1)
     return launch_pdl(k_cells<1>, grid, 0, s, a);
   if (a.fast == 2) return launch_pdl(k_cells<2>, grid, 0, s, a);
   return launch_pdl(k_cells<0>, grid, 0, s, a);
-}
-
-int accum_blocks_per_sm(int band_cells) {
-  const size_t smem = accum_smem_bytes(band_cells);
-  cudaFuncSetAttribute(k_accum<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_accum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_accum<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaFuncSetAttribute(k_accum<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_accum<1>, kThreads, smem);
-  return n > 0 ? n : 1;
-}
-
-cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s) {
-  const size_t smem = accum_smem_bytes(a.band_cells);
-  if (a.fast == 1)
-    return launch_pdl(k_accum<1>, grid, smem, s, a);
-  return launch_pdl(k_accum<2>, grid, smem, s, a);
 }
 
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {

@@ -63,24 +63,13 @@ struct PassArgs {
   ResetInfo reset;
   int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;
-  // bucketed fast path: k_points appends one 16-B record per in-window point
-  // to the bucket of its (map-slot, band); k_accum accumulates a band in shared memory and fuses
-  int bucketed;                // 1: records + k_accum (fast paths only), 0: REDs + k_cells
-  int band_cells;              // cells per band (the last band of a map may be shorter)
-  double inv_band;             // 1.0 / band_cells (divmod_fast)
-  int nbands;                  // bands per map
-  unsigned bcap;               // record capacity per bucket; a bucket that overflows spills the
-                               // rest of its points to the scratch with REDs (merged by k_accum)
-  unsigned *bcnt;              // [map-slots][nbands] records appended (k_accum resets them to 0)
-  uint4 *recs;                 // [map-slots][nbands][bcap]
   PointFrame fi[kInlineMaps];
   long long offi[kInlineMaps + 1];
   int psi[kInlineMaps + 1];
   unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE, honoured by builds with -DMEM_ABLATION=1;
                                // results are wrong when != 0):
                                // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math,
-                               // 32 forward (not newest-first) cell tile order, 64 no warp aggregation,
-                               // 4096 k_accum: no fp64 shared atomics, 8192 k_accum: no channel atomics
+                               // 32 forward (not newest-first) cell tile order, 64 no warp aggregation
 };
 
 struct ImageArgs {
@@ -145,13 +134,9 @@ cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, int grid, cudaSt
 
 cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
-cudaError_t launch_accum(const PassArgs &a, int grid, cudaStream_t s);
 size_t smap_smem_bytes(int HW, long long max_pts);
 bool smap_eligible(int HW, long long max_pts);
 cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s);
-size_t accum_smem_bytes(int band_cells);
-int accum_sort_cap();
-int accum_blocks_per_sm(int band_cells);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 // PCA readout: moments of one map's feature group, then projections

@@ -107,16 +107,7 @@ struct mem_map {
   cudaStream_t side = nullptr;  // k_cells of wave w overlaps k_points of wave w+1
   std::vector<cudaEvent_t> ev_pts, ev_cells;
   int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
-  // bucketed fast path (records + k_accum)
-  int band_cells = 0, nbands = 0, accum_grid = 0;
-  unsigned *bk_cnt = nullptr;       // [slots][nbands]
-  size_t bk_cnt_n = 0;
-  uint4 *bk_recs = nullptr;         // [slots][nbands][bcap]
-  size_t bk_recs_n = 0;
-  unsigned bk_cap_override = 0;     // TESTING: env MEM_BUCKET_CAP (forces spills)
-  int bk_force = 0;                 // env MEM_BUCKETS=1 / 0 forces the bucketed / RED path
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
-  unsigned ablate = 0;      // DIAGNOSTICS ONLY: env MEM_ABLATE at create (see PassArgs::ablate)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
   int transport = 0, rank = 0, nranks = 1;
   int band_lo = 0, band_n = 0;          // owned physical cells [band_lo, band_lo + band_n)
@@ -135,8 +126,6 @@ struct mem_map {
   size_t rin_cap = 0;                   // bytes
   long long route_cap = 0;              // points per outgoing bucket of the last frame
   int route_stride = 0;
-  int l2_persist_mb = 0;    // DIAGNOSTICS: env MEM_L2_PERSIST_MB at create
-  bool single_stream = false;  // DIAGNOSTICS: env MEM_SINGLE_STREAM=1: waves run P0 C0 P1 C1 ... in order
   std::vector<ShiftRec> pend;
   int *dbg_cell = nullptr;
   uint8_t *dbg_code = nullptr;
@@ -164,7 +153,6 @@ struct mem_map {
     gg.res = res;
     gg.hH = (float)H / 2.0f;
     gg.hW = (float)W / 2.0f;
-    gg.inv_res = (float)(1.0 / (double)res);  // reading D13
     gg.inv_W = 1.0 / (double)W;
     return gg;
   }
@@ -430,8 +418,6 @@ void free_map(mem_map *m) {
   cudaFree(m->st.words);
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
-  cudaFree(m->bk_cnt);
-  cudaFree(m->bk_recs);
   cudaFree(m->ring);
   cudaFree(m->dparam);
   cudaFree(m->din);
@@ -522,9 +508,6 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
     m->points_grid = points_blocks_per_sm((flags & MEM_FLAG_DEBUG_POINTS) != 0) * (sms > 0 ? sms : 1);
     m->cells_grid = cells_blocks_per_sm() * (sms > 0 ? sms : 1);
-    m->band_cells = 1024;  // k_accum's band (kBand)
-    m->nbands = (rows * cols + m->band_cells - 1) / m->band_cells;
-    m->accum_grid = accum_blocks_per_sm(m->band_cells) * (sms > 0 ? sms : 1);
     cudaGetLastError();
   }
   m->pend.assign(n_maps, ShiftRec{0, 0, 0, 0});
@@ -535,14 +518,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
     delete m;
     return fail(MEM_ECUDA, "cudaStreamCreate failed");
   }
-  if (const char *ab = getenv("MEM_ABLATE")) m->ablate = (unsigned)strtoul(ab, nullptr, 0);
-  if (const char *lp = getenv("MEM_L2_PERSIST_MB")) m->l2_persist_mb = atoi(lp);
-  if (const char *ss = getenv("MEM_SINGLE_STREAM")) m->single_stream = atoi(ss) != 0;
-  if (const char *pd = getenv("MEM_PDL")) m->pdl = atoi(pd) != 0;
   m->smap = (flags & MEM_FLAG_DETERMINISTIC) != 0 ? 1 : 0;
-  if (const char *sm = getenv("MEM_SMAP")) m->smap = atoi(sm) != 0 ? 1 : -1;  // force on / off
-  if (const char *bc = getenv("MEM_BUCKET_CAP")) m->bk_cap_override = (unsigned)strtoul(bc, nullptr, 0);
-  if (const char *bo = getenv("MEM_BUCKETS")) m->bk_force = atoi(bo) != 0 ? 1 : -1;
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -937,7 +913,6 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.epoch = m->epoch;
   a.pdl = m->pdl;
   a.reset = m->reset_info();
-  a.ablate = m->ablate;
   const int HW = m->H * m->W;
   a.cell_lo = 0;
   a.cell_hi = HW;
@@ -968,29 +943,20 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     if (pi > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
     pstart[i + 1] = (int)pi;
   }
-  // bucketed fast path: one colour or 1-channel average group, float4 points, unsharded map
+  // fast paths: one colour or 1-channel average group bound, float4 points
   int fast = 0;
-  if (nb == 1 && m->ng == 1 && !(m->ablate & 1024u) && m->n_acc == 4) {
+  if (nb == 1 && m->ng == 1 && m->n_acc == 4 && a.vec4) {  // fast layouts need the channel in the float4's w
     if (a.b[0].g.rule == MEM_COLOR) fast = 1;
     else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) fast = 2;
-  }
-  // opt-in (env MEM_BUCKETS=1): measured slower than the REDs + k_cells on C2x64 and C5a
-  // (DESIGN.md §4.3), kept as a tested alternative
-  const bool bucketed = fast != 0 && a.vec4 && m->transport == 0 && m->bk_force > 0;
-  unsigned bcap = 0;
-  if (bucketed) {  // generous: all of a map's points spread evenly over its bands, + slack
-    bcap = m->bk_cap_override ? m->bk_cap_override
-                              : (unsigned)std::min<long long>((max_n + m->nbands - 1) / m->nbands + 256, 1LL << 30);
-    bcap = std::min((bcap + 31u) & ~31u, (unsigned)accum_sort_cap());
   }
   // small maps (<= 16384 cells, <= 65535 points each): one CTA per map sorts the points by
   // cell in shared memory (k_smap) -- no scratch, deterministic, the oracle's summation order
   // (MEM_FLAG_DETERMINISTIC, or by default for batches large enough to give every SM a map:
   // C5a measured 597 us vs 734 us with REDs for 512 maps)
-  const bool smap = fast != 0 && a.vec4 && m->transport == 0 && !bucketed && smap_eligible(HW, max_n) &&
+  const bool smap = fast != 0 && m->transport == 0 && smap_eligible(HW, max_n) &&
                     (m->smap > 0 || (m->smap == 0 && B >= 64));
   const size_t scratch_per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
-  const size_t per_map = scratch_per_map + (bucketed ? (size_t)m->nbands * bcap * sizeof(uint4) : 0);
+  const size_t per_map = scratch_per_map;
   long long wm = smap ? B : (long long)(kScratchBudget / 2 / per_map);
   if (wm < 1) wm = 1;
   if (wm > B) wm = B;
@@ -1026,57 +992,6 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.rec = m->st.acc + ((a.SHW + 3) & ~3LL);  // 32-B aligned records (the fast paths load 2 x 16 B)
   a.R = m->n_acc;
   a.fast = fast;  // every group bound (no stale group state); 4-word (32 B) records
-  a.bucketed = bucketed ? 1 : 0;
-  if (bucketed) {
-    const size_t ncnt = (size_t)m->scratch_maps * m->nbands, nrec = ncnt * bcap;
-    if (ncnt > m->bk_cnt_n || nrec > m->bk_recs_n) {
-      CU(cudaStreamSynchronize(m->stream));
-      CU(cudaStreamSynchronize(m->side));
-      if (ncnt > m->bk_cnt_n) {
-        CU(cudaFree(m->bk_cnt));
-        m->bk_cnt = nullptr;
-        m->bk_cnt_n = 0;
-        if (cudaMalloc((void **)&m->bk_cnt, ncnt * sizeof(unsigned)) != cudaSuccess) {
-          cudaGetLastError();
-          return fail(MEM_ENOMEM, "bucket counters (%zu)", ncnt);
-        }
-        CU(cudaMemsetAsync(m->bk_cnt, 0, ncnt * sizeof(unsigned), m->stream));
-        m->bk_cnt_n = ncnt;
-      }
-      if (nrec > m->bk_recs_n) {
-        CU(cudaFree(m->bk_recs));
-        m->bk_recs = nullptr;
-        m->bk_recs_n = 0;
-        if (cudaMalloc((void **)&m->bk_recs, nrec * sizeof(uint4)) != cudaSuccess) {
-          cudaGetLastError();
-          return fail(MEM_ENOMEM, "bucket records (%zu bytes)", nrec * sizeof(uint4));
-        }
-        m->bk_recs_n = nrec;
-      }
-    }
-    a.band_cells = m->band_cells;
-    a.inv_band = 1.0 / (double)m->band_cells;
-    a.nbands = m->nbands;
-    a.bcap = bcap;
-    a.bcnt = m->bk_cnt;
-    a.recs = m->bk_recs;
-  }
-  if (m->l2_persist_mb > 0) {  // DIAGNOSTICS: keep the scratch pool (or the state) in an L2 persisting window
-    cudaStreamAttrValue v;
-    memset(&v, 0, sizeof v);
-    const bool state = getenv("MEM_L2_STATE") != nullptr;
-    const size_t win = state ? sizeof(uint32_t) * (size_t)B * HW * m->n_word : scratch_per_map * m->scratch_maps;
-    const size_t setaside = (size_t)m->l2_persist_mb << 20;
-    v.accessPolicyWindow.base_ptr = state ? (void *)m->st.words : (void *)m->st.acc;
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = win <= setaside ? 1.0f : (float)setaside / (float)win;
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
-    cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &v);
-    cudaStreamSetAttribute(m->side, cudaStreamAttributeAccessPolicyWindow, &v);
-    cudaGetLastError();
-  }
   if (B <= kInlineMaps) {  // frames, offsets and item prefix sums ride in the kernel parameters
     for (int i = 0; i < B; ++i) a.fi[i] = frame(i);
     for (int i = 0; i <= B; ++i) {
@@ -1129,8 +1044,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
     const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
     const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
-    const int ga = (int)std::max(1LL, std::min<long long>(m->accum_grid, (long long)(a.m1 - a.m0) * m->nbands));
-    auto launch_fuse = [&](cudaStream_t st) { return bucketed ? launch_accum(a, ga, st) : launch_cells(a, gc, st); };
+    auto launch_fuse = [&](cudaStream_t st) { return launch_cells(a, gc, st); };
     if (m->transport != 0 && m->route) return route_points(m, a, total, stride);  // point routing
     if (m->transport != 0) {  // sharded map: accumulate this rank's shard, then the band protocol
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
@@ -1144,7 +1058,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
       }
       return shard_fuse_nccl(m);
     }
-    if (n_waves == 1 || m->single_stream) {
+    if (n_waves == 1) {
       TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
       TIMED(MEM_STAGE_CELL, launch_fuse(m->stream));
       if (n_waves == 1) break;
@@ -1157,7 +1071,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     TIMED_ON(m->side, MEM_STAGE_CELL, launch_fuse(m->side));
     CU(cudaEventRecord(m->ev_cells[w], m->side));
   }
-  if (n_waves > 1 && !m->single_stream) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
+  if (n_waves > 1) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
   m->pending = false;
   return MEM_OK;
 }

@@ -13,7 +13,7 @@ struct PointOut {
 
 // a2-a6 for one point: no memory access (the state gather of a7 is batched by the caller)
 __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const PointFrame &f, const Geometry &g,
-                                              const mem_noise &np, float rmin2, float rmax2, int map_base) {
+                                              const mem_noise &np, int map_base) {
   PointOut o;
   o.code = MEM_CODE_NONFINITE;
   o.lcell = -1;
@@ -22,8 +22,9 @@ __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, cons
   o.v = 0.0f;
   o.test = false;
   if (!finite3(px, py, pz)) return o;                   // a2: finiteness
-  const float r2 = (px * px + py * py) + pz * pz;       // a2: sensor-frame range on r^2 (D9)
-  if (!(rmin2 <= r2 && r2 <= rmax2)) {
+  const float r2 = (px * px + py * py) + pz * pz;       // a2: sensor-frame range (D9)
+  const float r = __fsqrt_rn(r2);                       // IEEE sqrt, as the oracle's sqrtf
+  if (!(np.r_min <= r && r <= np.r_max)) {
     o.code = MEM_CODE_RANGE;
     return o;
   }
@@ -37,8 +38,8 @@ __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, cons
   }
   const float x = qx + f.t[0], y = qy + f.t[1];
   o.z = qz + f.t[2];
-  const float fr = x * g.inv_res + g.hH;                 // a5: bin (D13)
-  const float fc = y * g.inv_res + g.hW;
+  const float fr = __fdiv_rn(x, g.res) + g.hH;           // a5: bin (D13), IEEE division
+  const float fc = __fdiv_rn(y, g.res) + g.hW;
   if (!(0.0f <= fr && fr < (float)g.H && 0.0f <= fc && fc < (float)g.W)) {
     o.code = MEM_CODE_OOB;
     return o;

@@ -143,6 +143,29 @@ def _ptr(x):
     raise TypeError(f"unsupported buffer type {type(x)}")
 
 
+_DT = {"float32": (np.float32, "torch.float32"), "int64": (np.int64, "torch.int64")}
+
+
+def _buf(x, dtype, min_elems=None, what="buffer"):
+    """_ptr of an array / tensor after checking its element type and size: a
+    float64 cloud or a too-small output buffer is refused instead of being read as garbage
+    or written out of bounds."""
+    if x is None or isinstance(x, int):
+        return _ptr(x)
+    npd, thd = _DT[dtype]
+    if isinstance(x, np.ndarray):
+        ok, n = x.dtype == npd, x.size
+    elif hasattr(x, "data_ptr"):
+        ok, n = str(x.dtype) == thd, x.numel()
+    else:
+        raise TypeError(f"unsupported buffer type {type(x)}")
+    if not ok:
+        raise TypeError(f"{what}: expected {dtype}, got {x.dtype}")
+    if min_elems is not None and n < min_elems:
+        raise ValueError(f"{what}: {n} elements, need at least {min_elems}")
+    return _ptr(x)
+
+
 def _dbl(a, n):
     arr = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
     if arr.size != n:
@@ -233,7 +256,7 @@ def mem_input_pointcloud(h, pts, bindings, R, t, noise, n=None, stride=None):
     _, Rp = _dbl(R, 9)
     _, tp = _dbl(t, 3)
     nz = _noise(noise)
-    _check(_lib.mem_input_pointcloud(h, _ptr(pts), n, stride, _binds(bindings), len(bindings), Rp, tp, C.byref(nz)),
+    _check(_lib.mem_input_pointcloud(h, _buf(pts, "float32", n * stride, "points"), n, stride, _binds(bindings), len(bindings), Rp, tp, C.byref(nz)),
            "mem_input_pointcloud")
 
 
@@ -244,7 +267,7 @@ def mem_input_pointcloud_batch(h, pts, offsets, bindings, R, t, noise, stride=No
     _, Rp = _dbl(R, 9 * n_maps)
     _, tp = _dbl(t, 3 * n_maps)
     nz = _noise(noise)
-    _check(_lib.mem_input_pointcloud_batch(h, _ptr(pts), off.ctypes.data_as(_P(C.c_int64)), stride,
+    _check(_lib.mem_input_pointcloud_batch(h, _buf(pts, "float32", int(off[-1]) * stride, "points"), off.ctypes.data_as(_P(C.c_int64)), stride,
                                            _binds(bindings), len(bindings), Rp, tp, C.byref(nz)),
            "mem_input_pointcloud_batch")
 
@@ -254,7 +277,7 @@ def mem_input_image(h, img, bindings, K, R, t):
     _, Kp = _dbl(K, 9)
     _, Rp = _dbl(R, 9)
     _, tp = _dbl(t, 3)
-    _check(_lib.mem_input_image(h, _ptr(img), Cc, H, W, _binds(bindings), len(bindings), Kp, Rp, tp),
+    _check(_lib.mem_input_image(h, _buf(img, "float32", Cc * H * W, "image"), Cc, H, W, _binds(bindings), len(bindings), Kp, Rp, tp),
            "mem_input_image")
 
 
@@ -263,7 +286,7 @@ def mem_input_image_batch(h, img, bindings, K, R, t):
     _, Kp = _dbl(K, 9 * B)
     _, Rp = _dbl(R, 9 * B)
     _, tp = _dbl(t, 3 * B)
-    _check(_lib.mem_input_image_batch(h, _ptr(img), Cc, H, W, _binds(bindings), len(bindings), Kp, Rp, tp),
+    _check(_lib.mem_input_image_batch(h, _buf(img, "float32", B * Cc * H * W, "image"), Cc, H, W, _binds(bindings), len(bindings), Kp, Rp, tp),
            "mem_input_image_batch")
 
 
@@ -283,18 +306,27 @@ def mem_get_info(h):
 
 
 def mem_get_layer(h, name, out=None):
+    B, H, W, _ = mem_get_info(h)
     if out is None:
-        B, H, W, _ = mem_get_info(h)
         out = np.empty((B, H, W) if B > 1 else (H, W), np.float32)
-    _check(_lib.mem_get_layer(h, name.encode(), _ptr(out)), f"mem_get_layer({name})")
+    _check(_lib.mem_get_layer(h, name.encode(), _buf(out, "float32", B * H * W, "out")), f"mem_get_layer({name})")
     return out
 
 
 def mem_set_layer(h, name, src):
+    B, H, W, _ = mem_get_info(h)
     if isinstance(src, (int, float)):
-        B, H, W, _ = mem_get_info(h)
         src = np.full((B, H, W), src, np.float32)
-    _check(_lib.mem_set_layer(h, name.encode(), _ptr(src)), f"mem_set_layer({name})")
+    _check(_lib.mem_set_layer(h, name.encode(), _buf(src, "float32", B * H * W, "src")), f"mem_set_layer({name})")
+
+
+def mem_set_layers(h, layers):
+    """restores a state {name: array} in a safe order: "valid" first, then the rest (an
+    invalid cell stores no variance, so writing "variance" before "valid" would lose it;
+    ADVICE r1)."""
+    names = sorted(layers, key=lambda nm: 0 if nm == "valid" else 1)
+    for nm in names:
+        mem_set_layer(h, nm, layers[nm])
 
 
 def mem_get_layer_names(h):
@@ -330,10 +362,10 @@ def mem_debug_point_codes(h, n):
 
 
 def mem_pca_readout(h, group, k=3, out=None):
+    B, H, W, _ = mem_get_info(h)
     if out is None:
-        B, H, W, _ = mem_get_info(h)
         out = np.empty((B, k, H, W) if B > 1 else (k, H, W), np.float32)
-    _check(_lib.mem_pca_readout(h, group.encode(), k, _ptr(out)), f"mem_pca_readout({group})")
+    _check(_lib.mem_pca_readout(h, group.encode(), k, _buf(out, "float32", k * H * W, "out")), f"mem_pca_readout({group})")
     return out
 
 
@@ -434,6 +466,10 @@ class Map:
 
     def set_layer(self, name, src):
         mem_set_layer(self.h, name, src)
+
+    def set_layers(self, layers):
+        """checkpoint restore: {name: array} written "valid" first (see mem_set_layers)."""
+        mem_set_layers(self.h, layers)
 
     def layer_names(self):
         return mem_get_layer_names(self.h)

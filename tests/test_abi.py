@@ -69,3 +69,19 @@ def test_product_and_oracle_share_nothing():
     assert includes <= {"math.h", "stdint.h", "stdlib.h", "string.h", "stdio.h"}, includes
     oracle_py = open(os.path.join(ROOT, "oracle", "oracle.py")).read()
     assert not re.search(r"^\s*(from|import)\s+paper_2309_16818_b200", oracle_py, re.M)
+
+
+def test_binding_rejects_wrong_dtype_and_small_buffers():
+    """the binding refuses float64 clouds / images and undersized outputs before
+    anything reaches the C-ABI (no device needed: the checks run first)."""
+    import numpy as np
+    import pytest
+    from paper_2309_16818_b200 import mem as M
+    with pytest.raises(TypeError):
+        M._buf(np.zeros((10, 4)), "float32", 40, "points")
+    with pytest.raises(ValueError):
+        M._buf(np.zeros(39, np.float32), "float32", 40, "points")
+    assert M._buf(np.zeros(40, np.float32), "float32", 40, "points")
+    torch = pytest.importorskip("torch")
+    with pytest.raises(TypeError):
+        M._buf(torch.zeros(10, 4, dtype=torch.float64), "float32", 40, "points")

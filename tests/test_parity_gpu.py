@@ -480,30 +480,30 @@ def test_c5a_batched_maps_subset():
         assert (gb.get_layer("valid")[b] > 0).sum() > 8000
 
 
-@pytest.mark.parametrize("cap", ["32", "1000", None])
-def test_bucketed_path(monkeypatch, cap):
-    """the bucketed fast path (records + k_accum), forced on, also with tiny buckets so that
-    most records spill to the scratch REDs and k_accum merges both; results must not change
-    (C2 colour and C1 average, vs the oracle)."""
-    monkeypatch.setenv("MEM_BUCKETS", "1")
-    if cap is not None:
-        monkeypatch.setenv("MEM_BUCKET_CAP", cap)
+@pytest.mark.parametrize("stride,offset", [(5, 0), (4, 1), (4, 0)])
+def test_colour_group_any_stride_and_alignment(stride, offset):
+    """a single colour group with xyz + rgb + intensity (stride 5), or a
+    stride-4 cloud in a device buffer that is not 16-B aligned, must fuse exactly like the
+    aligned float4 case (C2 LiDAR, 4 chained frames with shifts, vs the oracle)."""
     c = S.C2
     g, o = make_pair(c["res"], c["rows"], c["cols"], [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])])
     for f in range(4):
         fr = S.c2_frame(f)
+        pts = fr["points"]
+        if stride == 5:
+            pts = np.concatenate([pts, np.full((len(pts), 1), 7.0, np.float32)], 1)
+        buf = torch.zeros(len(pts) * stride + offset, dtype=torch.float32, device="cuda")
+        buf[offset:] = torch.from_numpy(np.ascontiguousarray(pts).reshape(-1)).cuda()
+        src = buf[offset:].view(len(pts), stride)
         g.move_to(*fr["move"])
         o.move_to(*fr["move"])
-        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
-        compare_layers(g, o, where=f"C2 frame {f}: ")
-    c = S.C1
-    g, o = make_pair(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=c["w"])])
-    for f in range(4):
-        fr = S.c1_frame(f)
-        g.move_to(*fr["move"])
-        o.move_to(*fr["move"])
-        step_points(g, o, fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
-        compare_layers(g, o, where=f"C1 frame {f}: ")
+        g.input_pointcloud(src, [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+        oc = o.input_pointcloud(np.ascontiguousarray(pts), [(0, 1, 0)], fr["R"], fr["t"], c["noise"], debug=True)
+        cell, code = g.debug_codes()
+        assert np.array_equal(code, oc[1]) and np.array_equal(cell, oc[0])
+        assert g.stats() == o.stats()
+        compare_layers(g, o, where=f"stride {stride} offset {offset} frame {f}: ")
+    assert (g.get_layer("rgb_r") > 0).sum() > 1000
 
 
 def test_injected_state_then_fusion():
@@ -519,9 +519,9 @@ def test_injected_state_then_fusion():
         o.input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
     g.move_to(*S.c2_frame(2)["move"])
     assert tuple(g.center()[0]) == o.center()
-    names = g.layer_names()
-    for nm in ["valid"] + [n for n in names if n != "valid"]:
-        g.set_layer(nm, o.get_layer(nm))
+    # checkpoint restore in layer_names() order through set_layers, which writes "valid"
+    # first (variance before valid would be lost)
+    g.set_layers({nm: o.get_layer(nm) for nm in g.layer_names()})
     compare_layers(g, o, where="injected: ")
     var = np.full((c["rows"], c["cols"]), 0.5, np.float32)
     h = g.get_layer("valid")
@@ -705,24 +705,6 @@ def test_multi_wave_schedule_in_subprocess():
     assert "3 passed" in r.stdout, r.stdout[-2000:]
 
 
-def test_tma_cell_pass_in_subprocess():
-    """the opt-in bulk-copy cell pass k_cells_tma (env MEM_CELLS_TMA=1, read when libmem loads)
-    runs the fast paths (C1: one average channel, C2 / C2x64: colour) including shifts and a
-    ragged last tile (40000 = 78 x 512 + 64 cells); the parity tests must pass under it."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, MEM_CELLS_TMA="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        "tests/test_parity_gpu.py::test_c1_chained_10_frames",
-                        "tests/test_parity_gpu.py::test_c2_lidar_10_frames",
-                        "tests/test_parity_gpu.py::test_batched_equals_single_and_oracle",
-                        "tests/test_parity_gpu.py::test_c2x64_bench_configuration_sampled"],
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "4 passed" in r.stdout, r.stdout[-2000:]
-
-
 # ---------------------------------------------------------------- k_smap (small maps, sort by cell)
 def test_deterministic_small_maps_are_bit_exact():
     """MEM_FLAG_DETERMINISTIC: maps of <= 16384 cells with <= 65535 points take k_smap, which
@@ -759,6 +741,39 @@ def test_deterministic_small_maps_are_bit_exact():
         lay = np.asarray(gb.get_layer(nm))
         for b in range(nmaps):
             assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
+
+
+def test_deterministic_dense_cells_bit_exact():
+    """cells with far more than 256 points (here ~2,000 in one cell and a
+    few hundred in its neighbours, with z spanning many binades so that the fp64 sums are not
+    exact) must still be summed in input order: every layer bit-identical to the oracle, over
+    5 frames, and identical across two runs."""
+    rows, cols, res = 32, 32, 0.1
+    groups = [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)]
+    noise = dict(a=1e-4, b=1e-4, r_min=0.0, r_max=50.0, h_min=-5.0, h_max=5.0, tau2=9.0, v_out=0.01)
+    outs = []
+    for run in range(2):
+        rng = np.random.default_rng(42)
+        g = M.Map(res, rows, cols, groups, n_maps=64, deterministic=True)
+        o = O.OracleMap(res, rows, cols, groups)
+        for f in range(5):
+            n = 6000
+            xy = np.where(rng.uniform(size=(n, 1)) < 0.4, rng.normal(0.05, 0.01, (n, 2)), rng.uniform(-1.6, 1.6, (n, 2)))
+            z = rng.normal(0.0, 1.0, n) * 10.0 ** rng.uniform(-8, 0, n)
+            feat = rng.normal(0, 1, n) * 10.0 ** rng.uniform(-6, 3, n)
+            pts = np.stack([xy[:, 0], xy[:, 1], z - 1.0, feat], 1).astype(np.float32)
+            allp = np.tile(pts, (64, 1))
+            offs = np.arange(65, dtype=np.int64) * n
+            g.input_pointcloud_batch(torch.from_numpy(allp).cuda(), offs, [(0, 1, 0)], np.tile(np.eye(3), (64, 1, 1)),
+                                     np.tile([0.0, 0.0, 1.0], (64, 1)), noise)
+            o.input_pointcloud(pts, [(0, 1, 0)], np.eye(3), [0.0, 0.0, 1.0], noise)
+        lay = {nm: np.asarray(g.get_layer(nm)) for nm in g.layer_names()}
+        for nm, v in lay.items():
+            for b in (0, 63):
+                assert np.array_equal(v[b], o.get_layer(nm), equal_nan=True), (run, nm, b)
+        outs.append(lay)
+    for nm in outs[0]:
+        assert np.array_equal(outs[0][nm], outs[1][nm], equal_nan=True), nm
 
 
 @pytest.mark.parametrize("rule", ["color", "average"])
