@@ -48,3 +48,27 @@ __device__ __forceinline__ void reset_cell(const State &st, long long BHW, long 
   for (int l = 0; l < r.n_label; ++l) reinterpret_cast<int *>(st.words)[(long long)r.label_word[l] * BHW + cell] = -1;
   for (int fl = 0; fl < r.n_flag; ++fl) st.flags[(long long)fl * BHW + cell] = 0;
 }
+
+// per-lane code counters packed in one u64: 10 bits per code, flushed before they can wrap
+__device__ __forceinline__ void count_code(unsigned long long &packed, unsigned &n, int code, unsigned (&cnt)[8]) {
+  if (code >= 0) packed += 1ull << (10 * code);
+  if (++n == 1000u) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) cnt[stat_slot(c)] += (unsigned)(packed >> (10 * c)) & 1023u;
+    packed = 0ull;
+    n = 0;
+  }
+}
+
+// per-CTA counters: warp reduce, one smem add per warp, one global add per counter
+__device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cnt)[8], unsigned long long *out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const unsigned v = __reduce_add_sync(0xffffffffu, cnt[c]);
+    if (lane == 0 && v) atomicAdd(&s_cnt[c], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && s_cnt[threadIdx.x])
+    atomicAdd(&out[(blockIdx.x % kStatSlots) * 8 + threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+}

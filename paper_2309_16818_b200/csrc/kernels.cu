@@ -1,19 +1,17 @@
 // kernels.cu -- the sm_100a kernels of the MEM hot path,
 // one translation unit assembled from the .cuh parts included below, plus their launchers.
 //
-//   point_pass / k_points  a2-a8: persistent grid-stride over 128-point warp-items (cp.async
-//                   double-buffered float4 stream), filters, transform, bin, noise, one batched
-//                   gather for the Mahalanobis test, warp-aggregated native 64-bit REDs into the
-//                   per-cell scratch
-//   cell_pass / k_cells  a9-a10 + lazy a13: warp-persistent over 128-cell chunks: strip reset,
-//                   Kalman height fusion, per-group rules (fp64), scratch re-zeroed
-//   k_smap          batches of small maps: one CTA per map sorts its points by cell in shared
-//                   memory and fuses every cell in input order (deterministic, oracle order)
-//   k_route         sharded big map: route in-window points to their band owner
+//   point_pass / k_bin  a2-a6: one CTA per 2048-point tile: filters, transform, binning, noise
+//                   variance for every point (the oracle's fp32 expressions); the in-window
+//                   points split stably by cell band into per-tile runs (16-B records)
+//   k_band          a7-a10 + lazy a13: one CTA per (map, band): strip reset, the band's records
+//                   gathered in input order, stable block radix sort by cell, one thread per
+//                   cell: Mahalanobis test, fp64 sums in input order, Kalman height update and
+//                   the group rules -- the oracle's operations in the oracle's order
+//   k_route         sharded big map: route in-window points to their band owner (stable)
 //   k_image         a11-a12 (+ NEXT-1 occlusion walk): project, frustum, gather, fuse (N_j = 1)
 //   k_post          NEXT-3 plugins: normals, traversability, semantic argmax
 //   k_readout       k_shift (eager a13), k_read / k_write (a14), PCA readout (C4)
-//   k_merge         sharded big map (statistics exchange): typed fold of partial bands
 //
 // Everything is stream-ordered; no kernel synchronises the host.
 #include <algorithm>
@@ -22,68 +20,33 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "kernels.cuh"
 
-#ifndef MEM_POINTS_MINB
-#define MEM_POINTS_MINB 3  // resident CTAs per SM the register allocation of k_points targets
-#endif
-#ifndef MEM_PAIR_MIN
-#define MEM_PAIR_MIN 4  // colour fast path: pair lanes of the same cell when >= this many repeat
-#endif
 #ifndef MEM_OCC_BATCH
 #define MEM_OCC_BATCH 4  // occlusion walk: intermediate cells whose loads are issued together
 #endif
-// DIAGNOSTICS ONLY: env MEM_ABLATE switches parts of the kernels off (PassArgs::ablate) in a
-// build with -DMEM_ABLATION=1; production builds compile the checks out
-#ifndef MEM_ABLATION
-#define MEM_ABLATION 0
-#endif
-#define ABLATE(a, bit) (MEM_ABLATION && ((a).ablate & (bit)))
-#ifndef MEM_FULL_ITEMS
-#define MEM_FULL_ITEMS 1  // k_points: a variant of the item body without per-lane bounds for full items
-#endif
-#ifndef MEM_CELLS_MINB
-#define MEM_CELLS_MINB 3
-#endif
-
 namespace memk {
 
 #include "dev_common.cuh"
 #include "point_pass.cuh"
-#include "cell_pass.cuh"
-#include "k_points.cuh"
-#include "k_cells.cuh"
-#include "k_smap.cuh"
+#include "k_bin.cuh"
+#include "k_band.cuh"
 #include "k_route.cuh"
 #include "k_post.cuh"
 #include "k_image.cuh"
 #include "k_readout.cuh"
-#include "k_merge.cuh"
 
 // ---------------------------------------------------------------- launchers
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-int points_blocks_per_sm(bool debug) {
-  int n = 0;
-  if (debug)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<true, 0>, kThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_points<false, 0>, kThreads, 0);
-  return n > 0 ? n : 1;
-}
-
-int cells_blocks_per_sm() {
-  int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_cells<0>, kThreads, 0);
-  return n > 0 ? n : 1;
-}
-
-// Programmatic dependent launch: k_points and k_cells may be scheduled while the
+// Programmatic dependent launch: k_bin, k_band and the router may be scheduled while the
 // kernel before them on the stream drains (its CTAs retire); each waits on griddepcontrol.wait
 // before it reads anything the previous kernel wrote, and lets its own dependent launch early.
-template <class K>
-static cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, const PassArgs &a,
-                              int threads = kThreads) {
+template <class K, class... Extra>
+static cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, const PassArgs &a, int threads,
+                              const Extra &...extra) {
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3(grid);
@@ -95,30 +58,45 @@ static cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, c
   at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, a);
+  return cudaLaunchKernelEx(&cfg, kernel, a, extra...);
 }
 
-cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s) {
-  // the fast variants need the channel in the float4's w (vec4) and exactly one group bound
-  const int f = a.vec4 ? a.fast : 0;
-  const size_t fs = 0;  // no dynamic shared memory
-  if (a.dbg_cell) {
-    if (f == 1) return launch_pdl(k_points<true, 1>, grid, fs, s, a);
-    else if (f == 2) return launch_pdl(k_points<true, 2>, grid, fs, s, a);
-    else return launch_pdl(k_points<true, 0>, grid, fs, s, a);
-  } else {
-    if (f == 1) return launch_pdl(k_points<false, 1>, grid, fs, s, a);
-    else if (f == 2) return launch_pdl(k_points<false, 2>, grid, fs, s, a);
-    else return launch_pdl(k_points<false, 0>, grid, fs, s, a);
+cudaError_t launch_bin(const PassArgs &a, int tiles, cudaStream_t s) {
+  const bool dbg = a.dbg_cell != nullptr;
+  switch (a.fast) {
+    case 1: return dbg ? launch_pdl(k_bin<true, 1>, tiles, 0, s, a, kBinThreads) : launch_pdl(k_bin<false, 1>, tiles, 0, s, a, kBinThreads);
+    case 2: return dbg ? launch_pdl(k_bin<true, 2>, tiles, 0, s, a, kBinThreads) : launch_pdl(k_bin<false, 2>, tiles, 0, s, a, kBinThreads);
+    case 3: return dbg ? launch_pdl(k_bin<true, 3>, tiles, 0, s, a, kBinThreads) : launch_pdl(k_bin<false, 3>, tiles, 0, s, a, kBinThreads);
+    default: return dbg ? launch_pdl(k_bin<true, 0>, tiles, 0, s, a, kBinThreads) : launch_pdl(k_bin<false, 0>, tiles, 0, s, a, kBinThreads);
   }
-  return cudaGetLastError();
 }
 
-cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s) {
-  if (a.fast == 1)
-    return launch_pdl(k_cells<1>, grid, 0, s, a);
-  if (a.fast == 2) return launch_pdl(k_cells<2>, grid, 0, s, a);
-  return launch_pdl(k_cells<0>, grid, 0, s, a);
+size_t band_smem_bytes(int tmax, int band_cells) { return BandSmem(tmax, band_cells).total; }
+
+template <bool kDebug, int kFast>
+static cudaError_t launch_band_t(const PassArgs &a, size_t smem, cudaStream_t s) {
+  // the opt-in shared-memory limit is a per-device function attribute: raised once per device
+  static bool raised[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!raised[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(k_band<kDebug, kFast>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)band_smem_bytes(0, 0) + 160 * 1024);
+    if (e != cudaSuccess) return e;
+    raised[dev & 63] = true;
+  }
+  return launch_pdl(k_band<kDebug, kFast>, a.n_maps * a.nbands, smem, s, a, kBandThreads);
+}
+
+cudaError_t launch_band(const PassArgs &a, cudaStream_t s) {
+  const size_t smem = band_smem_bytes(a.tmax, a.band_cells);
+  const bool dbg = a.dbg_cell != nullptr;
+  switch (a.fast) {
+    case 1: return dbg ? launch_band_t<true, 1>(a, smem, s) : launch_band_t<false, 1>(a, smem, s);
+    case 2: return dbg ? launch_band_t<true, 2>(a, smem, s) : launch_band_t<false, 2>(a, smem, s);
+    case 3: return dbg ? launch_band_t<true, 3>(a, smem, s) : launch_band_t<false, 3>(a, smem, s);
+    default: return dbg ? launch_band_t<true, 0>(a, smem, s) : launch_band_t<false, 0>(a, smem, s);
+  }
 }
 
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {
@@ -126,32 +104,21 @@ cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s) {
-  // the opt-in shared-memory size is a per-device function attribute: set it for the current
-  // device on every launch (a host-side call; maps may live on different devices)
-  if (a.dbg_cell)
-    cudaFuncSetAttribute(a.fast == 1 ? k_smap<true, 1> : k_smap<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  else
-    cudaFuncSetAttribute(a.fast == 1 ? k_smap<false, 1> : k_smap<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof cfg);
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kSmapThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (a.dbg_cell) return a.fast == 1 ? cudaLaunchKernelEx(&cfg, k_smap<true, 1>, a) : cudaLaunchKernelEx(&cfg, k_smap<true, 2>, a);
-  return a.fast == 1 ? cudaLaunchKernelEx(&cfg, k_smap<false, 1>, a) : cudaLaunchKernelEx(&cfg, k_smap<false, 2>, a);
+cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, cudaStream_t s) {
+  if (r.tiles > 0) {
+    cudaError_t e = launch_pdl(k_route_count, r.tiles, 0, s, a, kBinThreads, r);
+    if (e != cudaSuccess) return e;
+  }
+  k_route_scan<<<1, kThreads, 0, s>>>(r);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || r.tiles == 0) return e;
+  return launch_pdl(k_route_scatter, r.tiles, 0, s, a, kBinThreads, r);
 }
 
-cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, int grid, cudaStream_t s) {
-  k_route<<<grid, kThreads, 0, s>>>(a, r);
+cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long long n, uint8_t *dst, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((n + kThreads - 1) / kThreads, 148LL * 8);
+  k_code_return<<<(unsigned)blocks, kThreads, 0, s>>>(codes, idx, n, dst);
   return cudaGetLastError();
 }
 
@@ -174,13 +141,6 @@ cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
 
 cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s) {
   k_pca_project<<<cdiv(a.geo.HW, kThreads), kThreads, 0, s>>>(a, pass);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s) {
-  const long long words = (long long)a.n * (1 + a.R);
-  const long long blocks = (words + kThreads - 1) / kThreads;
-  k_merge<<<(unsigned)(blocks < 148LL * 16 ? blocks : 148LL * 16), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

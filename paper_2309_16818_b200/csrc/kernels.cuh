@@ -4,14 +4,18 @@
 
 namespace memk {
 
-constexpr int kThreads = 256;           // 8 warps per CTA
-#ifndef MEM_WARP_PTS
-#define MEM_WARP_PTS 4
-#endif
-constexpr int kWarpPtsPerLane = MEM_WARP_PTS;  // point warp-item = 128 points (4 float4 loads in flight per lane)
-constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
-constexpr int kWarpCellsPerLane = 4;    // cell warp-item = 128 physical cells
-constexpr int kWarpCells = 32 * kWarpCellsPerLane;
+constexpr int kThreads = 256;           // 8 warps per CTA (image, readout, post, shift kernels)
+// k_bin: one CTA per tile of kTile consecutive points of one map, 8 points per thread
+constexpr int kBinThreads = 256;
+constexpr int kBinPerThread = 8;
+constexpr int kTile = kBinThreads * kBinPerThread;  // 2048
+constexpr int kMaxBands = 1024;         // bands per map (k_bin's per-warp band counters)
+// k_band: one CTA per (map, band); records sorted kChunkRecs at a time
+constexpr int kBandThreads = 256;
+constexpr int kBandIPT = 8;
+constexpr int kChunkRecs = kBandThreads * kBandIPT;  // 2048
+constexpr int kMaxBandCells = 16384;    // cells per band (sort keys <= 15 bits, per-cell arrays in smem)
+constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 
 // Control block of one point input (zeroed by one cudaMemsetAsync per call).
@@ -20,56 +24,55 @@ struct Control {  // two epochs: a point input adds to stats[epoch] and clears s
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
 };
 
-// reset description shared by k_cells (lazy strips) and k_shift
+// reset description shared by k_band (lazy strips) and k_shift
 struct ResetInfo {
   int n_word, n_flag, n_label;
   int label_word[kMaxGroups];
 };
 
-// Arguments of one wave (maps [m0, m1)) of a point input, shared by k_points and k_cells
-// (DESIGN.md §4.2).  Per-cell scratch of map m lives in map-slot scratch_slot(m) of the pool:
-// waves alternate between the two halves so that k_cells(w) overlaps k_points(w+1).
+// Arguments of one point input, shared by k_bin, k_band and the router.
+// The call's points are split into tiles of kTile consecutive points of one map (tiles of map
+// m: [tstart[m], tstart[m+1])); the physical cells [cell_lo, cell_hi) of every map are split
+// into bands of band_cells cells (the last one shorter).
 struct PassArgs {
   const float *pts;
   int stride;
   int vec4;                    // stride == 4 and 16-B aligned: one float4 per point
-  // per-map frames, point offsets [n_maps+1] and prefix sums of point warp-items [n_maps+1]:
-  // inline in the kernel parameters (fi, offi, psi) for n_maps <= kInlineMaps (no copy per
-  // call), else in a staged device buffer (frames, offsets, pstart non-null)
+  int n_maps;
+  // per-map frames, point offsets [n_maps+1] and tile prefix sums [n_maps+1]: inline in the
+  // kernel parameters (fi, offi, tsi) for n_maps <= kInlineMaps (no copy per call), else in a
+  // staged device buffer (frames, offsets, tstart non-null)
   const PointFrame *frames;
   const long long *offsets;
-  const int *pstart;
-  int m0, m1;                  // maps of this wave
-  int cell_lo, cell_hi;        // k_cells: physical cells [lo, hi) of each map (a row band when sharded)
-  int p_uniform;               // > 0: every map of the wave has exactly this many point warp-items
-  double inv_p_uniform;        // 1.0 / p_uniform (divmod_fast)
-  int slot0;                   // scratch map-slot of map m0 (map m -> slot slot0 + m - m0)
-  int q_per_map;               // cell warp-items per map
-  long long SHW;               // scratch map-slots * HW
-  unsigned long long *cnt;     // scratch counts [SHW]
-  unsigned long long *rec;     // scratch records [SHW][R]
-  int R;                       // record words per cell
-  int fast;                    // k_cells fast path: 1 = one colour group, 2 = one 1-channel average group
+  const int *tstart;
+  int t_uniform;               // > 0: every map has exactly this many tiles
+  double inv_t_uniform;        // 1.0 / t_uniform (divmod_fast)
+  int tmax;                    // most tiles of one map (k_band's shared memory)
+  int cell_lo, cell_hi;        // physical cells fused (a row band when sharded)
+  int band_cells, nbands, key_bits;
+  double inv_band, inv_nbands;
+  uint4 *recs;                 // [tiles][kTile] records (k_bin -> k_band)
+  unsigned *tinfo;             // [tiles][nbands] offset | count << 16 of each band's run
+  unsigned *ridx;              // [tiles][kTile] point index of each record (debug outputs only)
+  unsigned long long *scr;     // [n_maps][HW][R] per-cell partial sums of multi-chunk bands
+  int R;                       // scratch words per cell
+  int fast;                    // 1 = one colour group, 2 = one 1-channel average group (float4
+                               // points), 3 = no group bound (height only), 0 = generic
   int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)
   Geometry geo;
-  State st;                    // st.acc: [n_acc][map-slots][HW]
+  State st;
   mem_noise np;
   int nb;
   BindDesc b[kMaxBind];
   Control *ctl;
   int epoch;                   // stats epoch of this call (0/1)
   int pdl;                     // launch with programmatic stream serialization (see launch_pdl)
-  int smap_maxpts;             // k_smap: points of the largest map of the call (shared memory layout)
   ResetInfo reset;
   int *dbg_cell;               // optional per-point outputs (MEM_FLAG_DEBUG_POINTS)
   uint8_t *dbg_code;
   PointFrame fi[kInlineMaps];
   long long offi[kInlineMaps + 1];
-  int psi[kInlineMaps + 1];
-  unsigned ablate;             // DIAGNOSTICS ONLY (env MEM_ABLATE, honoured by builds with -DMEM_ABLATION=1;
-                               // results are wrong when != 0):
-                               // 1 skip cell updates, 2 skip REDs, 4 skip state gathers, 8 skip point math,
-                               // 32 forward (not newest-first) cell tile order, 64 no warp aggregation
+  int tsi[kInlineMaps + 1];
 };
 
 struct ImageArgs {
@@ -123,20 +126,24 @@ struct PostArgs {
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s);
 
 // sharded big map, point routing: every in-window point of this rank's shard is
-// copied (stride floats) into the bucket of the rank that owns its cell's row band
+// copied (stride floats) into the bucket of the rank that owns its cell's row band, in input
+// order (two passes over the shard's tiles: counts, then a stable scatter)
 struct RouteArgs {
   float *buf;                  // [nranks][cap][stride]
-  unsigned *cnt;               // [nranks] points appended per destination (zeroed before)
+  unsigned *src;               // [nranks][cap] shard index of each routed point (debug outputs), or null
+  unsigned *tcnt;              // [tiles][nranks] routed points per tile and owner, then their offsets
+  unsigned *cnt;               // [nranks] routed points per owner
   long long cap;               // points per bucket (= the shard's point count)
   int band_n;                  // cells per band
+  int nranks;
+  int tiles;
 };
-cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, int grid, cudaStream_t s);
+cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, cudaStream_t s);
+cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long long n, uint8_t *dst, cudaStream_t s);
 
-cudaError_t launch_points(const PassArgs &a, int grid, cudaStream_t s);
-cudaError_t launch_cells(const PassArgs &a, int grid, cudaStream_t s);
-size_t smap_smem_bytes(int HW, long long max_pts);
-bool smap_eligible(int HW, long long max_pts);
-cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_bin(const PassArgs &a, int tiles, cudaStream_t s);
+cudaError_t launch_band(const PassArgs &a, cudaStream_t s);
+size_t band_smem_bytes(int tmax, int band_cells);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 // PCA readout: moments of one map's feature group, then projections
@@ -155,19 +162,7 @@ struct PcaArgs {
 };
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s);
 cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s);
-// sharded map: fold the partial scratch of the other ranks for this rank's band
-struct MergeArgs {
-  unsigned long long *cnt;           // own scratch counts (band cells [lo, lo + n))
-  unsigned long long *rec;           // own scratch records [HW][R]
-  const unsigned long long *src_cnt; // nsrc partial count bands, each n words, contiguous
-  const unsigned long long *src_rec; // nsrc partial record bands, each n * R words
-  int nsrc, lo, n, R;
-  const uint8_t *wtype;              // [R]: 0 f64 sum, 1 u64 sum, 2 u64 max
-};
-cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s);
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s);
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s);
-int points_blocks_per_sm(bool debug);
-int cells_blocks_per_sm();
 
 }  // namespace memk

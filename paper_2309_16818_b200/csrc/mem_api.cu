@@ -19,9 +19,6 @@ using namespace memk;
 
 namespace {
 
-// L2 budget for the per-cell scratch of the maps in flight (2 waves); B200 L2 = 126 MB
-static const size_t kScratchBudget = getenv("MEM_SCRATCH_MB") ? (size_t)atol(getenv("MEM_SCRATCH_MB")) << 20 : 2048ull << 20;
-
 thread_local std::string g_err = "no error";
 
 mem_status fail(mem_status s, const char *fmt, ...) {
@@ -96,29 +93,33 @@ struct mem_map {
   size_t pca_cap = 0;
   Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
   size_t ctl_bytes = 0;
-  int pdl = 1;               // programmatic dependent launch (env MEM_PDL=0 disables)
-  int smap = 0;              // k_smap: 1 always (MEM_FLAG_DETERMINISTIC), 0 auto (batches >= 64), -1 never
+  int pdl = 1;               // programmatic dependent launch
   int occlusion = 0;         // image association with the Bresenham occlusion test (NEXT-1)
   float eps_occ = 1e-4f;
   int epoch = 1;             // stats epoch of the last point input (the first one uses 0)
   bool stats_empty = true;   // the last point input had no points (all counters 0)
-  int points_grid = 0;      // resident CTAs of k_points (persistent grid)
-  int cells_grid = 0;       // resident CTAs of k_cells
-  cudaStream_t side = nullptr;  // k_cells of wave w overlaps k_points of wave w+1
-  std::vector<cudaEvent_t> ev_pts, ev_cells;
-  int scratch_maps = 0;     // S: map-slots of per-cell scratch currently allocated
+  int sms = 148;            // SMs of the device (band count heuristic)
+  // point pass buffers: k_bin records and run table, debug indices, carry scratch
+  void *recs = nullptr, *tinfo = nullptr, *ridx = nullptr;
+  size_t recs_cap = 0, tinfo_cap = 0, ridx_cap = 0, scr_cap = 0;
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
   int transport = 0, rank = 0, nranks = 1;
   int band_lo = 0, band_n = 0;          // owned physical cells [band_lo, band_lo + band_n)
   ncclComm_t comm = nullptr;
-  unsigned long long *recv = nullptr;   // (nranks-1) partial bands: counts then records
-  uint8_t *wtype = nullptr;             // [R] record word types (merge)
-  bool exchange_pending = false;        // local transport: accumulated, not yet fused
-  PassArgs shard_args{};                // the k_cells arguments of the frame being fused
-  // point routing (default for sharded maps without MEM_FLAG_DEBUG_POINTS; env MEM_ROUTE=0: off)
-  bool route = false;
-  float *rbuf = nullptr;                // [nranks][cap][stride] outgoing points by owner band
+  bool exchange_pending = false;        // local transport: routed, owner passes not yet run
+  PassArgs shard_args{};                // the owner pass arguments of the frame being fused
+  float *rbuf = nullptr;                // [nranks][cap][stride] outgoing points by owner band, input order
+  unsigned *rsrc = nullptr;             // [nranks][cap] their shard indices (debug outputs)
+  size_t rsrc_cap = 0;
+  unsigned *rtile = nullptr;            // [tiles][nranks] routed points per tile and owner
+  size_t rtile_cap = 0;
+  int *odbg_cell = nullptr;             // owner pass debug outputs, by received position
+  uint8_t *odbg_code = nullptr;
+  size_t odbg_cap = 0;
+  uint8_t *rcode = nullptr;             // NCCL: codes of this shard's routed points, back from their owners
+  size_t rcode_cap = 0;
+  std::vector<unsigned> route_all;      // [nranks][nranks] routed counts of the last frame
   size_t rbuf_cap = 0;                  // bytes
   unsigned *rcnt = nullptr;             // [nranks] outgoing counts (device)
   unsigned *rall = nullptr;             // [nranks][nranks] all ranks' counts (device, NCCL)
@@ -409,12 +410,6 @@ void free_map(mem_map *m) {
   if (!m) return;
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
-  if (m->side) {
-    cudaStreamSynchronize(m->side);
-    cudaStreamDestroy(m->side);
-  }
-  for (cudaEvent_t e : m->ev_pts) cudaEventDestroy(e);
-  for (cudaEvent_t e : m->ev_cells) cudaEventDestroy(e);
   cudaFree(m->st.words);
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
@@ -423,12 +418,18 @@ void free_map(mem_map *m) {
   cudaFree(m->din);
   cudaFree(m->dout);
   cudaFree(m->pca_buf);
-  cudaFree(m->recv);
+  cudaFree(m->recs);
+  cudaFree(m->tinfo);
+  cudaFree(m->ridx);
+  cudaFree(m->rsrc);
+  cudaFree(m->rtile);
+  cudaFree(m->odbg_cell);
+  cudaFree(m->odbg_code);
+  cudaFree(m->rcode);
   cudaFree(m->rbuf);
   cudaFree(m->rcnt);
   cudaFree(m->rall);
   cudaFree(m->rin);
-  cudaFree(m->wtype);
   if (m->comm) ncclCommDestroy(m->comm);
   cudaFree(m->ctl);
   cudaFree(m->dbg_cell);
@@ -506,19 +507,10 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
-    m->points_grid = points_blocks_per_sm((flags & MEM_FLAG_DEBUG_POINTS) != 0) * (sms > 0 ? sms : 1);
-    m->cells_grid = cells_blocks_per_sm() * (sms > 0 ? sms : 1);
+    if (sms > 0) m->sms = sms;
     cudaGetLastError();
   }
   m->pend.assign(n_maps, ShiftRec{0, 0, 0, 0});
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
-    cudaGetLastError();
-    delete m;
-    return fail(MEM_ECUDA, "cudaStreamCreate failed");
-  }
-  m->smap = (flags & MEM_FLAG_DETERMINISTIC) != 0 ? 1 : 0;
   m->kx.assign(n_maps, 0);
   m->ky.assign(n_maps, 0);
   m->r0.assign(n_maps, 0);
@@ -526,7 +518,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   // layer registry (names: include/mem.h)
   m->n_word = 2;
   m->n_flag = 1;
-  m->n_acc = 2;  // record words: P, S, then the groups' fields
+  m->n_acc = 3;  // carry words per cell: P, S, n_in | n_out << 32, then the groups' fields
   add_layer(m, "elevation", LK_ELEV, kWordElev);
   add_layer(m, "variance", LK_VAR, kWordVar);
   add_layer(m, "valid", LK_VALID, kFlagValid);
@@ -600,17 +592,13 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   };
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
-      !alloc((void **)&m->st.acc, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc) + 32) ||
       !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
       !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
     return fail(MEM_ENOMEM, "device allocation of the map state failed");
   }
   mem_status s = MEM_OK;
-  m->scratch_maps = 1;
-  if (cudaMemsetAsync(m->st.acc, 0, sizeof(unsigned long long) * (size_t)rows * cols * (1 + m->n_acc) + 32,
-                      m->stream) != cudaSuccess ||
-      cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
+  if (cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }
   if (s == MEM_OK) s = reset_all(m);
@@ -653,77 +641,6 @@ mem_status mem_synchronize(mem_map *m) {
     if (r_ != ncclSuccess) return fail(MEM_ECOMM, "%s: %s", #expr, ncclGetErrorString(r_)); \
   } while (0)
 
-// merge the received partial bands, clear the scratch outside the band, fuse the band
-static mem_status shard_merge_and_fuse(mem_map *m, const unsigned long long *src, int nsrc) {
-  const int HW = m->H * m->W, R = m->n_acc;
-  PassArgs &a = m->shard_args;
-  if (nsrc > 0) {
-    MergeArgs mg;
-    memset(&mg, 0, sizeof mg);
-    mg.cnt = a.cnt;
-    mg.rec = a.rec;
-    mg.src_cnt = src;
-    mg.src_rec = src + (size_t)nsrc * m->band_n;
-    mg.nsrc = nsrc;
-    mg.lo = m->band_lo;
-    mg.n = m->band_n;
-    mg.R = R;
-    mg.wtype = m->wtype;
-    TIMED(MEM_STAGE_CELL, launch_merge(mg, m->stream));
-  }
-  // the other bands' statistics were sent to their owners: zero them for the next frame
-  const size_t w8 = sizeof(unsigned long long);
-  if (m->band_lo > 0) {
-    CU(cudaMemsetAsync(a.cnt, 0, w8 * m->band_lo, m->stream));
-    CU(cudaMemsetAsync(a.rec, 0, w8 * (size_t)m->band_lo * R, m->stream));
-  }
-  const int hi = m->band_lo + m->band_n;
-  if (hi < HW) {
-    CU(cudaMemsetAsync(a.cnt + hi, 0, w8 * (size_t)(HW - hi), m->stream));
-    CU(cudaMemsetAsync(a.rec + (size_t)hi * R, 0, w8 * (size_t)(HW - hi) * R, m->stream));
-  }
-  const long long citems = (m->band_n + kWarpCells - 1) / kWarpCells;
-  const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
-  TIMED(MEM_STAGE_CELL, launch_cells(a, gc, m->stream));
-  return MEM_OK;
-}
-
-// NCCL transport: bands to their owners (grouped send/recv), merge + band fusion, all-gather of
-// elevation / variance / valid (every rank's next Mahalanobis test needs the whole map)
-static mem_status shard_fuse_nccl(mem_map *m) {
-  const int G = m->nranks, R = m->n_acc, bn = m->band_n;
-  PassArgs &a = m->shard_args;
-  if (G > 1) {
-    NC(ncclGroupStart());
-    int slot = 0;
-    for (int p = 0; p < G; ++p) {
-      if (p == m->rank) continue;
-      unsigned long long *rc = m->recv + (size_t)slot * bn;
-      unsigned long long *rr = m->recv + (size_t)(G - 1) * bn + (size_t)slot * bn * R;
-      NC(ncclSend(a.cnt + (size_t)p * bn, bn, ncclUint64, p, m->comm, m->stream));
-      NC(ncclSend(a.rec + (size_t)p * bn * R, (size_t)bn * R, ncclUint64, p, m->comm, m->stream));
-      NC(ncclRecv(rc, bn, ncclUint64, p, m->comm, m->stream));
-      NC(ncclRecv(rr, (size_t)bn * R, ncclUint64, p, m->comm, m->stream));
-      ++slot;
-    }
-    NC(ncclGroupEnd());
-  }
-  mem_status s = shard_merge_and_fuse(m, m->recv, G - 1);
-  if (s != MEM_OK) return s;
-  if (G > 1) {
-    float *vals = reinterpret_cast<float *>(m->st.words);
-    const int HW = m->H * m->W;
-    NC(ncclGroupStart());
-    NC(ncclAllGather(vals + (size_t)kWordElev * HW + m->band_lo, vals + (size_t)kWordElev * HW, bn, ncclFloat32,
-                     m->comm, m->stream));
-    NC(ncclAllGather(vals + (size_t)kWordVar * HW + m->band_lo, vals + (size_t)kWordVar * HW, bn, ncclFloat32,
-                     m->comm, m->stream));
-    NC(ncclAllGather(m->st.flags + m->band_lo, m->st.flags, bn, ncclUint8, m->comm, m->stream));
-    NC(ncclGroupEnd());
-  }
-  return MEM_OK;
-}
-
 // all-gather every stored layer (readout of a sharded NCCL map)
 static mem_status shard_gather_all(mem_map *m) {
   if (m->transport != 1 || m->nranks == 1) return MEM_OK;
@@ -739,36 +656,97 @@ static mem_status shard_gather_all(mem_map *m) {
   return MEM_OK;
 }
 
-// point routing: the owner of a band fuses the in-window points it received (all in its band)
+// tiles of every map, bands of the physical cells [cell_lo, cell_hi), buffers; then k_bin and
+// k_band.  `a` carries the frames, the point offsets and the tile prefix sums
+// (inline or staged); `tiles` = all tiles of the call, `tmax` = most tiles of one map.
+static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax, long long max_n) {
+  const int B = a.n_maps;
+  const int cells = a.cell_hi - a.cell_lo;
+  if (tmax > kMaxTilesPerMap)
+    return fail(MEM_EINVAL, "a map takes at most %lld points per call", (long long)kMaxTilesPerMap * kTile);
+  // bands: about one sort chunk of records each if half of the points were in the window, at
+  // least two CTAs per SM over the call, at most kMaxBandCells cells and kMaxBands bands
+  long long nb = (long long)std::ceil(0.5 * (double)max_n / kChunkRecs);
+  nb = std::max(nb, (2LL * m->sms + B - 1) / B);
+  nb = std::max(nb, ((long long)cells + kMaxBandCells - 1) / kMaxBandCells);
+  nb = std::min<long long>(std::min<long long>(nb, kMaxBands), std::max(1, cells));
+  const int bc = (int)((cells + nb - 1) / nb);
+  if (bc > kMaxBandCells) return fail(MEM_EINVAL, "%d cells per map exceed the %d-band limit", cells, kMaxBands);
+  a.band_cells = bc;
+  a.nbands = (cells + bc - 1) / bc;
+  a.inv_band = 1.0 / (double)bc;
+  a.inv_nbands = 1.0 / (double)a.nbands;
+  int kb = 1;
+  while ((1 << kb) - 1 < bc) ++kb;
+  a.key_bits = kb;
+  a.tmax = (int)tmax;
+  const bool dbg = a.dbg_cell != nullptr;
+  if (grow(&m->recs, &m->recs_cap, sizeof(uint4) * (size_t)std::max(1, tiles) * kTile, m->stream) != MEM_OK ||
+      grow(&m->tinfo, &m->tinfo_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * a.nbands, m->stream) != MEM_OK ||
+      (dbg && grow(&m->ridx, &m->ridx_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * kTile, m->stream) != MEM_OK) ||
+      grow((void **)&m->st.acc, &m->scr_cap, sizeof(unsigned long long) * (size_t)B * m->H * m->W * m->n_acc,
+           m->stream) != MEM_OK)
+    return fail(MEM_ENOMEM, "point pass buffers (%d tiles)", tiles);
+  a.recs = reinterpret_cast<uint4 *>(m->recs);
+  a.tinfo = reinterpret_cast<unsigned *>(m->tinfo);
+  a.ridx = dbg ? reinterpret_cast<unsigned *>(m->ridx) : nullptr;
+  a.st = m->st;
+  a.scr = m->st.acc;
+  a.R = m->n_acc;
+  if (tiles > 0) TIMED(MEM_STAGE_POINT, launch_bin(a, tiles, m->stream));
+  TIMED(MEM_STAGE_CELL, launch_band(a, m->stream));
+  return MEM_OK;
+}
+
+// inline parameters of a one-map pass over n points
+static void one_map_params(PassArgs &b, long long n, int *tiles, long long *tmax) {
+  b.frames = nullptr;
+  b.offsets = nullptr;
+  b.tstart = nullptr;
+  b.n_maps = 1;
+  const long long t = (n + kTile - 1) / kTile;
+  b.offi[0] = 0;
+  b.offi[1] = n;
+  b.tsi[0] = 0;
+  b.tsi[1] = (int)t;
+  b.t_uniform = 0;
+  b.inv_t_uniform = 0.0;
+  *tiles = (int)t;
+  *tmax = t;
+}
+
+// point routing: the owner of a band fuses the in-window points it received (all in its band,
+// in global input order: by source rank, each source's in input order)
 static mem_status owner_pass(mem_map *m, const float *pts, long long n) {
   PassArgs b = m->shard_args;
   b.pts = pts;
   b.vec4 = (b.stride == 4 && ((uintptr_t)pts & 15) == 0) ? 1 : 0;
-  if (!b.vec4) b.fast = 0;
-  b.frames = nullptr;
-  b.offsets = nullptr;
-  b.pstart = nullptr;
-  b.m0 = 0;
-  b.m1 = 1;
-  b.slot0 = 0;
-  const long long items = (n + kWarpPoints - 1) / kWarpPoints;
-  if (items > 0x7fffffffLL) return fail(MEM_EINVAL, "too many routed points");
-  b.offi[0] = 0;
-  b.offi[1] = n;
-  b.psi[0] = 0;
-  b.psi[1] = (int)items;
-  b.p_uniform = (int)items;
-  b.inv_p_uniform = items > 0 ? 1.0 / (double)items : 0.0;
-  b.dbg_cell = nullptr;
-  b.dbg_code = nullptr;
-  if (items > 0) {
-    const int gp = (int)std::max(1LL, std::min<long long>(m->points_grid, (items + 7) / 8));
-    TIMED(MEM_STAGE_POINT, launch_points(b, gp, m->stream));
+  if (!b.vec4 && (b.fast == 1 || b.fast == 2)) b.fast = 0;
+  int tiles;
+  long long tmax;
+  one_map_params(b, n, &tiles, &tmax);
+  if (m->flags & MEM_FLAG_DEBUG_POINTS) {  // owner-side outputs by received position
+    if ((size_t)n > m->odbg_cap) {
+      CU(cudaStreamSynchronize(m->stream));
+      cudaFree(m->odbg_cell);
+      cudaFree(m->odbg_code);
+      m->odbg_cell = nullptr;
+      m->odbg_code = nullptr;
+      m->odbg_cap = 0;
+      const size_t c = n + n / 4 + 1024;
+      if (cudaMalloc(&m->odbg_cell, c * sizeof(int)) != cudaSuccess || cudaMalloc(&m->odbg_code, c) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MEM_ENOMEM, "owner debug buffers");
+      }
+      m->odbg_cap = c;
+    }
+    b.dbg_cell = m->odbg_cell;
+    b.dbg_code = m->odbg_code;
+  } else {
+    b.dbg_cell = nullptr;
+    b.dbg_code = nullptr;
   }
-  const long long citems = (m->band_n + kWarpCells - 1) / kWarpCells;
-  const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
-  TIMED(MEM_STAGE_CELL, launch_cells(b, gc, m->stream));
-  return MEM_OK;
+  return fuse_points(m, b, tiles, tmax, n);
 }
 
 static mem_status grow_floats(float **buf, size_t *cap_bytes, size_t need_floats, cudaStream_t s) {
@@ -776,10 +754,12 @@ static mem_status grow_floats(float **buf, size_t *cap_bytes, size_t need_floats
 }
 
 // NCCL transport of the routed points: counts all-gathered (one host sync), grouped send/recv
-// of the buckets into one contiguous buffer ordered by source rank, then the owner pass
+// of the buckets into one contiguous buffer ordered by source rank, then the owner pass; with
+// debug outputs the owners send every routed point's in/out code back to its source rank
 static mem_status shard_route_nccl(mem_map *m) {
   const int G = m->nranks, st = m->route_stride;
-  std::vector<unsigned> all((size_t)G * G, 0u);
+  std::vector<unsigned> &all = m->route_all;
+  all.assign((size_t)G * G, 0u);
   if (G > 1) {
     NC(ncclAllGather(m->rcnt, m->rall, G, ncclUint32, m->comm, m->stream));
     CU(cudaMemcpyAsync(all.data(), m->rall, sizeof(unsigned) * G * G, cudaMemcpyDeviceToHost, m->stream));
@@ -805,26 +785,54 @@ static mem_status shard_route_nccl(mem_map *m) {
     }
     NC(ncclGroupEnd());
   }
-  return owner_pass(m, m->rin, off[G]);
+  mem_status s = owner_pass(m, m->rin, off[G]);
+  if (s != MEM_OK || !(m->flags & MEM_FLAG_DEBUG_POINTS)) return s;
+  // codes back: owner slice [off[p], off[p+1]) -> source p, which scatters them to its points
+  if (grow((void **)&m->rcode, &m->rcode_cap, (size_t)G * std::max(1LL, m->route_cap), m->stream) != MEM_OK)
+    return fail(MEM_ENOMEM, "returned codes");
+  if (own)
+    CU(cudaMemcpyAsync(m->rcode + (size_t)m->rank * m->route_cap, m->odbg_code + off[m->rank], own,
+                       cudaMemcpyDeviceToDevice, m->stream));
+  if (G > 1) {
+    NC(ncclGroupStart());
+    for (int p = 0; p < G; ++p) {
+      if (p == m->rank) continue;
+      const size_t ns = all[(size_t)m->rank * G + p], nr = all[(size_t)p * G + m->rank];
+      if (nr) NC(ncclSend(m->odbg_code + off[p], nr, ncclUint8, p, m->comm, m->stream));
+      if (ns) NC(ncclRecv(m->rcode + (size_t)p * m->route_cap, ns, ncclUint8, p, m->comm, m->stream));
+    }
+    NC(ncclGroupEnd());
+  }
+  for (int p = 0; p < G; ++p) {
+    const size_t ns = all[(size_t)m->rank * G + p];
+    CU(launch_code_return(m->rcode + (size_t)p * m->route_cap, m->rsrc + (size_t)p * m->route_cap, ns, m->dbg_code,
+                          m->stream));
+  }
+  return MEM_OK;
 }
 
-// this rank's shard: drop / count / route (k_route)
+// this rank's shard: drop / count / route in input order (k_route_count, _scan, _scatter)
 static mem_status route_points(mem_map *m, PassArgs &a, long long n, int stride) {
   const int G = m->nranks;
-  if (grow_floats(&m->rbuf, &m->rbuf_cap, (size_t)G * std::max(1LL, n) * stride, m->stream) != MEM_OK)
+  const long long cap = std::max(1LL, n);
+  const int tiles = (int)((n + kTile - 1) / kTile);
+  const bool dbg = (m->flags & MEM_FLAG_DEBUG_POINTS) != 0;
+  if (grow_floats(&m->rbuf, &m->rbuf_cap, (size_t)G * cap * stride, m->stream) != MEM_OK ||
+      grow((void **)&m->rtile, &m->rtile_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * G, m->stream) != MEM_OK ||
+      (dbg && grow((void **)&m->rsrc, &m->rsrc_cap, sizeof(unsigned) * (size_t)G * cap, m->stream) != MEM_OK))
     return fail(MEM_ENOMEM, "route buckets");
-  CU(cudaMemsetAsync(m->rcnt, 0, sizeof(unsigned) * G, m->stream));
   RouteArgs r;
   r.buf = m->rbuf;
+  r.src = dbg ? m->rsrc : nullptr;
+  r.tcnt = m->rtile;
   r.cnt = m->rcnt;
-  r.cap = std::max(1LL, n);
+  r.cap = cap;
   r.band_n = m->band_n;
-  m->route_cap = r.cap;
+  r.nranks = G;
+  r.tiles = tiles;
+  m->route_cap = cap;
   m->route_stride = stride;
-  if (n > 0) {
-    const int grid = (int)std::max(1LL, std::min<long long>(4LL * m->points_grid, (n + kThreads - 1) / kThreads));
-    TIMED(MEM_STAGE_POINT, launch_route(a, r, grid, m->stream));
-  }
+  TIMED(MEM_STAGE_POINT, launch_route(a, r, m->stream));
   a.cell_lo = m->band_lo;
   a.cell_hi = m->band_lo + m->band_n;
   m->shard_args = a;
@@ -904,6 +912,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   }
   a.pts = (const float *)dpts;
   a.stride = stride;
+  a.n_maps = B;
   a.ring = m->ring;
   a.geo = m->geo();
   a.st = m->st;
@@ -916,11 +925,11 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   const int HW = m->H * m->W;
   a.cell_lo = 0;
   a.cell_hi = HW;
-  a.q_per_map = (HW + kWarpCells - 1) / kWarpCells;
   if (m->flags & MEM_FLAG_DEBUG_POINTS) {
     a.dbg_cell = m->dbg_cell;
     a.dbg_code = m->dbg_code;
   }
+  if (total > 0xffffffffLL) return fail(MEM_EINVAL, "at most 2^32 - 1 points per call");
   auto frame = [&](int i) {
     const MapFrame mf = make_frame(m, i, R + 9 * i, t + 3 * i, nullptr);
     PointFrame f;
@@ -933,147 +942,67 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     f.c0 = m->c0[i];
     return f;
   };
-  // ---- wave schedule: waves of Wm maps, scratch pool = 2 waves
   a.vec4 = (stride == 4 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
-  std::vector<int> pstart(B + 1);
-  pstart[0] = 0;
+  // fast paths (k_bin carries the channel word in the record): one colour or 1-channel average
+  // group bound to the float4's w (never for other strides or unaligned buffers);
+  // no binding at all: height only
+  a.fast = 0;
+  if (nb == 0) {
+    a.fast = 3;
+  } else if (nb == 1 && a.vec4 && a.b[0].topk == 0 && a.b[0].ch_offset == 0) {
+    if (a.b[0].g.rule == MEM_COLOR) a.fast = 1;
+    else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) a.fast = 2;
+  }
+  // tiles of kTile points per map
+  std::vector<int> tstart(B + 1);
+  tstart[0] = 0;
+  long long tmax = 0;
   for (int i = 0; i < B; ++i) {
     const long long ni = offsets ? offsets[i + 1] - offsets[i] : total;
-    const long long pi = pstart[i] + (ni + kWarpPoints - 1) / kWarpPoints;
-    if (pi > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
-    pstart[i + 1] = (int)pi;
+    const long long ti = (ni + kTile - 1) / kTile;
+    tmax = std::max(tmax, ti);
+    if (tstart[i] + ti > 0x7fffffffLL) return fail(MEM_EINVAL, "too many points in one call");
+    tstart[i + 1] = (int)(tstart[i] + ti);
   }
-  // fast paths: one colour or 1-channel average group bound, float4 points
-  int fast = 0;
-  if (nb == 1 && m->ng == 1 && m->n_acc == 4 && a.vec4) {  // fast layouts need the channel in the float4's w
-    if (a.b[0].g.rule == MEM_COLOR) fast = 1;
-    else if (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1) fast = 2;
-  }
-  // small maps (<= 16384 cells, <= 65535 points each): one CTA per map sorts the points by
-  // cell in shared memory (k_smap) -- no scratch, deterministic, the oracle's summation order
-  // (MEM_FLAG_DETERMINISTIC, or by default for batches large enough to give every SM a map:
-  // C5a measured 597 us vs 734 us with REDs for 512 maps)
-  const bool smap = fast != 0 && m->transport == 0 && smap_eligible(HW, max_n) &&
-                    (m->smap > 0 || (m->smap == 0 && B >= 64));
-  const size_t scratch_per_map = sizeof(unsigned long long) * (size_t)HW * (1 + m->n_acc);
-  const size_t per_map = scratch_per_map;
-  long long wm = smap ? B : (long long)(kScratchBudget / 2 / per_map);
-  if (wm < 1) wm = 1;
-  if (wm > B) wm = B;
-  const int n_waves = (int)((B + wm - 1) / wm);
-  wm = (B + n_waves - 1) / n_waves;  // balanced waves
-  const int slots = (int)(n_waves == 1 ? wm : 2 * wm);  // one wave uses half 0 only
-  if (!smap && slots > m->scratch_maps) {  // grow the scratch pool (zeroed)
-    CU(cudaStreamSynchronize(m->stream));
-    CU(cudaStreamSynchronize(m->side));
-    CU(cudaFree(m->st.acc));
-    m->st.acc = nullptr;
-    const size_t bytes = scratch_per_map * slots + 32;  // + the records' 32-B alignment pad
-    if (cudaMalloc((void **)&m->st.acc, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      m->scratch_maps = 0;
-      return fail(MEM_ENOMEM, "scratch allocation (%zu bytes) failed", bytes);
-    }
-    CU(cudaMemsetAsync(m->st.acc, 0, bytes, m->stream));
-    m->scratch_maps = slots;
-  }
-  if ((int)m->ev_pts.size() < n_waves) {
-    for (int i = (int)m->ev_pts.size(); i < n_waves; ++i) {
-      cudaEvent_t e1 = nullptr, e2 = nullptr;
-      CU(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-      m->ev_pts.push_back(e1);
-      m->ev_cells.push_back(e2);
-    }
-  }
-  a.st = m->st;
-  a.SHW = (long long)m->scratch_maps * HW;
-  a.cnt = m->st.acc;
-  a.rec = m->st.acc + ((a.SHW + 3) & ~3LL);  // 32-B aligned records (the fast paths load 2 x 16 B)
-  a.R = m->n_acc;
-  a.fast = fast;  // every group bound (no stale group state); 4-word (32 B) records
-  if (B <= kInlineMaps) {  // frames, offsets and item prefix sums ride in the kernel parameters
+  a.t_uniform = tstart[1] - tstart[0];
+  for (int i = 1; i < B && a.t_uniform > 0; ++i)
+    if (tstart[i + 1] - tstart[i] != a.t_uniform) a.t_uniform = 0;
+  a.inv_t_uniform = a.t_uniform > 0 ? 1.0 / (double)a.t_uniform : 0.0;
+  if (B <= kInlineMaps) {  // frames, offsets and tile prefix sums ride in the kernel parameters
     for (int i = 0; i < B; ++i) a.fi[i] = frame(i);
     for (int i = 0; i <= B; ++i) {
       a.offi[i] = offsets ? offsets[i] : (i == 0 ? 0 : total);
-      a.psi[i] = pstart[i];
+      a.tsi[i] = tstart[i];
     }
   } else {
-    // parameter blob: frames [B] | offsets [B+1] (i64) | pstart [B+1] (i32)
+    // parameter blob: frames [B] | offsets [B+1] (i64) | tstart [B+1] (i32)
     const size_t off_at = (sizeof(PointFrame) * B + 15) & ~(size_t)15;  // int64 alignment
-    const size_t ps_at = off_at + sizeof(long long) * (B + 1);
-    std::vector<unsigned char> blob(ps_at + sizeof(int) * (B + 1));
+    const size_t ts_at = off_at + sizeof(long long) * (B + 1);
+    std::vector<unsigned char> blob(ts_at + sizeof(int) * (B + 1));
     PointFrame *fr = reinterpret_cast<PointFrame *>(blob.data());
     for (int i = 0; i < B; ++i) fr[i] = frame(i);
     memcpy(blob.data() + off_at, offsets, sizeof(long long) * (B + 1));
-    memcpy(blob.data() + ps_at, pstart.data(), sizeof(int) * (B + 1));
+    memcpy(blob.data() + ts_at, tstart.data(), sizeof(int) * (B + 1));
     void *d = nullptr;
     s = stage_params(m, blob.data(), blob.size(), &d);
     if (s != MEM_OK) return s;
     a.frames = reinterpret_cast<const PointFrame *>(d);
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
-    a.pstart = reinterpret_cast<const int *>((char *)d + ps_at);
+    a.tstart = reinterpret_cast<const int *>((char *)d + ts_at);
   }
-  if (smap) {
-    a.m0 = 0;
-    a.m1 = B;
-    a.fast = fast;
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
-    const int grid = (int)std::max(1, std::min(B, sms > 0 ? sms : 1));
-    a.smap_maxpts = (int)max_n;
-    TIMED(MEM_STAGE_POINT, launch_smap(a, grid, smap_smem_bytes(HW, max_n), m->stream));
-    m->pending = false;
-    return MEM_OK;
+  if (m->transport != 0 && m->nranks > 1) {  // sharded map: route the shard's points to their owners
+    a.fast = a.fast == 3 ? 3 : 0;             // (the owner pass re-checks the float4 fast paths)
+    if (nb == 1 && (a.b[0].g.rule == MEM_COLOR || (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1)) &&
+        a.b[0].topk == 0 && a.b[0].ch_offset == 0 && stride == 4)
+      a.fast = a.b[0].g.rule == MEM_COLOR ? 1 : 2;
+    return route_points(m, a, total, stride);
   }
-  // k_points(w) on the caller's stream; k_cells(w) on the side stream after it; k_points(w+2)
-  // reuses the scratch half of wave w, so it waits for k_cells(w).  The call ends joined.
-  for (int w = 0; w < n_waves; ++w) {
-    a.m0 = (int)(w * wm);
-    a.m1 = (int)((w + 1) * wm < B ? (w + 1) * wm : B);
-    a.slot0 = (w & 1) * (int)wm;
-    a.p_uniform = pstart[a.m0 + 1] - pstart[a.m0];  // > 0 only if every map of the wave has it
-    for (int i = a.m0; i < a.m1 && a.p_uniform > 0; ++i)
-      if (pstart[i + 1] - pstart[i] != a.p_uniform) a.p_uniform = 0;
-    a.inv_p_uniform = a.p_uniform > 0 ? 1.0 / (double)a.p_uniform : 0.0;
-    const long long pitems = pstart[a.m1] - pstart[a.m0];
-    const long long citems = (long long)(a.m1 - a.m0) * a.q_per_map;
-    // one wave: persistent grid; several waves: short-lived CTAs (~2 items per warp) so that
-    // the high-priority k_cells of the previous wave is scheduled as they retire
-    const long long per_cta = n_waves == 1 ? 8 : 16;
-    const long long gcap = n_waves == 1 ? m->points_grid : 1LL << 30;
-    const int gp = (int)std::max(1LL, std::min<long long>(gcap, (pitems + per_cta - 1) / per_cta));
-    const int gc = (int)std::max(1LL, std::min<long long>(m->cells_grid, (citems + 7) / 8));
-    auto launch_fuse = [&](cudaStream_t st) { return launch_cells(a, gc, st); };
-    if (m->transport != 0 && m->route) return route_points(m, a, total, stride);  // point routing
-    if (m->transport != 0) {  // sharded map: accumulate this rank's shard, then the band protocol
-      TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
-      a.cell_lo = m->band_lo;
-      a.cell_hi = m->band_lo + m->band_n;
-      m->shard_args = a;
-      m->pending = false;
-      if (m->transport == 2) {
-        m->exchange_pending = true;
-        return MEM_OK;
-      }
-      return shard_fuse_nccl(m);
-    }
-    if (n_waves == 1) {
-      TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
-      TIMED(MEM_STAGE_CELL, launch_fuse(m->stream));
-      if (n_waves == 1) break;
-      continue;
-    }
-    if (w >= 2) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[w - 2], 0));
-    TIMED(MEM_STAGE_POINT, launch_points(a, gp, m->stream));
-    CU(cudaEventRecord(m->ev_pts[w], m->stream));
-    CU(cudaStreamWaitEvent(m->side, m->ev_pts[w], 0));
-    TIMED_ON(m->side, MEM_STAGE_CELL, launch_fuse(m->side));
-    CU(cudaEventRecord(m->ev_cells[w], m->side));
+  if (m->transport != 0) {  // one rank: the whole map is this rank's band
+    a.cell_lo = m->band_lo;
+    a.cell_hi = m->band_lo + m->band_n;
   }
-  if (n_waves > 1) CU(cudaStreamWaitEvent(m->stream, m->ev_cells[n_waves - 1], 0));
   m->pending = false;
-  return MEM_OK;
+  return fuse_points(m, a, tstart[B], tmax, max_n);
 }
 
 mem_status mem_input_pointcloud(mem_map *m, const float *pts, int64_t n, int stride, const mem_binding *bind,
@@ -1118,7 +1047,7 @@ static mem_status input_image(mem_map *m, const float *img, int C, int IH, int I
   a.img = (const float *)dimg;
   a.occlusion = m->occlusion;
   a.eps_occ = m->eps_occ;
-  if (m->transport == 1 && m->route && m->occlusion && m->nranks > 1) {
+  if (m->transport == 1 && m->occlusion && m->nranks > 1) {
     // routed NCCL shards only keep their own band current: the occlusion walk needs the rest
     const int HW = m->H * m->W, bn = m->band_n;
     float *vals = reinterpret_cast<float *>(m->st.words);
@@ -1589,40 +1518,12 @@ mem_status mem_create_sharded(float resolution, int rows, int cols, const mem_la
   m->nranks = nranks;
   m->band_n = rows / nranks * cols;
   m->band_lo = rank * m->band_n;
-  // point routing unless per-point debug codes are wanted (their outlier decision would be taken
-  // on another rank); env MEM_ROUTE=0 selects the statistics exchange
-  // (one rank has nothing to exchange: the statistics path is then the plain fused path;
-  // env MEM_ROUTE=1 forces routing, MEM_ROUTE=0 disables it)
-  m->route = nranks > 1 && !(flags & MEM_FLAG_DEBUG_POINTS);
-  if (const char *rt = getenv("MEM_ROUTE")) m->route = !(flags & MEM_FLAG_DEBUG_POINTS) && atoi(rt) != 0;
+  // every point input routes the shard's in-window points to their band owners
   if (cudaMalloc((void **)&m->rcnt, sizeof(unsigned) * nranks) != cudaSuccess ||
       cudaMalloc((void **)&m->rall, sizeof(unsigned) * nranks * nranks) != cudaSuccess) {
     cudaGetLastError();
     free_map(m);
     return fail(MEM_ENOMEM, "route counters");
-  }
-  // record word types for the merge: P, S f64 sums; per group (see GroupDesc::acc0)
-  std::vector<uint8_t> wt(m->n_acc, 0);
-  for (int gi = 0; gi < m->ng; ++gi) {
-    const GroupDesc &g = m->g[gi];
-    if (g.rule == MEM_CLASS_MAX) {
-      wt[g.acc0] = 2;
-    } else if (g.rule == MEM_COLOR) {
-      wt[g.acc0] = wt[g.acc0 + 1] = 1;
-    } else {
-      wt[g.acc0] = 1;  // count, then f64 sums
-    }
-  }
-  const size_t recv_words = (size_t)(nranks - 1) * m->band_n * (1 + m->n_acc);
-  if (cudaMalloc((void **)&m->wtype, wt.size() + 1) != cudaSuccess ||
-      (recv_words && cudaMalloc((void **)&m->recv, recv_words * 8) != cudaSuccess)) {
-    cudaGetLastError();
-    free_map(m);
-    return fail(MEM_ENOMEM, "sharded buffers");
-  }
-  if (cudaMemcpy(m->wtype, wt.data(), wt.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-    free_map(m);
-    return fail(MEM_ECUDA, "wtype upload");
   }
   if (m->transport == 1) {
     ncclUniqueId id;
@@ -1649,11 +1550,8 @@ mem_status mem_shard_local_sync(mem_map **sh, int G) {
       return fail(MEM_EINVAL, "shard %d did not take the same inputs as shard 0", r);
   mem_map *m0 = sh[0];
   if (set_device(m0)) return MEM_ECUDA;
-  const int R = m0->n_acc, bn = m0->band_n, HW = m0->H * m0->W;
-  const size_t w8 = sizeof(unsigned long long);
-  for (int r = 1; r < G; ++r)
-    if (sh[r]->route != m0->route) return fail(MEM_EINVAL, "shards disagree on point routing");
-  if (m0->route && m0->exchange_pending) {  // point routing: buckets to their owners, owner passes
+  const int HW = m0->H * m0->W, bn = m0->band_n;
+  if (m0->exchange_pending) {  // point routing: buckets to their owners, owner passes
     const int st = m0->route_stride;
     std::vector<unsigned> cnt((size_t)G * G);
     for (int p = 0; p < G; ++p)
@@ -1675,25 +1573,17 @@ mem_status mem_shard_local_sync(mem_map **sh, int G) {
       }
       mem_status s = owner_pass(sh[r], sh[r]->rin, n_in);
       if (s != MEM_OK) return s;
+      if (sh[r]->flags & MEM_FLAG_DEBUG_POINTS) {  // the owner's in/out codes back to the sources
+        off = 0;
+        for (int p = 0; p < G; ++p) {
+          const long long k = cnt[(size_t)p * G + r];
+          if (sh[p]->flags & MEM_FLAG_DEBUG_POINTS)
+            CU(launch_code_return(sh[r]->odbg_code + off, sh[p]->rsrc + (size_t)r * sh[p]->route_cap, k,
+                                  sh[p]->dbg_code, m0->stream));
+          off += k;
+        }
+      }
     }
-    for (int r = 0; r < G; ++r) sh[r]->exchange_pending = false;
-  }
-  // exchange: rank r receives band r of every other shard (device copies)
-  for (int r = 0; r < G && m0->exchange_pending; ++r) {
-    int slot = 0;
-    for (int p = 0; p < G; ++p) {
-      if (p == r) continue;
-      unsigned long long *rc = sh[r]->recv + (size_t)slot * bn;
-      unsigned long long *rr = sh[r]->recv + (size_t)(G - 1) * bn + (size_t)slot * bn * R;
-      CU(cudaMemcpyAsync(rc, sh[p]->shard_args.cnt + (size_t)r * bn, w8 * bn, cudaMemcpyDeviceToDevice, m0->stream));
-      CU(cudaMemcpyAsync(rr, sh[p]->shard_args.rec + (size_t)r * bn * R, w8 * (size_t)bn * R, cudaMemcpyDeviceToDevice,
-                         m0->stream));
-      ++slot;
-    }
-  }
-  for (int r = 0; r < G && m0->exchange_pending; ++r) {
-    mem_status s = shard_merge_and_fuse(sh[r], sh[r]->recv, G - 1);
-    if (s != MEM_OK) return s;
   }
   for (int r = 0; r < G; ++r) sh[r]->exchange_pending = false;
   // full replication (after point clouds and images alike): every layer's band r from shard r to all others

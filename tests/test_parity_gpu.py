@@ -688,23 +688,6 @@ def test_topk_points_and_images_vs_oracle():
             pts, [(0, 2 * k, 0, k)], np.eye(3), [0.0, 0.0, 1.0], noise)
 
 
-def test_multi_wave_schedule_in_subprocess():
-    """a tiny scratch budget (env MEM_SCRATCH_MB, read when libmem loads) splits the batched
-    maps into several waves: k_cells of wave w on the side stream, scratch halves reused.  The
-    batched parity tests must still pass under it."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, MEM_SCRATCH_MB="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        "tests/test_parity_gpu.py::test_uniform_batch_sweep_vs_oracle",
-                        "tests/test_parity_gpu.py::test_batched_equals_single_and_oracle",
-                        "tests/test_parity_gpu.py::test_c5a_batched_maps_subset"],
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "3 passed" in r.stdout, r.stdout[-2000:]
-
-
 # ---------------------------------------------------------------- k_smap (small maps, sort by cell)
 def test_deterministic_small_maps_are_bit_exact():
     """MEM_FLAG_DETERMINISTIC: maps of <= 16384 cells with <= 65535 points take k_smap, which

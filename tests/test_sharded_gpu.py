@@ -263,8 +263,8 @@ def test_routed_shards_c5b_and_images():
             compare_layers(s, oi, where=f"routed image frame {f} shard {r}: ")
 
 
-def test_nccl_single_rank_routed(monkeypatch):
-    monkeypatch.setenv("MEM_ROUTE", "1")  # one rank takes the statistics path unless forced
+def test_nccl_single_rank_c2():
+    """one NCCL rank owns the whole map: the plain point pass on its band, vs the oracle."""
     c = S.C2
     groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
     g = M.Map.sharded(c["res"], c["rows"], c["cols"], groups, 0, 1, nccl_id=M.mem_nccl_unique_id())
@@ -276,4 +276,4 @@ def test_nccl_single_rank_routed(monkeypatch):
         g.input_pointcloud(torch.from_numpy(fr["points"]).cuda(), [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
         o.input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
         assert g.stats() == o.stats()
-        compare_layers(g, o, where=f"NCCL routed frame {f}: ")
+        compare_layers(g, o, where=f"NCCL frame {f}: ")
