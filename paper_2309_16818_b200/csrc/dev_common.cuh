@@ -72,3 +72,54 @@ __device__ __forceinline__ void flush_stats(unsigned *s_cnt, const unsigned (&cn
   if (threadIdx.x < 8 && s_cnt[threadIdx.x])
     atomicAdd(&out[(blockIdx.x % kStatSlots) * 8 + threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
+
+// ---------------------------------------------------------------- bulk copy (TMA) / mbarrier PTX
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// global -> shared bulk copy (16-B aligned, size a multiple of 16) completing on an mbarrier
+__device__ __forceinline__ void bulk_load(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000)
+        : "memory");
+  } while (!ok);
+}
+
+// block-wide exclusive scan of one value per thread; returns the prefix, *total the sum
+template <int kT>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *s_part, unsigned *total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  __syncthreads();  // s_part may still be read by a previous scan
+  if (lane == 31) s_part[wid] = incl;
+  __syncthreads();
+  unsigned wpre = 0u, tot = 0u;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    const unsigned p = s_part[w];
+    wpre += w < wid ? p : 0u;
+    tot += p;
+  }
+  *total = tot;
+  return wpre + incl - v;
+}
+

@@ -37,11 +37,12 @@ __device__ __forceinline__ int map_of_tile(const PassArgs &a, int tile) {
 // so every band's records sit in input order in each tile region and k_band can gather them
 // in input order without any global ordering pass.
 //
-// Record (16 B): x = cell within the band (bits 0-15), y = z (fp32), z = v (fp32), w = payload
-// (fast paths: the point's channel word; generic: the point index).
+// Record (16 B): x = cell within the band (bits 0-15) | usable-channel bit of bound group b
+// (bit 16 + b, generic path), y = z (fp32), z = v (fp32), w = payload (fast paths: the point's
+// channel word; generic: the point index).
 template <bool kDebug, int kFast>
 __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ PassArgs a) {
-  __shared__ uint16_t s_wcnt[kBinThreads / 32][kMaxBands];  // per warp and band: running count, then base
+  __shared__ uint16_t s_wcnt[(kBinThreads / 32) * kMaxBands];  // [warp][band] (row stride NB): running count, then base
   __shared__ unsigned s_bofs[kMaxBands];                     // tile offset of each band's run
   __shared__ unsigned s_cnt[8];
   __shared__ unsigned s_part[kBinThreads / 32];
@@ -53,11 +54,13 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
   const long long end = beg + kTile < mend ? beg + kTile : mend;
   const int NB = a.nbands;
   if (tid < 8) s_cnt[tid] = 0;
-  for (int i = tid; i < (kBinThreads / 32) * NB; i += kBinThreads) s_wcnt[i / NB][i % NB] = 0;
+  for (int i = tid; i < (kBinThreads / 32) * NB; i += kBinThreads) s_wcnt[i] = 0;
   pdl_wait();  // the previous call's k_band may still read the record buffers
   pdl_trigger();
-  if (blockIdx.x == 0)  // the other epoch is the next point input's (no memset per call)
+  if (blockIdx.x == 0) {  // the other epoch is the next point input's (no memset per call)
     for (int i = tid; i < kStatSlots * 8; i += kBinThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;
+    if (tid == 0) a.ctl->n_rec = a.ctl->n_seg = a.ctl->n_lseg = 0u;
+  }
   __syncthreads();
   const Geometry &g = a.geo;
   const PointFrame f = frame_of(a, m);
@@ -98,12 +101,15 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
     zz[u] = vv[u] = 0.0f;
     pay[u] = 0u;
     if (i < end) {
-      const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, 0);
+      const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, 0, a.r2lo, a.r2hi);
       if (kDebug) a.dbg_cell[i] = o.lcell;
       if (o.cell >= a.cell_lo && o.cell < a.cell_hi) {
         int loc;
         key[u] = divmod_fast(o.cell - a.cell_lo, a.band_cells, a.inv_band, loc);
         lc[u] = (unsigned)loc;
+        if (kFast == 0) {  // per bound group: are the point's channels usable (D31, D38)? bits 16..31
+          for (int bi = 0; bi < a.nb; ++bi) lc[u] |= chan_ok(a, a.b[bi], (unsigned)i) ? (1u << (16 + bi)) : 0u;
+        }
         zz[u] = o.z;
         vv[u] = o.v;
         pay[u] = kFast == 1 || kFast == 2 ? __float_as_uint(q[u].w) : (unsigned)i;
@@ -121,11 +127,11 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
     // stable rank among the warp's points of the same band (steps are in input order)
     const unsigned peers = __match_any_sync(0xffffffffu, key[u]);
     unsigned base = 0u;
-    if (key[u] >= 0) base = s_wcnt[wid][key[u]];
+    if (key[u] >= 0) base = s_wcnt[wid * NB + key[u]];
     __syncwarp();
     if (key[u] >= 0) {
       rk[u] = base + (unsigned)__popc(peers & lanemask_lt());
-      if (lane == __ffs(peers) - 1) s_wcnt[wid][key[u]] = (uint16_t)(base + __popc(peers));
+      if (lane == __ffs(peers) - 1) s_wcnt[wid * NB + key[u]] = (uint16_t)(base + __popc(peers));
     }
     __syncwarp();
   }
@@ -135,8 +141,8 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
     unsigned run = 0u;
 #pragma unroll
     for (int w = 0; w < kBinThreads / 32; ++w) {
-      const unsigned c = s_wcnt[w][b];
-      s_wcnt[w][b] = (uint16_t)run;
+      const unsigned c = s_wcnt[w * NB + b];
+      s_wcnt[w * NB + b] = (uint16_t)run;
       run += c;
     }
     s_bofs[b] = run;
@@ -144,35 +150,18 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
   __syncthreads();
   // exclusive scan of the band totals over the bands (thread t owns bands [t*k, (t+1)*k))
   {
-    constexpr int kPer = (kMaxBands + kBinThreads - 1) / kBinThreads;
-    unsigned v[kPer], sum = 0u;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int b = tid * kPer + k;
-      v[k] = b < NB ? s_bofs[b] : 0u;
-      sum += v[k];
-    }
-    unsigned incl = sum;  // warp inclusive scan
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += t;
-    }
-    if (lane == 31) s_part[wid] = incl;
-    __syncthreads();
-    unsigned wpre = 0u;
-#pragma unroll
-    for (int w = 0; w < kBinThreads / 32; ++w) wpre += w < wid ? s_part[w] : 0u;
-    unsigned run = wpre + incl - sum;
+    const int per = (NB + kBinThreads - 1) / kBinThreads;
+    const int b0 = tid * per, b1 = b0 + per < NB ? b0 + per : NB;
+    unsigned sum = 0u;
+    for (int b = b0; b < b1; ++b) sum += s_bofs[b];
+    unsigned tot;
+    unsigned run = block_excl_scan<kBinThreads>(sum, s_part, &tot);
     unsigned *ti = a.tinfo + (long long)tile * NB;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int b = tid * kPer + k;
-      if (b < NB) {
-        s_bofs[b] = run;
-        ti[b] = run | (v[k] << 16);
-      }
-      run += v[k];
+    for (int b = b0; b < b1; ++b) {
+      const unsigned v = s_bofs[b];
+      s_bofs[b] = run;
+      ti[b] = run | (v << 16);
+      run += v;
     }
   }
   __syncthreads();
@@ -180,7 +169,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
 #pragma unroll
   for (int u = 0; u < kBinPerThread; ++u) {
     if (key[u] < 0) continue;
-    const unsigned pos = s_bofs[key[u]] + s_wcnt[wid][key[u]] + rk[u];
+    const unsigned pos = s_bofs[key[u]] + s_wcnt[wid * NB + key[u]] + rk[u];
     __stcg(rt + pos, make_uint4(lc[u], __float_as_uint(zz[u]), __float_as_uint(vv[u]), pay[u]));
     if (kDebug) a.ridx[(long long)tile * kTile + pos] = (unsigned)(wbeg + u * 32 + lane);
   }

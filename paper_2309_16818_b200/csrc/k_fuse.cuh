@@ -1,0 +1,416 @@
+// k_fuse.cuh -- k_fuse: a7-a10 for every touched cell of a point input, in input order
+// (DESIGN.md §4.2).  Part of the single translation unit kernels.cu (included inside namespace
+// memk, in order).
+#pragma once
+
+// ---------------------------------------------------------------- k_fuse
+// Persistent grid-stride over the call's segments (one touched cell each: its records are
+// contiguous in the sorted array, in input order, k_sort).  One thread per cell runs the
+// oracle's per-point loop: the Mahalanobis test against the pre-frame state (a7), then the
+// sufficient statistics summed sequentially in input order -- P += (double)(1/v),
+// S += (double)(z/v), channel sums in fp64, colour in integers (a8) -- then the Kalman height
+// update and the group rules (a9, a10) with the oracle's expressions.  The results are the
+// oracle's, operation for operation, whatever the thread schedule or launch configuration
+// (reading D39).  kFast: 1 one colour group, 2 one 1-channel average group (the channel word
+// rides in the record), 3 no group, 0 generic (channels read from the points by index).
+// the state of one cell after its frame statistics: a9 (Kalman height, D7/D11) and, for the fast
+// groups, a10 (Eq.(1)+(2)); the generic groups follow in fuse_generic
+template <int kFast>
+__device__ __forceinline__ void fuse_state(const PassArgs &a, long long gc, float h, float s2, uint8_t vd0,
+                                           const float *th, uint8_t ob, unsigned nin, unsigned nout, double P,
+                                           double S, unsigned cr, unsigned cg, unsigned cb, unsigned na, double X) {
+  constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
+  const long long BHW = a.geo.BHW;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  uint8_t vd = vd0;
+  kalman_height(h, s2, vd, (double)nin, (double)nout, P, S, a.np.v_out);
+  if (vd) {
+    vals[(long long)kWordElev * BHW + gc] = h;
+    vals[(long long)kWordVar * BHW + gc] = s2;
+    if (!vd0) a.st.flags[(long long)kFlagValid * BHW + gc] = 1;
+  }
+  if (NCH > 0 && na != 0u) {
+    const GroupDesc &gd = a.b[0].g;
+    const unsigned sums[3] = {cr, cg, cb};
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      vals[(long long)(gd.word0 + k) * BHW + gc] =
+          rule_average(th[k], ob != 0, kFast == 1 ? (double)sums[k] : X, (double)na, gd.w);
+    if (!ob) a.st.flags[(long long)gd.flag * BHW + gc] = 1;
+  }
+}
+
+// a10 for the generic groups of one cell: per group, per channel, in input order (channels
+// read from the points by index, usable-channel bits in the records)
+__device__ __noinline__ void fuse_generic(const PassArgs &a, long long gc, const uint4 *rec, int n) {
+  const long long BHW = a.geo.BHW;
+  float *vals = reinterpret_cast<float *>(a.st.words);
+  // a10, generic groups: per group, per channel, in input order (channels read by point index)
+  for (int bi = 0; bi < a.nb; ++bi) {
+    const BindDesc &b = a.b[bi];
+    const GroupDesc &gd = b.g;
+    if (gd.rule == MEM_COLOR) {  // D20: packed 0x00RRGGBB, never skipped
+      unsigned r_ = 0u, g_ = 0u, b_ = 0u;
+      for (int r = 0; r < n; ++r) {
+        const uint32_t bits = __float_as_uint(chan_value(a, b, __ldcg(&rec[r].w), 0));
+        r_ += (bits >> 16) & 255u;
+        g_ += (bits >> 8) & 255u;
+        b_ += bits & 255u;
+      }
+      uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
+      const bool obb = *obs != 0;
+      const unsigned sums[3] = {r_, g_, b_};
+      for (int k = 0; k < 3; ++k) {
+        float *t = vals + (long long)(gd.word0 + k) * BHW + gc;
+        *t = rule_average(*t, obb, (double)sums[k], (double)n, gd.w);
+      }
+      *obs = 1;
+      continue;
+    }
+    if (gd.rule == MEM_CLASS_MAX) {  // D19: the frame's winner, an order-free maximum
+      unsigned long long key = 0ull;
+      for (int r = 0; r < n; ++r) {
+        const uint4 q = __ldcg(rec + r);
+        if (q.x >> (16 + bi) & 1u) {
+          const unsigned long long k = chan_key(a, b, q.w);
+          key = k > key ? k : key;
+        }
+      }
+      if (key != 0ull) {
+        reinterpret_cast<int *>(a.st.words)[(long long)gd.label * BHW + gc] =
+            gd.nch - 1 - (int)(uint32_t)(key & 0xffffffffull);
+        vals[(long long)gd.word0 * BHW + gc] = f32_of_ord((uint32_t)(key >> 32));
+      }
+      continue;
+    }
+    // the points whose channels are usable (D31, D38): bit 16 + bi of the record (k_bin)
+    unsigned ng = 0u;
+    for (int r = 0; r < n; ++r) ng += __ldcg(&rec[r].x) >> (16 + bi) & 1u;
+    if (ng == 0u) continue;  // no finite point: the group is not updated (D31)
+    uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
+    const bool obb = *obs != 0;
+    for (int k = 0; k < gd.nch; ++k) {
+      double sum = 0.0;
+      for (int r = 0; r < n; ++r) {
+        const uint4 q = __ldcg(rec + r);
+        if (q.x >> (16 + bi) & 1u) sum += (double)chan_value(a, b, q.w, k);
+      }
+      float *t = vals + (long long)(gd.word0 + k) * BHW + gc;
+      switch (gd.rule) {
+        case MEM_AVERAGE:
+        case MEM_CLASS_AVERAGE: *t = rule_average(*t, obb, sum, (double)ng, gd.w); break;
+        case MEM_GAUSSIAN: {
+          float *vr = vals + (long long)(gd.word0 + gd.nch + k) * BHW + gc;
+          float mu = *t, vv = *vr;
+          rule_gaussian(mu, vv, obb, sum, (double)ng, gd);
+          *t = mu;
+          *vr = vv;
+          break;
+        }
+        case MEM_CLASS_BAYESIAN: *t = rule_dirichlet(*t, obb, sum, gd.a0); break;
+        default: break;
+      }
+    }
+    *obs = 1;
+  }
+}
+
+// the loads of one short cell (its pre-frame state and its first kCellB records), issued
+// together so that a thread can have the next cell's loads in flight while it fuses this one
+constexpr int kCellB = 4;
+template <int kFast>
+struct CellIn {
+  uint4 seg;
+  float h, s2, th[kFast == 1 ? 3 : 1];
+  uint8_t vd, ob;
+  uint4 q[kCellB];
+};
+
+template <int kFast>
+__device__ __forceinline__ void load_cell(const PassArgs &a, unsigned s, CellIn<kFast> &c) {
+  constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
+  const long long BHW = a.geo.BHW;
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  c.seg = __ldcg(a.segs + s);
+  const long long gc = c.seg.x;
+  c.h = __ldcg(vals + (long long)kWordElev * BHW + gc);
+  c.s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
+  c.vd = __ldcg(a.st.flags + (long long)kFlagValid * BHW + gc);
+  c.ob = 0;
+  if (NCH > 0) {
+    const GroupDesc &gd = a.b[0].g;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) c.th[k] = __ldcg(vals + (long long)(gd.word0 + k) * BHW + gc);
+    c.ob = __ldcg(a.st.flags + (long long)gd.flag * BHW + gc);
+  }
+  const uint4 *rec = a.srec + c.seg.y;
+#pragma unroll
+  for (int u = 0; u < kCellB; ++u)
+    if (u < (int)c.seg.z) c.q[u] = __ldcg(rec + u);
+}
+
+// a7 + a8 for the short cell's points in input order, then a9 + a10 (one thread)
+template <bool kDebug, int kFast>
+__device__ __forceinline__ void fuse_cell(const PassArgs &a, const CellIn<kFast> &c, unsigned (&cnt)[8]) {
+  const long long gc = c.seg.x;  // m * HW + physical cell
+  const uint4 *rec = a.srec + c.seg.y;
+  const int n = (int)c.seg.z;
+  const float h = c.h, s2 = c.s2;
+  const float tau2 = a.np.tau2;
+  double P = 0.0, S = 0.0;
+  unsigned nin = 0u, nout = 0u;
+  unsigned cr = 0u, cg = 0u, cb = 0u, na = 0u;  // colour sums and count / average count
+  double X = 0.0;                               // 1-channel average sum
+  auto point = [&](const uint4 q, int r) {
+    const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
+    const float d = z - h;  // a7 (D10): NaN state (invalid cell) compares false
+    const bool outl = d * d > tau2 * (s2 + v);
+    if (outl) {
+      ++nout;
+    } else {
+      ++nin;
+      const float w = 1.0f / v;  // a8: the oracle's fp32 terms, summed in fp64 in input order
+      P += (double)w;
+      S += (double)(z * w);
+    }
+    if (kFast == 1) {  // D20: packed 0x00RRGGBB, exact integer sums
+      cr += (q.w >> 16) & 255u;
+      cg += (q.w >> 8) & 255u;
+      cb += q.w & 255u;
+      ++na;
+    } else if (kFast == 2) {  // D31: a non-finite channel skips the group
+      const float ch = __uint_as_float(q.w);
+      if (isfinite(ch)) {
+        ++na;
+        X += (double)ch;
+      }
+    }
+    if (kDebug) a.dbg_code[__ldcg(a.sridx + c.seg.y + r)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
+  };
+#pragma unroll
+  for (int u = 0; u < kCellB; ++u)
+    if (u < n) point(c.q[u], u);
+  for (int r = kCellB; r < n; r += kCellB) {  // the rest of a longer cell, kCellB in flight
+    uint4 qb[kCellB];
+#pragma unroll
+    for (int u = 0; u < kCellB; ++u)
+      if (r + u < n) qb[u] = __ldcg(rec + r + u);
+#pragma unroll
+    for (int u = 0; u < kCellB; ++u)
+      if (r + u < n) point(qb[u], r + u);
+  }
+  cnt[5] += nin;
+  cnt[6] += nout;
+  ++cnt[7];
+  fuse_state<kFast>(a, gc, h, s2, c.vd, c.th, c.ob, nin, nout, P, S, cr, cg, cb, na, X);
+  if constexpr (kFast == 0) fuse_generic(a, gc, rec, n);
+}
+
+// One long cell (more than kShortSeg points) on one warp: lane l takes record b0 + l of each
+// batch of 32 (coalesced loads, the per-point fp32 terms in parallel), then every lane folds
+// the batch's terms in lane order -- i.e. input order -- with shuffles, so the fp64 sums are the
+// oracle's sequential ones; integer sums and counts are order-free warp reductions.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+template <bool kDebug, int kFast>
+__device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 seg, unsigned (&cnt)[8]) {
+  constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
+  const int lane = threadIdx.x & 31;
+  const Geometry &g = a.geo;
+  const long long BHW = g.BHW;
+  const long long gc = seg.x;
+  const uint4 *rec = a.srec + seg.y;
+  const int n = (int)seg.z;
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  const float h = __ldcg(vals + (long long)kWordElev * BHW + gc), s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
+  const uint8_t vd0 = __ldcg(a.st.flags + (long long)kFlagValid * BHW + gc);
+  float th[NCH > 0 ? NCH : 1];
+  uint8_t ob = 0;
+  if (NCH > 0) {
+    const GroupDesc &gd = a.b[0].g;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) th[k] = __ldcg(vals + (long long)(gd.word0 + k) * BHW + gc);
+    ob = __ldcg(a.st.flags + (long long)gd.flag * BHW + gc);
+  }
+  const float tau2 = a.np.tau2;
+  double P = 0.0, S = 0.0, X = 0.0;
+  unsigned nin = 0u, nout = 0u, cr = 0u, cg = 0u, cb = 0u, na = 0u;
+  uint4 q = make_uint4(0u, 0u, 0u, 0u);
+  if (lane < n) q = __ldcg(rec + lane);
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int m_ = n - b0 < 32 ? n - b0 : 32;
+    const bool act = lane < m_;
+    uint4 nq = make_uint4(0u, 0u, 0u, 0u);  // the next batch in flight while this one folds
+    if (b0 + 32 + lane < n) nq = __ldcg(rec + b0 + 32 + lane);
+    const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
+    const float d = z - h;  // a7 (D10)
+    const bool outl = act && d * d > tau2 * (s2 + v);
+    const bool inl = act && !outl;
+    float w = 0.0f, zw = 0.0f;
+    if (inl) {
+      w = 1.0f / v;  // a8: the oracle's fp32 terms
+      zw = z * w;
+    }
+    const unsigned im = __ballot_sync(0xffffffffu, inl);
+    nin += __popc(im);
+    nout += __popc(__ballot_sync(0xffffffffu, outl));
+    float c = 0.0f;
+    unsigned fm = 0u;
+    if (kFast == 1) {  // D20: exact integer sums, order-free
+      cr += __reduce_add_sync(0xffffffffu, act ? (q.w >> 16) & 255u : 0u);
+      cg += __reduce_add_sync(0xffffffffu, act ? (q.w >> 8) & 255u : 0u);
+      cb += __reduce_add_sync(0xffffffffu, act ? q.w & 255u : 0u);
+      na += m_;
+    } else if (kFast == 2) {  // D31
+      c = __uint_as_float(q.w);
+      fm = __ballot_sync(0xffffffffu, act && isfinite(c));
+      na += __popc(fm);
+    }
+    for (int j0 = 0; j0 < m_; j0 += 8) {  // input order; 8 lanes' terms fetched ahead of the adds
+      float wj[8], zj[8], cj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        wj[u] = __shfl_sync(0xffffffffu, w, j0 + u);
+        zj[u] = __shfl_sync(0xffffffffu, zw, j0 + u);
+        if (kFast == 2) cj[u] = __shfl_sync(0xffffffffu, c, j0 + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < m_ && (im >> (j0 + u) & 1u)) {
+          P += (double)wj[u];
+          S += (double)zj[u];
+        }
+        if (kFast == 2 && j0 + u < m_ && (fm >> (j0 + u) & 1u)) X += (double)cj[u];
+      }
+    }
+    if (kDebug && act) a.dbg_code[__ldcg(a.sridx + seg.y + b0 + lane)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
+    q = nq;
+  }
+  if (lane == 0) {
+    cnt[5] += nin;
+    cnt[6] += nout;
+    ++cnt[7];
+    fuse_state<kFast>(a, gc, h, s2, vd0, th, ob, nin, nout, P, S, cr, cg, cb, na, X);
+  }
+  if constexpr (kFast == 0) {  // generic groups, warp-parallel over the points of each batch
+    float *wv = reinterpret_cast<float *>(a.st.words);
+    for (int bi = 0; bi < a.nb; ++bi) {
+      const BindDesc &b = a.b[bi];
+      const GroupDesc &gd = b.g;
+      if (gd.rule == MEM_COLOR) {
+        unsigned r_ = 0u, g_ = 0u, b_ = 0u;
+        for (int b0 = 0; b0 < n; b0 += 32) {
+          unsigned bits = 0u;
+          if (b0 + lane < n) bits = __float_as_uint(chan_value(a, b, __ldcg(&rec[b0 + lane].w), 0));
+          r_ += __reduce_add_sync(0xffffffffu, (bits >> 16) & 255u);
+          g_ += __reduce_add_sync(0xffffffffu, (bits >> 8) & 255u);
+          b_ += __reduce_add_sync(0xffffffffu, bits & 255u);
+        }
+        if (lane == 0) {
+          uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
+          const bool obb = *obs != 0;
+          const unsigned sums[3] = {r_, g_, b_};
+          for (int k = 0; k < 3; ++k) {
+            float *t = wv + (long long)(gd.word0 + k) * BHW + gc;
+            *t = rule_average(*t, obb, (double)sums[k], (double)n, gd.w);
+          }
+          *obs = 1;
+        }
+        continue;
+      }
+      if (gd.rule == MEM_CLASS_MAX) {  // D19: order-free maximum
+        unsigned long long key = 0ull;
+        for (int b0 = 0; b0 < n; b0 += 32) {
+          unsigned long long k = 0ull;
+          if (b0 + lane < n) {
+            const uint4 r = __ldcg(rec + b0 + lane);
+            if (r.x >> (16 + bi) & 1u) k = chan_key(a, b, r.w);
+          }
+          k = warp_max_u64(k);
+          key = k > key ? k : key;
+        }
+        if (lane == 0 && key != 0ull) {
+          reinterpret_cast<int *>(a.st.words)[(long long)gd.label * BHW + gc] =
+              gd.nch - 1 - (int)(uint32_t)(key & 0xffffffffull);
+          wv[(long long)gd.word0 * BHW + gc] = f32_of_ord((uint32_t)(key >> 32));
+        }
+        continue;
+      }
+      unsigned ng = 0u;
+      for (int b0 = 0; b0 < n; b0 += 32)
+        ng += __popc(__ballot_sync(0xffffffffu, b0 + lane < n && (__ldcg(&rec[b0 + lane].x) >> (16 + bi) & 1u)));
+      if (ng == 0u) continue;  // D31
+      uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
+      const bool obb = *obs != 0;
+      for (int k = 0; k < gd.nch; ++k) {
+        double sum = 0.0;
+        for (int b0 = 0; b0 < n; b0 += 32) {
+          float val = 0.0f;
+          bool ok = false;
+          if (b0 + lane < n) {
+            const uint4 r = __ldcg(rec + b0 + lane);
+            ok = r.x >> (16 + bi) & 1u;
+            if (ok) val = chan_value(a, b, r.w, k);
+          }
+          const unsigned om = __ballot_sync(0xffffffffu, ok);
+          const int m_ = n - b0 < 32 ? n - b0 : 32;
+          for (int j = 0; j < m_; ++j) {  // input order
+            const float vj = __shfl_sync(0xffffffffu, val, j);
+            if (om >> j & 1u) sum += (double)vj;
+          }
+        }
+        if (lane == 0) {
+          float *t = wv + (long long)(gd.word0 + k) * BHW + gc;
+          switch (gd.rule) {
+            case MEM_AVERAGE:
+            case MEM_CLASS_AVERAGE: *t = rule_average(*t, obb, sum, (double)ng, gd.w); break;
+            case MEM_GAUSSIAN: {
+              float *vr = wv + (long long)(gd.word0 + gd.nch + k) * BHW + gc;
+              float mu = *t, vv = *vr;
+              rule_gaussian(mu, vv, obb, sum, (double)ng, gd);
+              *t = mu;
+              *vr = vv;
+              break;
+            }
+            case MEM_CLASS_BAYESIAN: *t = rule_dirichlet(*t, obb, sum, gd.a0); break;
+            default: break;
+          }
+        }
+      }
+      if (lane == 0) *obs = 1;
+    }
+  }
+}
+
+template <bool kDebug, int kFast>
+__global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ PassArgs a) {
+  __shared__ unsigned s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+  unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const unsigned nseg = *(volatile unsigned *)&a.ctl->n_seg, nlong = *(volatile unsigned *)&a.ctl->n_lseg;
+  // long cells first (a warp each), then the short ones (a thread each)
+  const unsigned gw = (blockIdx.x * kFuseThreads + threadIdx.x) >> 5, nw = gridDim.x * (kFuseThreads / 32);
+  for (unsigned s = gw; s < nlong; s += nw) fuse_cell_warp<kDebug, kFast>(a, __ldcg(a.segs + (a.seg_cap - 1 - s)), cnt);
+  const unsigned step = gridDim.x * kFuseThreads;
+  unsigned s = blockIdx.x * kFuseThreads + threadIdx.x;
+  if (s < nseg) {  // software pipeline: the next cell's loads in flight while this one fuses
+    CellIn<kFast> cur, nxt;
+    load_cell<kFast>(a, s, cur);
+    for (; s < nseg; s += step) {
+      if (s + step < nseg) load_cell<kFast>(a, s + step, nxt);
+      fuse_cell<kDebug, kFast>(a, cur, cnt);
+      cur = nxt;
+    }
+  }
+  flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
+}

@@ -17,7 +17,7 @@ __device__ __forceinline__ void route_tile_bins(const PassArgs &a, const RouteAr
     dst[u] = -1;
     if (i >= end) continue;
     const float *q = a.pts + i * (long long)a.stride;
-    const PointOut o = bin_point(__ldg(q), __ldg(q + 1), __ldg(q + 2), f, a.geo, a.np, 0);
+    const PointOut o = bin_point(__ldg(q), __ldg(q + 1), __ldg(q + 2), f, a.geo, a.np, 0, a.r2lo, a.r2hi);
     if (o.cell >= 0) {
       dst[u] = o.cell / r.band_n;
     } else if (kCount) {

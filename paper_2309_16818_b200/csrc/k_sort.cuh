@@ -1,0 +1,216 @@
+// k_sort.cuh -- k_sort: the in-window points of one cell band, sorted by cell STABLY (input
+// order within each cell), plus the lazy ring-shift reset of the band (a13).
+// Part of the single translation unit kernels.cu (included inside namespace memk, in order).
+#pragma once
+
+// ---------------------------------------------------------------- k_sort
+// One CTA per (map, band of band_cells physical cells).  k_bin left the band's in-window points
+// as per-tile runs (input order within each run, runs in tile order), so walking the runs in
+// tile order visits the band's points in input order (band position p).  The CTA
+//   1. resets the band's cells in the strips that scrolled in with the pending shift (a13);
+//   2. prefix-sums the runs' counts (tinfo) over the map's tiles;
+//   3. counts the records per cell (shared-memory atomics: order-free integers);
+//   4. turns the counts into cell starts (exclusive scan over the cells); every touched cell
+//      becomes a segment {cell, first sorted record, count} of the call's list (k_fuse; cells
+//      of more than kShortSeg points at the back);
+//   5. ranks every record among the earlier records of its cell -- warp w walks the positions
+//      [w*S, (w+1)*S) in input order, 32 at a time (__match_any_sync rank + the warp's running
+//      count per cell), then each cell's per-warp counts are prefix-summed over the warps --
+//      and scatters the record to (cell start + rank): a stable counting sort, each cell's
+//      records in the input order the oracle sums them in.
+// Bands of more than kSortCap records run step 5 window by window.
+struct SortSmem {  // dynamic shared memory layout of k_sort (host and device)
+  size_t bar, rec, tcnt, tpre, cst, wc, rank, total;
+  __host__ __device__ SortSmem(int tmax, int band_cells) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+      const size_t at = o;
+      o = (o + bytes + 15) & ~(size_t)15;
+      return at;
+    };
+    bar = take(16);                                                           // mbarrier (bulk copies)
+    rec = take(sizeof(uint4) * kSortCap);                                     // the window's records
+    tcnt = take(sizeof(unsigned) * (size_t)tmax);
+    tpre = take(sizeof(unsigned) * (size_t)(tmax + 1));
+    cst = take(sizeof(unsigned) * (size_t)band_cells);                       // count -> start
+    wc = take(sizeof(uint16_t) * (kSortThreads / 32) * (size_t)band_cells);   // [warp][cell]
+    rank = take(sizeof(uint16_t) * kSortCap);
+    total = o;
+  }
+};
+
+template <bool kDebug>
+__global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ PassArgs a) {
+  constexpr int kW = kSortThreads / 32;
+  __shared__ unsigned s_part[kW];
+  __shared__ unsigned s_base[3];  // this band's first record / short segment / long segment
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const Geometry &g = a.geo;
+  int bb;
+  const int m = divmod_fast(blockIdx.x, a.nbands, a.inv_nbands, bb);
+  const int c0 = a.cell_lo + bb * a.band_cells;
+  const int c1 = c0 + a.band_cells < a.cell_hi ? c0 + a.band_cells : a.cell_hi;
+  const int ncell = c1 - c0;
+  const int t0 = ts_of(a, m), T = ts_of(a, m + 1) - t0;
+  const SortSmem L(a.tmax, a.band_cells);
+  const unsigned bar = smem_addr(s_dyn + L.bar);
+  uint4 *rec_s = reinterpret_cast<uint4 *>(s_dyn + L.rec);
+  unsigned *tcnt_s = reinterpret_cast<unsigned *>(s_dyn + L.tcnt);
+  unsigned *tpre_s = reinterpret_cast<unsigned *>(s_dyn + L.tpre);
+  unsigned *cst_s = reinterpret_cast<unsigned *>(s_dyn + L.cst);
+  uint16_t *wc_s = reinterpret_cast<uint16_t *>(s_dyn + L.wc);
+  uint16_t *rank_s = reinterpret_cast<uint16_t *>(s_dyn + L.rank);
+  const long long gb = (long long)m * g.HW + c0;  // global index of the band's first cell
+  for (int i = tid; i < ncell; i += kSortThreads) cst_s[i] = 0u;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  pdl_wait();
+  pdl_trigger();
+  const PointFrame f = frame_of(a, m);
+  if (bb == 0 && tid == 0) a.ring[m] = make_int2(f.r0, f.c0);
+  // 1. a13: the band's cells in the strips that scrolled in are reset (before k_fuse reads them)
+  if (f.sr != 0 || f.sc != 0) {
+    for (int i = tid; i < ncell; i += kSortThreads) {
+      int pcol;
+      const int prow = divmod_fast(c0 + i, g.W, g.inv_W, pcol);
+      int row = prow - f.r0, col = pcol - f.c0;
+      row += row < 0 ? g.H : 0;
+      col += col < 0 ? g.W : 0;
+      if (in_strip(row, col, f, g)) reset_cell(a.st, g.BHW, gb + i, a.reset);
+    }
+  }
+  // 2. the runs of this band in the map's tiles, and their prefix (input order)
+  unsigned K = 0u;
+  for (int tb = 0; tb < T; tb += kSortThreads) {
+    const int t = tb + tid;
+    const unsigned v = t < T ? __ldcg(a.tinfo + (long long)(t0 + t) * a.nbands + bb) : 0u;
+    unsigned tot;
+    const unsigned pre = block_excl_scan<kSortThreads>(v >> 16, s_part, &tot);
+    if (t < T) {
+      tcnt_s[t] = v;
+      tpre_s[t] = K + pre;
+    }
+    K += tot;
+  }
+  if (tid == 0) tpre_s[T] = K;
+  __syncthreads();
+  const int nwin = (int)((K + kSortCap - 1) / kSortCap);
+  unsigned phase = 0u;
+  // the window [p0, p0 + n) of band positions into rec_s: one bulk copy per tile run (warp 0),
+  // all in flight together; every thread waits for the lot
+  auto load_window = [&](unsigned p0, unsigned n) {
+    if (wid == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(bar, 16u * n);
+      __syncwarp();
+      for (int t = lane; t < T; t += 32) {
+        const unsigned lo = tpre_s[t] > p0 ? tpre_s[t] : p0, hi = tpre_s[t + 1] < p0 + n ? tpre_s[t + 1] : p0 + n;
+        if (hi > lo)
+          bulk_load(smem_addr(rec_s + (lo - p0)),
+                    a.recs + (long long)(t0 + t) * kTile + (tcnt_s[t] & 0xffffu) + (lo - tpre_s[t]), 16u * (hi - lo),
+                    bar);
+      }
+    }
+    mbar_wait(bar, phase & 1u);
+    ++phase;
+  };
+  // 3. records per cell (order-free); a band of one window keeps its records for step 5
+  for (int w = 0; w < nwin; ++w) {
+    const unsigned p0 = (unsigned)w * kSortCap, n = K - p0 < (unsigned)kSortCap ? K - p0 : (unsigned)kSortCap;
+    if (w > 0) __syncthreads();  // rec_s is refilled
+    load_window(p0, n);
+    for (unsigned j = tid; j < n; j += kSortThreads) atomicAdd(&cst_s[rec_s[j].x & 0xffffu], 1u);
+  }
+  __syncthreads();
+  // 4. cell starts (exclusive over the cells) and the touched cells' segments; thread t owns
+  // the cells [t*cpt, (t+1)*cpt)
+  {
+    const int cpt = (ncell + kSortThreads - 1) / kSortThreads;
+    const int cb = tid * cpt, ce = cb + cpt < ncell ? cb + cpt : ncell;
+    unsigned tot = 0u, ns = 0u, nl = 0u;
+    for (int cc = cb; cc < ce; ++cc) {
+      const unsigned x = cst_s[cc];
+      tot += x;
+      ns += x != 0u && x <= (unsigned)kShortSeg;
+      nl += x > (unsigned)kShortSeg;
+    }
+    unsigned K2, nshort, nlong;
+    unsigned st = block_excl_scan<kSortThreads>(tot, s_part, &K2);
+    unsigned ss = block_excl_scan<kSortThreads>(ns, s_part, &nshort);
+    unsigned sl = block_excl_scan<kSortThreads>(nl, s_part, &nlong);
+    if (tid == 0) {
+      s_base[0] = K ? atomicAdd(&a.ctl->n_rec, K) : 0u;
+      s_base[1] = nshort ? atomicAdd(&a.ctl->n_seg, nshort) : 0u;
+      s_base[2] = nlong ? atomicAdd(&a.ctl->n_lseg, nlong) : 0u;
+    }
+    __syncthreads();
+    const unsigned rbase = s_base[0], sbase = s_base[1], lbase = s_base[2];
+    // short segments from the front of the list, long ones from its back (k_fuse: a thread per
+    // short cell, a warp per long one)
+    for (int cc = cb; cc < ce; ++cc) {
+      const unsigned x = cst_s[cc];
+      cst_s[cc] = rbase + st;
+      if (x) {
+        const uint4 sgm = make_uint4((unsigned)(gb + cc), rbase + st, x, 0u);
+        if (x <= (unsigned)kShortSeg) a.segs[sbase + ss++] = sgm;
+        else a.segs[a.seg_cap - 1 - (lbase + sl++)] = sgm;
+      }
+      st += x;
+    }
+  }
+  // 5. stable scatter, window by window
+  for (int w = 0; w < nwin; ++w) {
+    const unsigned p0 = (unsigned)w * kSortCap, n = K - p0 < (unsigned)kSortCap ? K - p0 : (unsigned)kSortCap;
+    const unsigned S = ((n + kW - 1) / kW + 31) / 32 * 32;  // window positions per warp
+    for (int i = tid; i < kW * ncell; i += kSortThreads) wc_s[i] = 0;
+    __syncthreads();
+    if (nwin > 1) load_window(p0, n);
+    // warp wid ranks the positions [wid*S, (wid+1)*S) in input order
+    for (unsigned b0 = wid * S; b0 < (wid + 1) * S && b0 < n; b0 += 32) {
+      const unsigned j = b0 + lane;
+      const int key = j < n ? (int)(rec_s[j].x & 0xffffu) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      unsigned base = 0u;
+      if (key >= 0) base = wc_s[wid * ncell + key];
+      __syncwarp();
+      if (key >= 0) {
+        rank_s[j] = (uint16_t)(base + __popc(peers & lanemask_lt()));
+        if (lane == __ffs(peers) - 1) wc_s[wid * ncell + key] = (uint16_t)(base + __popc(peers));
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int cc = tid; cc < ncell; cc += kSortThreads) {  // warp bases: exclusive over the warps
+      unsigned run = 0u;
+#pragma unroll
+      for (int ww = 0; ww < kW; ++ww) {
+        const unsigned x = wc_s[ww * ncell + cc];
+        wc_s[ww * ncell + cc] = (uint16_t)run;
+        run += x;
+      }
+    }
+    __syncthreads();
+    for (unsigned j = tid; j < n; j += kSortThreads) {
+      const uint4 r = rec_s[j];
+      const unsigned key = r.x & 0xffffu;
+      const unsigned pos = cst_s[key] + wc_s[(j / S) * ncell + key] + rank_s[j];
+      __stcg(a.srec + pos, r);
+      if (kDebug) {  // the point index of the record (debug outputs only)
+        const unsigned p = p0 + j;
+        int lo = 0, hi = T - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (tpre_s[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        a.sridx[pos] = __ldcg(a.ridx + (long long)(t0 + lo) * kTile + (tcnt_s[lo] & 0xffffu) + (p - tpre_s[lo]));
+      }
+    }
+    __syncthreads();
+    if (w + 1 < nwin) {  // the cells' starts move past this window's records
+      for (unsigned j = tid; j < n; j += kSortThreads) atomicAdd(&cst_s[rec_s[j].x & 0xffffu], 1u);
+      __syncthreads();
+    }
+  }
+}

@@ -4,10 +4,11 @@
 //   point_pass / k_bin  a2-a6: one CTA per 2048-point tile: filters, transform, binning, noise
 //                   variance for every point (the oracle's fp32 expressions); the in-window
 //                   points split stably by cell band into per-tile runs (16-B records)
-//   k_band          a7-a10 + lazy a13: one CTA per (map, band): strip reset, the band's records
-//                   gathered in input order, stable block radix sort by cell, one thread per
-//                   cell: Mahalanobis test, fp64 sums in input order, Kalman height update and
-//                   the group rules -- the oracle's operations in the oracle's order
+//   k_sort          lazy a13 + stable counting sort: one CTA per (map, band): strip reset, the
+//                   band's records in input order sorted by cell (input order kept per cell)
+//   k_fuse          a7-a10: one thread per touched cell: Mahalanobis test, fp64 sums in input
+//                   order, Kalman height update and the group rules -- the oracle's operations
+//                   in the oracle's order
 //   k_route         sharded big map: route in-window points to their band owner (stable)
 //   k_image         a11-a12 (+ NEXT-1 occlusion walk): project, frustum, gather, fuse (N_j = 1)
 //   k_post          NEXT-3 plugins: normals, traversability, semantic argmax
@@ -20,8 +21,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cub/block/block_radix_sort.cuh>
-
 #include "kernels.cuh"
 
 #ifndef MEM_OCC_BATCH
@@ -32,7 +31,8 @@ namespace memk {
 #include "dev_common.cuh"
 #include "point_pass.cuh"
 #include "k_bin.cuh"
-#include "k_band.cuh"
+#include "k_sort.cuh"
+#include "k_fuse.cuh"
 #include "k_route.cuh"
 #include "k_post.cuh"
 #include "k_image.cuh"
@@ -71,31 +71,46 @@ cudaError_t launch_bin(const PassArgs &a, int tiles, cudaStream_t s) {
   }
 }
 
-size_t band_smem_bytes(int tmax, int band_cells) { return BandSmem(tmax, band_cells).total; }
-
-template <bool kDebug, int kFast>
-static cudaError_t launch_band_t(const PassArgs &a, size_t smem, cudaStream_t s) {
+template <bool kDebug>
+static cudaError_t launch_sort_t(const PassArgs &a, size_t smem, cudaStream_t s) {
   // the opt-in shared-memory limit is a per-device function attribute: raised once per device
   static bool raised[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!raised[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(k_band<kDebug, kFast>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)band_smem_bytes(0, 0) + 160 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_sort<kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     raised[dev & 63] = true;
   }
-  return launch_pdl(k_band<kDebug, kFast>, a.n_maps * a.nbands, smem, s, a, kBandThreads);
+  return launch_pdl(k_sort<kDebug>, a.n_maps * a.nbands, smem, s, a, kSortThreads);
 }
 
-cudaError_t launch_band(const PassArgs &a, cudaStream_t s) {
-  const size_t smem = band_smem_bytes(a.tmax, a.band_cells);
+cudaError_t launch_sort(const PassArgs &a, cudaStream_t s) {
+  const size_t smem = SortSmem(a.tmax, a.band_cells).total;
+  return a.dbg_cell ? launch_sort_t<true>(a, smem, s) : launch_sort_t<false>(a, smem, s);
+}
+
+template <bool kDebug, int kFast>
+static cudaError_t launch_fuse_t(const PassArgs &a, cudaStream_t s) {
+  static int grid[64] = {};  // resident CTAs per device (persistent grid)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!grid[dev & 63]) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fuse<kDebug, kFast>, kFuseThreads, 0);
+    grid[dev & 63] = std::max(1, sms) * std::max(1, per);
+  }
+  return launch_pdl(k_fuse<kDebug, kFast>, grid[dev & 63], 0, s, a, kFuseThreads);
+}
+
+cudaError_t launch_fuse(const PassArgs &a, cudaStream_t s) {
   const bool dbg = a.dbg_cell != nullptr;
   switch (a.fast) {
-    case 1: return dbg ? launch_band_t<true, 1>(a, smem, s) : launch_band_t<false, 1>(a, smem, s);
-    case 2: return dbg ? launch_band_t<true, 2>(a, smem, s) : launch_band_t<false, 2>(a, smem, s);
-    case 3: return dbg ? launch_band_t<true, 3>(a, smem, s) : launch_band_t<false, 3>(a, smem, s);
-    default: return dbg ? launch_band_t<true, 0>(a, smem, s) : launch_band_t<false, 0>(a, smem, s);
+    case 1: return dbg ? launch_fuse_t<true, 1>(a, s) : launch_fuse_t<false, 1>(a, s);
+    case 2: return dbg ? launch_fuse_t<true, 2>(a, s) : launch_fuse_t<false, 2>(a, s);
+    case 3: return dbg ? launch_fuse_t<true, 3>(a, s) : launch_fuse_t<false, 3>(a, s);
+    default: return dbg ? launch_fuse_t<true, 0>(a, s) : launch_fuse_t<false, 0>(a, s);
   }
 }
 

@@ -9,12 +9,15 @@ constexpr int kThreads = 256;           // 8 warps per CTA (image, readout, post
 constexpr int kBinThreads = 256;
 constexpr int kBinPerThread = 8;
 constexpr int kTile = kBinThreads * kBinPerThread;  // 2048
-constexpr int kMaxBands = 1024;         // bands per map (k_bin's per-warp band counters)
-// k_band: one CTA per (map, band); records sorted kChunkRecs at a time
-constexpr int kBandThreads = 256;
-constexpr int kBandIPT = 8;
-constexpr int kChunkRecs = kBandThreads * kBandIPT;  // 2048
-constexpr int kMaxBandCells = 16384;    // cells per band (sort keys <= 15 bits, per-cell arrays in smem)
+constexpr int kMaxBands = 2048;         // bands per map (k_bin's per-warp band counters)
+// k_sort: one CTA per (map, band); the band's records counting-sorted kSortCap at a time
+constexpr int kSortThreads = 128;
+constexpr int kSortCap = 2048;          // records ranked per window (shared memory)
+constexpr int kSortChunk = 2048;        // band sizing: records expected per band
+constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in shared memory)
+// k_fuse: persistent grid-stride over the touched cells, one thread each
+constexpr int kFuseThreads = 128;
+constexpr int kShortSeg = 32;          // cells of at most this many points: a thread each; longer: a warp
 constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 
@@ -22,6 +25,7 @@ constexpr int kInlineMaps = 128;        // maps whose frames travel in the kerne
 constexpr int kStatSlots = 64;  // CTAs add their counters to slot blockIdx % 64 (no hot address)
 struct Control {  // two epochs: a point input adds to stats[epoch] and clears stats[epoch ^ 1]
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
+  unsigned n_rec, n_seg, n_lseg;               // this call's sorted records, short / long segments (k_sort)
 };
 
 // reset description shared by k_band (lazy strips) and k_shift
@@ -51,17 +55,21 @@ struct PassArgs {
   int cell_lo, cell_hi;        // physical cells fused (a row band when sharded)
   int band_cells, nbands, key_bits;
   double inv_band, inv_nbands;
-  uint4 *recs;                 // [tiles][kTile] records (k_bin -> k_band)
+  uint4 *recs;                 // [tiles][kTile] records (k_bin -> k_sort)
   unsigned *tinfo;             // [tiles][nbands] offset | count << 16 of each band's run
   unsigned *ridx;              // [tiles][kTile] point index of each record (debug outputs only)
-  unsigned long long *scr;     // [n_maps][HW][R] per-cell partial sums of multi-chunk bands
-  int R;                       // scratch words per cell
+  uint4 *srec;                 // records sorted by cell, input order within a cell (k_sort -> k_fuse)
+  unsigned *sridx;             // their point indices (debug outputs only)
+  uint4 *segs;                 // one per touched cell: {m * HW + cell, first sorted record, count, 0};
+                               // short cells from the front, long cells from the back
+  unsigned seg_cap;
   int fast;                    // 1 = one colour group, 2 = one 1-channel average group (float4
                                // points), 3 = no group bound (height only), 0 = generic
   int2 *ring;                  // device ring offsets, updated to the frames' (r0, c0)
   Geometry geo;
   State st;
   mem_noise np;
+  float r2lo, r2hi;            // a2: r_min <= sqrtf(r2) <= r_max  <=>  r2lo <= r2 <= r2hi (host, exact)
   int nb;
   BindDesc b[kMaxBind];
   Control *ctl;
@@ -142,8 +150,8 @@ cudaError_t launch_route(const PassArgs &a, const RouteArgs &r, cudaStream_t s);
 cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long long n, uint8_t *dst, cudaStream_t s);
 
 cudaError_t launch_bin(const PassArgs &a, int tiles, cudaStream_t s);
-cudaError_t launch_band(const PassArgs &a, cudaStream_t s);
-size_t band_smem_bytes(int tmax, int band_cells);
+cudaError_t launch_sort(const PassArgs &a, cudaStream_t s);
+cudaError_t launch_fuse(const PassArgs &a, cudaStream_t s);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 // PCA readout: moments of one map's feature group, then projections

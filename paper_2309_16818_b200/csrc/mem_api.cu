@@ -17,6 +17,10 @@
 
 using namespace memk;
 
+#ifndef MEM_BAND_RECS
+#define MEM_BAND_RECS 2048  // records aimed at per band (k_sort)
+#endif
+
 namespace {
 
 thread_local std::string g_err = "no error";
@@ -79,12 +83,14 @@ struct mem_map {
   std::vector<Layer> layers;
   State st{};
   int2 *ring = nullptr;
+  float *bin_t = nullptr;    // a5 thresholds: rows [H+1] then columns [W+1] (Geometry::xt, yt)
   std::vector<long long> kx, ky;
   std::vector<int> r0, c0;
   // staging
   void *dparam = nullptr;
   size_t dparam_cap = 0;
   PinnedRing pin;
+  unsigned *seen_rec = nullptr;  // pinned: in-window records of a recent point input (band sizing)
   void *din = nullptr;
   size_t din_cap = 0;
   float *dout = nullptr;
@@ -99,9 +105,10 @@ struct mem_map {
   int epoch = 1;             // stats epoch of the last point input (the first one uses 0)
   bool stats_empty = true;   // the last point input had no points (all counters 0)
   int sms = 148;            // SMs of the device (band count heuristic)
-  // point pass buffers: k_bin records and run table, debug indices, carry scratch
-  void *recs = nullptr, *tinfo = nullptr, *ridx = nullptr;
-  size_t recs_cap = 0, tinfo_cap = 0, ridx_cap = 0, scr_cap = 0;
+  // point pass buffers: k_bin records and run table, sorted records, segments,
+  // debug point indices
+  void *recs = nullptr, *tinfo = nullptr, *ridx = nullptr, *srec = nullptr, *sridx = nullptr, *segs = nullptr;
+  size_t recs_cap = 0, tinfo_cap = 0, ridx_cap = 0, srec_cap = 0, sridx_cap = 0, segs_cap = 0;
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
   int transport = 0, rank = 0, nranks = 1;
@@ -155,6 +162,9 @@ struct mem_map {
     gg.hH = (float)H / 2.0f;
     gg.hW = (float)W / 2.0f;
     gg.inv_W = 1.0 / (double)W;
+    gg.xt = bin_t;
+    gg.yt = bin_t ? bin_t + (H + 1) : nullptr;
+    gg.inv_res = (float)(1.0 / (double)res);
     return gg;
   }
 };
@@ -281,6 +291,63 @@ bool rotation_ok(const double *R) {
   const double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
                      R[2] * (R[3] * R[7] - R[4] * R[6]);
   return std::fabs(det - 1.0) <= 1e-6;
+}
+
+// ---- exact thresholds of the oracle's fp32 decisions (readings D9, D13).  Every
+// float is mapped to an integer key in its numeric order; a monotone predicate over the floats
+// is then bisected on the keys.
+static long long fkey(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return (u & 0x80000000u) ? -(long long)(u & 0x7fffffffu) : (long long)u;
+}
+static float kfloat(long long k) {
+  const uint32_t u = k >= 0 ? (uint32_t)k : (0x80000000u | (uint32_t)(-k));
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+// least float in [lo, hi] (keys) where pred turns true (pred monotone false -> true; pred(hi) true)
+template <class P>
+static float least_true(long long lo, long long hi, P pred) {
+  while (lo < hi) {
+    const long long mid = lo + (hi - lo) / 2;
+    if (pred(kfloat(mid))) hi = mid; else lo = mid + 1;
+  }
+  return kfloat(lo);
+}
+// xt[k] = least x with fl(fl(x / res) + half) >= k, k = 0..n (a5, reading D13)
+static void bin_thresholds(float res, int n, std::vector<float> &t) {
+  const float half = (float)n / 2.0f;
+  t.resize(n + 1);
+  const long long lo = fkey(-INFINITY), hi = fkey(INFINITY);
+  for (int k = 0; k <= n; ++k) {
+    volatile float kf = (float)k;
+    t[k] = least_true(lo, hi, [&](float x) {
+      volatile float q = x / res;  // IEEE fp32 division, then fp32 addition (no contraction)
+      volatile float fr = q + half;
+      return fr >= kf;
+    });
+  }
+}
+// r_min <= sqrtf(r2) <= r_max  <=>  lo <= r2 <= hi over r2 >= +0 (a2, reading D9); an empty
+// set gives lo = +inf, hi = -1
+static void range_thresholds(float r_min, float r_max, float *lo, float *hi) {
+  const long long k0 = fkey(0.0f), kinf = fkey(INFINITY);
+  auto ge_min = [&](float x) { volatile float r = std::sqrt(x); return r >= r_min; };
+  auto gt_max = [&](float x) { volatile float r = std::sqrt(x); return !(r <= r_max); };
+  if (!ge_min(INFINITY) || gt_max(0.0f)) {
+    *lo = INFINITY;
+    *hi = -1.0f;
+    return;
+  }
+  *lo = least_true(k0, kinf, ge_min);
+  if (!gt_max(INFINITY)) {
+    *hi = INFINITY;
+  } else {
+    const float first_out = least_true(k0, kinf, gt_max);
+    *hi = kfloat(fkey(first_out) - 1);
+  }
 }
 
 // a1: frame setup on the host -- t relative to the map centre in fp64, then fp32 (D13)
@@ -414,6 +481,7 @@ void free_map(mem_map *m) {
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
   cudaFree(m->ring);
+  cudaFree(m->bin_t);
   cudaFree(m->dparam);
   cudaFree(m->din);
   cudaFree(m->dout);
@@ -421,6 +489,9 @@ void free_map(mem_map *m) {
   cudaFree(m->recs);
   cudaFree(m->tinfo);
   cudaFree(m->ridx);
+  cudaFree(m->srec);
+  cudaFree(m->sridx);
+  cudaFree(m->segs);
   cudaFree(m->rsrc);
   cudaFree(m->rtile);
   cudaFree(m->odbg_cell);
@@ -434,6 +505,7 @@ void free_map(mem_map *m) {
   cudaFree(m->ctl);
   cudaFree(m->dbg_cell);
   cudaFree(m->dbg_code);
+  if (m->seen_rec) cudaFreeHost(m->seen_rec);
   for (int i = 0; i < PinnedRing::kSlots; ++i) {
     if (m->pin.host[i]) cudaFreeHost(m->pin.host[i]);
     if (m->pin.ev[i]) cudaEventDestroy(m->pin.ev[i]);
@@ -518,7 +590,7 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   // layer registry (names: include/mem.h)
   m->n_word = 2;
   m->n_flag = 1;
-  m->n_acc = 3;  // carry words per cell: P, S, n_in | n_out << 32, then the groups' fields
+  m->n_acc = 3;  // (per-cell statistic words: P, S, n_in | n_out << 32, then the groups' fields)
   add_layer(m, "elevation", LK_ELEV, kWordElev);
   add_layer(m, "variance", LK_VAR, kWordVar);
   add_layer(m, "valid", LK_VALID, kFlagValid);
@@ -593,11 +665,23 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
       !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
+      !alloc((void **)&m->bin_t, sizeof(float) * (rows + 1 + cols + 1)) ||
       !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
     return fail(MEM_ENOMEM, "device allocation of the map state failed");
   }
   mem_status s = MEM_OK;
+  {
+    std::vector<float> tr, tc;
+    bin_thresholds(resolution, rows, tr);
+    bin_thresholds(resolution, cols, tc);
+    tr.insert(tr.end(), tc.begin(), tc.end());
+    if (cudaMemcpy(m->bin_t, tr.data(), sizeof(float) * tr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      free_map(m);
+      return fail(MEM_ECUDA, "binning thresholds upload");
+    }
+  }
   if (cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -664,13 +748,18 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   const int cells = a.cell_hi - a.cell_lo;
   if (tmax > kMaxTilesPerMap)
     return fail(MEM_EINVAL, "a map takes at most %lld points per call", (long long)kMaxTilesPerMap * kTile);
-  // bands: about one sort chunk of records each if half of the points were in the window, at
-  // least two CTAs per SM over the call, at most kMaxBandCells cells and kMaxBands bands
-  long long nb = (long long)std::ceil(0.5 * (double)max_n / kChunkRecs);
+  // bands: about MEM_BAND_RECS in-window records each, estimated from a recent call of this
+  // map (its record count comes back to pinned host memory asynchronously; the first call
+  // assumes half of the points in the window) -- the sizing changes speed, never results --
+  // at least two CTAs per SM over the call, at most kMaxBandCells cells and kMaxBands bands
+  double recs_per_map = 0.5 * (double)max_n;
+  if (m->seen_rec && *(volatile unsigned *)m->seen_rec > 0u)
+    recs_per_map = std::min(recs_per_map * 2.0, 1.25 * (double)*(volatile unsigned *)m->seen_rec / B);
+  long long nb = (long long)std::ceil(recs_per_map / MEM_BAND_RECS);
   nb = std::max(nb, (2LL * m->sms + B - 1) / B);
   nb = std::max(nb, ((long long)cells + kMaxBandCells - 1) / kMaxBandCells);
   nb = std::min<long long>(std::min<long long>(nb, kMaxBands), std::max(1, cells));
-  const int bc = (int)((cells + nb - 1) / nb);
+  const int bc = (int)(((cells + nb - 1) / nb + 15) / 16 * 16);  // 16-B aligned state slices (bulk copies)
   if (bc > kMaxBandCells) return fail(MEM_EINVAL, "%d cells per map exceed the %d-band limit", cells, kMaxBands);
   a.band_cells = bc;
   a.nbands = (cells + bc - 1) / bc;
@@ -681,20 +770,29 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   a.key_bits = kb;
   a.tmax = (int)tmax;
   const bool dbg = a.dbg_cell != nullptr;
-  if (grow(&m->recs, &m->recs_cap, sizeof(uint4) * (size_t)std::max(1, tiles) * kTile, m->stream) != MEM_OK ||
+  const size_t nrec = (size_t)std::max(1, tiles) * kTile;
+  const size_t nseg = std::min(nrec, (size_t)B * cells);
+  if (grow(&m->recs, &m->recs_cap, sizeof(uint4) * nrec, m->stream) != MEM_OK ||
+      grow(&m->srec, &m->srec_cap, sizeof(uint4) * nrec, m->stream) != MEM_OK ||
+      grow(&m->segs, &m->segs_cap, sizeof(uint4) * nseg, m->stream) != MEM_OK ||
       grow(&m->tinfo, &m->tinfo_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * a.nbands, m->stream) != MEM_OK ||
-      (dbg && grow(&m->ridx, &m->ridx_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * kTile, m->stream) != MEM_OK) ||
-      grow((void **)&m->st.acc, &m->scr_cap, sizeof(unsigned long long) * (size_t)B * m->H * m->W * m->n_acc,
-           m->stream) != MEM_OK)
+      (dbg && (grow(&m->ridx, &m->ridx_cap, sizeof(unsigned) * nrec, m->stream) != MEM_OK ||
+               grow(&m->sridx, &m->sridx_cap, sizeof(unsigned) * nrec, m->stream) != MEM_OK)))
     return fail(MEM_ENOMEM, "point pass buffers (%d tiles)", tiles);
   a.recs = reinterpret_cast<uint4 *>(m->recs);
+  a.srec = reinterpret_cast<uint4 *>(m->srec);
+  a.segs = reinterpret_cast<uint4 *>(m->segs);
+  a.seg_cap = (unsigned)nseg;
   a.tinfo = reinterpret_cast<unsigned *>(m->tinfo);
   a.ridx = dbg ? reinterpret_cast<unsigned *>(m->ridx) : nullptr;
+  a.sridx = dbg ? reinterpret_cast<unsigned *>(m->sridx) : nullptr;
   a.st = m->st;
-  a.scr = m->st.acc;
-  a.R = m->n_acc;
   if (tiles > 0) TIMED(MEM_STAGE_POINT, launch_bin(a, tiles, m->stream));
-  TIMED(MEM_STAGE_CELL, launch_band(a, m->stream));
+  TIMED(MEM_STAGE_CELL, launch_sort(a, m->stream));
+  if (tiles > 0) TIMED(MEM_STAGE_CELL, launch_fuse(a, m->stream));
+  if (!m->seen_rec && cudaMallocHost((void **)&m->seen_rec, sizeof(unsigned)) == cudaSuccess) *m->seen_rec = 0u;
+  cudaGetLastError();
+  if (m->seen_rec) CU(cudaMemcpyAsync(m->seen_rec, &m->ctl->n_rec, sizeof(unsigned), cudaMemcpyDeviceToHost, m->stream));
   return MEM_OK;
 }
 
@@ -917,6 +1015,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.geo = m->geo();
   a.st = m->st;
   a.np = *np;
+  range_thresholds(np->r_min, np->r_max, &a.r2lo, &a.r2hi);
   a.nb = nb;
   a.ctl = m->ctl;
   a.epoch = m->epoch;

@@ -12,8 +12,19 @@ struct PointOut {
 };
 
 // a2-a6 for one point: no memory access (the state gather of a7 is batched by the caller)
+// the row (or column) of map coordinate x: max{k : x >= t[k]}, -1 outside [t[0], t[n]); the
+// first guess floor(x / res + n/2) by a reciprocal is within one of it and corrected exactly
+__device__ __forceinline__ int bin_axis(float x, const float *t, int n, float inv_res, float half) {
+  if (!(x >= __ldg(t) && x < __ldg(t + n))) return -1;
+  int k = (int)floorf(x * inv_res + half);
+  k = k < 0 ? 0 : k > n - 1 ? n - 1 : k;
+  if (x < __ldg(t + k)) --k;
+  else if (x >= __ldg(t + k + 1)) ++k;
+  return k;
+}
+
 __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const PointFrame &f, const Geometry &g,
-                                              const mem_noise &np, int map_base) {
+                                              const mem_noise &np, int map_base, float r2lo, float r2hi) {
   PointOut o;
   o.code = MEM_CODE_NONFINITE;
   o.lcell = -1;
@@ -23,8 +34,9 @@ __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, cons
   o.test = false;
   if (!finite3(px, py, pz)) return o;                   // a2: finiteness
   const float r2 = (px * px + py * py) + pz * pz;       // a2: sensor-frame range (D9)
-  const float r = __fsqrt_rn(r2);                       // IEEE sqrt, as the oracle's sqrtf
-  if (!(np.r_min <= r && r <= np.r_max)) {
+  // r_min <= sqrtf(r2) <= r_max, decided on r2 against the exact equivalent bounds the host
+  // derived from the correctly rounded sqrt (PassArgs::r2lo / r2hi): the oracle's decision
+  if (!(r2 >= r2lo && r2 <= r2hi)) {
     o.code = MEM_CODE_RANGE;
     return o;
   }
@@ -103,4 +115,39 @@ struct TopK {
     return ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(K - best);
   }
 };
+
+
+// the channel value k of a bound group for the point at index pi (dense or top-k, D38)
+__device__ __forceinline__ float chan_value(const PassArgs &a, const BindDesc &b, unsigned pi, int k) {
+  const float *ch = a.pts + (long long)pi * a.stride + 3 + b.ch_offset;
+  if (b.topk > 0) return TopK{ch, 1, b.topk, b.g.nch - 1}.value(k);
+  return __ldg(ch + k);
+}
+
+// D31 / D38: the group takes the point iff its channels are finite (top-k: valid pairs);
+// colour never skips (D20)
+__device__ __forceinline__ bool chan_ok(const PassArgs &a, const BindDesc &b, unsigned pi) {
+  if (b.g.rule == MEM_COLOR) return true;
+  const float *ch = a.pts + (long long)pi * a.stride + 3 + b.ch_offset;
+  if (b.topk > 0) return TopK{ch, 1, b.topk, b.g.nch - 1}.ok();
+  for (int k = 0; k < b.nch; ++k)
+    if (!isfinite(__ldg(ch + k))) return false;
+  return true;
+}
+
+// D19: (conf, lowest class) of the point as one u64 key
+__device__ __forceinline__ unsigned long long chan_key(const PassArgs &a, const BindDesc &b, unsigned pi) {
+  const float *ch = a.pts + (long long)pi * a.stride + 3 + b.ch_offset;
+  if (b.topk > 0) return TopK{ch, 1, b.topk, b.g.nch - 1}.key();
+  int best = 0;
+  float bv = __ldg(ch);
+  for (int k = 1; k < b.nch; ++k) {
+    const float c = __ldg(ch + k);
+    if (c > bv) {
+      bv = c;
+      best = k;
+    }
+  }
+  return ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
+}
 
