@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
   pdl_trigger();
   if (blockIdx.x == 0) {  // the other epoch is the next point input's (no memset per call)
     for (int i = tid; i < kStatSlots * 8; i += kBinThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;
-    if (tid == 0) a.ctl->n_rec = a.ctl->n_seg = a.ctl->n_lseg = 0u;
+    if (tid == 0) a.ctl->n_rec = a.ctl->n_seg = a.ctl->n_lseg = a.ctl->n_mseg = 0u;
   }
   __syncthreads();
   const Geometry &g = a.geo;

@@ -42,7 +42,7 @@ __device__ __forceinline__ void fuse_state(const PassArgs &a, long long gc, floa
 
 // a10 for the generic groups of one cell: per group, per channel, in input order (channels
 // read from the points by index, usable-channel bits in the records)
-__device__ __noinline__ void fuse_generic(const PassArgs &a, long long gc, const uint4 *rec, int n) {
+__device__ __forceinline__ void fuse_generic(const PassArgs &a, long long gc, const uint4 *rec, int n) {
   const long long BHW = a.geo.BHW;
   float *vals = reinterpret_cast<float *>(a.st.words);
   // a10, generic groups: per group, per channel, in input order (channels read by point index)
@@ -127,11 +127,11 @@ struct CellIn {
 };
 
 template <int kFast>
-__device__ __forceinline__ void load_cell(const PassArgs &a, unsigned s, CellIn<kFast> &c) {
+__device__ __forceinline__ void load_cell(const PassArgs &a, const uint4 seg, CellIn<kFast> &c) {
   constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
   const long long BHW = a.geo.BHW;
   const float *vals = reinterpret_cast<const float *>(a.st.words);
-  c.seg = __ldcg(a.segs + s);
+  c.seg = seg;
   const long long gc = c.seg.x;
   c.h = __ldcg(vals + (long long)kWordElev * BHW + gc);
   c.s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
@@ -219,36 +219,60 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
-template <bool kDebug, int kFast>
-__device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 seg, unsigned (&cnt)[8]) {
+// One cell on a group of G lanes (G = 8: mid-size cells, 4 per warp; G = 32: long cells): lane
+// li of the group takes record b0 + li of each batch of G, and every lane of the group folds the
+// batch's terms in lane order -- input order -- with shuffles.
+template <int G>
+__device__ __forceinline__ unsigned group_sum(unsigned v) {
+  if constexpr (G == 32) {
+    return __reduce_add_sync(0xffffffffu, v);
+  } else {
+#pragma unroll
+    for (int d = G / 2; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+  }
+}
+
+template <bool kDebug, int kFast, int G>
+__device__ __forceinline__ void fuse_cell_group(const PassArgs &a, const uint4 seg, unsigned (&cnt)[8]) {
   constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, li = lane & (G - 1);
+  const unsigned gsh = (unsigned)(lane & ~(G - 1));  // the group's first lane
   const Geometry &g = a.geo;
   const long long BHW = g.BHW;
   const long long gc = seg.x;
   const uint4 *rec = a.srec + seg.y;
-  const int n = (int)seg.z;
+  const int n = (int)seg.z;  // 0: this group has no cell (uniform control flow is kept)
   const float *vals = reinterpret_cast<const float *>(a.st.words);
-  const float h = __ldcg(vals + (long long)kWordElev * BHW + gc), s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
-  const uint8_t vd0 = __ldcg(a.st.flags + (long long)kFlagValid * BHW + gc);
-  float th[NCH > 0 ? NCH : 1];
+  float h = 0.0f, s2 = 0.0f;
+  uint8_t vd0 = 0;
+  float th[NCH > 0 ? NCH : 1] = {};
   uint8_t ob = 0;
-  if (NCH > 0) {
-    const GroupDesc &gd = a.b[0].g;
+  if (n > 0) {
+    h = __ldcg(vals + (long long)kWordElev * BHW + gc);
+    s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
+    vd0 = __ldcg(a.st.flags + (long long)kFlagValid * BHW + gc);
+    if (NCH > 0) {
+      const GroupDesc &gd = a.b[0].g;
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) th[k] = __ldcg(vals + (long long)(gd.word0 + k) * BHW + gc);
-    ob = __ldcg(a.st.flags + (long long)gd.flag * BHW + gc);
+      for (int k = 0; k < NCH; ++k) th[k] = __ldcg(vals + (long long)(gd.word0 + k) * BHW + gc);
+      ob = __ldcg(a.st.flags + (long long)gd.flag * BHW + gc);
+    }
   }
   const float tau2 = a.np.tau2;
   double P = 0.0, S = 0.0, X = 0.0;
   unsigned nin = 0u, nout = 0u, cr = 0u, cg = 0u, cb = 0u, na = 0u;
+  // the longest cell of the warp's groups bounds the batch loop (every lane runs it)
+  int nmax = n;
+#pragma unroll
+  for (int d = 16; d >= G; d >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, d));
   uint4 q = make_uint4(0u, 0u, 0u, 0u);
-  if (lane < n) q = __ldcg(rec + lane);
-  for (int b0 = 0; b0 < n; b0 += 32) {
-    const int m_ = n - b0 < 32 ? n - b0 : 32;
-    const bool act = lane < m_;
+  if (li < n) q = __ldcg(rec + li);
+  for (int b0 = 0; b0 < nmax; b0 += G) {
+    const int m_ = n - b0 < G ? (n - b0 > 0 ? n - b0 : 0) : G;
+    const bool act = li < m_;
     uint4 nq = make_uint4(0u, 0u, 0u, 0u);  // the next batch in flight while this one folds
-    if (b0 + 32 + lane < n) nq = __ldcg(rec + b0 + 32 + lane);
+    if (b0 + G + li < n) nq = __ldcg(rec + b0 + G + li);
     const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
     const float d = z - h;  // a7 (D10)
     const bool outl = act && d * d > tau2 * (s2 + v);
@@ -258,36 +282,96 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
       w = 1.0f / v;  // a8: the oracle's fp32 terms
       zw = z * w;
     }
-    const unsigned im = __ballot_sync(0xffffffffu, inl);
+    constexpr unsigned gmask = (unsigned)((1ull << G) - 1ull);
+    const unsigned im = (__ballot_sync(0xffffffffu, inl) >> gsh) & gmask;
     nin += __popc(im);
-    nout += __popc(__ballot_sync(0xffffffffu, outl));
+    nout += __popc((__ballot_sync(0xffffffffu, outl) >> gsh) & gmask);
     float c = 0.0f;
     unsigned fm = 0u;
     if (kFast == 1) {  // D20: exact integer sums, order-free
-      cr += __reduce_add_sync(0xffffffffu, act ? (q.w >> 16) & 255u : 0u);
-      cg += __reduce_add_sync(0xffffffffu, act ? (q.w >> 8) & 255u : 0u);
-      cb += __reduce_add_sync(0xffffffffu, act ? q.w & 255u : 0u);
+      cr += group_sum<G>(act ? (q.w >> 16) & 255u : 0u);
+      cg += group_sum<G>(act ? (q.w >> 8) & 255u : 0u);
+      cb += group_sum<G>(act ? q.w & 255u : 0u);
       na += m_;
     } else if (kFast == 2) {  // D31
       c = __uint_as_float(q.w);
-      fm = __ballot_sync(0xffffffffu, act && isfinite(c));
+      fm = (__ballot_sync(0xffffffffu, act && isfinite(c)) >> gsh) & gmask;
       na += __popc(fm);
     }
-    for (int j0 = 0; j0 < m_; j0 += 8) {  // input order; 8 lanes' terms fetched ahead of the adds
+    for (int j0 = 0; j0 < G; j0 += 8) {  // input order; 8 lanes' terms fetched ahead of the adds
       float wj[8], zj[8], cj[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        wj[u] = __shfl_sync(0xffffffffu, w, j0 + u);
-        zj[u] = __shfl_sync(0xffffffffu, zw, j0 + u);
-        if (kFast == 2) cj[u] = __shfl_sync(0xffffffffu, c, j0 + u);
+        wj[u] = __shfl_sync(0xffffffffu, w, j0 + u, G);
+        zj[u] = __shfl_sync(0xffffffffu, zw, j0 + u, G);
+        if (kFast == 2) cj[u] = __shfl_sync(0xffffffffu, c, j0 + u, G);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (j0 + u < m_ && (im >> (j0 + u) & 1u)) {
+        if (im >> (j0 + u) & 1u) {
           P += (double)wj[u];
           S += (double)zj[u];
         }
-        if (kFast == 2 && j0 + u < m_ && (fm >> (j0 + u) & 1u)) X += (double)cj[u];
+        if (kFast == 2 && (fm >> (j0 + u) & 1u)) X += (double)cj[u];
+      }
+    }
+    if (kDebug && act) a.dbg_code[__ldcg(a.sridx + seg.y + b0 + li)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
+    q = nq;
+  }
+  if (li == 0 && n > 0) {
+    cnt[5] += nin;
+    cnt[6] += nout;
+    ++cnt[7];
+    fuse_state<kFast>(a, gc, h, s2, vd0, th, ob, nin, nout, P, S, cr, cg, cb, na, X);
+  }
+}
+
+template <bool kDebug, int kFast>
+__device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 seg, unsigned (&cnt)[8]) {
+  constexpr int NCH = kFast == 1 ? 3 : kFast == 2 ? 1 : 0;
+  const int lane = threadIdx.x & 31;
+  const Geometry &g = a.geo;
+  const long long BHW = g.BHW;
+  const long long gc = seg.x;
+  const uint4 *rec = a.srec + seg.y;
+  const int n = (int)seg.z;
+  if constexpr (kFast != 0) {  // a 16-lane group (the upper half-warp idles; ptxas rejects the
+                               // 32-lane colour variant: C7600)
+    fuse_cell_group<kDebug, kFast, 16>(a, lane < 16 ? seg : make_uint4(0u, 0u, 0u, 0u), cnt);
+    return;
+  }
+  const float *vals = reinterpret_cast<const float *>(a.st.words);
+  const float h = __ldcg(vals + (long long)kWordElev * BHW + gc), s2 = __ldcg(vals + (long long)kWordVar * BHW + gc);
+  const uint8_t vd0 = __ldcg(a.st.flags + (long long)kFlagValid * BHW + gc);
+  float th[NCH > 0 ? NCH : 1];
+  uint8_t ob = 0;
+  const float tau2 = a.np.tau2;
+  double P = 0.0, S = 0.0, X = 0.0;
+  unsigned nin = 0u, nout = 0u, cr = 0u, cg = 0u, cb = 0u, na = 0u;
+  uint4 q = make_uint4(0u, 0u, 0u, 0u);
+  if (lane < n) q = __ldcg(rec + lane);
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int m_ = n - b0 < 32 ? n - b0 : 32;
+    const bool act = lane < m_;
+    uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+    if (b0 + 32 + lane < n) nq = __ldcg(rec + b0 + 32 + lane);
+    const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
+    const float d = z - h;  // a7 (D10)
+    const bool outl = act && d * d > tau2 * (s2 + v);
+    const bool inl = act && !outl;
+    float w = 0.0f, zw = 0.0f;
+    if (inl) {
+      w = 1.0f / v;
+      zw = z * w;
+    }
+    const unsigned im = __ballot_sync(0xffffffffu, inl);
+    nin += __popc(im);
+    nout += __popc(__ballot_sync(0xffffffffu, outl));
+    for (int j = 0; j < m_; ++j) {  // input order
+      const float wj = __shfl_sync(0xffffffffu, w, j), zj = __shfl_sync(0xffffffffu, zw, j);
+      if (im >> j & 1u) {
+        P += (double)wj;
+        S += (double)zj;
       }
     }
     if (kDebug && act) a.dbg_code[__ldcg(a.sridx + seg.y + b0 + lane)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
@@ -389,27 +473,34 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
   }
 }
 
-template <bool kDebug, int kFast>
-__global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ PassArgs a) {
+// kPart 0: the short cells (a thread each); kPart 1: long cells (16 lanes each), then mid-size
+// ones (8 lanes each).  Two kernels, so that the common short-cell kernel keeps few registers.
+template <bool kDebug, int kFast, int kPart>
+__global__ void __launch_bounds__(kFuseThreads, kPart == 0 ? 8 : 4) k_fuse(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   pdl_wait();
   pdl_trigger();
   __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const unsigned nseg = *(volatile unsigned *)&a.ctl->n_seg, nlong = *(volatile unsigned *)&a.ctl->n_lseg;
-  // long cells first (a warp each), then the short ones (a thread each)
-  const unsigned gw = (blockIdx.x * kFuseThreads + threadIdx.x) >> 5, nw = gridDim.x * (kFuseThreads / 32);
-  for (unsigned s = gw; s < nlong; s += nw) fuse_cell_warp<kDebug, kFast>(a, __ldcg(a.segs + (a.seg_cap - 1 - s)), cnt);
-  const unsigned step = gridDim.x * kFuseThreads;
-  unsigned s = blockIdx.x * kFuseThreads + threadIdx.x;
-  if (s < nseg) {  // software pipeline: the next cell's loads in flight while this one fuses
-    CellIn<kFast> cur, nxt;
-    load_cell<kFast>(a, s, cur);
-    for (; s < nseg; s += step) {
-      if (s + step < nseg) load_cell<kFast>(a, s + step, nxt);
-      fuse_cell<kDebug, kFast>(a, cur, cnt);
-      cur = nxt;
+  if constexpr (kPart == 1) {
+    const unsigned nlong = *(volatile unsigned *)&a.ctl->n_lseg, nmid = *(volatile unsigned *)&a.ctl->n_mseg;
+    const unsigned gw = (blockIdx.x * kFuseThreads + threadIdx.x) >> 5, nw = gridDim.x * (kFuseThreads / 32);
+    for (unsigned s = gw; s < nlong; s += nw) fuse_cell_warp<kDebug, kFast>(a, __ldcg(a.segs + (a.seg_cap - 1 - s)), cnt);
+    if constexpr (kFast != 0) {
+      const unsigned grp = (blockIdx.x * kFuseThreads + threadIdx.x) >> 3, ngrp = gridDim.x * (kFuseThreads / 8);
+      for (unsigned s0 = grp & ~3u; s0 < nmid; s0 += ngrp) {  // warp-uniform trip count
+        const unsigned s = s0 + (grp & 3u);
+        const uint4 sg = s < nmid ? __ldcg(a.segs + a.seg_cap + s) : make_uint4(0u, 0u, 0u, 0u);
+        fuse_cell_group<kDebug, kFast, 8>(a, sg, cnt);
+      }
+    }
+  } else {
+    const unsigned nseg = *(volatile unsigned *)&a.ctl->n_seg;
+    for (unsigned s = blockIdx.x * kFuseThreads + threadIdx.x; s < nseg; s += gridDim.x * kFuseThreads) {
+      CellIn<kFast> c;
+      load_cell<kFast>(a, __ldcg(a.segs + s), c);
+      fuse_cell<kDebug, kFast>(a, c, cnt);
     }
   }
   flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);

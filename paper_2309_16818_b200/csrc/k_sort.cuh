@@ -43,7 +43,7 @@ template <bool kDebug>
 __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ PassArgs a) {
   constexpr int kW = kSortThreads / 32;
   __shared__ unsigned s_part[kW];
-  __shared__ unsigned s_base[3];  // this band's first record / short segment / long segment
+  __shared__ unsigned s_base[4];  // this band's first record / short / long / mid-size segment
   extern __shared__ __align__(16) unsigned char s_dyn[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geometry &g = a.geo;
@@ -129,32 +129,40 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
   {
     const int cpt = (ncell + kSortThreads - 1) / kSortThreads;
     const int cb = tid * cpt, ce = cb + cpt < ncell ? cb + cpt : ncell;
-    unsigned tot = 0u, ns = 0u, nl = 0u;
+    // fast paths: short cells (<= kShortSeg points) a thread each, mid-size cells (<= kMidSeg)
+    // 8 lanes each, long cells 16 lanes each; generic groups: a thread or a warp
+    const unsigned smax = a.fast ? (unsigned)kShortSeg : (unsigned)kMidSeg, mmax = (unsigned)kMidSeg;
+    unsigned tot = 0u, ns = 0u, nm = 0u, nl = 0u;
     for (int cc = cb; cc < ce; ++cc) {
       const unsigned x = cst_s[cc];
       tot += x;
-      ns += x != 0u && x <= (unsigned)kShortSeg;
-      nl += x > (unsigned)kShortSeg;
+      ns += x != 0u && x <= smax;
+      nm += x > smax && x <= mmax;
+      nl += x > mmax;
     }
-    unsigned K2, nshort, nlong;
+    unsigned K2, nsm, nlong;
     unsigned st = block_excl_scan<kSortThreads>(tot, s_part, &K2);
-    unsigned ss = block_excl_scan<kSortThreads>(ns, s_part, &nshort);
+    const unsigned psm = block_excl_scan<kSortThreads>(ns | (nm << 16), s_part, &nsm);
     unsigned sl = block_excl_scan<kSortThreads>(nl, s_part, &nlong);
+    const unsigned nshort = nsm & 0xffffu, nmid = nsm >> 16;
     if (tid == 0) {
       s_base[0] = K ? atomicAdd(&a.ctl->n_rec, K) : 0u;
       s_base[1] = nshort ? atomicAdd(&a.ctl->n_seg, nshort) : 0u;
       s_base[2] = nlong ? atomicAdd(&a.ctl->n_lseg, nlong) : 0u;
+      s_base[3] = nmid ? atomicAdd(&a.ctl->n_mseg, nmid) : 0u;
     }
     __syncthreads();
-    const unsigned rbase = s_base[0], sbase = s_base[1], lbase = s_base[2];
-    // short segments from the front of the list, long ones from its back (k_fuse: a thread per
-    // short cell, a warp per long one)
+    const unsigned rbase = s_base[0], lbase = s_base[2];
+    unsigned ss = s_base[1] + (psm & 0xffffu), sm = a.seg_cap + s_base[3] + (psm >> 16);
+    // short segments from the front of the list, long ones from its back, mid-size ones in
+    // its second half
     for (int cc = cb; cc < ce; ++cc) {
       const unsigned x = cst_s[cc];
       cst_s[cc] = rbase + st;
       if (x) {
         const uint4 sgm = make_uint4((unsigned)(gb + cc), rbase + st, x, 0u);
-        if (x <= (unsigned)kShortSeg) a.segs[sbase + ss++] = sgm;
+        if (x <= smax) a.segs[ss++] = sgm;
+        else if (x <= mmax) a.segs[sm++] = sgm;
         else a.segs[a.seg_cap - 1 - (lbase + sl++)] = sgm;
       }
       st += x;

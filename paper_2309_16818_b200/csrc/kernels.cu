@@ -90,18 +90,25 @@ cudaError_t launch_sort(const PassArgs &a, cudaStream_t s) {
   return a.dbg_cell ? launch_sort_t<true>(a, smem, s) : launch_sort_t<false>(a, smem, s);
 }
 
-template <bool kDebug, int kFast>
-static cudaError_t launch_fuse_t(const PassArgs &a, cudaStream_t s) {
+template <bool kDebug, int kFast, int kPart>
+static cudaError_t launch_fuse_p(const PassArgs &a, cudaStream_t s) {
   static int grid[64] = {};  // resident CTAs per device (persistent grid)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!grid[dev & 63]) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fuse<kDebug, kFast>, kFuseThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fuse<kDebug, kFast, kPart>, kFuseThreads, 0);
     grid[dev & 63] = std::max(1, sms) * std::max(1, per);
   }
-  return launch_pdl(k_fuse<kDebug, kFast>, grid[dev & 63], 0, s, a, kFuseThreads);
+  return launch_pdl(k_fuse<kDebug, kFast, kPart>, grid[dev & 63], 0, s, a, kFuseThreads);
+}
+
+template <bool kDebug, int kFast>
+static cudaError_t launch_fuse_t(const PassArgs &a, cudaStream_t s) {
+  cudaError_t e = launch_fuse_p<kDebug, kFast, 1>(a, s);  // long and mid-size cells
+  if (e != cudaSuccess) return e;
+  return launch_fuse_p<kDebug, kFast, 0>(a, s);  // short cells
 }
 
 cudaError_t launch_fuse(const PassArgs &a, cudaStream_t s) {

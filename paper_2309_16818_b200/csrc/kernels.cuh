@@ -12,12 +12,13 @@ constexpr int kTile = kBinThreads * kBinPerThread;  // 2048
 constexpr int kMaxBands = 2048;         // bands per map (k_bin's per-warp band counters)
 // k_sort: one CTA per (map, band); the band's records counting-sorted kSortCap at a time
 constexpr int kSortThreads = 128;
-constexpr int kSortCap = 2048;          // records ranked per window (shared memory)
+constexpr int kSortCap = 1024;          // records ranked per window (shared memory)
 constexpr int kSortChunk = 2048;        // band sizing: records expected per band
 constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in shared memory)
 // k_fuse: persistent grid-stride over the touched cells, one thread each
 constexpr int kFuseThreads = 128;
-constexpr int kShortSeg = 32;          // cells of at most this many points: a thread each; longer: a warp
+constexpr int kShortSeg = 8;           // cells of at most this many points: a thread each
+constexpr int kMidSeg = 64;            // at most this many: 8 lanes each (fast paths); longer: 16 lanes / a warp
 constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 
@@ -25,7 +26,7 @@ constexpr int kInlineMaps = 128;        // maps whose frames travel in the kerne
 constexpr int kStatSlots = 64;  // CTAs add their counters to slot blockIdx % 64 (no hot address)
 struct Control {  // two epochs: a point input adds to stats[epoch] and clears stats[epoch ^ 1]
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
-  unsigned n_rec, n_seg, n_lseg;               // this call's sorted records, short / long segments (k_sort)
+  unsigned n_rec, n_seg, n_lseg, n_mseg;       // this call's sorted records, short / long / mid segments (k_sort)
 };
 
 // reset description shared by k_band (lazy strips) and k_shift
@@ -61,7 +62,8 @@ struct PassArgs {
   uint4 *srec;                 // records sorted by cell, input order within a cell (k_sort -> k_fuse)
   unsigned *sridx;             // their point indices (debug outputs only)
   uint4 *segs;                 // one per touched cell: {m * HW + cell, first sorted record, count, 0};
-                               // short cells from the front, long cells from the back
+                               // short cells from the front, long cells from the back,
+                               // mid-size cells from seg_cap on
   unsigned seg_cap;
   int fast;                    // 1 = one colour group, 2 = one 1-channel average group (float4
                                // points), 3 = no group bound (height only), 0 = generic

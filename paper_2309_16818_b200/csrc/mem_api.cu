@@ -18,7 +18,7 @@
 using namespace memk;
 
 #ifndef MEM_BAND_RECS
-#define MEM_BAND_RECS 2048  // records aimed at per band (k_sort)
+#define MEM_BAND_RECS 768  // records aimed at per band (k_sort)
 #endif
 
 namespace {
@@ -774,7 +774,7 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   const size_t nseg = std::min(nrec, (size_t)B * cells);
   if (grow(&m->recs, &m->recs_cap, sizeof(uint4) * nrec, m->stream) != MEM_OK ||
       grow(&m->srec, &m->srec_cap, sizeof(uint4) * nrec, m->stream) != MEM_OK ||
-      grow(&m->segs, &m->segs_cap, sizeof(uint4) * nseg, m->stream) != MEM_OK ||
+      grow(&m->segs, &m->segs_cap, 2 * sizeof(uint4) * nseg, m->stream) != MEM_OK ||
       grow(&m->tinfo, &m->tinfo_cap, sizeof(unsigned) * (size_t)std::max(1, tiles) * a.nbands, m->stream) != MEM_OK ||
       (dbg && (grow(&m->ridx, &m->ridx_cap, sizeof(unsigned) * nrec, m->stream) != MEM_OK ||
                grow(&m->sridx, &m->sridx_cap, sizeof(unsigned) * nrec, m->stream) != MEM_OK)))
