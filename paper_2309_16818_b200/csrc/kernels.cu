@@ -26,13 +26,23 @@
 #ifndef MEM_OCC_BATCH
 #define MEM_OCC_BATCH 4  // occlusion walk: intermediate cells whose loads are issued together
 #endif
+#ifndef MEM_PAIR_MIN
+#define MEM_PAIR_MIN 4  // colour RED path: pair lanes of the same cell when >= this many repeat
+#endif
+#ifndef MEM_FULL_ITEMS
+#define MEM_FULL_ITEMS 1  // k_points: a variant of the item body without per-lane bounds for full items
+#endif
+
 namespace memk {
 
 #include "dev_common.cuh"
 #include "point_pass.cuh"
 #include "k_bin.cuh"
+#include "k_red.cuh"
 #include "k_sort.cuh"
 #include "k_fuse.cuh"
+#include "k_cells.cuh"
+#include "k_smap.cuh"
 #include "k_route.cuh"
 #include "k_post.cuh"
 #include "k_image.cuh"
@@ -119,6 +129,65 @@ cudaError_t launch_fuse(const PassArgs &a, cudaStream_t s) {
     case 3: return dbg ? launch_fuse_t<true, 3>(a, s) : launch_fuse_t<false, 3>(a, s);
     default: return dbg ? launch_fuse_t<true, 0>(a, s) : launch_fuse_t<false, 0>(a, s);
   }
+}
+
+// the RED path (k_points, k_cells, k_refold): persistent grids sized once per device
+template <class K>
+static int resident_grid(K kernel, int threads, int slot) {
+  static int grid[64][16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &gd = grid[dev & 63][slot];
+  if (!gd) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+    gd = std::max(1, sms) * std::max(1, per);
+  }
+  return gd;
+}
+
+template <bool kDebug, int kFast>
+static cudaError_t launch_points_t(const PassArgs &a, cudaStream_t s) {
+  const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1]) ;
+  int g = resident_grid(k_points<kDebug, kFast>, kThreads, kFast + (kDebug ? 3 : 0));
+  if (items > 0) g = (int)std::max(1LL, std::min<long long>(g, (items + 7) / 8));
+  return launch_pdl(k_points<kDebug, kFast>, g, 0, s, a, kThreads);
+}
+
+cudaError_t launch_points(const PassArgs &a, cudaStream_t s) {
+  const bool dbg = a.dbg_cell != nullptr;
+  const int f = a.fast == 3 ? 0 : a.fast;
+  if (f == 1) return dbg ? launch_points_t<true, 1>(a, s) : launch_points_t<false, 1>(a, s);
+  if (f == 2) return dbg ? launch_points_t<true, 2>(a, s) : launch_points_t<false, 2>(a, s);
+  return dbg ? launch_points_t<true, 0>(a, s) : launch_points_t<false, 0>(a, s);
+}
+
+template <int kFast>
+static cudaError_t launch_cells_t(const PassArgs &a, cudaStream_t s) {
+  const long long chunks = (long long)a.n_maps * ((a.cell_hi - a.cell_lo + kChunk - 1) / kChunk);
+  const int g = (int)std::max(1LL, std::min<long long>(resident_grid(k_cells<kFast>, kThreads, 6 + kFast),
+                                                       (chunks + 7) / 8));
+  cudaError_t e = launch_pdl(k_cells<kFast>, g, 0, s, a, kThreads);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_refold<kFast>, 148, 0, s, a, kThreads);
+}
+
+cudaError_t launch_cells(const PassArgs &a, cudaStream_t s) {
+  const int f = a.fast == 3 ? 0 : a.fast;
+  if (f == 1) return launch_cells_t<1>(a, s);
+  if (f == 2) return launch_cells_t<2>(a, s);
+  return launch_cells_t<0>(a, s);
+}
+
+cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s) {
+  // the opt-in shared-memory size is a per-device function attribute: set it for the current
+  // device on every launch (a host-side call; maps may live on different devices)
+  const bool dbg = a.dbg_cell != nullptr;
+  auto k = dbg ? (a.fast == 1 ? k_smap<true, 1> : k_smap<true, 2>) : (a.fast == 1 ? k_smap<false, 1> : k_smap<false, 2>);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k, grid, smem, s, a, kSmapThreads);
 }
 
 cudaError_t launch_post(const PostArgs &a, cudaStream_t s) {

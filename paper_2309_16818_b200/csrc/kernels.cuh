@@ -21,12 +21,16 @@ constexpr int kShortSeg = 8;           // cells of at most this many points: a t
 constexpr int kMidSeg = 64;            // at most this many: 8 lanes each (fast paths); longer: 16 lanes / a warp
 constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
+// k_points: persistent grid-stride over 128-point warp-items (4 points per lane)
+constexpr int kWarpPtsPerLane = 4;
+constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
 
 // Control block of one point input (zeroed by one cudaMemsetAsync per call).
 constexpr int kStatSlots = 64;  // CTAs add their counters to slot blockIdx % 64 (no hot address)
 struct Control {  // two epochs: a point input adds to stats[epoch] and clears stats[epoch ^ 1]
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
   unsigned n_rec, n_seg, n_lseg, n_mseg;       // this call's sorted records, short / long / mid segments (k_sort)
+  unsigned n_fb;                               // cells k_cells could not certify (k_refold)
 };
 
 // reset description shared by k_band (lazy strips) and k_shift
@@ -50,6 +54,15 @@ struct PassArgs {
   const PointFrame *frames;
   const long long *offsets;
   const int *tstart;
+  const int *pstart;           // k_points: prefix sums of 128-point warp-items per map (staged)
+  int m0, m1;                  // k_points / k_smap: maps [m0, m1) = all maps of the call
+  int smap_maxpts;             // k_smap: points of the largest map of the call (shared memory layout)
+  int p_uniform;               // > 0: every map has exactly this many warp-items
+  double inv_p_uniform;
+  unsigned long long *cnt;     // RED path scratch [n_maps][HW]: count word
+  unsigned long long *rec;     // [n_maps][HW][4]: P, S, group words
+  unsigned *cert;              // [n_maps][HW][4]: certificates {~min, max} of |z/v| and |channel|
+  long long *fb;               // cells k_cells could not certify (m * HW + cell), for k_refold
   int t_uniform;               // > 0: every map has exactly this many tiles
   double inv_t_uniform;        // 1.0 / t_uniform (divmod_fast)
   int tmax;                    // most tiles of one map (k_band's shared memory)
@@ -83,6 +96,7 @@ struct PassArgs {
   PointFrame fi[kInlineMaps];
   long long offi[kInlineMaps + 1];
   int tsi[kInlineMaps + 1];
+  int psi[kInlineMaps + 1];
 };
 
 struct ImageArgs {
@@ -154,6 +168,11 @@ cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long l
 cudaError_t launch_bin(const PassArgs &a, int tiles, cudaStream_t s);
 cudaError_t launch_sort(const PassArgs &a, cudaStream_t s);
 cudaError_t launch_fuse(const PassArgs &a, cudaStream_t s);
+cudaError_t launch_points(const PassArgs &a, cudaStream_t s);
+size_t smap_smem_bytes(int HW, long long max_pts);
+bool smap_eligible(int HW, long long max_pts);
+cudaError_t launch_smap(const PassArgs &a, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_cells(const PassArgs &a, cudaStream_t s);
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s);
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 // PCA readout: moments of one map's feature group, then projections

@@ -89,6 +89,8 @@ struct mem_map {
   // staging
   void *dparam = nullptr;
   size_t dparam_cap = 0;
+  void *dparam2 = nullptr;  // k_points item prefix sums of large batches
+  size_t dparam2_cap = 0;
   PinnedRing pin;
   unsigned *seen_rec = nullptr;  // pinned: in-window records of a recent point input (band sizing)
   void *din = nullptr;
@@ -109,6 +111,9 @@ struct mem_map {
   // debug point indices
   void *recs = nullptr, *tinfo = nullptr, *ridx = nullptr, *srec = nullptr, *sridx = nullptr, *segs = nullptr;
   size_t recs_cap = 0, tinfo_cap = 0, ridx_cap = 0, srec_cap = 0, sridx_cap = 0, segs_cap = 0;
+  // RED path scratch (zeroed once, re-zeroed by k_cells): count words, records, certificates, fallback list
+  void *rcnt_s = nullptr, *rrec_s = nullptr, *rcert_s = nullptr, *rfb_s = nullptr;
+  size_t red_cells = 0;  // cells the RED scratch holds
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
   int transport = 0, rank = 0, nranks = 1;
@@ -483,6 +488,7 @@ void free_map(mem_map *m) {
   cudaFree(m->ring);
   cudaFree(m->bin_t);
   cudaFree(m->dparam);
+  cudaFree(m->dparam2);
   cudaFree(m->din);
   cudaFree(m->dout);
   cudaFree(m->pca_buf);
@@ -492,6 +498,10 @@ void free_map(mem_map *m) {
   cudaFree(m->srec);
   cudaFree(m->sridx);
   cudaFree(m->segs);
+  cudaFree(m->rcnt_s);
+  cudaFree(m->rrec_s);
+  cudaFree(m->rcert_s);
+  cudaFree(m->rfb_s);
   cudaFree(m->rsrc);
   cudaFree(m->rtile);
   cudaFree(m->odbg_cell);
@@ -740,11 +750,100 @@ static mem_status shard_gather_all(mem_map *m) {
   return MEM_OK;
 }
 
+// P = sum 1/v is certified exact for every cell of a call at once: its terms lie in
+// [fl(1/v_max), fl(1/v_min)], v_min / v_max from the range bounds of r2, and the certificate
+// e_max - e_min + ceil(log2(max points per cell)) <= 29 (k_red.cuh) holds for all cells
+static bool p_certified(const PassArgs &a, long long max_n) {
+  if (!(a.r2lo <= a.r2hi)) return true;  // no point passes the range filter
+  const float vlo = a.np.a + a.np.b * a.r2lo, vhi = a.np.a + a.np.b * a.r2hi;
+  if (!std::isfinite(vhi) || !(vlo > 0.0f)) return false;
+  const float wmax = 1.0f / vlo, wmin = 1.0f / vhi;
+  uint32_t bmax, bmin;
+  memcpy(&bmax, &wmax, 4);
+  memcpy(&bmin, &wmin, 4);
+  const int emax = std::max<int>((bmax >> 23) & 255, 1), emin = std::max<int>((bmin >> 23) & 255, 1);
+  int lg = 0;
+  while ((1LL << lg) < max_n) ++lg;
+  return emax - emin + lg <= 29;
+}
+
+// the RED path for the fast groups: k_points (certified REDs), k_cells (fuse
+// the certified cells, list the others), k_refold (the others, in input order)
+static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offsets, long long total) {
+  const int B = a.n_maps;
+  const size_t cells = (size_t)B * m->H * m->W;
+  if (cells > m->red_cells) {
+    CU(cudaStreamSynchronize(m->stream));
+    cudaFree(m->rcnt_s);
+    cudaFree(m->rrec_s);
+    cudaFree(m->rcert_s);
+    cudaFree(m->rfb_s);
+    m->rcnt_s = m->rrec_s = m->rcert_s = m->rfb_s = nullptr;
+    m->red_cells = 0;
+    if (cudaMalloc(&m->rcnt_s, 8 * cells) != cudaSuccess || cudaMalloc(&m->rrec_s, 32 * cells) != cudaSuccess ||
+        cudaMalloc(&m->rcert_s, 16 * cells) != cudaSuccess || cudaMalloc(&m->rfb_s, 8 * cells) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MEM_ENOMEM, "RED scratch (%zu cells)", cells);
+    }
+    CU(cudaMemsetAsync(m->rcnt_s, 0, 8 * cells, m->stream));
+    CU(cudaMemsetAsync(m->rrec_s, 0, 32 * cells, m->stream));
+    CU(cudaMemsetAsync(m->rcert_s, 0, 16 * cells, m->stream));
+    m->red_cells = cells;
+  }
+  a.cnt = reinterpret_cast<unsigned long long *>(m->rcnt_s);
+  a.rec = reinterpret_cast<unsigned long long *>(m->rrec_s);
+  a.cert = reinterpret_cast<unsigned *>(m->rcert_s);
+  a.fb = reinterpret_cast<long long *>(m->rfb_s);
+  a.st = m->st;
+  a.m0 = 0;
+  a.m1 = B;
+  // warp-items of 128 points per map (inline prefix sums; staged ones ride in a second blob)
+  std::vector<int> ps(B + 1, 0);
+  for (int i = 0; i < B; ++i) {
+    const long long ni = offsets ? offsets[i + 1] - offsets[i] : total;
+    ps[i + 1] = ps[i] + (int)((ni + kWarpPoints - 1) / kWarpPoints);
+  }
+  a.p_uniform = ps[1] - ps[0];
+  for (int i = 1; i < B && a.p_uniform > 0; ++i)
+    if (ps[i + 1] - ps[i] != a.p_uniform) a.p_uniform = 0;
+  a.inv_p_uniform = a.p_uniform > 0 ? 1.0 / (double)a.p_uniform : 0.0;
+  if (B <= kInlineMaps) {
+    for (int i = 0; i <= B; ++i) a.psi[i] = ps[i];
+    a.pstart = nullptr;
+  } else {
+    void *d = nullptr;
+    if (grow(&m->dparam2, &m->dparam2_cap, sizeof(int) * (B + 1), m->stream) != MEM_OK) return MEM_ENOMEM;
+    CU(cudaMemcpyAsync(m->dparam2, ps.data(), sizeof(int) * (B + 1), cudaMemcpyHostToDevice, m->stream));
+    CU(cudaStreamSynchronize(m->stream));  // ps is a local vector
+    d = m->dparam2;
+    a.pstart = reinterpret_cast<const int *>(d);
+  }
+  if (ps[B] > 0) TIMED(MEM_STAGE_POINT, launch_points(a, m->stream));
+  TIMED(MEM_STAGE_CELL, launch_cells(a, m->stream));
+  return MEM_OK;
+}
+
 // tiles of every map, bands of the physical cells [cell_lo, cell_hi), buffers; then k_bin and
 // k_band.  `a` carries the frames, the point offsets and the tile prefix sums
 // (inline or staged); `tiles` = all tiles of the call, `tmax` = most tiles of one map.
-static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax, long long max_n) {
+static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax, long long max_n,
+                              const int64_t *offsets = nullptr, long long total = 0) {
   const int B = a.n_maps;
+  // batches of small maps with one colour / 1-channel average group (C5a): one CTA per map
+  // sorts its points by cell in shared memory and sums them in input order (k_smap)
+  if ((a.fast == 1 || a.fast == 2) && a.vec4 && B >= 64 && a.cell_lo == 0 && a.cell_hi == m->H * m->W &&
+      smap_eligible(m->H * m->W, max_n)) {
+    a.st = m->st;
+    a.m0 = 0;
+    a.m1 = B;
+    a.smap_maxpts = (int)max_n;
+    const int grid = std::max(1, std::min(B, m->sms));
+    TIMED(MEM_STAGE_POINT, launch_smap(a, grid, smap_smem_bytes(m->H * m->W, max_n), m->stream));
+    return MEM_OK;
+  }
+  // the fast groups (one colour / one 1-channel average group on float4 points, or height
+  // only) take the RED path when the call's P sums are certified; everything else sorts
+  if (a.fast != 0 && p_certified(a, max_n)) return fuse_points_red(m, a, offsets, total);
   const int cells = a.cell_hi - a.cell_lo;
   if (tmax > kMaxTilesPerMap)
     return fail(MEM_EINVAL, "a map takes at most %lld points per call", (long long)kMaxTilesPerMap * kTile);
@@ -844,7 +943,7 @@ static mem_status owner_pass(mem_map *m, const float *pts, long long n) {
     b.dbg_cell = nullptr;
     b.dbg_code = nullptr;
   }
-  return fuse_points(m, b, tiles, tmax, n);
+  return fuse_points(m, b, tiles, tmax, n, nullptr, n);
 }
 
 static mem_status grow_floats(float **buf, size_t *cap_bytes, size_t need_floats, cudaStream_t s) {
@@ -1101,7 +1200,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.cell_hi = m->band_lo + m->band_n;
   }
   m->pending = false;
-  return fuse_points(m, a, tstart[B], tmax, max_n);
+  return fuse_points(m, a, tstart[B], tmax, max_n, offsets, total);
 }
 
 mem_status mem_input_pointcloud(mem_map *m, const float *pts, int64_t n, int stride, const mem_binding *bind,
