@@ -14,8 +14,11 @@ def is_int_layer(name):
     return name == "valid" or name.endswith("_observed") or name.endswith("_label")
 
 
-def compare_layers(gpu_map, ora_map, names=None, where=""):
-    """returns dict name -> max abs diff; asserts the parity bar."""
+def compare_layers(gpu_map, ora_map, names=None, where="", exact=True):
+    """returns dict name -> max abs diff; asserts the parity bar.  With exact=True (the
+    default) every layer must also equal the oracle BIT FOR BIT: every point path sums in the
+    oracle's order or in certified-exact arithmetic (reading D39), and the image
+    path evaluates the oracle's expressions in its order."""
     names = names or gpu_map.layer_names()
     out = {}
     for nm in names:
@@ -34,6 +37,9 @@ def compare_layers(gpu_map, ora_map, names=None, where=""):
             tol = ATOL + RTOL * np.abs(oo)
             bad = d > tol
             assert not bad.any(), f"{where}{nm}: {bad.sum()} values beyond tolerance, max diff {d.max()}"
+            if exact:
+                neq = gg != oo
+                assert not neq.any(), f"{where}{nm}: {neq.sum()} values differ from the oracle in the last bits (max {d.max()})"
             out[nm] = float(d.max()) if d.size else 0.0
     return out
 
