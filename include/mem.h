@@ -128,12 +128,16 @@ enum { MEM_CODE_INLIER = 0, MEM_CODE_OUTLIER = 1, MEM_CODE_NONFINITE = 2, MEM_CO
        MEM_CODE_HEIGHT = 4, MEM_CODE_OOB = 5 };
 
 #define MEM_FLAG_DEBUG_POINTS 1u /* record per-point (cell, code) of the last point input */
-/* Deterministic small maps: a point input of a map with <= 16384 cells and <= 65535 points per
- * map, one colour or one 1-channel average group and float4 points is fused by a sort-by-cell
- * kernel (one CTA per map) that sums every cell's points in input order with the oracle's
- * formulas -- bit-identical to the CPU oracle and from run to run (the default path sums with
- * fp64 atomics in arbitrary order, equal to ~1e-16).  Other inputs are unaffected. */
+/* Every point input is deterministic and performs the oracle's arithmetic (DESIGN.md reading
+ * D39): the per-cell sums are either added in input order (sort-by-cell paths) or with
+ * fp64 atomics whose exactness is certified per cell (any order gives the exact sum, hence the
+ * sequential one), uncertified cells being recomputed in input order.  The flag is kept for
+ * compatibility and has no effect. */
 #define MEM_FLAG_DETERMINISTIC 2u
+/* Validation: always fuse point inputs by the sort-by-cell pipeline (k_bin, k_sort, k_fuse)
+ * instead of the certified-atomic path or the small-map kernel; results are bit-identical
+ * either way (tests/test_full_size_gpu.py checks it). */
+#define MEM_FLAG_FUSE_SORTED 4u
 
 /* ---- lifetime -------------------------------------------------------------------- */
 

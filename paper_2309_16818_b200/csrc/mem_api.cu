@@ -831,7 +831,8 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   const int B = a.n_maps;
   // batches of small maps with one colour / 1-channel average group (C5a): one CTA per map
   // sorts its points by cell in shared memory and sums them in input order (k_smap)
-  if ((a.fast == 1 || a.fast == 2) && a.vec4 && B >= 64 && a.cell_lo == 0 && a.cell_hi == m->H * m->W &&
+  const bool sorted = (m->flags & MEM_FLAG_FUSE_SORTED) != 0;
+  if (!sorted && (a.fast == 1 || a.fast == 2) && a.vec4 && B >= 64 && a.cell_lo == 0 && a.cell_hi == m->H * m->W &&
       smap_eligible(m->H * m->W, max_n)) {
     a.st = m->st;
     a.m0 = 0;
@@ -843,7 +844,7 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   }
   // the fast groups (one colour / one 1-channel average group on float4 points, or height
   // only) take the RED path when the call's P sums are certified; everything else sorts
-  if (a.fast != 0 && p_certified(a, max_n)) return fuse_points_red(m, a, offsets, total);
+  if (!sorted && a.fast != 0 && p_certified(a, max_n)) return fuse_points_red(m, a, offsets, total);
   const int cells = a.cell_hi - a.cell_lo;
   if (tmax > kMaxTilesPerMap)
     return fail(MEM_EINVAL, "a map takes at most %lld points per call", (long long)kMaxTilesPerMap * kTile);

@@ -24,6 +24,7 @@ MEM_AVERAGE, MEM_GAUSSIAN, MEM_CLASS_AVERAGE, MEM_CLASS_BAYESIAN, MEM_CLASS_MAX,
 CODE_INLIER, CODE_OUTLIER, CODE_NONFINITE, CODE_RANGE, CODE_HEIGHT, CODE_OOB = range(6)
 MEM_FLAG_DEBUG_POINTS = 1
 MEM_FLAG_DETERMINISTIC = 2
+MEM_FLAG_FUSE_SORTED = 4
 RULES = dict(average=MEM_AVERAGE, gaussian=MEM_GAUSSIAN, class_average=MEM_CLASS_AVERAGE,
              class_bayesian=MEM_CLASS_BAYESIAN, class_max=MEM_CLASS_MAX, color=MEM_COLOR)
 STAT_NAMES = ["n_input", "n_nonfinite", "n_range", "n_height", "n_oob", "n_inlier", "n_outlier", "n_cells_touched"]
@@ -392,9 +393,10 @@ class Map:
     """Owning wrapper of a mem_map handle (one map, or n_maps batched maps)."""
 
     def __init__(self, resolution, rows, cols, groups=(), n_maps=1, debug_points=False, stream=None, _handle=None,
-                 deterministic=False):
+                 deterministic=False, fuse_sorted=False):
         self.rows, self.cols, self.res, self.n_maps = rows, cols, resolution, n_maps
-        flags = (MEM_FLAG_DEBUG_POINTS if debug_points else 0) | (MEM_FLAG_DETERMINISTIC if deterministic else 0)
+        flags = ((MEM_FLAG_DEBUG_POINTS if debug_points else 0) | (MEM_FLAG_DETERMINISTIC if deterministic else 0)
+                 | (MEM_FLAG_FUSE_SORTED if fuse_sorted else 0))
         self.h = _handle if _handle is not None else mem_create(resolution, rows, cols, groups, flags, stream, n_maps)
         self._last_n = 0
 
