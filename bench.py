@@ -147,36 +147,54 @@ def traffic_record():
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def oracle_rate(frames, budget_s=12.0, threads=None, frames_per_map=None):
-    """the oracle as it stands, one map per host thread (ctypes releases the GIL)."""
-    from oracle import oracle as O
-    O.lib()
-    threads = threads or os.cpu_count() or 1
-    c = S.C2
-    done = [0] * threads
+class OracleFleet:
+    """host threads, each owning ONE persistent oracle C2 map (ctypes releases the GIL): the
+    oracle as it stands, in steady state (every frame fuses into an already built map)."""
 
-    def work(k):
-        m = O.OracleMap(c["res"], c["rows"], c["cols"], c2_groups())
+    def __init__(self, frames, threads=None):
+        from oracle import oracle as O
+        O.lib()
+        self.frames = frames
+        self.threads = threads or os.cpu_count() or 1
+        c = S.C2
+        self.maps = [O.OracleMap(c["res"], c["rows"], c["cols"], c2_groups()) for _ in range(self.threads)]
+        self.next = [k for k in range(self.threads)]
+
+    def run(self, frames_per_map=None, budget_s=None):
+        """every thread fuses frames_per_map frames (or for budget_s seconds) into its map;
+        returns (frames fused, seconds)."""
+        c = S.C2
+        done = [0] * self.threads
+
+        def work(k):
+            t0 = time.perf_counter()
+            i = 0
+            while True:
+                fr = self.frames[self.next[k] % POOL]
+                self.next[k] += 1
+                self.maps[k].move_to(*fr["move"])
+                self.maps[k].input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
+                i += 1
+                if (frames_per_map and i >= frames_per_map) or (budget_s and time.perf_counter() - t0 > budget_s):
+                    break
+            done[k] = i
+
         t0 = time.perf_counter()
-        i = 0
-        while True:
-            fr = frames[(i + k) % POOL]
-            m.move_to(*fr["move"])
-            m.input_pointcloud(fr["points"], [(0, 1, 0)], fr["R"], fr["t"], c["noise"])
-            i += 1
-            if (frames_per_map and i >= frames_per_map) or (not frames_per_map and time.perf_counter() - t0 > budget_s):
-                break
-        done[k] = i
+        ts = [threading.Thread(target=work, args=(k,)) for k in range(self.threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return sum(done), time.perf_counter() - t0
 
-    t0 = time.perf_counter()
-    ts = [threading.Thread(target=work, args=(k,)) for k in range(threads)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    dt = time.perf_counter() - t0
-    n_frames = sum(done)
-    return n_frames * 131072 / dt, n_frames / dt, threads, n_frames, dt
+
+def oracle_rate(frames, budget_s=12.0, threads=None):
+    """the oracle's steady-state C2 rate on the host's cores (one persistent map per thread,
+    one warm-up frame each first)."""
+    fleet = OracleFleet(frames, threads)
+    fleet.run(frames_per_map=1)
+    nf, dt = fleet.run(budget_s=budget_s)
+    return nf * 131072 / dt, nf / dt, fleet.threads, nf, dt
 
 
 # ------------------------------------------------------------------ reference arm
@@ -193,14 +211,16 @@ def run_reference(a):
     if rank != 0:
         return 0
     frames = frame_pool()
-    threads = os.cpu_count() or 1
-    # each step: every host thread fuses one map-frame (a bounded sample of the C2x64 step)
+    fleet = OracleFleet(frames)
+    threads = fleet.threads
+    # each step: every host thread fuses one frame into its own persistent map (a bounded
+    # sample of the C2x64 step: `threads` of its 64 map-frames)
     for _ in range(a.warmup):
-        oracle_rate(frames, threads=threads, frames_per_map=1)
+        fleet.run(frames_per_map=1)
     t0 = time.perf_counter()
     nf = 0
     for _ in range(a.steps):
-        _, _, _, n, _ = oracle_rate(frames, threads=threads, frames_per_map=1)
+        n, _ = fleet.run(frames_per_map=1)
         nf += n
     dt = time.perf_counter() - t0
     pts = nf * 131072 / dt
@@ -212,8 +232,8 @@ def run_reference(a):
         "map_updates_per_s": nf / dt,
         "cpu_baseline": {"value": pts, "unit": "points/s", "cores": threads, "kind": "oracle",
                          "sample": f"each step a bounded sample of the C2x{a.maps} step: {threads} of its "
-                                   f"{a.maps} map-frames (131072 pts each), one per host thread; "
-                                   f"{a.steps} steps"},
+                                   f"{a.maps} map-frames (131072 pts each), one persistent map per host "
+                                   f"thread; {a.steps} steps after {a.warmup} warm-up steps"},
         "e2e": {"value": pts, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -233,6 +253,63 @@ def timed_loop(torch, stream, n, fn):
     e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / n
+
+
+def graph_sequence(torch, M, mp, step_fn, n=10, reps=30):
+    """SPEC.md:518-521 / PAPER.md:410 protocol: an n-frame sequence captured ONCE as a CUDA
+    graph (every launch of the n frames), replayed `reps` times, each replay timed with CUDA
+    events on the capture stream; returns mean and std of the time per frame (us).  The map
+    keeps fusing (each replay applies the same n frames to the evolving state); it is a timing
+    map and is discarded afterwards."""
+    s = torch.cuda.Stream()
+    M.mem_set_stream(mp.h, s)
+    with torch.cuda.stream(s):
+        for i in range(3):
+            step_fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(n):
+            step_fn(i)
+    per = []
+    with torch.cuda.stream(s):  # CUDAGraph.replay launches on the current stream
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1) * 1e3 / n)
+    return {"frames_per_replay": n, "replays": reps, "us_per_frame_mean": float(np.mean(per)),
+            "us_per_frame_std": float(np.std(per)), "us_per_frame_min": float(np.min(per))}
+
+
+def oracle_threads(jobs, threads=None):
+    """runs the callables in `jobs` on `threads` host threads (ctypes releases the GIL);
+    returns the wall seconds and the thread count."""
+    threads = min(threads or os.cpu_count() or 1, len(jobs))
+    nxt = [0]
+    lock = threading.Lock()
+
+    def work():
+        while True:
+            with lock:
+                k = nxt[0]
+                nxt[0] += 1
+            if k >= len(jobs):
+                return
+            jobs[k]()
+
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=work) for _ in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return time.perf_counter() - t0, threads
 
 
 def side_c5a(torch, M, stream, rank, world, steps=20):
@@ -263,7 +340,27 @@ def side_c5a(torch, M, stream, rank, world, steps=20):
 
     ms = timed_loop(torch, stream, steps, step)
     mp.close()
+    cpu = None
+    if rank == 0 and os.environ.get("MEM_BENCH_NO_CPU") != "1":
+        # the oracle on every host core: persistent maps (the 256 generated ones), one frame
+        # each per job, frames 0 then 1 (a bounded sample of the 4096-map step)
+        from oracle import oracle as O
+        O.lib()
+        oras = [O.OracleMap(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])])
+                for _ in range(256)]
+        pts = [fr["points"].reshape(256, P, 4) for fr in pool]
+
+        def job(k, f):
+            return lambda: (oras[k].move_to(*pool[f]["move"][k]),
+                            oras[k].input_pointcloud(pts[f][k], [(0, 1, 0)], pool[f]["R"][k], pool[f]["t"][k], c["noise"]))
+
+        oracle_threads([job(k, 0) for k in range(256)])
+        dt, th = oracle_threads([job(k, 1) for k in range(256)])
+        cpu = {"kind": "oracle", "cores": th, "map_updates_per_s": 256 / dt, "points_per_s": 256 * P / dt,
+               "sample": "256 C5a map-frames (32768 pts each) on all host threads, persistent maps",
+               "projected_ms_per_step_4096_maps": 4096 / (256 / dt) * 1e3}
     return {"workload": f"C5a: 4096 maps 128x128@0.1m x 32768 pts, {mine} maps on this rank", "ms_per_step": ms,
+            "cpu_oracle": cpu,
             "maps_per_rank": mine, "points_per_s_rank": mine * P / (ms * 1e-3),
             "map_updates_per_s_rank": mine / (ms * 1e-3), "scaling": "strong (4096 maps total)"}
 
@@ -302,7 +399,19 @@ def side_c5b(torch, M, stream, rank, world, dist, steps=10):
     mp.profile(False)
     prof = mp.profile_read(reset=True)
     mp.close()
+    cpu = None
+    if rank == 0 and world == 1 and os.environ.get("MEM_BENCH_NO_CPU") != "1":
+        from oracle import oracle as O
+        o = O.OracleMap(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])])
+        for f in range(2):
+            o.move_to(*frames[f]["move"])
+            t0 = time.perf_counter()
+            o.input_pointcloud(frames[f]["points"], [(0, 1, 0)], frames[f]["R"], frames[f]["t"], c["noise"])
+            dt = time.perf_counter() - t0
+        cpu = {"kind": "oracle", "cores": 1, "ms_per_frame": dt * 1e3, "points_per_s": c["points"] / dt,
+               "sample": "the second of two 4M-point frames on one host core"}
     return {"workload": f"C5b: one 2000x2000@0.04m map, {c['points']} pts/frame point-sharded over {world} rank(s)",
+            "cpu_oracle": cpu,
             "ms_per_frame_max_over_ranks": ms, "points_per_s": c["points"] / (ms * 1e-3),
             "stage_ms_rank0": {k: v[0] for k, v in prof.items() if v[1]}, "transport": "NCCL",
             "scaling": "strong (4M points total)"}
@@ -360,7 +469,7 @@ def side_paper_sweep(torch, M, stream, iters=300):
     return out
 
 
-def side_c3_c4(torch, M, stream, frames=2):
+def side_c3_c4(torch, M, stream, frames=10):
     out = {}
     c = S.C3
     fr = [S.c3_frame(f) for f in range(frames)]
@@ -390,6 +499,33 @@ def side_c3_c4(torch, M, stream, frames=2):
     mp.profile(False)
     prof = mp.profile_read(reset=True)
     out["c3"]["stage_ms"] = {k: v[0] for k, v in prof.items() if v[1]}
+    # the SPEC.md:518-521 protocol: the 10-frame sequence as one CUDA graph, 30 replays
+    mg = M.Map(c["res"], c["rows"], c["cols"], groups)
+
+    def g_step(i):
+        f, d = fr[i % frames], dev[i % frames]
+        mg.move_to(*f["move"])
+        for cl, dp in zip(f["clouds"], d["clouds"]):
+            mg.input_pointcloud(dp, [], cl["R"], cl["t"], c["noise"])
+        im = f["image"]
+        mg.input_image(d["img"], binds, im["K"], im["R"], im["t"])
+
+    out["c3"]["graph_10_frames"] = graph_sequence(torch, M, mg, g_step, n=frames, reps=30)
+    mg.close()
+    if os.environ.get("MEM_BENCH_NO_CPU") != "1":  # the oracle on one host core, one frame
+        from oracle import oracle as O
+        o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+        for k in range(2):
+            f = fr[k]
+            t0 = time.perf_counter()
+            o.move_to(*f["move"])
+            for cl in f["clouds"]:
+                o.input_pointcloud(cl["points"], [], cl["R"], cl["t"], c["noise"])
+            im = f["image"]
+            o.input_image(im["img"], binds, im["K"], im["R"], im["t"])
+            dt = time.perf_counter() - t0
+        out["c3"]["cpu_oracle"] = {"kind": "oracle", "cores": 1, "ms_per_frame": dt * 1e3,
+                                   "points_per_s": npts / dt, "sample": "the second of two C3 frames, one host core"}
     # NEXT-3 plugins on the fused C3 map (device outputs)
     o3 = torch.empty((3, c["rows"], c["cols"]), device="cuda")
     t1 = torch.empty((1, c["rows"], c["cols"]), device="cuda")
@@ -434,12 +570,28 @@ def side_c3_c4(torch, M, stream, frames=2):
     out["c4"] = {"workload": "C4: 250x250@0.04m, 64-channel 480x640 feature image, 64 x average + PCA readout",
                  "ms_per_image": ms4, "images_per_s": 1e3 / ms4, "pca_readout_ms_wall": pca_ms,
                  "image_bytes": int(dims[0].numel() * 4)}
+    if os.environ.get("MEM_BENCH_NO_CPU") != "1":  # the oracle on one host core: an image, a PCA readout
+        from oracle import oracle as O
+        o4 = O.OracleMap(c4["res"], c4["rows"], c4["cols"], [dict(name="feat", rule=0, n_channels=c4["d"], w=c4["w"])])
+        o4.move_to(*f0["move"])
+        for cl in f0["clouds"]:
+            o4.input_pointcloud(cl["points"], [], cl["R"], cl["t"], c["noise"])
+        o4.input_image(ims[0]["img"], [(0, c4["d"], 0)], ims[0]["K"], ims[0]["R"], ims[0]["t"])
+        t0 = time.perf_counter()
+        o4.input_image(ims[1]["img"], [(0, c4["d"], 0)], ims[1]["K"], ims[1]["R"], ims[1]["t"])
+        t1 = time.perf_counter()
+        o4.pca_readout("feat", 3)
+        t2 = time.perf_counter()
+        out["c4"]["cpu_oracle"] = {"kind": "oracle", "cores": 1, "ms_per_image": (t1 - t0) * 1e3,
+                                   "pca_readout_ms": (t2 - t1) * 1e3, "sample": "one image, one readout, one host core"}
     m4.close()
     return out
 
 
 # ------------------------------------------------------------------ GPU arm
 def run_mem(a):
+    if a.no_cpu:
+        os.environ["MEM_BENCH_NO_CPU"] = "1"
     import torch
     import torch.distributed as dist
 
@@ -468,10 +620,11 @@ def run_mem(a):
     binds = [(0, 1, 0)]
 
     def step(s, src=None):
-        k = s % POOL
+        # device inputs: the 16-step pool; host inputs (e2e): the first len(src) steps of it,
+        # points and poses of the same step
+        k = s % POOL if src is None else s % len(src)
         mp.move_to_batch(xys[k])
-        mp.input_pointcloud_batch(batches[k] if src is None else src[k % len(src)], offsets, binds, Rs[k], ts[k],
-                                  c["noise"])
+        mp.input_pointcloud_batch(batches[k] if src is None else src[k], offsets, binds, Rs[k], ts[k], c["noise"])
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -569,6 +722,16 @@ def run_mem(a):
         single = {"us_per_frame": l0.elapsed_time(l1) * 10.0, "points_per_s": 100 * npts / (l0.elapsed_time(l1) * 1e-3)}
         sm.close()
 
+    # the SPEC.md:518-521 protocol on the headline step: 10 steps captured as one CUDA graph,
+    # 30 replays, mean +- std per step (a separate timing map)
+    graph = None
+    if rank == 0:
+        mg = M.Map(c["res"], c["rows"], c["cols"], c2_groups(), n_maps=M_)
+        graph = graph_sequence(torch, M, mg, lambda i: (mg.move_to_batch(xys[i % POOL]), mg.input_pointcloud_batch(
+            batches[i % POOL], offsets, binds, Rs[i % POOL], ts[i % POOL], c["noise"])), n=10, reps=30)
+        graph["points_per_s"] = npts * M_ / (graph["us_per_frame_mean"] * 1e-6)
+        mg.close()
+
     sides = {}
     if not a.no_sides:
         sides["c5a"] = side_c5a(torch, M, stream, rank, world)
@@ -591,8 +754,8 @@ def run_mem(a):
     if rank == 0 and world == 1 and not a.no_cpu:
         pts_s, maps_s, cores, nf, dt = oracle_rate(frames, budget_s=12.0)
         cpu = {"value": pts_s, "unit": "points/s", "cores": cores, "kind": "oracle",
-               "sample": f"{nf} C2 map-frames (131072 pts each) in {dt:.1f} s, one map per host thread",
-               "map_updates_per_s": maps_s}
+               "sample": f"{nf} C2 map-frames (131072 pts each) in {dt:.1f} s, one persistent map per host "
+                         f"thread (steady state)", "map_updates_per_s": maps_s}
 
     if rank == 0:
         line = {
@@ -615,6 +778,7 @@ def run_mem(a):
             "clocks": clk.summary(t_on, t_off),
             "e2e": e2e,
             "single_map_c2": single,
+            "graph_10_steps": graph,
             "cpu_baseline": cpu,
             "side_lines": sides,
             "frame_stats_last_step": stats,
