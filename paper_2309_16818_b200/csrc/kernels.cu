@@ -224,9 +224,19 @@ cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+int pca_parts(int HW) { return (int)std::min<long long>(2 * 148, (HW + kPcaTile - 1) / kPcaTile); }
+
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
-  const int tile = kPcaTileBytes / (4 * a.d);
-  k_pca_moments<<<cdiv(a.geo.HW, tile), kThreads, kPcaTileBytes, s>>>(a);
+  k_pca_moments<<<a.nparts, kThreads, sizeof(float) * a.d * (kPcaTile + 1), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pca_eigen(const PcaArgs &a, cudaStream_t s) {
+  const int dp = (a.d + 1) & ~1;
+  const size_t smem = 2 * sizeof(double) * (size_t)dp * (dp + 1);
+  cudaError_t e = cudaFuncSetAttribute(k_pca_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_pca_eigen<<<1, kPcaEigThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

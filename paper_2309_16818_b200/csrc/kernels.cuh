@@ -183,13 +183,18 @@ struct PcaArgs {
   int map;                     // map index
   int word0, d, flag;          // feature layers [word0, word0 + d), observed flag layer
   double *sums;                // [d] sum x, then [d (d + 1) / 2] sum x_a x_b (a <= b), then count
+  double *part;                // [nparts][d + d (d + 1) / 2 + 1] partial moments of the CTAs
+  int nparts;
+  double *proj;                // [k][H*W] projections (pass 0 -> pass 1)
   int k;                       // components
   const double *mean;          // [d]
   const double *comp;          // [k][d]
   unsigned long long *minmax;  // [k][2] order-preserving keys of min and max projections
   float *out;                  // [k][H][W] logical
 };
+int pca_parts(int HW);
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s);
+cudaError_t launch_pca_eigen(const PcaArgs &a, cudaStream_t s);
 cudaError_t launch_pca_project(const PcaArgs &a, int pass, cudaStream_t s);
 cudaError_t launch_read(const ReadArgs &a, cudaStream_t s);
 cudaError_t launch_write(const ReadArgs &a, cudaStream_t s);

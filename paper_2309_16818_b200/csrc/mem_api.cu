@@ -1419,46 +1419,6 @@ mem_status mem_set_layer(mem_map *m, const char *name, const float *src) {
 
 // cyclic Jacobi eigen-decomposition of a symmetric d x d matrix (row-major, destroyed);
 // eigenvalues in w, eigenvectors in the columns of V
-static void jacobi_eigen(std::vector<double> &A, int d, std::vector<double> &w, std::vector<double> &V) {
-  V.assign((size_t)d * d, 0.0);
-  for (int i = 0; i < d; ++i) V[(size_t)i * d + i] = 1.0;
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < d; ++j) {
-        const double x = A[(size_t)i * d + j] * A[(size_t)i * d + j];
-        tot += x;
-        if (i != j) off += x;
-      }
-    if (off <= 1e-30 * tot || off == 0.0) break;
-    for (int p = 0; p < d; ++p)
-      for (int q = p + 1; q < d; ++q) {
-        const double apq = A[(size_t)p * d + q];
-        if (apq == 0.0) continue;
-        const double theta = (A[(size_t)q * d + q] - A[(size_t)p * d + p]) / (2.0 * apq);
-        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
-        for (int k = 0; k < d; ++k) {  // A <- A J (columns p, q)
-          const double akp = A[(size_t)k * d + p], akq = A[(size_t)k * d + q];
-          A[(size_t)k * d + p] = c * akp - sn * akq;
-          A[(size_t)k * d + q] = sn * akp + c * akq;
-        }
-        for (int k = 0; k < d; ++k) {  // A <- J^T A (rows p, q)
-          const double apk = A[(size_t)p * d + k], aqk = A[(size_t)q * d + k];
-          A[(size_t)p * d + k] = c * apk - sn * aqk;
-          A[(size_t)q * d + k] = sn * apk + c * aqk;
-        }
-        for (int k = 0; k < d; ++k) {  // V <- V J
-          const double vkp = V[(size_t)k * d + p], vkq = V[(size_t)k * d + q];
-          V[(size_t)k * d + p] = c * vkp - sn * vkq;
-          V[(size_t)k * d + q] = sn * vkp + c * vkq;
-        }
-      }
-  }
-  w.resize(d);
-  for (int i = 0; i < d; ++i) w[i] = A[(size_t)i * d + i];
-}
-
 mem_status mem_pca_readout(mem_map *m, const char *group, int k, float *out) {
   if (check_map(m)) return MEM_EINVAL;
   if (!group || !out) return fail(MEM_EINVAL, "group and out must be non-NULL");
@@ -1477,8 +1437,10 @@ mem_status mem_pca_readout(mem_map *m, const char *group, int k, float *out) {
   const int HW = m->H * m->W;
   const int pairs = d * (d + 1) / 2;
   const size_t nsums = (size_t)d + pairs + 1;
-  // device scratch: sums | mean | comp | minmax
-  const size_t need = sizeof(double) * (nsums + d + (size_t)k * d) + sizeof(unsigned long long) * 2 * k + 64;
+  // device scratch: sums | mean | comp | minmax | partial moments | projections
+  const int nparts = pca_parts(HW);
+  const size_t need = sizeof(double) * (nsums + d + (size_t)k * d) + sizeof(unsigned long long) * 2 * k +
+                      sizeof(double) * ((size_t)nparts * nsums + (size_t)k * HW) + 64;
   st = grow(&m->pca_buf, &m->pca_cap, need, m->stream);
   if (st != MEM_OK) return st;
   double *dsums = reinterpret_cast<double *>(m->pca_buf);
@@ -1506,50 +1468,19 @@ mem_status mem_pca_readout(mem_map *m, const char *group, int k, float *out) {
   a.mean = dmean;
   a.comp = dcomp;
   a.minmax = dmm;
-  std::vector<double> hs(nsums), cov((size_t)d * d), w, V, mean(d), comp((size_t)k * d);
+  a.part = reinterpret_cast<double *>(dmm + 2 * k);
+  a.nparts = nparts;
+  a.proj = a.part + (size_t)nparts * nsums;
+  if ((d + 1) / 2 * 2 > 64) return fail(MEM_EINVAL, "PCA on the device takes at most 64 channels (got %d)", d);
+  // per map: moments -> eigen-solve (one CTA) -> projection and min-max scaling, all on the
+  // stream; nothing returns to the host
   for (int b = 0; b < m->B; ++b) {
     a.map = b;
     a.out = dout + (size_t)b * k * HW;
-    CU(cudaMemsetAsync(dsums, 0, sizeof(double) * nsums, m->stream));
     TIMED(MEM_STAGE_READ, launch_pca_moments(a, m->stream));
-    CU(cudaMemcpyAsync(hs.data(), dsums, sizeof(double) * nsums, cudaMemcpyDeviceToHost, m->stream));
-    CU(cudaStreamSynchronize(m->stream));
-    const double n = hs[d + pairs];
-    std::fill(comp.begin(), comp.end(), 0.0);
-    if (n > 0.0) {
-      for (int i = 0; i < d; ++i) mean[i] = hs[i] / n;
-      int p = d;
-      for (int i = 0; i < d; ++i)
-        for (int j = i; j < d; ++j, ++p) {
-          const double c = hs[p] / n - mean[i] * mean[j];
-          cov[(size_t)i * d + j] = cov[(size_t)j * d + i] = c;
-        }
-      jacobi_eigen(cov, d, w, V);
-      std::vector<int> order(d);
-      for (int i = 0; i < d; ++i) order[i] = i;
-      std::sort(order.begin(), order.end(), [&](int x, int y) { return w[x] > w[y]; });
-      const double lmax = w[order[0]];
-      for (int c = 0; c < k; ++c) {
-        const int e = order[c];
-        if (!(w[e] > 0.0) || w[e] <= 1e-12 * lmax) break;  // rank exhausted: component stays 0
-        int big = 0;
-        for (int i = 1; i < d; ++i)
-          if (std::fabs(V[(size_t)i * d + e]) > std::fabs(V[(size_t)big * d + e])) big = i;
-        const double sg = V[(size_t)big * d + e] < 0.0 ? -1.0 : 1.0;  // D25
-        for (int i = 0; i < d; ++i) comp[(size_t)c * d + i] = sg * V[(size_t)i * d + e];
-      }
-    } else {
-      std::fill(mean.begin(), mean.end(), 0.0);
-    }
-    CU(cudaMemcpyAsync(dmean, mean.data(), sizeof(double) * d, cudaMemcpyHostToDevice, m->stream));
-    CU(cudaMemcpyAsync(dcomp, comp.data(), sizeof(double) * k * d, cudaMemcpyHostToDevice, m->stream));
-    for (int c = 0; c < k; ++c) {  // min keys start at all-ones, max keys at zero
-      CU(cudaMemsetAsync(dmm + 2 * c, 0xff, sizeof(unsigned long long), m->stream));
-      CU(cudaMemsetAsync(dmm + 2 * c + 1, 0, sizeof(unsigned long long), m->stream));
-    }
+    TIMED(MEM_STAGE_READ, launch_pca_eigen(a, m->stream));
     TIMED(MEM_STAGE_READ, launch_pca_project(a, 0, m->stream));
     TIMED(MEM_STAGE_READ, launch_pca_project(a, 1, m->stream));
-    CU(cudaStreamSynchronize(m->stream));  // mean / comp are host vectors reused by the next map
   }
   if (!dev) {
     CU(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, m->stream));
