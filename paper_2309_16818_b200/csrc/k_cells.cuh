@@ -1,4 +1,4 @@
-// k_cells.cuh -- k_cells (a9-a10 + lazy a13 after k_points) and k_refold (the sequential
+// k_cells.cuh -- k_cells (a9-a10 + lazy a13 after k_points), k_collect + k_refold (the sequential
 // recomputation of uncertified cells).  Part of the single translation unit kernels.cu
 // (included inside namespace memk, in order).
 #pragma once
@@ -81,9 +81,14 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
         }
         if (!ob[u]) a.st.flags[(long long)gd.flag * BHW + c] = 1;
       }
-    } else {  // uncertified: recomputed in input order by k_refold
+    } else {  // uncertified: its points listed by k_collect, recomputed in input order by k_refold
       const unsigned k = atomicAdd(&a.ctl->n_fb, 1u);
-      a.fb[k] = (long long)c;
+      const unsigned n = n_in + n_out;  // the cell's in-window points
+      const unsigned off = atomicAdd(&a.ctl->n_fbpts, n);
+      a.fb[2 * k] = (unsigned long long)c;
+      a.fb[2 * k + 1] = (unsigned long long)off | (unsigned long long)n << 32;
+      a.fbmark[c] = (int)k;
+      a.fbmap[m] = 1u;
     }
     // re-zero the scratch for the next point input
     unsigned long long *r = a.rec + (long long)c * 4;
@@ -172,17 +177,150 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
   flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
-// ---------------------------------------------------------------- k_refold
-// The cells k_cells could not certify (their fp64 sums might depend on the order of the REDs):
-// one CTA per listed cell walks its map's points in input order, 256 at a time -- a2-a7 for each
-// (bin_point, the Mahalanobis test against the pre-frame state, which k_cells left untouched)
-// -- compacts the points of the cell in order (ballots and a block scan) and folds their terms
-// sequentially in fp64, exactly as the oracle does; then a9 + a10 (fuse_state).  A rare path:
-// the certificate fails only when a cell's terms span more than ~29 binades minus log2(n).
+// ---------------------------------------------------------------- k_collect, k_refold
+// The cells k_cells could not certify (their fp64 sums might depend on the order of the REDs)
+// are recomputed from their points in input order, exactly as the oracle folds them.
+//
+// k_collect: a grid-stride pass over the warp-items of the maps that have such a cell (nothing
+// when there is none): a2-a6 for each point (bin_point); a point whose cell is listed appends
+// its index (relative to the map's first point) to the cell's slice of fblist (an atomic slot:
+// any order).
 template <int kFast>
-__global__ void __launch_bounds__(kThreads) k_refold(const __grid_constant__ PassArgs a) {
-  __shared__ float s_z[kThreads], s_v[kThreads], s_c[kThreads];
-  __shared__ unsigned s_part[kThreads / 32];
+__global__ void __launch_bounds__(kThreads) k_collect(const __grid_constant__ PassArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  if (*(volatile unsigned *)&a.ctl->n_fb == 0u) return;
+  const Geometry &g = a.geo;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = gridDim.x * (kThreads / 32);
+  const int gw = blockIdx.x * (kThreads / 32) + wid;
+  const int i0 = ps_of(a, a.m0), i1 = ps_of(a, a.m1);
+  for (int it = i0 + gw; it < i1; it += nwarps) {
+    const Item t = item_of(a, it, i0);
+    if (__ldcg(a.fbmap + t.m) == 0u) continue;  // warp-uniform
+    const PointFrame f = frame_of(a, t.m);
+    const int map_base = t.m * g.HW;
+#pragma unroll
+    for (int u = 0; u < kWarpPtsPerLane; ++u) {
+      const long long i = t.base + u * 32 + lane;
+      if (i >= t.end) continue;
+      const float *p = a.pts + i * (long long)a.stride;
+      const PointOut o = bin_point(__ldg(p), __ldg(p + 1), __ldg(p + 2), f, g, a.np, map_base, a.r2lo, a.r2hi);
+      if (o.cell < 0) continue;
+      const int k = __ldcg(a.fbmark + o.cell);
+      if (k < 0) continue;
+      const unsigned off = (unsigned)__ldcg(a.fb + 2 * k + 1);
+      const unsigned slot = atomicAdd(a.fbfill + k, 1u);
+      a.fblist[off + slot] = (unsigned)(i - t.beg);
+    }
+  }
+}
+
+// k_refold: one CTA per listed cell.  Its point indices are sorted into input order (a block
+// radix sort in shared memory; cells of more than kRefoldCap points walk the whole map instead).
+// Then, 512 points at a time, warps 1-15 evaluate the next chunk's per-point
+// terms -- a2-a7 (bin_point, the Mahalanobis test against the pre-frame state, which k_cells
+// left untouched), the oracle's fp32 terms 1/v and z*(1/v) of the inliers, the channel -- while
+// one thread of warp 0 folds the current chunk into the fp64 sums P, S (, X) in input order,
+// operation for operation the oracle's loop (a term of +0.0 stands for a skipped point: the
+// sums start at +0.0 and never become -0.0, so adding +0.0 leaves them bit-identical).  The
+// integer statistics are order-free (shared-memory atomics).  Then a9 + a10 (fuse_state).
+constexpr int kRefoldThreads = 512;
+constexpr int kRefoldItems = 32;
+constexpr int kRefoldCap = kRefoldThreads * kRefoldItems;  // points of a cell sorted in shared memory
+constexpr int kRefoldChunk = 512;                          // terms folded per step
+
+struct RefoldTerms {
+  unsigned nin, nout, cr, cg, cb, na;
+};
+
+// the terms of point i (absolute index) of map m for a cell `cell` (global index); returns
+// false if the point does not reach the cell (the scan path)
+template <int kFast>
+__device__ __forceinline__ bool refold_term(const PassArgs &a, const PointFrame &f, int map_base, long long i,
+                                            long long cell, float h, float s2, float &w, float &zw, float &c,
+                                            RefoldTerms &t) {
+  const float *p = a.pts + i * (long long)a.stride;
+  const PointOut o = bin_point(__ldg(p), __ldg(p + 1), __ldg(p + 2), f, a.geo, a.np, map_base, a.r2lo, a.r2hi);
+  w = zw = c = 0.0f;
+  if ((long long)o.cell != cell) return false;
+  const float z = o.z, v = o.v;
+  const float d = z - h;  // a7 (D10)
+  if (d * d > a.np.tau2 * (s2 + v)) {
+    ++t.nout;
+  } else {
+    ++t.nin;
+    w = 1.0f / v;  // a8: the oracle's fp32 terms
+    zw = z * w;
+  }
+  if (kFast == 1) {  // D20: exact integer sums
+    const uint32_t bits = __float_as_uint(__ldg(p + 3));
+    t.cr += (bits >> 16) & 255u;
+    t.cg += (bits >> 8) & 255u;
+    t.cb += bits & 255u;
+    ++t.na;
+  } else if (kFast == 2) {  // D31: finite channels only
+    const float ch = __ldg(p + 3);
+    if (isfinite(ch)) {
+      ++t.na;
+      c = ch;
+    }
+  }
+  return true;
+}
+
+// the oracle's sequential fold of n terms (inputs in order; loads issued 4 ahead of the adds)
+template <int kFast>
+__device__ __forceinline__ void refold_fold(const float *w, const float *zw, const float *c, int n, double &P,
+                                            double &S, double &X) {
+  int j = 0;
+  for (; j + 4 <= n; j += 4) {
+    float wj[4], zj[4], cj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      wj[u] = w[j + u];
+      zj[u] = zw[j + u];
+      cj[u] = kFast == 2 ? c[j + u] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      P += (double)wj[u];
+      S += (double)zj[u];
+      if (kFast == 2) X += (double)cj[u];
+    }
+  }
+  for (; j < n; ++j) {
+    P += (double)w[j];
+    S += (double)zw[j];
+    if (kFast == 2) X += (double)c[j];
+  }
+}
+
+template <int kFast>
+struct RefoldSmem {
+  using Sort = cub::BlockRadixSort<unsigned, kRefoldThreads, kRefoldItems>;
+  static constexpr int NC = kFast == 2 ? kRefoldChunk : 1;
+  struct Bufs {
+    float w[2][kRefoldChunk], zw[2][kRefoldChunk], c[2][NC];
+  };
+  union {
+    typename Sort::TempStorage sort;
+    Bufs b;
+  } u;
+  unsigned idx[kRefoldCap];
+};
+template <int kFast>
+size_t refold_smem_bytes() { return sizeof(RefoldSmem<kFast>); }
+
+template <int kFast>
+__global__ void __launch_bounds__(kRefoldThreads) k_refold(const __grid_constant__ PassArgs a) {
+  using Sort = typename RefoldSmem<kFast>::Sort;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  RefoldSmem<kFast> &sm = *reinterpret_cast<RefoldSmem<kFast> *>(s_raw);
+  auto &s_u = sm.u;
+  unsigned *s_idx = sm.idx;
+  __shared__ unsigned s_t[6];
+  __shared__ unsigned s_part[kRefoldThreads / 32];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   pdl_wait();
@@ -193,61 +331,85 @@ __global__ void __launch_bounds__(kThreads) k_refold(const __grid_constant__ Pas
   const unsigned nfb = *(volatile unsigned *)&a.ctl->n_fb;
   const float *vals = reinterpret_cast<const float *>(a.st.words);
   for (unsigned k = blockIdx.x; k < nfb; k += gridDim.x) {
-    const long long gc = __ldcg(a.fb + k);
-    const int m = (int)(gc / g.HW), phys = (int)(gc - (long long)m * g.HW);
+    const long long gc = (long long)__ldcg(a.fb + 2 * k);
+    const unsigned long long e = __ldcg(a.fb + 2 * k + 1);
+    const unsigned off = (unsigned)e, n = (unsigned)(e >> 32);
+    const int m = (int)(gc / g.HW);
+    const int map_base = m * g.HW;
     const PointFrame f = frame_of(a, m);
     const long long beg = off_of(a, m), end = off_of(a, m + 1);
     const float h = __ldcg(vals + (long long)kWordElev * g.BHW + gc), s2 = __ldcg(vals + (long long)kWordVar * g.BHW + gc);
+    if (threadIdx.x < 6) s_t[threadIdx.x] = 0u;
+    RefoldTerms t = {0u, 0u, 0u, 0u, 0u, 0u};
     double P = 0.0, S = 0.0, X = 0.0;
-    unsigned nin = 0u, nout = 0u, cr = 0u, cg = 0u, cb = 0u, na = 0u;
-    for (long long b0 = beg; b0 < end; b0 += kThreads) {
-      const long long i = b0 + threadIdx.x;
-      bool in = false;
-      float z = 0.0f, v = 0.0f, ch = 0.0f;
-      if (i < end) {
-        const float *p = a.pts + i * (long long)a.stride;
-        const PointOut o = bin_point(__ldg(p), __ldg(p + 1), __ldg(p + 2), f, g, a.np, 0, a.r2lo, a.r2hi);
-        if (o.cell == phys) {
-          in = true;
-          z = o.z;
-          v = o.v;
-          if (kFast != 0) ch = __ldg(p + 3);
-        }
+    if (n <= (unsigned)kRefoldCap) {
+      // the cell's point indices into input order
+      const unsigned span = (unsigned)(end - beg);
+      const int end_bit = span <= 1u ? 1 : 32 - __clz(span - 1u);
+      unsigned keys[kRefoldItems];
+#pragma unroll
+      for (int q = 0; q < kRefoldItems; ++q) {  // any arrangement: coalesced loads
+        const unsigned j = q * kRefoldThreads + threadIdx.x;
+        keys[q] = j < n ? __ldcg(a.fblist + off + j) : 0xffffffffu;
       }
-      unsigned tot;
-      const unsigned pos = block_excl_scan<kThreads>(in ? 1u : 0u, s_part, &tot);
-      if (in) {
-        s_z[pos] = z;
-        s_v[pos] = v;
-        s_c[pos] = ch;
+      Sort(s_u.sort).Sort(keys, 0, end_bit);
+#pragma unroll
+      for (int q = 0; q < kRefoldItems; ++q) {  // the sorted keys: blocked arrangement
+        const unsigned j = threadIdx.x * kRefoldItems + q;
+        if (j < n) s_idx[j] = keys[q];
       }
+      __syncthreads();  // s_idx complete; the sort's storage (aliasing the term buffers) is free
+      const int nch = (int)((n + kRefoldChunk - 1) / kRefoldChunk);
+      const int len0 = n < (unsigned)kRefoldChunk ? (int)n : kRefoldChunk;
+      for (int j = threadIdx.x; j < len0; j += kRefoldThreads)
+        refold_term<kFast>(a, f, map_base, beg + s_idx[j], gc, h, s2, s_u.b.w[0][j], s_u.b.zw[0][j],
+                           s_u.b.c[0][kFast == 2 ? j : 0], t);
       __syncthreads();
-      if (threadIdx.x == 0) {  // the oracle's per-point loop, in input order
-        for (unsigned j = 0; j < tot; ++j) {
-          const float zj = s_z[j], vj = s_v[j];
-          const float d = zj - h;  // a7 (D10)
-          if (d * d > a.np.tau2 * (s2 + vj)) {
-            ++nout;
-          } else {
-            ++nin;
-            const float w = 1.0f / vj;
-            P += (double)w;
-            S += (double)(zj * w);
+      for (int ch = 0; ch < nch; ++ch) {
+        const int b = ch & 1;
+        if (threadIdx.x < 32) {  // warp 0: the fold of chunk ch
+          if (threadIdx.x == 0) {
+            const int len = (int)n - ch * kRefoldChunk < kRefoldChunk ? (int)n - ch * kRefoldChunk : kRefoldChunk;
+            refold_fold<kFast>(s_u.b.w[b], s_u.b.zw[b], s_u.b.c[b], len, P, S, X);
           }
-          if (kFast == 1) {
-            const uint32_t bits = __float_as_uint(s_c[j]);
-            cr += (bits >> 16) & 255u;
-            cg += (bits >> 8) & 255u;
-            cb += bits & 255u;
-            ++na;
-          } else if (kFast == 2 && isfinite(s_c[j])) {
-            ++na;
-            X += (double)s_c[j];
-          }
+        } else if (ch + 1 < nch) {  // warps 1-15: the terms of chunk ch + 1
+          const int j0 = (ch + 1) * kRefoldChunk;
+          const int len = (int)n - j0 < kRefoldChunk ? (int)n - j0 : kRefoldChunk;
+          for (int j = threadIdx.x - 32; j < len; j += kRefoldThreads - 32)
+            refold_term<kFast>(a, f, map_base, beg + s_idx[j0 + j], gc, h, s2, s_u.b.w[b ^ 1][j],
+                               s_u.b.zw[b ^ 1][j], s_u.b.c[b ^ 1][kFast == 2 ? j : 0], t);
         }
+        __syncthreads();
       }
-      __syncthreads();
+    } else {
+      // more points than the sort holds: walk the map's points in input order, 512 at a time,
+      // and compact the cell's terms in order (block scan)
+      for (long long b0 = beg; b0 < end; b0 += kRefoldThreads) {
+        const long long i = b0 + threadIdx.x;
+        float w = 0.0f, zw = 0.0f, c = 0.0f;
+        const bool in = i < end && refold_term<kFast>(a, f, map_base, i, gc, h, s2, w, zw, c, t);
+        unsigned tot;
+        const unsigned pos = block_excl_scan<kRefoldThreads>(in ? 1u : 0u, s_part, &tot);
+        if (in) {
+          s_u.b.w[0][pos] = w;
+          s_u.b.zw[0][pos] = zw;
+          if (kFast == 2) s_u.b.c[0][pos] = c;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) refold_fold<kFast>(s_u.b.w[0], s_u.b.zw[0], s_u.b.c[0], (int)tot, P, S, X);
+        __syncthreads();
+      }
     }
+    // the integer statistics (order-free)
+    if (t.nin) atomicAdd(&s_t[0], t.nin);
+    if (t.nout) atomicAdd(&s_t[1], t.nout);
+    if (kFast == 1 && t.na) {
+      atomicAdd(&s_t[2], t.cr);
+      atomicAdd(&s_t[3], t.cg);
+      atomicAdd(&s_t[4], t.cb);
+    }
+    if (t.na) atomicAdd(&s_t[5], t.na);
+    __syncthreads();
     if (threadIdx.x == 0) {
       ++cnt[7];
       float th[3] = {0.0f, 0.0f, 0.0f};
@@ -258,7 +420,10 @@ __global__ void __launch_bounds__(kThreads) k_refold(const __grid_constant__ Pas
         ob = __ldcg(a.st.flags + (long long)gd.flag * g.BHW + gc);
       }
       fuse_state<kFast == 0 ? 3 : kFast>(a, gc, h, s2, __ldcg(a.st.flags + (long long)kFlagValid * g.BHW + gc), th, ob,
-                                         nin, nout, P, S, cr, cg, cb, na, X);
+                                         s_t[0], s_t[1], P, S, s_t[2], s_t[3], s_t[4], s_t[5], X);
+      a.fbmark[gc] = -1;  // the lists are empty again for the next point input
+      a.fbfill[k] = 0u;
+      a.fbmap[m] = 0u;
     }
     __syncthreads();
   }

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
   pdl_trigger();
   if (blockIdx.x == 0) {  // the other epoch is the next point input's (no memset per call)
     for (int i = threadIdx.x; i < kStatSlots * 8; i += kThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;
-    if (threadIdx.x == 0) a.ctl->n_fb = 0u;
+    if (threadIdx.x == 0) a.ctl->n_fb = a.ctl->n_fbpts = 0u;
   }
   __syncthreads();
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // by mem_stats slot

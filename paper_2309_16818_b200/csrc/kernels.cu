@@ -23,6 +23,8 @@
 
 #include "kernels.cuh"
 
+#include <cub/block/block_radix_sort.cuh>
+
 #ifndef MEM_OCC_BATCH
 #define MEM_OCC_BATCH 4  // occlusion walk: intermediate cells whose loads are issued together
 #endif
@@ -170,7 +172,16 @@ static cudaError_t launch_cells_t(const PassArgs &a, cudaStream_t s) {
                                                        (chunks + 7) / 8));
   cudaError_t e = launch_pdl(k_cells<kFast>, g, 0, s, a, kThreads);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_refold<kFast>, 148, 0, s, a, kThreads);
+  // uncertified cells (none: both kernels return at once)
+  const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1]);
+  int gc = resident_grid(k_collect<kFast>, kThreads, 9 + kFast);
+  if (items > 0) gc = (int)std::max(1LL, std::min<long long>(gc, (items + 7) / 8));
+  e = launch_pdl(k_collect<kFast>, gc, 0, s, a, kThreads);
+  if (e != cudaSuccess) return e;
+  const size_t smem = refold_smem_bytes<kFast>();
+  e = cudaFuncSetAttribute(k_refold<kFast>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_refold<kFast>, 148, smem, s, a, kRefoldThreads);
 }
 
 cudaError_t launch_cells(const PassArgs &a, cudaStream_t s) {

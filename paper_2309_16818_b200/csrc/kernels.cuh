@@ -31,6 +31,7 @@ struct Control {  // two epochs: a point input adds to stats[epoch] and clears s
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
   unsigned n_rec, n_seg, n_lseg, n_mseg;       // this call's sorted records, short / long / mid segments (k_sort)
   unsigned n_fb;                               // cells k_cells could not certify (k_refold)
+  unsigned n_fbpts;                            // their points (k_collect list length)
 };
 
 // reset description shared by k_band (lazy strips) and k_shift
@@ -62,7 +63,12 @@ struct PassArgs {
   unsigned long long *cnt;     // RED path scratch [n_maps][HW]: count word
   unsigned long long *rec;     // [n_maps][HW][4]: P, S, group words
   unsigned *cert;              // [n_maps][HW][4]: certificates {~min, max} of |z/v| and |channel|
-  long long *fb;               // cells k_cells could not certify (m * HW + cell), for k_refold
+  unsigned long long *fb;      // [2 k]: the k-th cell k_cells could not certify (m * HW + cell);
+                               // [2 k + 1]: its list offset | point count << 32 (k_collect, k_refold)
+  int *fbmark;                 // [n_maps][HW]: k of an uncertified cell, else -1 (reset by k_refold)
+  unsigned *fbfill;            // [k]: points k_collect has listed for cell k (reset by k_refold)
+  unsigned *fbmap;             // [n_maps]: != 0 if the map has an uncertified cell (reset by k_refold)
+  unsigned *fblist;            // point indices (relative to the map's first point) of those cells
   int t_uniform;               // > 0: every map has exactly this many tiles
   double inv_t_uniform;        // 1.0 / t_uniform (divmod_fast)
   int tmax;                    // most tiles of one map (k_band's shared memory)

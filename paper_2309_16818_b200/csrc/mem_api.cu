@@ -13,6 +13,30 @@
 #include <string>
 #include <vector>
 
+// host-side checkpoint timing of the point input (diagnostics: -DMEM_HOST_PROF=1, off by default)
+#if MEM_HOST_PROF
+#include <chrono>
+static double g_hp[32];
+static long long g_hp_n;
+static void hp_report();
+static std::chrono::high_resolution_clock::time_point g_hp_t0;
+#define HP_START() (g_hp_t0 = std::chrono::high_resolution_clock::now(), ++g_hp_n == 100 ? hp_report() : (void)0)
+#define HP(i) (g_hp[i] += std::chrono::duration<double, std::micro>(std::chrono::high_resolution_clock::now() - g_hp_t0).count())
+static void hp_report() {
+  if (!g_hp_n) return;
+  fprintf(stderr, "host prof (%lld calls, us since call start):", g_hp_n);
+  for (int i = 0; i < 32; ++i)
+    if (g_hp[i] != 0.0) fprintf(stderr, " [%d] %.2f", i, g_hp[i] / g_hp_n);
+  fprintf(stderr, "\n");
+  for (int i = 0; i < 32; ++i) g_hp[i] = 0.0;
+  g_hp_n = 0;
+}
+#else
+#define HP_START() ((void)0)
+#define HP(i) ((void)0)
+static void hp_report() {}
+#endif
+
 #include "kernels.cuh"
 
 using namespace memk;
@@ -113,6 +137,8 @@ struct mem_map {
   size_t recs_cap = 0, tinfo_cap = 0, ridx_cap = 0, srec_cap = 0, sridx_cap = 0, segs_cap = 0;
   // RED path scratch (zeroed once, re-zeroed by k_cells): count words, records, certificates, fallback list
   void *rcnt_s = nullptr, *rrec_s = nullptr, *rcert_s = nullptr, *rfb_s = nullptr;
+  void *rmark_s = nullptr, *rfill_s = nullptr, *rmapfb_s = nullptr, *rlist_s = nullptr;
+  size_t rlist_cap = 0;
   size_t red_cells = 0;  // cells the RED scratch holds
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
@@ -502,6 +528,10 @@ void free_map(mem_map *m) {
   cudaFree(m->rrec_s);
   cudaFree(m->rcert_s);
   cudaFree(m->rfb_s);
+  cudaFree(m->rmark_s);
+  cudaFree(m->rfill_s);
+  cudaFree(m->rmapfb_s);
+  cudaFree(m->rlist_s);
   cudaFree(m->rsrc);
   cudaFree(m->rtile);
   cudaFree(m->odbg_cell);
@@ -712,6 +742,7 @@ mem_status mem_create(float resolution, int rows, int cols, const mem_layer_spec
 }
 
 mem_status mem_destroy(mem_map *m) {
+  hp_report();
   free_map(m);
   return MEM_OK;
 }
@@ -774,26 +805,38 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
   const size_t cells = (size_t)B * m->H * m->W;
   if (cells > m->red_cells) {
     CU(cudaStreamSynchronize(m->stream));
-    cudaFree(m->rcnt_s);
-    cudaFree(m->rrec_s);
-    cudaFree(m->rcert_s);
-    cudaFree(m->rfb_s);
-    m->rcnt_s = m->rrec_s = m->rcert_s = m->rfb_s = nullptr;
-    m->red_cells = 0;
-    if (cudaMalloc(&m->rcnt_s, 8 * cells) != cudaSuccess || cudaMalloc(&m->rrec_s, 32 * cells) != cudaSuccess ||
-        cudaMalloc(&m->rcert_s, 16 * cells) != cudaSuccess || cudaMalloc(&m->rfb_s, 8 * cells) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(MEM_ENOMEM, "RED scratch (%zu cells)", cells);
+    void **bufs[] = {&m->rcnt_s, &m->rrec_s, &m->rcert_s, &m->rfb_s, &m->rmark_s, &m->rfill_s, &m->rmapfb_s};
+    const size_t bytes[] = {8 * cells, 32 * cells, 16 * cells, 16 * cells, 4 * cells, 4 * cells, 4 * (size_t)B};
+    for (void **b : bufs) {
+      cudaFree(*b);
+      *b = nullptr;
     }
-    CU(cudaMemsetAsync(m->rcnt_s, 0, 8 * cells, m->stream));
-    CU(cudaMemsetAsync(m->rrec_s, 0, 32 * cells, m->stream));
-    CU(cudaMemsetAsync(m->rcert_s, 0, 16 * cells, m->stream));
+    m->red_cells = 0;
+    for (int i = 0; i < 7; ++i)
+      if (cudaMalloc(bufs[i], bytes[i]) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MEM_ENOMEM, "RED scratch (%zu cells)", cells);
+      }
+    CU(cudaMemsetAsync(m->rcnt_s, 0, bytes[0], m->stream));
+    CU(cudaMemsetAsync(m->rrec_s, 0, bytes[1], m->stream));
+    CU(cudaMemsetAsync(m->rcert_s, 0, bytes[2], m->stream));
+    CU(cudaMemsetAsync(m->rmark_s, 0xff, bytes[4], m->stream));  // -1: no uncertified cell
+    CU(cudaMemsetAsync(m->rfill_s, 0, bytes[5], m->stream));
+    CU(cudaMemsetAsync(m->rmapfb_s, 0, bytes[6], m->stream));
     m->red_cells = cells;
   }
+  // the point list of the uncertified cells: at most every point of the call
+  HP(7);
+  const long long npts = offsets ? offsets[B] - offsets[0] : total;
+  if (grow(&m->rlist_s, &m->rlist_cap, 4 * (size_t)std::max(1LL, npts), m->stream) != MEM_OK) return MEM_ENOMEM;
   a.cnt = reinterpret_cast<unsigned long long *>(m->rcnt_s);
   a.rec = reinterpret_cast<unsigned long long *>(m->rrec_s);
   a.cert = reinterpret_cast<unsigned *>(m->rcert_s);
-  a.fb = reinterpret_cast<long long *>(m->rfb_s);
+  a.fb = reinterpret_cast<unsigned long long *>(m->rfb_s);
+  a.fbmark = reinterpret_cast<int *>(m->rmark_s);
+  a.fbfill = reinterpret_cast<unsigned *>(m->rfill_s);
+  a.fbmap = reinterpret_cast<unsigned *>(m->rmapfb_s);
+  a.fblist = reinterpret_cast<unsigned *>(m->rlist_s);
   a.st = m->st;
   a.m0 = 0;
   a.m1 = B;
@@ -818,8 +861,12 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
     d = m->dparam2;
     a.pstart = reinterpret_cast<const int *>(d);
   }
+  HP(8);
   if (ps[B] > 0) TIMED(MEM_STAGE_POINT, launch_points(a, m->stream));
+  else CU(cudaMemsetAsync(&m->ctl->n_fb, 0, sizeof(unsigned) * 2, m->stream));  // k_points clears them
+  HP(9);
   TIMED(MEM_STAGE_CELL, launch_cells(a, m->stream));
+  HP(10);
   return MEM_OK;
 }
 
@@ -1045,6 +1092,7 @@ static mem_status route_points(mem_map *m, PassArgs &a, long long n, int stride)
 static mem_status input_points(mem_map *m, const float *pts, const int64_t *offsets, int64_t n_single, int stride,
                                const mem_binding *bind, int nb, const double *R, const double *t,
                                const mem_noise *np) {
+  HP_START();
   if (check_map(m)) return MEM_EINVAL;
   if (stride < 3) return fail(MEM_EINVAL, "stride %d < 3", stride);
   if (!R || !t || !np) return fail(MEM_EINVAL, "R, t and noise must be non-NULL");
@@ -1072,11 +1120,15 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     if (!rotation_ok(R + 9 * i)) return fail(MEM_EPOSE, "map %d: R is not a rotation (SPEC.md:128)", i);
   for (int i = 0; i < 3 * B; ++i)
     if (!std::isfinite(t[i])) return fail(MEM_EINVAL, "t must be finite");
+  HP(0);
   PassArgs a;
   memset(&a, 0, sizeof a);
+  HP(1);
   mem_status s = resolve_bindings(m, bind, nb, false, stride, a.b);
   if (s != MEM_OK) return s;
+  HP(2);
   if (set_device(m)) return MEM_ECUDA;
+  HP(3);
   if (m->flags & MEM_FLAG_DEBUG_POINTS) {
     if ((size_t)total > m->dbg_cap) {
       CU(cudaStreamSynchronize(m->stream));
@@ -1108,6 +1160,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     s = stage_input(m, pts, sizeof(float) * (size_t)total * stride, &dpts);
     if (s != MEM_OK) return s;
   }
+  HP(4);
   a.pts = (const float *)dpts;
   a.stride = stride;
   a.n_maps = B;
@@ -1116,6 +1169,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
   a.st = m->st;
   a.np = *np;
   range_thresholds(np->r_min, np->r_max, &a.r2lo, &a.r2hi);
+  HP(5);
   a.nb = nb;
   a.ctl = m->ctl;
   a.epoch = m->epoch;
@@ -1189,6 +1243,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
     a.tstart = reinterpret_cast<const int *>((char *)d + ts_at);
   }
+  HP(6);
   if (m->transport != 0 && m->nranks > 1) {  // sharded map: route the shard's points to their owners
     a.fast = a.fast == 3 ? 3 : 0;             // (the owner pass re-checks the float4 fast paths)
     if (nb == 1 && (a.b[0].g.rule == MEM_COLOR || (a.b[0].g.rule == MEM_AVERAGE && a.b[0].g.nch == 1)) &&
@@ -1201,7 +1256,9 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.cell_hi = m->band_lo + m->band_n;
   }
   m->pending = false;
-  return fuse_points(m, a, tstart[B], tmax, max_n, offsets, total);
+  s = fuse_points(m, a, tstart[B], tmax, max_n, offsets, total);
+  HP(11);
+  return s;
 }
 
 mem_status mem_input_pointcloud(mem_map *m, const float *pts, int64_t n, int stride, const mem_binding *bind,

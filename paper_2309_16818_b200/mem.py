@@ -168,10 +168,14 @@ def _buf(x, dtype, min_elems=None, what="buffer"):
 
 
 def _dbl(a, n):
-    arr = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    """n doubles as a ctypes array (a copy: ~1 us, where ndarray.ctypes.data_as costs ~5 us)."""
+    arr = np.asarray(a, np.float64)
     if arr.size != n:
         raise ValueError(f"expected {n} doubles, got {arr.size}")
-    return arr, arr.ctypes.data_as(_P(C.c_double))
+    if not arr.flags["C_CONTIGUOUS"]:
+        arr = np.ascontiguousarray(arr)
+    buf = (C.c_double * n).from_buffer_copy(arr)
+    return buf, buf
 
 
 def _binds(bindings):

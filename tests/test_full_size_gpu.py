@@ -217,24 +217,33 @@ def test_paths_give_identical_bits(case):
     assert runs[0][1] == runs[1][1] == runs[2][1]
 
 
-def test_uncertified_cells_are_refolded_exactly():
+@pytest.mark.parametrize("rows,n,group", [(16, 20000, "average"), (4, 100000, "average"), (8, 50000, "colour"),
+                                          (16, 20000, None), (2, 30000, None)])
+def test_uncertified_cells_are_refolded_exactly(rows, n, group):
     """Cells whose height terms z/v span more binades than the certificate allows (z from 1e-12
     to 1 m in one cell) cannot be summed by atomics in an order-free way: they must be
-    recomputed in input order (k_refold) and still equal the oracle bit for bit."""
-    rng = np.random.default_rng(11)
-    rows = cols = 16
+    recomputed in input order (k_collect + k_refold) and still equal the oracle bit for bit.
+    Cells of up to 4096 points take the sorted-list path, larger ones (4 x 4 map, 100k points;
+    2 x 2 map, 30k points) the whole-map walk; colour, 1-channel average and height only."""
+    rng = np.random.default_rng(11 + rows)
+    cols = rows
     res = 0.1
+    half = rows * res / 2 - 0.01
     noise = dict(a=1e-4, b=0.0, r_min=0.0, r_max=100.0, h_min=-10.0, h_max=10.0, tau2=1e30, v_out=0.01)
-    g = M.Map(res, rows, cols, [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)], debug_points=True)
-    o = O.OracleMap(res, rows, cols, [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)])
-    for f in range(5):
-        n = 20000
-        xy = rng.uniform(-0.79, 0.79, (n, 2))
+    groups = {"average": [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)],
+              "colour": [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5)], None: []}[group]
+    binds = [] if group is None else [(0, 1, 0)]
+    g = M.Map(res, rows, cols, groups, debug_points=True)
+    o = O.OracleMap(res, rows, cols, groups)
+    for f in range(4):
+        xy = rng.uniform(-half, half, (n, 2))
         z = rng.choice([1e-12, 1e-9, 1e-6, 1e-3, 1.0], n) * rng.choice([-1.0, 1.0], n) * rng.uniform(1, 2, n)
         feat = rng.choice([1e-20, 1e-10, 1.0, 1e10], n) * rng.uniform(1, 2, n)
         pts = np.stack([xy[:, 0], xy[:, 1], z - 1.0, feat], 1).astype(np.float32)
-        g.input_pointcloud(torch.from_numpy(pts).cuda(), [(0, 1, 0)], np.eye(3), [0.0, 0.0, 1.0], noise)
-        cell, code = o.input_pointcloud(pts, [(0, 1, 0)], np.eye(3), [0.0, 0.0, 1.0], noise, debug=True)
+        if group == "colour":
+            pts[:, 3] = S.pack_rgb(rng.integers(0, 256, (n, 3)).astype(np.uint8)).view(np.float32)
+        g.input_pointcloud(torch.from_numpy(pts).cuda(), binds, np.eye(3), [0.0, 0.0, 1.0], noise)
+        cell, code = o.input_pointcloud(pts, binds, np.eye(3), [0.0, 0.0, 1.0], noise, debug=True)
         gc, gk = g.debug_codes()
         assert np.array_equal(gk, code) and np.array_equal(gc, cell)
         assert g.stats() == o.stats()
