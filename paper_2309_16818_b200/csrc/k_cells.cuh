@@ -19,7 +19,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
   uint8_t *validp = a.st.flags + (long long)kFlagValid * BHW;
   double P[N], S[N];
   unsigned long long w0[N], w1[N];
-  uint4 ce[N];
+  uint2 ce[N];
   float h[N], s2[N], th[N][NCH > 0 ? NCH : 1];
   uint8_t vd[N], ob[N];
 #pragma unroll
@@ -32,7 +32,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     S[u] = __longlong_as_double((long long)ps.y);
     w0[u] = ww.x;
     w1[u] = ww.y;
-    ce[u] = __ldcg(reinterpret_cast<const uint4 *>(a.cert) + c);
+    ce[u] = __ldcg(reinterpret_cast<const uint2 *>(a.cert) + c);
     h[u] = elev[c];
     s2[u] = var[c];
     vd[u] = validp[c];
@@ -52,7 +52,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     const unsigned n_out = kFast == 1 ? (unsigned)w1[u] : (unsigned)(cnt[u] >> 32);
     const unsigned n_in = kFast == 1 ? (unsigned)(cnt[u] >> 32) - n_out : (unsigned)(cnt[u] & 0xffffffffull);
     const unsigned ng = kFast == 1 ? (unsigned)(cnt[u] >> 32) : kFast == 2 ? (unsigned)w0[u] : 0u;
-    const bool ok = cert_ok(make_uint2(ce[u].x, ce[u].y), n_in) && (kFast != 2 || cert_ok(make_uint2(ce[u].z, ce[u].w), ng));
+    const bool ok = cert_ok(ce[u].x, n_in) && (kFast != 2 || cert_ok(ce[u].y, ng));
     if (ok) {
       ++stc[7];
       // a9: Kalman height fusion (D7, D11)
@@ -95,7 +95,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     __stcg(a.cnt + c, 0ull);
     __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
     __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
-    __stcg(reinterpret_cast<uint4 *>(a.cert) + c, make_uint4(0u, 0u, 0u, 0u));
+    __stcg(reinterpret_cast<uint2 *>(a.cert) + c, make_uint2(0u, 0u));
   }
 }
 

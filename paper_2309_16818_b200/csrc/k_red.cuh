@@ -13,14 +13,27 @@
 // the average channel sum); k_cells checks them and hands any uncertified cell to k_refold,
 // which recomputes it sequentially in input order.  P = sum 1/v is certified once per call on
 // the host from the range of v.
-__device__ __forceinline__ void red_max_u32(unsigned *p, unsigned v) {
-  asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+//
+// Storage: one 8-byte word per cell, four bf16 slots {e_max(S), 255 - e_min(S), e_max(X),
+// 255 - e_min(X)} (exponent fields, subnormals counted as 1; integers <= 255 are exact in bf16,
+// 0 = no non-zero term), reduced by ONE red.max.v2.bf16x2 per run of points (the four slots
+// are independent maxima).
+__device__ __forceinline__ unsigned bf16_int(unsigned v) { return __float_as_uint((float)v) >> 16; }
+__device__ __forceinline__ unsigned int_bf16(unsigned h) { return (unsigned)__uint_as_float(h << 16); }
+// {~min |t| bits, max |t| bits} (register form, 0 = no non-zero term) -> bf16x2 slots
+__device__ __forceinline__ unsigned cert_slots(uint2 c) {
+  if (c.y == 0u) return 0u;
+  const unsigned emin = max((~c.x >> 23) & 255u, 1u), emax = max((c.y >> 23) & 255u, 1u);
+  return bf16_int(emax) | bf16_int(255u - emin) << 16;
+}
+__device__ __forceinline__ void red_max_cert(unsigned *p, unsigned s, unsigned x) {  // p: 8-byte aligned
+  asm volatile("red.relaxed.gpu.global.max.noftz.v2.bf16x2 [%0], {%1, %2};" ::"l"(p), "r"(s), "r"(x) : "memory");
 }
 __device__ __forceinline__ unsigned cert_ceil_log2(unsigned n) { return n <= 1u ? 0u : 32u - __clz(n - 1u); }
-// c = {~min |t| bits, max |t| bits} (0 = no non-zero term); n = number of terms
-__device__ __forceinline__ bool cert_ok(uint2 c, unsigned n) {
-  if (c.y == 0u) return true;  // every term zero
-  const unsigned emin = max((~c.x >> 23) & 255u, 1u), emax = max((c.y >> 23) & 255u, 1u);
+// slots of one sum (bf16x2 word); n = number of terms
+__device__ __forceinline__ bool cert_ok(unsigned w, unsigned n) {
+  if (w == 0u) return true;  // every term zero
+  const unsigned emax = int_bf16(w & 0xffffu), emin = 255u - int_bf16(w >> 16);
   return emax - emin + cert_ceil_log2(n) <= 29u;
 }
 
@@ -58,31 +71,49 @@ __device__ __forceinline__ void red_add_f64(unsigned long long *p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-// Segmented reduction over the lanes of `peers` (the lanes holding the same cell): the lowest
-// lane of each peer group ends with the group's total.  Tree over the rank within the group:
-// ceil(log2(group size)) rounds, every lane participates in every shuffle (after E. Westphal,
-// "warp-aggregated atomics").  `Op` is + or max.
-template <class T, class Op>
-__device__ __forceinline__ T reduce_peers(unsigned peers, T x, Op op) {
-  const int lane = threadIdx.x & 31;
-  unsigned rel = (unsigned)__popc(peers & lanemask_lt());
-  unsigned rest = peers & ~(lanemask_lt() | (1u << lane));  // peers above me
-  while (__any_sync(0xffffffffu, rest != 0u)) {
-    const int next = __ffs(rest);
-    const T t = __shfl_sync(0xffffffffu, x, next > 0 ? next - 1 : lane);
-    if (next) x = op(x, t);
-    rest &= ~__ballot_sync(0xffffffffu, rel & 1u);  // odd ranks are folded into their neighbour
-    rel >>= 1;
-  }
-  return x;
+// Segmented reduction over runs of consecutive lanes holding the same cell (`heads`: the first
+// lane of every run): after five shuffle-down steps the head lane of each run holds the run's
+// total.  One pass reduces every statistic of the point (shared control flow).  A cell whose
+// lanes are not contiguous gets one total per run (one RED set each): exact all the same.
+__device__ __forceinline__ bool same_run_below(unsigned heads, int lane, int d) {
+  // lanes (lane, lane + d] belong to lane's run (no head among them)
+  return lane + d <= 31 && (heads & (((1u << d) - 1u) << (lane + 1))) == 0u;
 }
-struct OpAdd {
-  template <class T>
-  __device__ T operator()(T a, T b) const { return a + b; }
-};
-struct OpMaxU {
-  __device__ unsigned operator()(unsigned a, unsigned b) const { return a > b ? a : b; }
-};
+template <int kFast>
+__device__ __forceinline__ void reduce_runs(unsigned heads, double &w, double &zw, uint2 &cs, unsigned &rg,
+                                            unsigned &bb, double &v, uint2 &cx) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const bool ok = same_run_below(heads, lane, d);
+    const double tw = __shfl_down_sync(0xffffffffu, w, d), tz = __shfl_down_sync(0xffffffffu, zw, d);
+    const unsigned c0 = __shfl_down_sync(0xffffffffu, cs.x, d), c1 = __shfl_down_sync(0xffffffffu, cs.y, d);
+    unsigned r0 = 0u, r1 = 0u, x0 = 0u, x1 = 0u;
+    double tv = 0.0;
+    if (kFast == 1) {
+      r0 = __shfl_down_sync(0xffffffffu, rg, d);
+      r1 = __shfl_down_sync(0xffffffffu, bb, d);
+    } else if (kFast == 2) {
+      tv = __shfl_down_sync(0xffffffffu, v, d);
+      x0 = __shfl_down_sync(0xffffffffu, cx.x, d);
+      x1 = __shfl_down_sync(0xffffffffu, cx.y, d);
+    }
+    if (ok) {
+      w += tw;
+      zw += tz;
+      cs.x = max(cs.x, c0);
+      cs.y = max(cs.y, c1);
+      if (kFast == 1) {
+        rg += r0;
+        bb += r1;
+      } else if (kFast == 2) {
+        v += tv;
+        cx.x = max(cx.x, x0);
+        cx.y = max(cx.y, x1);
+      }
+    }
+  }
+}
 
 // |t| as the certificate pair {~bits, bits} (0, 0 for t = 0)
 __device__ __forceinline__ uint2 cert_of(float t) {
@@ -92,8 +123,8 @@ __device__ __forceinline__ uint2 cert_of(float t) {
 
 // a8: scatter-accumulate the sufficient statistics of the warp's current points (one per lane,
 // `o.cell < 0` = dropped) into their scratch cells `sc`.  Lanes hitting the same cell are
-// combined first (__match_any_sync + reduce_peers) when >= 16 lanes repeat their neighbour's
-// cell (dense clouds), so that one lane issues the REDs of the group.  All 32 lanes must call
+// combined first (reduce_runs over runs of consecutive lanes) when >= 16 lanes repeat their
+// neighbour's cell (dense clouds), so that one lane issues the REDs of each run.  All 32 lanes must call
 // this.  kFast: 1 = one colour group, 2 = one 1-channel average group, 0 = no group (height).
 // Scratch per cell: count word (colour: b | n << 32, else n_in | n_out << 32), record
 // [P, S, colour: r | g << 32 / average: n_g, colour: n_out / average: X], certificates
@@ -101,18 +132,26 @@ __device__ __forceinline__ uint2 cert_of(float t) {
 template <int kFast>
 __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, float ch0) {
   unsigned long long *rec = a.rec + (long long)sc * 4;
-  unsigned *cert = a.cert + (long long)sc * 4;
+  unsigned *cert = a.cert + (long long)sc * 2;
   const bool act = o.cell >= 0;
   const unsigned act_b = __ballot_sync(0xffffffffu, act);
   if (act_b == 0u) return;
   const int lane = threadIdx.x & 31;
   const unsigned key = act ? (unsigned)sc : 0xffffffffu;
   const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
-  const unsigned dup = __ballot_sync(0xffffffffu, act && lane > 0 && prev == key);
+  const unsigned same = __ballot_sync(0xffffffffu, lane > 0 && prev == key);
+  const unsigned dup = same & act_b;
   const bool agg = __popc(dup) >= 16;
-  const unsigned peers = agg ? __match_any_sync(0xffffffffu, key) : (1u << lane);
   const bool single = !agg;
-  const bool leader = act && (__ffs(peers) - 1 == lane);
+  // agg: runs of consecutive lanes of one cell are reduced to their head lane (reduce_runs)
+  const unsigned heads = ~same;
+  unsigned peers = 1u << lane;  // the lanes whose statistics this lane holds after the reduction
+  if (agg) {
+    const unsigned above = heads & ~((2u << lane) - 1u);  // heads after this lane (lane 31: none)
+    const unsigned upto = above ? (above & (0u - above)) - 1u : 0xffffffffu;
+    peers = upto & ~((1u << lane) - 1u);
+  }
+  const bool leader = act && (single || (heads >> lane & 1u));
   const bool inl = act && o.code == MEM_CODE_INLIER;
   const unsigned in_b = __ballot_sync(0xffffffffu, inl);
   // height statistics (inliers): sum 1/v, sum z/v, the certificate of z/v
@@ -125,27 +164,28 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     zw = (double)t;
     cs = cert_of(t);
   }
-  if (!single) {
-    w = reduce_peers(peers, w, OpAdd());
-    zw = reduce_peers(peers, zw, OpAdd());
-    cs.x = reduce_peers(peers, cs.x, OpMaxU());
-    cs.y = reduce_peers(peers, cs.y, OpMaxU());
+  // the group's statistics: colour words (kFast 1), the channel (kFast 2)
+  unsigned rg = 0u, bb = 0u;
+  double v = 0.0;
+  uint2 cx = make_uint2(0u, 0u);
+  bool fin = false;
+  if (kFast == 1 && act) {
+    const uint32_t bits = __float_as_uint(ch0);
+    rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
+    bb = bits & 255u;
+  } else if (kFast == 2) {
+    fin = act && isfinite(ch0);
+    v = fin ? (double)ch0 : 0.0;
+    cx = fin ? cert_of(ch0) : make_uint2(0u, 0u);
   }
+  const unsigned fin_b = kFast == 2 ? __ballot_sync(0xffffffffu, fin) : 0u;
+  if (!single) reduce_runs<kFast>(heads, w, zw, cs, rg, bb, v, cx);
   if constexpr (kFast == 1) {
     // colour: count word b | n << 32 (n = every filtered in-bounds point, D20; n > 0 marks the
     // cell touched), record [P, S, r | g << 32, n_out]; n_in > 0 iff P > 0 (every 1/v > 0)
-    unsigned rg = 0u, bb = 0u;
-    if (act) {
-      const uint32_t bits = __float_as_uint(ch0);
-      rg = ((bits >> 16) & 255u) | (((bits >> 8) & 255u) << 16);
-      bb = bits & 255u;
-    }
-    unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+    unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers & act_b);
     bool lead = leader;
-    if (!single) {
-      rg = reduce_peers(peers, rg, OpAdd());
-      bb = reduce_peers(peers, bb, OpAdd());
-    } else if (__popc(dup) >= MEM_PAIR_MIN) {
+    if (single && __popc(dup) >= MEM_PAIR_MIN) {
       // a LiDAR scan line puts ~30% of its in-window points in the cell of the previous
       // lane: the head of each run absorbs its successor, so such a pair costs one RED set
       const bool fol = dup >> lane & 1u;
@@ -172,10 +212,7 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       if (n_in) {
         red_add_f64(rec + kRecP, w);
         red_add_f64(rec + kRecS, zw);
-        if (cs.y) {
-          red_max_u32(cert, cs.x);
-          red_max_u32(cert + 1, cs.y);
-        }
+        if (cs.y) red_max_cert(cert, cert_slots(cs), 0u);
       }
       red_add_u64(rec + 2, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
       if (n_all != n_in) red_add_u64(rec + 3, (unsigned long long)(n_all - n_in));
@@ -183,35 +220,21 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
     return;
   }
   if (leader) {
-    const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers);
+    const unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers & act_b);
     red_add_u64(&a.cnt[sc], (unsigned long long)n_in | ((unsigned long long)(n_all - n_in) << 32));
     if (n_in) {
       red_add_f64(rec + kRecP, w);
       red_add_f64(rec + kRecS, zw);
-      if (cs.y) {
-        red_max_u32(cert, cs.x);
-        red_max_u32(cert + 1, cs.y);
-      }
     }
-  }
-  if constexpr (kFast == 2) {  // Eq.(1) sums of one channel; non-finite values skip the group (D31)
-    const bool fin = act && isfinite(ch0);
-    double v = fin ? (double)ch0 : 0.0;
-    uint2 cx = fin ? cert_of(ch0) : make_uint2(0u, 0u);
-    unsigned ng = fin ? 1u : 0u;
-    if (!single) {
-      ng = (unsigned)__popc(peers & __ballot_sync(0xffffffffu, fin));
-      v = reduce_peers(peers, v, OpAdd());
-      cx.x = reduce_peers(peers, cx.x, OpMaxU());
-      cx.y = reduce_peers(peers, cx.y, OpMaxU());
-    }
-    if (leader && ng) {
-      red_add_u64(rec + 2, (unsigned long long)ng);
-      red_add_f64(rec + 3, v);
-      if (cx.y) {
-        red_max_u32(cert + 2, cx.x);
-        red_max_u32(cert + 3, cx.y);
+    if constexpr (kFast == 2) {  // Eq.(1) sums of one channel; non-finite values skip the group (D31)
+      const unsigned ng = (unsigned)__popc(peers & fin_b);
+      if (ng) {
+        red_add_u64(rec + 2, (unsigned long long)ng);
+        red_add_f64(rec + 3, v);
       }
+      if ((n_in && cs.y) || (ng && cx.y)) red_max_cert(cert, n_in ? cert_slots(cs) : 0u, ng ? cert_slots(cx) : 0u);
+    } else if (n_in && cs.y) {
+      red_max_cert(cert, cert_slots(cs), 0u);
     }
   }
 }
@@ -393,8 +416,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
       cur = nxt;
     }
   } else {
+    float *s3 = reinterpret_cast<float *>(s_pts[wid][0]);  // 384 floats of the warp's item (vec3)
     for (int it = i0 + gw; it < i1; it += nwarps) {
       const Item t = item_of(a, it, i0);
+      if (a.vec3 && t.end - t.base >= kWarpPoints) {
+        // stride 3, a full item: 96 coalesced float4 loads (3 per lane), the 128 points then
+        // read back from shared memory (stride 3 words: conflict-free)
+        const float4 *src = reinterpret_cast<const float4 *>(a.pts + t.base * 3);
+        float4 v[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = ld_stream_f4(reinterpret_cast<const float *>(src + k * 32 + lane), pol);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) reinterpret_cast<float4 *>(s3)[k * 32 + lane] = v[k];
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kWarpPtsPerLane; ++u) {
+          const float *q = s3 + 3 * (u * 32 + lane);
+          px[u] = q[0]; py[u] = q[1]; pz[u] = q[2]; pw[u] = 0.0f;
+        }
+        __syncwarp();  // the slice is rewritten by the warp's next item
+        process_item<kDebug, kFast, MEM_FULL_ITEMS != 0>(a, t, px, py, pz, pw, packed, npk, cnt);
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < kWarpPtsPerLane; ++u) {  // all loads first (memory-level parallelism)
         const long long i = t.base + u * 32 + lane;

@@ -48,6 +48,7 @@ struct PassArgs {
   const float *pts;
   int stride;
   int vec4;                    // stride == 4 and 16-B aligned: one float4 per point
+  int vec3;                    // stride == 3, 16-B aligned, every map offset a multiple of 4: 3 float4 per 4 points
   int n_maps;
   // per-map frames, point offsets [n_maps+1] and tile prefix sums [n_maps+1]: inline in the
   // kernel parameters (fi, offi, tsi) for n_maps <= kInlineMaps (no copy per call), else in a
@@ -62,7 +63,7 @@ struct PassArgs {
   double inv_p_uniform;
   unsigned long long *cnt;     // RED path scratch [n_maps][HW]: count word
   unsigned long long *rec;     // [n_maps][HW][4]: P, S, group words
-  unsigned *cert;              // [n_maps][HW][4]: certificates {~min, max} of |z/v| and |channel|
+  unsigned *cert;              // [n_maps][HW][2]: certificate slots (bf16x2: S, X; k_red.cuh)
   unsigned long long *fb;      // [2 k]: the k-th cell k_cells could not certify (m * HW + cell);
                                // [2 k + 1]: its list offset | point count << 32 (k_collect, k_refold)
   int *fbmark;                 // [n_maps][HW]: k of an uncertified cell, else -1 (reset by k_refold)

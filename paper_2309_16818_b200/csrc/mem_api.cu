@@ -806,7 +806,7 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
   if (cells > m->red_cells) {
     CU(cudaStreamSynchronize(m->stream));
     void **bufs[] = {&m->rcnt_s, &m->rrec_s, &m->rcert_s, &m->rfb_s, &m->rmark_s, &m->rfill_s, &m->rmapfb_s};
-    const size_t bytes[] = {8 * cells, 32 * cells, 16 * cells, 16 * cells, 4 * cells, 4 * cells, 4 * (size_t)B};
+    const size_t bytes[] = {8 * cells, 32 * cells, 8 * cells, 16 * cells, 4 * cells, 4 * cells, 4 * (size_t)B};
     for (void **b : bufs) {
       cudaFree(*b);
       *b = nullptr;
@@ -1196,6 +1196,9 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     return f;
   };
   a.vec4 = (stride == 4 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
+  a.vec3 = (stride == 3 && ((uintptr_t)dpts & 15) == 0) ? 1 : 0;
+  for (int i = 0; i <= B && a.vec3 && offsets; ++i)
+    if (offsets[i] & 3) a.vec3 = 0;
   // fast paths (k_bin carries the channel word in the record): one colour or 1-channel average
   // group bound to the float4's w (never for other strides or unaligned buffers);
   // no binding at all: height only

@@ -1,5 +1,6 @@
-# k_sort / k_fuse of one C3 depth cloud and k_bin of the C2x64 step under ncu --set full
-python tools/c3_probe.py 3 > gpurun_out/plain_c3.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_sort|k_fuse" -s 8 -c 2 -o gpurun_out/prof_c3 python tools/c3_probe.py 3 > gpurun_out/ncu1.log 2>&1; \
-CMD="python bench.py --steps 2 --warmup 2 --no-sides --no-e2e --no-cpu"
-ncu --set full --clock-control none --import-source on -k regex:"k_bin" -s 2 -c 1 -o gpurun_out/prof_bin2 $CMD > gpurun_out/ncu2.log 2>&1; tail -n 2 gpurun_out/ncu1.log gpurun_out/ncu2.log
+# ncu --set full of the C3 frame's kernels (one launch each after warm-up): k_points, k_cells,
+# k_collect, k_refold, k_image.  usage: bash tools/prof_c3.sh <tag>
+TAG=${1:-c3}
+python tools/c3_probe.py 3 > gpurun_out/${TAG}_plain_c3.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_points|k_cells|k_refold|k_collect|k_image" -s 40 -c 6 \
+    -o gpurun_out/${TAG}_full_c3 python tools/c3_probe.py 3 > gpurun_out/${TAG}_ncu_c3.log 2>&1; tail -n 2 gpurun_out/${TAG}_ncu_c3.log
