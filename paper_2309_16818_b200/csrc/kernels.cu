@@ -16,6 +16,7 @@
 //
 // Everything is stream-ordered; no kernel synchronises the host.
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -238,13 +239,18 @@ cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
 int pca_parts(int HW) { return (int)std::min<long long>(2 * 148, (HW + kPcaTile - 1) / kPcaTile); }
 
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
-  k_pca_moments<<<a.nparts, kThreads, sizeof(float) * a.d * (kPcaTile + 1), s>>>(a);
+  const size_t smem = sizeof(double) * kPcaTile * pca_ldc(a.d);
+  cudaError_t e = cudaFuncSetAttribute(k_pca_moments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_pca_moments<<<a.nparts, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pca_eigen(const PcaArgs &a, cudaStream_t s) {
-  const int dp = (a.d + 1) & ~1;
-  const size_t smem = 2 * sizeof(double) * (size_t)dp * (dp + 1);
+  const int nv = a.d + a.d * (a.d + 1) / 2 + 1;
+  k_pca_sum<<<cdiv(nv, 32), kThreads, 0, s>>>(a);
+  // A [d][d + 1], eigenvectors [k][d], LU scratch [4][k][d]
+  const size_t smem = sizeof(double) * ((size_t)a.d * (a.d + 1) + 5 * (size_t)a.k * a.d);
   cudaError_t e = cudaFuncSetAttribute(k_pca_eigen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_pca_eigen<<<1, kPcaEigThreads, smem, s>>>(a);

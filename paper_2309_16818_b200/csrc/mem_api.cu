@@ -1477,8 +1477,6 @@ mem_status mem_set_layer(mem_map *m, const char *name, const float *src) {
   return MEM_OK;
 }
 
-// cyclic Jacobi eigen-decomposition of a symmetric d x d matrix (row-major, destroyed);
-// eigenvalues in w, eigenvectors in the columns of V
 mem_status mem_pca_readout(mem_map *m, const char *group, int k, float *out) {
   if (check_map(m)) return MEM_EINVAL;
   if (!group || !out) return fail(MEM_EINVAL, "group and out must be non-NULL");
