@@ -276,8 +276,8 @@ MEM_API mem_status mem_set_layer(mem_map *map, const char *name, const float *sr
 /* PCA readout of a feature group (BASELINE configs[3]):
  * per map, over the cells where the group is observed: covariance of the group's values
  * (average / class_average: theta; gaussian: means) from fp64 moments, top-k eigenvectors
- * (parallel cyclic Jacobi in one CTA on the device; each sign makes its largest-|coefficient|
- * positive), projections min-max scaled to [0, 1] (0 when the component is constant or beyond
+ * (one CTA on the device: Householder tridiagonalisation, Sturm multisection, inverse
+ * iteration; each sign makes its largest-|coefficient| positive), projections min-max scaled to [0, 1] (0 when the component is constant or beyond
  * the covariance's rank, and on unobserved cells).  out: n_maps x k x rows x cols float32,
  * logical row-major, host or device.  Stream-ordered: nothing returns to the host (a host
  * `out` is copied back and the stream synchronised).

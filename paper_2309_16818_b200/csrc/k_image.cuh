@@ -71,72 +71,89 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 }
 
 // ---------------------------------------------------------------- k_image (a11-a12)
-// The per-channel rules (average, class_average, color, class_bayesian, gaussian) with N_j = 1,
-// kImgBatch channels at a time: the pixel and state loads of a batch are all issued before its
-// math and stores (apply_group's per-channel load -> store chain is one L2 round trip per
-// channel, since the compiler cannot move a load over a store to a possibly aliasing layer).
-// Same rule calls, same operands, same order: results are identical to apply_group's.
+// kImgLanes lanes per logical cell (consecutive lanes of one warp: a "group"); every lane of a
+// group computes the cell's projection (a11, identical operands and order), the occlusion walk
+// runs on the group's first lane.  The channels of a binding are split over the lanes --
+// channel k on lane k % L -- so each lane's pixel and state loads (at most kImgBatch channels
+// per batch) are all in flight together; the D21 finiteness test is an AND over the group and
+// the class_max argmax a (value, lowest channel) reduction over the group.  Every channel is
+// fused by exactly the rule calls of apply_group (same operands, same order per channel), so
+// results are identical to the one-thread-per-cell form.
 #ifndef MEM_IMG_BATCH
 #define MEM_IMG_BATCH 16
 #endif
+#ifndef MEM_IMG_LANES
+#define MEM_IMG_LANES 4
+#endif
 constexpr int kImgBatch = MEM_IMG_BATCH;
+constexpr int kImgLanes = MEM_IMG_LANES;
+// the group's channels k = sub, sub + L, ... of one binding fused with N_j = 1
 __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW, long long cell, const GroupDesc &g,
-                                                 const float *ch, long long plane) {
+                                                 const float *ch, long long plane, int sub, unsigned gmask) {
   float *vals = reinterpret_cast<float *>(st.words);
   uint8_t *obs = st.flags + (long long)g.flag * BHW + cell;
   const bool observed = *obs != 0;
   const bool dir = g.rule == MEM_CLASS_BAYESIAN;
+  constexpr int L = kImgLanes;
   if (g.rule == MEM_GAUSSIAN) {  // two words per channel: mean at word0 + k, variance at word0 + nch + k
-    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch) {
+    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch * L) {
       float p[kImgBatch], mu[kImgBatch], var[kImgBatch];
 #pragma unroll
       for (int u = 0; u < kImgBatch; ++u) {
-        if (k0 + u < g.nch) {
-          p[u] = __ldg(ch + (long long)(k0 + u) * plane);
-          mu[u] = vals[(long long)(g.word0 + k0 + u) * BHW + cell];
-          var[u] = vals[(long long)(g.word0 + g.nch + k0 + u) * BHW + cell];
+        const int k = k0 + u * L + sub;
+        if (k < g.nch) {
+          p[u] = __ldg(ch + (long long)k * plane);
+          mu[u] = vals[(long long)(g.word0 + k) * BHW + cell];
+          var[u] = vals[(long long)(g.word0 + g.nch + k) * BHW + cell];
         }
       }
 #pragma unroll
       for (int u = 0; u < kImgBatch; ++u) {
-        if (k0 + u < g.nch) {
+        const int k = k0 + u * L + sub;
+        if (k < g.nch) {
           rule_gaussian(mu[u], var[u], observed, (double)p[u], 1.0, g);
-          vals[(long long)(g.word0 + k0 + u) * BHW + cell] = mu[u];
-          vals[(long long)(g.word0 + g.nch + k0 + u) * BHW + cell] = var[u];
+          vals[(long long)(g.word0 + k) * BHW + cell] = mu[u];
+          vals[(long long)(g.word0 + g.nch + k) * BHW + cell] = var[u];
         }
       }
     }
-    *obs = 1;
-    return;
-  }
-  for (int k0 = 0; k0 < g.nch; k0 += kImgBatch) {
-    float p[kImgBatch], th[kImgBatch];
+  } else {
+    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch * L) {
+      float p[kImgBatch], th[kImgBatch];
 #pragma unroll
-    for (int u = 0; u < kImgBatch; ++u) {
-      if (k0 + u < g.nch) {
-        p[u] = __ldg(ch + (long long)(k0 + u) * plane);
-        th[u] = vals[(long long)(g.word0 + k0 + u) * BHW + cell];
+      for (int u = 0; u < kImgBatch; ++u) {
+        const int k = k0 + u * L + sub;
+        if (k < g.nch) {
+          p[u] = __ldg(ch + (long long)k * plane);
+          th[u] = vals[(long long)(g.word0 + k) * BHW + cell];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kImgBatch; ++u) {
+        const int k = k0 + u * L + sub;
+        if (k < g.nch)
+          vals[(long long)(g.word0 + k) * BHW + cell] =
+              dir ? rule_dirichlet(th[u], observed, (double)p[u], g.a0) : rule_average(th[u], observed, (double)p[u], 1.0, g.w);
       }
     }
-#pragma unroll
-    for (int u = 0; u < kImgBatch; ++u) {
-      if (k0 + u < g.nch)
-        vals[(long long)(g.word0 + k0 + u) * BHW + cell] =
-            dir ? rule_dirichlet(th[u], observed, (double)p[u], g.a0) : rule_average(th[u], observed, (double)p[u], 1.0, g.w);
-    }
   }
-  *obs = 1;
+  __syncwarp(gmask);  // every lane has read `observed`
+  if (sub == 0) *obs = 1;
 }
 
 #ifndef MEM_IMG_THREADS
 #define MEM_IMG_THREADS 256
 #endif
-// one thread per logical cell; 256-thread CTAs measured faster than 64 / 128
 constexpr int kImgThreads = MEM_IMG_THREADS;
+constexpr int kImgCells = kImgThreads / kImgLanes;  // cells per CTA
 __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ ImageArgs a) {
+  constexpr int L = kImgLanes;
   const Geometry &g = a.geo;
   const int m = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+  const unsigned gmask = (unsigned)((1ull << L) - 1ull) << (lane & ~(L - 1));
+  const int t = blockIdx.x * kImgCells + (int)(threadIdx.x / L);
+  // every exit below depends on the cell only: uniform over the group
   if (t >= g.HW) return;
   const int row = t / g.W, col = t - (t / g.W) * g.W;  // logical cell
   const int2 ring = a.ring[m];
@@ -161,51 +178,70 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
   const float v = f.K[3] * uy + f.K[4];
   const float fu = floorf(u + 0.5f), fv = floorf(v + 0.5f);  // nearest pixel (D16)
   if (!(0.0f <= fu && fu < (float)a.IW && 0.0f <= fv && fv < (float)a.IH)) return;  // frustum
-  if (a.occlusion && !cell_visible(a, m, row, col, f.t[0], f.t[1], f.t[2], hcell, ring)) return;
+  if (a.occlusion) {  // the walk on the group's first lane
+    bool vis = false;
+    if (sub == 0) vis = cell_visible(a, m, row, col, f.t[0], f.t[1], f.t[2], hcell, ring);
+    if (!__shfl_sync(gmask, vis, 0, L)) return;
+  }
   const long long plane = (long long)a.IH * a.IW;
   const float *pix = a.img + (long long)m * a.map_stride + (long long)(int)fv * a.IW + (int)fu;
   // a12: sample and fuse with N_j = 1
   for (int bi = 0; bi < a.nb; ++bi) {
     const BindDesc &b = a.b[bi];
     const float *ch = pix + (long long)b.ch_offset * plane;
-    if (b.topk > 0) {  // top-k pairs (D38)
-      const TopK tk{ch, plane, b.topk, b.g.nch - 1};
-      if (!tk.ok()) continue;
-      const unsigned long long key = b.g.rule == MEM_CLASS_MAX ? tk.key() : 0ull;
-      apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)tk.value(k); }, key);
+    if (b.topk > 0) {  // top-k pairs (D38): the group's first lane
+      if (sub == 0) {
+        const TopK tk{ch, plane, b.topk, b.g.nch - 1};
+        if (tk.ok()) {
+          const unsigned long long key = b.g.rule == MEM_CLASS_MAX ? tk.key() : 0ull;
+          apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)tk.value(k); }, key);
+        }
+      }
+      __syncwarp(gmask);
       continue;
     }
+    // D21 finiteness over all channels, and class_max's first maximum in channel order
     bool fin = true;
-    for (int k0 = 0; k0 < b.nch; k0 += kImgBatch) {  // loads of a batch in flight together
+    float bv = -INFINITY;
+    int best = -1;
+    for (int k0 = 0; k0 < b.nch; k0 += kImgBatch * L) {  // loads of a batch in flight together
       float c[kImgBatch];
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) c[u] = k0 + u < b.nch ? __ldg(ch + (long long)(k0 + u) * plane) : 0.0f;
+      for (int q = 0; q < kImgBatch; ++q) {
+        const int k = k0 + q * L + sub;
+        c[q] = k < b.nch ? __ldg(ch + (long long)k * plane) : 0.0f;
+      }
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) fin &= (bool)isfinite(c[u]);
-    }
-    if (!fin) continue;  // D21
-    unsigned long long key = 0ull;
-    if (b.g.rule == MEM_CLASS_MAX) {
-      int best = 0;
-      float bv = __ldg(ch);
-      for (int k0 = 1; k0 < b.nch; k0 += kImgBatch) {  // first maximum in channel order wins
-        float c[kImgBatch];
-#pragma unroll
-        for (int u = 0; u < kImgBatch; ++u) c[u] = k0 + u < b.nch ? __ldg(ch + (long long)(k0 + u) * plane) : 0.0f;
-#pragma unroll
-        for (int u = 0; u < kImgBatch; ++u) {
-          if (k0 + u < b.nch && c[u] > bv) {
-            bv = c[u];
-            best = k0 + u;
+      for (int q = 0; q < kImgBatch; ++q) {
+        const int k = k0 + q * L + sub;
+        if (k < b.nch) {
+          fin &= (bool)isfinite(c[q]);
+          if (best < 0 || c[q] > bv) {  // this lane's channels in increasing order
+            bv = c[q];
+            best = k;
           }
         }
       }
-      key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
     }
-    if (b.g.rule != MEM_CLASS_MAX) {
-      image_fuse_words(a.st, g.BHW, cell, b.g, ch, plane);
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) {
+      fin &= (bool)__shfl_xor_sync(gmask, (int)fin, o, L);
+      const float ov = __shfl_xor_sync(gmask, bv, o, L);
+      const int ob = __shfl_xor_sync(gmask, best, o, L);
+      if (ob >= 0 && (best < 0 || ov > bv || (ov == bv && ob < best))) {  // larger, or equal and earlier
+        bv = ov;
+        best = ob;
+      }
+    }
+    if (!fin) continue;  // D21 (uniform over the group)
+    if (b.g.rule == MEM_CLASS_MAX) {
+      if (sub == 0) {
+        const unsigned long long key = ((unsigned long long)ord_f32(bv) << 32) | (unsigned)(b.nch - 1 - best);
+        apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)__ldg(ch + k * plane); }, key);
+      }
+      __syncwarp(gmask);
       continue;
     }
-    apply_group(a.st, g.BHW, cell, b.g, 1.0, [&](int k) { return (double)__ldg(ch + k * plane); }, key);
+    image_fuse_words(a.st, g.BHW, cell, b.g, ch, plane, sub, gmask);
   }
 }

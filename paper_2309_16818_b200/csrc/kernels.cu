@@ -226,7 +226,7 @@ cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long l
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
-  k_image<<<dim3(cdiv(a.geo.HW, kImgThreads), a.geo.n_maps), kImgThreads, 0, s>>>(a);
+  k_image<<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
