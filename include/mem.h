@@ -163,26 +163,24 @@ MEM_API mem_status mem_synchronize(mem_map *map);
 
 /* ---- one big map sharded across ranks ----------------------------
  * Rank r owns the physical row band [r*rows/nranks, (r+1)*rows/nranks) (rows divisible by
- * nranks) and every rank takes its own shard of each frame's points.  Two protocols:
- *  - point routing (default for nranks > 1): each rank filters and bins its shard, counts its dropped
- *    points, and sends every in-window point to the owner of its cell's band; the owner tests,
- *    accumulates and fuses what it received (in source-rank order) for its band only.  A rank
- *    keeps only its own band current (the readout all-gathers; an image input with occlusion
- *    all-gathers elevation and valid first).
- *  - statistics exchange (maps created with MEM_FLAG_DEBUG_POINTS, whose per-point codes need
- *    the test on the routing rank, or env MEM_ROUTE=0): every rank accumulates its shard into
- *    full-map per-cell statistics, which are moved to the band owners, folded by a typed merge
- *    kernel (f64 sums, u64 sums, u64 max) and fused for the band; elevation, variance and
- *    valid are then all-gathered for the next frame's Mahalanobis test.
+ * nranks) and every rank takes its own shard of each frame's points.  Point routing: each rank
+ * filters and bins its shard, counts its dropped points, and sends every in-window point to the
+ * owner of its cell's band (a stable scatter: input order within each destination); the owner
+ * tests, accumulates and fuses what it received -- source ranks in order, each in input order,
+ * i.e. the global input order -- for its band only, so every cell equals the unsharded map bit
+ * for bit.  A rank keeps only its own band current (the readout all-gathers; an image input
+ * with occlusion all-gathers elevation and valid first).  With MEM_FLAG_DEBUG_POINTS the
+ * owners' inlier / outlier codes are returned to the source ranks.
  * Counters (mem_frame_stats) are per rank and add up to the unsharded counters.  Transport:
- *  - NCCL (nccl_id != NULL, one process per GPU): grouped ncclSend/ncclRecv of the bands and
- *    ncclAllGather, stream-ordered on the map's stream.  Every call on a sharded map is
+ *  - NCCL (nccl_id != NULL, one process per GPU): the per-destination counts all-gathered
+ *    (one host synchronisation per point input), the points moved with grouped
+ *    ncclSend/ncclRecv, stream-ordered on the map's stream.  Every call on a sharded map is
  *    collective (all ranks, same order); mem_get_layer all-gathers every layer first.
  *  - local (nccl_id == NULL): the nranks shards live in one process on one device (testing
- *    and single-GPU emulation); mem_input_pointcloud only accumulates, and
- *    mem_shard_local_sync(shards) performs the exchange, the band fusion and a full state
- *    replication with device copies; call it after every input (point cloud or image), with
- *    every shard having taken the same sequence of calls.  All shards must use the same stream.
+ *    and single-GPU emulation); mem_input_pointcloud only routes, and
+ *    mem_shard_local_sync(shards) moves the routed points with device copies and runs the
+ *    owners' passes; call it after every point input, with every shard having taken the same
+ *    sequence of calls.  All shards must use the same stream.
  * Images: every rank takes the whole image and fuses the cells of its own band (the image
  * fusion is per cell, PAPER §3.3); moves are replicated (every rank calls mem_move_to).
  * Errors: EINVAL (rows % nranks, rank range, shards out of step), ENOMEM, ECOMM (NCCL), ECUDA. */

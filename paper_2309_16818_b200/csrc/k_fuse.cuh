@@ -83,18 +83,31 @@ __device__ __forceinline__ void fuse_generic(const PassArgs &a, long long gc, co
       }
       continue;
     }
-    // the points whose channels are usable (D31, D38): bit 16 + bi of the record (k_bin)
-    unsigned ng = 0u;
-    for (int r = 0; r < n; ++r) ng += __ldcg(&rec[r].x) >> (16 + bi) & 1u;
+    // the points whose channels are usable (D31, D38): bit 16 + bi of the record (k_bin); a
+    // short cell (n <= kShortSeg): its point indices in registers, then per channel every
+    // point's value in flight together, summed in input order
+    unsigned ng = 0u, okm = 0u, pidx[kShortSeg];
+#pragma unroll
+    for (int r = 0; r < kShortSeg; ++r) {
+      pidx[r] = 0u;
+      if (r < n) {
+        const uint4 q = __ldcg(rec + r);
+        pidx[r] = q.w;
+        if (q.x >> (16 + bi) & 1u) okm |= 1u << r;
+      }
+    }
+    ng = __popc(okm);
     if (ng == 0u) continue;  // no finite point: the group is not updated (D31)
     uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
     const bool obb = *obs != 0;
     for (int k = 0; k < gd.nch; ++k) {
+      float cv[kShortSeg];
+#pragma unroll
+      for (int r = 0; r < kShortSeg; ++r) cv[r] = (okm >> r & 1u) ? chan_value(a, b, pidx[r], k) : 0.0f;
       double sum = 0.0;
-      for (int r = 0; r < n; ++r) {
-        const uint4 q = __ldcg(rec + r);
-        if (q.x >> (16 + bi) & 1u) sum += (double)chan_value(a, b, q.w, k);
-      }
+#pragma unroll
+      for (int r = 0; r < kShortSeg; ++r)
+        if (okm >> r & 1u) sum += (double)cv[r];
       float *t = vals + (long long)(gd.word0 + k) * BHW + gc;
       switch (gd.rule) {
         case MEM_AVERAGE:
@@ -348,8 +361,12 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
   const float tau2 = a.np.tau2;
   double P = 0.0, S = 0.0, X = 0.0;
   unsigned nin = 0u, nout = 0u, cr = 0u, cg = 0u, cb = 0u, na = 0u;
+  // pass 1: the a7 decisions, the counts, and the fp64 sums as warp trees together with the
+  // exactness certificate of the cell's terms (k_red.cuh): when it holds, every partial sum is
+  // exact and the trees equal the oracle's sequential sums bit for bit
   uint4 q = make_uint4(0u, 0u, 0u, 0u);
   if (lane < n) q = __ldcg(rec + lane);
+  unsigned ewmax = 0u, ewmin = 255u, ezmax = 0u, ezmin = 255u;
   for (int b0 = 0; b0 < n; b0 += 32) {
     const int m_ = n - b0 < 32 ? n - b0 : 32;
     const bool act = lane < m_;
@@ -363,19 +380,60 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
     if (inl) {
       w = 1.0f / v;
       zw = z * w;
-    }
-    const unsigned im = __ballot_sync(0xffffffffu, inl);
-    nin += __popc(im);
-    nout += __popc(__ballot_sync(0xffffffffu, outl));
-    for (int j = 0; j < m_; ++j) {  // input order
-      const float wj = __shfl_sync(0xffffffffu, w, j), zj = __shfl_sync(0xffffffffu, zw, j);
-      if (im >> j & 1u) {
-        P += (double)wj;
-        S += (double)zj;
+      const unsigned ew = max((__float_as_uint(w) >> 23) & 255u, 1u);
+      ewmax = max(ewmax, ew);
+      ewmin = min(ewmin, ew);
+      if (zw != 0.0f) {
+        const unsigned ez = max((__float_as_uint(zw) >> 23) & 255u, 1u);
+        ezmax = max(ezmax, ez);
+        ezmin = min(ezmin, ez);
       }
     }
+    nin += __popc(__ballot_sync(0xffffffffu, inl));
+    nout += __popc(__ballot_sync(0xffffffffu, outl));
+    double tw = (double)w, tz = (double)zw;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tw += __shfl_xor_sync(0xffffffffu, tw, o);
+      tz += __shfl_xor_sync(0xffffffffu, tz, o);
+    }
+    P += tw;
+    S += tz;
     if (kDebug && act) a.dbg_code[__ldcg(a.sridx + seg.y + b0 + lane)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
     q = nq;
+  }
+  ewmax = __reduce_max_sync(0xffffffffu, ewmax);
+  ewmin = __reduce_min_sync(0xffffffffu, ewmin);
+  ezmax = __reduce_max_sync(0xffffffffu, ezmax);
+  ezmin = __reduce_min_sync(0xffffffffu, ezmin);
+  const unsigned lg = cert_ceil_log2(nin);
+  const bool exact = (nin == 0u || ewmax - ewmin + lg <= 29u) && (ezmax < ezmin || ezmax - ezmin + lg <= 29u);
+  if (!exact) {  // pass 2: the oracle's sequential fold
+    P = S = 0.0;
+    if (lane < n) q = __ldcg(rec + lane);
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int m_ = n - b0 < 32 ? n - b0 : 32;
+      const bool act = lane < m_;
+      uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+      if (b0 + 32 + lane < n) nq = __ldcg(rec + b0 + 32 + lane);
+      const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
+      const float d = z - h;  // a7 (D10)
+      const bool inl = act && !(d * d > tau2 * (s2 + v));
+      float w = 0.0f, zw = 0.0f;
+      if (inl) {
+        w = 1.0f / v;
+        zw = z * w;
+      }
+      const unsigned im = __ballot_sync(0xffffffffu, inl);
+      for (int j = 0; j < m_; ++j) {  // input order
+        const float wj = __shfl_sync(0xffffffffu, w, j), zj = __shfl_sync(0xffffffffu, zw, j);
+        if (im >> j & 1u) {
+          P += (double)wj;
+          S += (double)zj;
+        }
+      }
+      q = nq;
+    }
   }
   if (lane == 0) {
     cnt[5] += nin;
@@ -433,24 +491,53 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
       if (ng == 0u) continue;  // D31
       uint8_t *obs = a.st.flags + (long long)gd.flag * BHW + gc;
       const bool obb = *obs != 0;
-      for (int k = 0; k < gd.nch; ++k) {
-        double sum = 0.0;
+      // lane = point: each channel's values of a batch of 32 points are gathered by one warp
+      // load and summed by a warp tree; lane kk of block k0 keeps channel k0 + kk's sum and the
+      // exactness certificate of its terms (k_red.cuh: exponent range + ceil(log2 ng) <= 29 makes
+      // every partial sum exact, so the tree sums equal the oracle's sequential ones); a channel
+      // whose certificate fails is re-summed by its lane sequentially in input order
+      for (int k0 = 0; k0 < gd.nch; k0 += 32) {
+        const int nk = gd.nch - k0 < 32 ? gd.nch - k0 : 32;
+        double acc = 0.0;
+        unsigned emx = 0u, emn = 255u;
         for (int b0 = 0; b0 < n; b0 += 32) {
-          float val = 0.0f;
+          unsigned pid = 0u;
           bool ok = false;
           if (b0 + lane < n) {
             const uint4 r = __ldcg(rec + b0 + lane);
             ok = r.x >> (16 + bi) & 1u;
-            if (ok) val = chan_value(a, b, r.w, k);
+            pid = r.w;
           }
-          const unsigned om = __ballot_sync(0xffffffffu, ok);
-          const int m_ = n - b0 < 32 ? n - b0 : 32;
-          for (int j = 0; j < m_; ++j) {  // input order
-            const float vj = __shfl_sync(0xffffffffu, val, j);
-            if (om >> j & 1u) sum += (double)vj;
+          for (int kk0 = 0; kk0 < nk; kk0 += 4) {
+            float cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cv[u] = ok && kk0 + u < nk ? chan_value(a, b, pid, k0 + kk0 + u) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const unsigned e = cv[u] != 0.0f ? max((__float_as_uint(cv[u]) >> 23) & 255u, 1u) : 0u;
+              const unsigned ex = __reduce_max_sync(0xffffffffu, e);
+              const unsigned en = __reduce_min_sync(0xffffffffu, e ? e : 255u);
+              double t = (double)cv[u];
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+              if (lane == kk0 + u) {
+                acc += t;
+                emx = max(emx, ex);
+                emn = min(emn, en);
+              }
+            }
           }
         }
-        if (lane == 0) {
+        const int k = k0 + lane;
+        if (lane < nk && !(emx < emn || emx - emn + cert_ceil_log2(ng) <= 29u)) {
+          acc = 0.0;  // uncertified: the oracle's sequential sum of this channel
+          for (int r = 0; r < n; ++r) {
+            const uint4 q = __ldcg(rec + r);
+            if (q.x >> (16 + bi) & 1u) acc += (double)chan_value(a, b, q.w, k);
+          }
+        }
+        const double sum = acc;
+        if (lane < nk) {
           float *t = wv + (long long)(gd.word0 + k) * BHW + gc;
           switch (gd.rule) {
             case MEM_AVERAGE:
@@ -468,6 +555,7 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
           }
         }
       }
+      __syncwarp();  // every lane has read `obb`
       if (lane == 0) *obs = 1;
     }
   }

@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
     const int cpt = (ncell + kSortThreads - 1) / kSortThreads;
     const int cb = tid * cpt, ce = cb + cpt < ncell ? cb + cpt : ncell;
     // fast paths: short cells (<= kShortSeg points) a thread each, mid-size cells (<= kMidSeg)
-    // 8 lanes each, long cells 16 lanes each; generic groups: a thread or a warp
-    const unsigned smax = a.fast ? (unsigned)kShortSeg : (unsigned)kMidSeg, mmax = (unsigned)kMidSeg;
+    // 8 lanes each, long cells 16 lanes each; generic groups: a thread (<= kShortSeg) or a warp
+    const unsigned smax = (unsigned)kShortSeg, mmax = a.fast ? (unsigned)kMidSeg : (unsigned)kShortSeg;
     unsigned tot = 0u, ns = 0u, nm = 0u, nl = 0u;
     for (int cc = cb; cc < ce; ++cc) {
       const unsigned x = cst_s[cc];
