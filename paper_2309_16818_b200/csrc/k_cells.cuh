@@ -181,19 +181,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
 // The cells k_cells could not certify (their fp64 sums might depend on the order of the REDs)
 // are recomputed from their points in input order, exactly as the oracle folds them.
 //
-// k_collect: a grid-stride pass over the warp-items of the maps that have such a cell (nothing
-// when there is none): a2-a6 for each point (bin_point); a point whose cell is listed appends
-// its index (relative to the map's first point) to the cell's slice of fblist (an atomic slot:
-// any order).
-template <int kFast>
-__global__ void __launch_bounds__(kThreads) k_collect(const __grid_constant__ PassArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  if (*(volatile unsigned *)&a.ctl->n_fb == 0u) return;
+// k_refold is a cooperative launch (all CTAs resident) and returns at once when no cell is
+// listed.  Phase 1 (collect_points): a grid-stride pass over the warp-items of the maps that
+// have a listed cell: a2-a6 for each point (bin_point); a point whose cell is listed appends its
+// index (relative to the map's first point) to the cell's slice of fblist (an atomic slot: any
+// order).  A grid barrier, then phase 2 below.
+__device__ __forceinline__ void collect_points(const PassArgs &a) {
   const Geometry &g = a.geo;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nwarps = gridDim.x * (kThreads / 32);
-  const int gw = blockIdx.x * (kThreads / 32) + wid;
+  const int nwarps = gridDim.x * (blockDim.x / 32);
+  const int gw = blockIdx.x * (blockDim.x / 32) + wid;
   const int i0 = ps_of(a, a.m0), i1 = ps_of(a, a.m1);
   for (int it = i0 + gw; it < i1; it += nwarps) {
     const Item t = item_of(a, it, i0);
@@ -329,6 +326,9 @@ __global__ void __launch_bounds__(kRefoldThreads) k_refold(const __grid_constant
   unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const Geometry &g = a.geo;
   const unsigned nfb = *(volatile unsigned *)&a.ctl->n_fb;
+  if (nfb == 0u) return;  // uniform over the grid
+  collect_points(a);
+  cooperative_groups::this_grid().sync();
   const float *vals = reinterpret_cast<const float *>(a.st.words);
   for (unsigned k = blockIdx.x; k < nfb; k += gridDim.x) {
     const long long gc = (long long)__ldcg(a.fb + 2 * k);

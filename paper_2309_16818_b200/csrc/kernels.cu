@@ -24,6 +24,7 @@
 
 #include "kernels.cuh"
 
+#include <cooperative_groups.h>
 #include <cub/block/block_radix_sort.cuh>
 
 #ifndef MEM_OCC_BATCH
@@ -173,16 +174,32 @@ static cudaError_t launch_cells_t(const PassArgs &a, cudaStream_t s) {
                                                        (chunks + 7) / 8));
   cudaError_t e = launch_pdl(k_cells<kFast>, g, 0, s, a, kThreads);
   if (e != cudaSuccess) return e;
-  // uncertified cells (none: both kernels return at once)
-  const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1]);
-  int gc = resident_grid(k_collect<kFast>, kThreads, 9 + kFast);
-  if (items > 0) gc = (int)std::max(1LL, std::min<long long>(gc, (items + 7) / 8));
-  e = launch_pdl(k_collect<kFast>, gc, 0, s, a, kThreads);
-  if (e != cudaSuccess) return e;
+  // uncertified cells (none: k_refold returns at once): a cooperative launch (its collect
+  // phase and its folds are separated by a grid barrier), every CTA resident
   const size_t smem = refold_smem_bytes<kFast>();
   e = cudaFuncSetAttribute(k_refold<kFast>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_refold<kFast>, 148, smem, s, a, kRefoldThreads);
+  static int coop[64][4] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &grid = coop[dev & 63][kFast];
+  if (!grid) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refold<kFast>, kRefoldThreads, smem);
+    grid = std::max(1, sms * std::max(1, std::min(per, 1)));
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRefoldThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_refold<kFast>, a);
 }
 
 cudaError_t launch_cells(const PassArgs &a, cudaStream_t s) {
