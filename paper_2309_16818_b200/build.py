@@ -58,6 +58,14 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_variant(out, defines):
+    """A copy of libmem built with other launch configurations (compile-time -D macros) at
+    `out` -- for the launch-configuration invariance test only; the shipped library is LIB."""
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *sources(), *LIBS]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -222,7 +222,10 @@ __device__ __forceinline__ void collect_points(const PassArgs &a) {
 // operation for operation the oracle's loop (a term of +0.0 stands for a skipped point: the
 // sums start at +0.0 and never become -0.0, so adding +0.0 leaves them bit-identical).  The
 // integer statistics are order-free (shared-memory atomics).  Then a9 + a10 (fuse_state).
-constexpr int kRefoldThreads = 512;
+#ifndef MEM_REFOLD_THREADS
+#define MEM_REFOLD_THREADS 512
+#endif
+constexpr int kRefoldThreads = MEM_REFOLD_THREADS;
 constexpr int kRefoldItems = 32;
 constexpr int kRefoldCap = kRefoldThreads * kRefoldItems;  // points of a cell sorted in shared memory
 constexpr int kRefoldChunk = 512;                          // terms folded per step

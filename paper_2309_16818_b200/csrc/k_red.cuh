@@ -416,18 +416,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ 
       cur = nxt;
     }
   } else {
-    float *s3 = reinterpret_cast<float *>(s_pts[wid][0]);  // 384 floats of the warp's item (vec3)
+    float *s3 = reinterpret_cast<float *>(s_pts[wid][0]);  // the 3 x kWarpPoints floats of the warp's item (vec3)
     for (int it = i0 + gw; it < i1; it += nwarps) {
       const Item t = item_of(a, it, i0);
       if (a.vec3 && t.end - t.base >= kWarpPoints) {
         // stride 3, a full item: 96 coalesced float4 loads (3 per lane), the 128 points then
         // read back from shared memory (stride 3 words: conflict-free)
         const float4 *src = reinterpret_cast<const float4 *>(a.pts + t.base * 3);
-        float4 v[3];
+        constexpr int kV3 = 3 * kWarpPoints / 4;  // float4 of the item
+        float4 v[(kV3 + 31) / 32];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) v[k] = ld_stream_f4(reinterpret_cast<const float *>(src + k * 32 + lane), pol);
+        for (int k = 0; k < (kV3 + 31) / 32; ++k)
+          if (k * 32 + lane < kV3) v[k] = ld_stream_f4(reinterpret_cast<const float *>(src + k * 32 + lane), pol);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) reinterpret_cast<float4 *>(s3)[k * 32 + lane] = v[k];
+        for (int k = 0; k < (kV3 + 31) / 32; ++k)
+          if (k * 32 + lane < kV3) reinterpret_cast<float4 *>(s3)[k * 32 + lane] = v[k];
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < kWarpPtsPerLane; ++u) {

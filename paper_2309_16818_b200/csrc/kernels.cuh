@@ -6,23 +6,35 @@ namespace memk {
 
 constexpr int kThreads = 256;           // 8 warps per CTA (image, readout, post, shift kernels)
 // k_bin: one CTA per tile of kTile consecutive points of one map, 8 points per thread
-constexpr int kBinThreads = 256;
+#ifndef MEM_BIN_THREADS
+#define MEM_BIN_THREADS 256
+#endif
+constexpr int kBinThreads = MEM_BIN_THREADS;
 constexpr int kBinPerThread = 8;
 constexpr int kTile = kBinThreads * kBinPerThread;  // 2048
 constexpr int kMaxBands = 2048;         // bands per map (k_bin's per-warp band counters)
 // k_sort: one CTA per (map, band); the band's records counting-sorted kSortCap at a time
-constexpr int kSortThreads = 128;
+#ifndef MEM_SORT_THREADS
+#define MEM_SORT_THREADS 128
+#endif
+constexpr int kSortThreads = MEM_SORT_THREADS;
 constexpr int kSortCap = 1024;          // records ranked per window (shared memory)
 constexpr int kSortChunk = 2048;        // band sizing: records expected per band
 constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in shared memory)
 // k_fuse: persistent grid-stride over the touched cells, one thread each
-constexpr int kFuseThreads = 128;
+#ifndef MEM_FUSE_THREADS
+#define MEM_FUSE_THREADS 128
+#endif
+constexpr int kFuseThreads = MEM_FUSE_THREADS;
 constexpr int kShortSeg = 8;           // cells of at most this many points: a thread each
 constexpr int kMidSeg = 64;            // at most this many: 8 lanes each (fast paths); longer: 16 lanes / a warp
 constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 // k_points: persistent grid-stride over 128-point warp-items (4 points per lane)
-constexpr int kWarpPtsPerLane = 4;
+#ifndef MEM_WARP_PTS
+#define MEM_WARP_PTS 4
+#endif
+constexpr int kWarpPtsPerLane = MEM_WARP_PTS;
 constexpr int kWarpPoints = 32 * kWarpPtsPerLane;
 
 // Control block of one point input (zeroed by one cudaMemsetAsync per call).

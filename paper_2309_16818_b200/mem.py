@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmem.so")
+# MEM_LIB: a variant build of the same sources (tests/test_launch_config_gpu.py only)
+LIB_PATH = os.environ.get("MEM_LIB") or os.path.join(HERE, "libmem.so")
 
 MEM_OK, MEM_EINVAL, MEM_EDUPNAME, MEM_ENOTFOUND, MEM_ERULE, MEM_EPOSE, MEM_ECUDA, MEM_ENOMEM, MEM_ECOMM = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
