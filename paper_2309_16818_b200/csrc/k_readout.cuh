@@ -276,12 +276,13 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// 1 / a to ~1 ulp: the MUFU approximation and two Newton steps (|a| >= DBL_MIN here)
+// 1 / a to a few ulp: the MUFU approximation and three Newton steps (|a| >= DBL_MIN here)
 __device__ __forceinline__ double rcp64(double a) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
-  r = fma(r, fma(-a, r, 1.0), r);
-  return fma(r, fma(-a, r, 1.0), r);
+  r = r + r * (1.0 - a * r);  // unfused (no FMA anywhere in the library, tests/test_abi.py)
+  r = r + r * (1.0 - a * r);
+  return r + r * (1.0 - a * r);
 }
 // number of eigenvalues of T (diagonal dg, squared off-diagonal e2) below x (Sturm count)
 __device__ __forceinline__ int sturm_count(const double *dg, const double *e2, int n, double x, double pivmin) {
