@@ -77,11 +77,6 @@ struct Geometry {
   long long BHW;  // n_maps * HW: stride between layers (< 2^31, so cell indices fit in int)
   float res, hH, hW;
   double inv_W;   // 1.0 / W for divmod_w (index arithmetic only)
-  // a5 binning thresholds (reading D13): xt[k] = the least fp32 x with
-  // fl(fl(x / res) + H/2) >= k, k = 0..H (yt likewise over W), computed once on the host from
-  // the oracle's expression; row = max{k : x >= xt[k]}, in the window iff xt[0] <= x < xt[H]
-  const float *xt, *yt;
-  float inv_res;  // (float)(1 / res): only the first guess of the row before the exact correction
 };
 
 struct State {

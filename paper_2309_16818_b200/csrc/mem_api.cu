@@ -107,7 +107,6 @@ struct mem_map {
   std::vector<Layer> layers;
   State st{};
   int2 *ring = nullptr;
-  float *bin_t = nullptr;    // a5 thresholds: rows [H+1] then columns [W+1] (Geometry::xt, yt)
   std::vector<long long> kx, ky;
   std::vector<int> r0, c0;
   // staging
@@ -193,9 +192,6 @@ struct mem_map {
     gg.hH = (float)H / 2.0f;
     gg.hW = (float)W / 2.0f;
     gg.inv_W = 1.0 / (double)W;
-    gg.xt = bin_t;
-    gg.yt = bin_t ? bin_t + (H + 1) : nullptr;
-    gg.inv_res = (float)(1.0 / (double)res);
     return gg;
   }
 };
@@ -346,20 +342,6 @@ static float least_true(long long lo, long long hi, P pred) {
     if (pred(kfloat(mid))) hi = mid; else lo = mid + 1;
   }
   return kfloat(lo);
-}
-// xt[k] = least x with fl(fl(x / res) + half) >= k, k = 0..n (a5, reading D13)
-static void bin_thresholds(float res, int n, std::vector<float> &t) {
-  const float half = (float)n / 2.0f;
-  t.resize(n + 1);
-  const long long lo = fkey(-INFINITY), hi = fkey(INFINITY);
-  for (int k = 0; k <= n; ++k) {
-    volatile float kf = (float)k;
-    t[k] = least_true(lo, hi, [&](float x) {
-      volatile float q = x / res;  // IEEE fp32 division, then fp32 addition (no contraction)
-      volatile float fr = q + half;
-      return fr >= kf;
-    });
-  }
 }
 // r_min <= sqrtf(r2) <= r_max  <=>  lo <= r2 <= hi over r2 >= +0 (a2, reading D9); an empty
 // set gives lo = +inf, hi = -1
@@ -512,7 +494,6 @@ void free_map(mem_map *m) {
   cudaFree(m->st.flags);
   cudaFree(m->st.acc);
   cudaFree(m->ring);
-  cudaFree(m->bin_t);
   cudaFree(m->dparam);
   cudaFree(m->dparam2);
   cudaFree(m->din);
@@ -705,23 +686,11 @@ mem_status mem_create_batch(int n_maps, float resolution, int rows, int cols, co
   if (!alloc((void **)&m->st.words, sizeof(uint32_t) * BHW * m->n_word) ||
       !alloc((void **)&m->st.flags, (size_t)BHW * m->n_flag) ||
       !alloc((void **)&m->ring, sizeof(int2) * n_maps) ||
-      !alloc((void **)&m->bin_t, sizeof(float) * (rows + 1 + cols + 1)) ||
       !alloc((void **)&m->ctl, m->ctl_bytes = sizeof(Control))) {
     free_map(m);
     return fail(MEM_ENOMEM, "device allocation of the map state failed");
   }
   mem_status s = MEM_OK;
-  {
-    std::vector<float> tr, tc;
-    bin_thresholds(resolution, rows, tr);
-    bin_thresholds(resolution, cols, tc);
-    tr.insert(tr.end(), tc.begin(), tc.end());
-    if (cudaMemcpy(m->bin_t, tr.data(), sizeof(float) * tr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-      cudaGetLastError();
-      free_map(m);
-      return fail(MEM_ECUDA, "binning thresholds upload");
-    }
-  }
   if (cudaMemsetAsync(m->ctl, 0, m->ctl_bytes, m->stream) != cudaSuccess) {
     s = fail(MEM_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
   }

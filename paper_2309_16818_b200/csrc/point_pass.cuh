@@ -12,17 +12,6 @@ struct PointOut {
 };
 
 // a2-a6 for one point: no memory access (the state gather of a7 is batched by the caller)
-// the row (or column) of map coordinate x: max{k : x >= t[k]}, -1 outside [t[0], t[n]); the
-// first guess floor(x / res + n/2) by a reciprocal is within one of it and corrected exactly
-__device__ __forceinline__ int bin_axis(float x, const float *t, int n, float inv_res, float half) {
-  if (!(x >= __ldg(t) && x < __ldg(t + n))) return -1;
-  int k = (int)floorf(x * inv_res + half);
-  k = k < 0 ? 0 : k > n - 1 ? n - 1 : k;
-  if (x < __ldg(t + k)) --k;
-  else if (x >= __ldg(t + k + 1)) ++k;
-  return k;
-}
-
 __device__ __forceinline__ PointOut bin_point(float px, float py, float pz, const PointFrame &f, const Geometry &g,
                                               const mem_noise &np, int map_base, float r2lo, float r2hi) {
   PointOut o;
