@@ -160,14 +160,15 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
   const int prow = wrap(row + ring.x, g.H);
   if (prow < a.row_lo || prow >= a.row_hi) return;  // another rank's band (sharded map)
   const long long cell = (long long)m * g.HW + (long long)prow * g.W + wrap(col + ring.y, g.W);
-  if (!a.st.flags[(long long)kFlagValid * g.BHW + cell]) return;
-  const MapFrame &f = a.frames ? a.frames[m] : a.f0;
   const float *vals = reinterpret_cast<const float *>(a.st.words);
+  const uint8_t valid = a.st.flags[(long long)kFlagValid * g.BHW + cell];
+  const float hcell = vals[(long long)kWordElev * g.BHW + cell];  // loaded with the flag (one round trip)
+  if (!valid) return;
+  const MapFrame &f = a.frames ? a.frames[m] : a.f0;
   // a11: cell centre at its elevation, relative to the map centre (D13), into the camera (D17)
   const float xc = ((float)row + 0.5f - g.hH) * g.res;
   const float yc = ((float)col + 0.5f - g.hW) * g.res;
   const float dx = xc - f.t[0], dy = yc - f.t[1];
-  const float hcell = vals[(long long)kWordElev * g.BHW + cell];
   const float dz = hcell - f.t[2];
   const float pcx = (f.R[0] * dx + f.R[3] * dy) + f.R[6] * dz;
   const float pcy = (f.R[1] * dx + f.R[4] * dy) + f.R[7] * dz;
