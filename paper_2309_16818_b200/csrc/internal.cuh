@@ -34,6 +34,9 @@ constexpr int kFlagValid = 0;
 // or two 32-B sectors.  Record words 0, 1 are the height statistics:
 constexpr int kRecP = 0;    // f64: sum 1/v over inliers
 constexpr int kRecS = 1;    // f64: sum z/v over inliers
+// colour RED path: count-word fields b (25 bits) | n (18) | n_out (18) hold any cell of a map of
+// at most this many points per call (b <= 255 n < 2^25); larger maps take the sort path
+constexpr long long kColourMaxPts = 131586;
 
 struct GroupDesc {
   int rule, nch;

@@ -32,7 +32,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     S[u] = __longlong_as_double((long long)ps.y);
     w0[u] = ww.x;
     w1[u] = ww.y;
-    ce[u] = __ldcg(reinterpret_cast<const uint2 *>(a.cert) + c);
+    if (kFast == 2) ce[u] = __ldcg(reinterpret_cast<const uint2 *>(a.cert) + c);
     h[u] = elev[c];
     s2[u] = var[c];
     vd[u] = validp[c];
@@ -48,10 +48,12 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
   for (int u = 0; u < N; ++u) {
     if (phys[u] < 0) continue;
     const int c = m * g.HW + phys[u];
-    // counts: colour count word b | n << 32 with n_out in the record, else n_in | n_out << 32
-    const unsigned n_out = kFast == 1 ? (unsigned)w1[u] : (unsigned)(cnt[u] >> 32);
-    const unsigned n_in = kFast == 1 ? (unsigned)(cnt[u] >> 32) - n_out : (unsigned)(cnt[u] & 0xffffffffull);
-    const unsigned ng = kFast == 1 ? (unsigned)(cnt[u] >> 32) : kFast == 2 ? (unsigned)w0[u] : 0u;
+    // counts: colour count word b | n << 25 | n_out << 43, else n_in | n_out << 32; colour and
+    // height only keep the certificate in record word 3
+    if (kFast != 2) ce[u] = make_uint2((unsigned)w1[u], (unsigned)(w1[u] >> 32));
+    const unsigned n_out = kFast == 1 ? (unsigned)(cnt[u] >> 43) : (unsigned)(cnt[u] >> 32);
+    const unsigned n_in = kFast == 1 ? (unsigned)((cnt[u] >> 25) & 0x3ffffull) - n_out : (unsigned)(cnt[u] & 0xffffffffull);
+    const unsigned ng = kFast == 1 ? (unsigned)((cnt[u] >> 25) & 0x3ffffull) : kFast == 2 ? (unsigned)w0[u] : 0u;
     const bool ok = cert_ok(ce[u].x, n_in) && (kFast != 2 || cert_ok(ce[u].y, ng));
     if (ok) {
       ++stc[7];
@@ -72,7 +74,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
           double sk;
           if (kFast == 1) {
             const uint32_t v = k == 0 ? (uint32_t)(w0[u] & 0xffffffffull)
-                                      : k == 1 ? (uint32_t)(w0[u] >> 32) : (uint32_t)(cnt[u] & 0xffffffffull);
+                                      : k == 1 ? (uint32_t)(w0[u] >> 32) : (uint32_t)(cnt[u] & 0x1ffffffull);
             sk = (double)v;  // exact integer colour sums (D20)
           } else {
             sk = __longlong_as_double((long long)w1[u]);
@@ -95,7 +97,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     __stcg(a.cnt + c, 0ull);
     __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
     __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
-    __stcg(reinterpret_cast<uint2 *>(a.cert) + c, make_uint2(0u, 0u));
+    if (kFast == 2) __stcg(reinterpret_cast<uint2 *>(a.cert) + c, make_uint2(0u, 0u));
   }
 }
 

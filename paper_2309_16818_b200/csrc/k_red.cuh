@@ -132,7 +132,9 @@ __device__ __forceinline__ uint2 cert_of(float t) {
 template <int kFast>
 __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOut &o, int sc, float ch0) {
   unsigned long long *rec = a.rec + (long long)sc * 4;
-  unsigned *cert = a.cert + (long long)sc * 2;
+  // the certificate word: record word 3 (colour, height only: the same 32-B sector as P and S),
+  // the separate array for the average group (whose record holds n_g and X)
+  unsigned *cert = kFast == 2 ? a.cert + (long long)sc * 2 : reinterpret_cast<unsigned *>(rec + 3);
   const bool act = o.cell >= 0;
   const unsigned act_b = __ballot_sync(0xffffffffu, act);
   if (act_b == 0u) return;
@@ -181,8 +183,8 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
   const unsigned fin_b = kFast == 2 ? __ballot_sync(0xffffffffu, fin) : 0u;
   if (!single) reduce_runs<kFast>(heads, w, zw, cs, rg, bb, v, cx);
   if constexpr (kFast == 1) {
-    // colour: count word b | n << 32 (n = every filtered in-bounds point, D20; n > 0 marks the
-    // cell touched), record [P, S, r | g << 32, n_out]; n_in > 0 iff P > 0 (every 1/v > 0)
+    // colour: count word b | n << 25 | n_out << 43 (n = every filtered in-bounds point, D20;
+    // n > 0 marks the cell touched), record [P, S, r | g << 32, certificate]
     unsigned n_in = (unsigned)__popc(peers & in_b), n_all = (unsigned)__popc(peers & act_b);
     bool lead = leader;
     if (single && __popc(dup) >= MEM_PAIR_MIN) {
@@ -207,15 +209,15 @@ __device__ __forceinline__ void accumulate_warp(const PassArgs &a, const PointOu
       }
       lead = act && !absorbed;
     }
-    if (lead) {
-      red_add_u64(&a.cnt[sc], (unsigned long long)bb | ((unsigned long long)n_all << 32));
+    if (lead) {  // count word b | n << 25 | n_out << 43 (kColourMaxPts: no field overflows)
+      red_add_u64(&a.cnt[sc], (unsigned long long)bb | ((unsigned long long)n_all << 25) |
+                                  ((unsigned long long)(n_all - n_in) << 43));
       if (n_in) {
         red_add_f64(rec + kRecP, w);
         red_add_f64(rec + kRecS, zw);
         if (cs.y) red_max_cert(cert, cert_slots(cs), 0u);
       }
       red_add_u64(rec + 2, (unsigned long long)(rg & 0xffffu) | ((unsigned long long)(rg >> 16) << 32));
-      if (n_all != n_in) red_add_u64(rec + 3, (unsigned long long)(n_all - n_in));
     }
     return;
   }

@@ -860,7 +860,8 @@ static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax
   }
   // the fast groups (one colour / one 1-channel average group on float4 points, or height
   // only) take the RED path when the call's P sums are certified; everything else sorts
-  if (!sorted && a.fast != 0 && p_certified(a, max_n)) return fuse_points_red(m, a, offsets, total);
+  if (!sorted && a.fast != 0 && p_certified(a, max_n) && (a.fast != 1 || max_n <= kColourMaxPts))
+    return fuse_points_red(m, a, offsets, total);
   const int cells = a.cell_hi - a.cell_lo;
   if (tmax > kMaxTilesPerMap)
     return fail(MEM_EINVAL, "a map takes at most %lld points per call", (long long)kMaxTilesPerMap * kTile);
