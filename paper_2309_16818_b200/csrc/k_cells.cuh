@@ -25,14 +25,15 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
 #pragma unroll
   for (int u = 0; u < N; ++u) {  // one round of loads
     if (phys[u] < 0) continue;
-    const int c = m * g.HW + phys[u];
-    const ulonglong2 *r = reinterpret_cast<const ulonglong2 *>(a.rec + (long long)c * 4);
+    const int c = m * g.HW + phys[u];                // state
+    const int q = (m - a.m0) * g.HW + phys[u];       // scratch (this wave's maps)
+    const ulonglong2 *r = reinterpret_cast<const ulonglong2 *>(a.rec + (long long)q * 4);
     const ulonglong2 ps = __ldcg(r), ww = __ldcg(r + 1);
     P[u] = __longlong_as_double((long long)ps.x);
     S[u] = __longlong_as_double((long long)ps.y);
     w0[u] = ww.x;
     w1[u] = ww.y;
-    if (kFast == 2) ce[u] = __ldcg(reinterpret_cast<const uint2 *>(a.cert) + c);
+    if (kFast == 2) ce[u] = __ldcg(reinterpret_cast<const uint2 *>(a.cert) + q);
     h[u] = elev[c];
     s2[u] = var[c];
     vd[u] = validp[c];
@@ -92,12 +93,13 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
       a.fbmark[c] = (int)k;
       a.fbmap[m] = 1u;
     }
-    // re-zero the scratch for the next point input
-    unsigned long long *r = a.rec + (long long)c * 4;
-    __stcg(a.cnt + c, 0ull);
+    // re-zero the scratch for the next wave / point input
+    const int q = (m - a.m0) * g.HW + phys[u];
+    unsigned long long *r = a.rec + (long long)q * 4;
+    __stcg(a.cnt + q, 0ull);
     __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
     __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
-    if (kFast == 2) __stcg(reinterpret_cast<uint2 *>(a.cert) + c, make_uint2(0u, 0u));
+    if (kFast == 2) __stcg(reinterpret_cast<uint2 *>(a.cert) + q, make_uint2(0u, 0u));
   }
 }
 
@@ -124,14 +126,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
   const int nwarps = gridDim.x * (kThreads / 32);
   const int gw = blockIdx.x * (kThreads / 32) + wid;
   const int cpm = (a.cell_hi - a.cell_lo + kChunk - 1) / kChunk;  // chunks per map (band)
-  const int total = a.n_maps * cpm;
+  const int total = (a.m1 - a.m0) * cpm;  // this wave's maps
   int *sp = s_phys[wid];
   unsigned long long *sc = s_cntv[wid];
   for (int rt = gw; rt < total; rt += nwarps) {
     const int chunk = total - 1 - rt;
-    const int m = chunk / cpm;
-    const int t0 = a.cell_lo + (chunk - m * cpm) * kChunk;
-    const int sb = m * g.HW;
+    const int mi = chunk / cpm;
+    const int m = a.m0 + mi;
+    const int t0 = a.cell_lo + (chunk - mi * cpm) * kChunk;
+    const int sb = mi * g.HW;  // scratch
     unsigned long long cv[kChunkPerLane];
 #pragma unroll
     for (int u = 0; u < kChunkPerLane; ++u) {  // counts first (memory-level parallelism)

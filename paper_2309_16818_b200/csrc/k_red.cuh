@@ -294,7 +294,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   const int lane = threadIdx.x & 31;
   const PointFrame f = frame_of(a, t.m);
   const int map_base = t.m * g.HW;
-  const int sb = t.m * g.HW;  // the map's scratch cells
+  const int sb = (t.m - a.m0) * g.HW;  // the map's scratch cells (this wave's maps)
   // points of the item present: [0, nv) (32-bit indices within the item)
   const int nv = kFull ? kWarpPoints : t.end - t.base < kWarpPoints ? (int)(t.end - t.base) : kWarpPoints;
   PointOut o[kWarpPtsPerLane];

@@ -153,7 +153,7 @@ static int resident_grid(K kernel, int threads, int slot) {
 
 template <bool kDebug, int kFast>
 static cudaError_t launch_points_t(const PassArgs &a, cudaStream_t s) {
-  const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1]) ;
+  const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1] - a.psi[a.m0]);
   int g = resident_grid(k_points<kDebug, kFast>, kThreads, kFast + (kDebug ? 3 : 0));
   if (items > 0) g = (int)std::max(1LL, std::min<long long>(g, (items + 7) / 8));
   return launch_pdl(k_points<kDebug, kFast>, g, 0, s, a, kThreads);
@@ -169,7 +169,7 @@ cudaError_t launch_points(const PassArgs &a, cudaStream_t s) {
 
 template <int kFast>
 static cudaError_t launch_cells_t(const PassArgs &a, cudaStream_t s) {
-  const long long chunks = (long long)a.n_maps * ((a.cell_hi - a.cell_lo + kChunk - 1) / kChunk);
+  const long long chunks = (long long)(a.m1 - a.m0) * ((a.cell_hi - a.cell_lo + kChunk - 1) / kChunk);
   const int g = (int)std::max(1LL, std::min<long long>(resident_grid(k_cells<kFast>, kThreads, 6 + kFast),
                                                        (chunks + 7) / 8));
   cudaError_t e = launch_pdl(k_cells<kFast>, g, 0, s, a, kThreads);

@@ -137,7 +137,7 @@ struct mem_map {
   // RED path scratch (zeroed once, re-zeroed by k_cells): count words, records, certificates, fallback list
   void *rcnt_s = nullptr, *rrec_s = nullptr, *rcert_s = nullptr, *rfb_s = nullptr;
   void *rmark_s = nullptr, *rfill_s = nullptr, *rmapfb_s = nullptr, *rlist_s = nullptr;
-  size_t rlist_cap = 0;
+  size_t rlist_cap = 0, red_all = 0;
   size_t red_cells = 0;  // cells the RED scratch holds
   bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
@@ -769,22 +769,32 @@ static bool p_certified(const PassArgs &a, long long max_n) {
 
 // the RED path for the fast groups: k_points (certified REDs), k_cells (fuse
 // the certified cells, list the others), k_refold (the others, in input order)
+#ifndef MEM_WAVE_MB
+#define MEM_WAVE_MB 0  // RED scratch budget: 0 = all maps of a call in one wave
+#endif
 static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offsets, long long total) {
   const int B = a.n_maps;
-  const size_t cells = (size_t)B * m->H * m->W;
-  if (cells > m->red_cells) {
+  const size_t HW = (size_t)m->H * m->W;
+  // waves of maps whose scratch (count word + record (+ certificate)) fits the budget; the
+  // scratch is reused by every wave
+  const size_t per_cell = 8 + 32 + (a.fast == 2 ? 8 : 0);
+  int wmaps = B;
+  if (MEM_WAVE_MB > 0) wmaps = (int)std::max<size_t>(1, std::min<size_t>(B, (size_t)MEM_WAVE_MB * 1048576 / (per_cell * HW)));
+  const size_t cells = (size_t)wmaps * HW, all = (size_t)B * HW;
+  if (cells > m->red_cells || all > m->red_all) {
     CU(cudaStreamSynchronize(m->stream));
     void **bufs[] = {&m->rcnt_s, &m->rrec_s, &m->rcert_s, &m->rfb_s, &m->rmark_s, &m->rfill_s, &m->rmapfb_s};
-    const size_t bytes[] = {8 * cells, 32 * cells, 8 * cells, 16 * cells, 4 * cells, 4 * cells, 4 * (size_t)B};
+    const size_t nc = std::max(cells, m->red_cells), na = std::max(all, m->red_all);
+    const size_t bytes[] = {8 * nc, 32 * nc, 8 * nc, 16 * nc, 4 * na, 4 * nc, 4 * (na / HW + 1)};
     for (void **b : bufs) {
       cudaFree(*b);
       *b = nullptr;
     }
-    m->red_cells = 0;
+    m->red_cells = m->red_all = 0;
     for (int i = 0; i < 7; ++i)
       if (cudaMalloc(bufs[i], bytes[i]) != cudaSuccess) {
         cudaGetLastError();
-        return fail(MEM_ENOMEM, "RED scratch (%zu cells)", cells);
+        return fail(MEM_ENOMEM, "RED scratch (%zu cells)", nc);
       }
     CU(cudaMemsetAsync(m->rcnt_s, 0, bytes[0], m->stream));
     CU(cudaMemsetAsync(m->rrec_s, 0, bytes[1], m->stream));
@@ -792,7 +802,8 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
     CU(cudaMemsetAsync(m->rmark_s, 0xff, bytes[4], m->stream));  // -1: no uncertified cell
     CU(cudaMemsetAsync(m->rfill_s, 0, bytes[5], m->stream));
     CU(cudaMemsetAsync(m->rmapfb_s, 0, bytes[6], m->stream));
-    m->red_cells = cells;
+    m->red_cells = nc;
+    m->red_all = na;
   }
   // the point list of the uncertified cells: at most every point of the call
   HP(7);
@@ -807,8 +818,6 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
   a.fbmap = reinterpret_cast<unsigned *>(m->rmapfb_s);
   a.fblist = reinterpret_cast<unsigned *>(m->rlist_s);
   a.st = m->st;
-  a.m0 = 0;
-  a.m1 = B;
   // warp-items of 128 points per map (inline prefix sums; staged ones ride in a second blob)
   std::vector<int> ps(B + 1, 0);
   for (int i = 0; i < B; ++i) {
@@ -831,10 +840,13 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
     a.pstart = reinterpret_cast<const int *>(d);
   }
   HP(8);
-  if (ps[B] > 0) TIMED(MEM_STAGE_POINT, launch_points(a, m->stream));
-  else CU(cudaMemsetAsync(&m->ctl->n_fb, 0, sizeof(unsigned) * 2, m->stream));  // k_points clears them
-  HP(9);
-  TIMED(MEM_STAGE_CELL, launch_cells(a, m->stream));
+  for (int w0 = 0; w0 < B; w0 += wmaps) {
+    a.m0 = w0;
+    a.m1 = std::min(B, w0 + wmaps);
+    if (ps[a.m1] > ps[a.m0]) TIMED(MEM_STAGE_POINT, launch_points(a, m->stream));
+    else CU(cudaMemsetAsync(&m->ctl->n_fb, 0, sizeof(unsigned) * 2, m->stream));  // k_points clears them
+    TIMED(MEM_STAGE_CELL, launch_cells(a, m->stream));
+  }
   HP(10);
   return MEM_OK;
 }
