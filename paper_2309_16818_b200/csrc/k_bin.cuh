@@ -34,7 +34,7 @@ __device__ __forceinline__ int map_of_tile(const PassArgs &a, int tile) {
 // points are split by cell band, stably: a lane's rank among the warp's earlier points of the
 // same band comes from __match_any_sync plus a per-warp running count in shared memory; the
 // tile then lays its records out band after band (tinfo[tile][band] = offset | count << 16),
-// so every band's records sit in input order in each tile region and k_band can gather them
+// so every band's records sit in input order in each tile region and k_sort can gather them
 // in input order without any global ordering pass.
 //
 // Record (16 B): x = cell within the band (bits 0-15) | usable-channel bit of bound group b
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const __grid_constant__ Pas
   const int NB = a.nbands;
   if (tid < 8) s_cnt[tid] = 0;
   for (int i = tid; i < (kBinThreads / 32) * NB; i += kBinThreads) s_wcnt[i] = 0;
-  pdl_wait();  // the previous call's k_band may still read the record buffers
+  pdl_wait();  // the previous call's k_sort may still read the record buffers
   pdl_trigger();
   if (blockIdx.x == 0) {  // the other epoch is the next point input's (no memset per call)
     for (int i = tid; i < kStatSlots * 8; i += kBinThreads) (&a.ctl->stats[a.epoch ^ 1][0][0])[i] = 0ull;

@@ -1,4 +1,4 @@
-// k_cells.cuh -- k_cells (a9-a10 + lazy a13 after k_points), k_collect + k_refold (the sequential
+// k_cells.cuh -- k_cells (a9-a10 + lazy a13 after k_points) and k_refold (the sequential
 // recomputation of uncertified cells).  Part of the single translation unit kernels.cu
 // (included inside namespace memk, in order).
 #pragma once
@@ -84,7 +84,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
         }
         if (!ob[u]) a.st.flags[(long long)gd.flag * BHW + c] = 1;
       }
-    } else {  // uncertified: its points listed by k_collect, recomputed in input order by k_refold
+    } else {  // uncertified: its points listed and recomputed in input order by k_refold
       const unsigned k = atomicAdd(&a.ctl->n_fb, 1u);
       const unsigned n = n_in + n_out;  // the cell's in-window points
       const unsigned off = atomicAdd(&a.ctl->n_fbpts, n);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ P
   flush_stats(s_cnt, cnt, &a.ctl->stats[a.epoch][0][0]);
 }
 
-// ---------------------------------------------------------------- k_collect, k_refold
+// ---------------------------------------------------------------- k_refold
 // The cells k_cells could not certify (their fp64 sums might depend on the order of the REDs)
 // are recomputed from their points in input order, exactly as the oracle folds them.
 //

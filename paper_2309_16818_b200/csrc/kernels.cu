@@ -55,7 +55,7 @@ namespace memk {
 // ---------------------------------------------------------------- launchers
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-// Programmatic dependent launch: k_bin, k_band and the router may be scheduled while the
+// Programmatic dependent launch: k_bin, k_sort and the router may be scheduled while the
 // kernel before them on the stream drains (its CTAs retire); each waits on griddepcontrol.wait
 // before it reads anything the previous kernel wrote, and lets its own dependent launch early.
 template <class K, class... Extra>

@@ -28,7 +28,7 @@ constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in sh
 constexpr int kFuseThreads = MEM_FUSE_THREADS;
 constexpr int kShortSeg = 8;           // cells of at most this many points: a thread each
 constexpr int kMidSeg = 64;            // at most this many: 8 lanes each (fast paths); longer: 16 lanes / a warp
-constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_band keeps their runs in smem)
+constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_sort keeps their runs in smem)
 constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
 // k_points: persistent grid-stride over 128-point warp-items (4 points per lane)
 #ifndef MEM_WARP_PTS
@@ -43,16 +43,16 @@ struct Control {  // two epochs: a point input adds to stats[epoch] and clears s
   unsigned long long stats[2][kStatSlots][8];  // mem_stats order (n_input is derived on the host)
   unsigned n_rec, n_seg, n_lseg, n_mseg;       // this call's sorted records, short / long / mid segments (k_sort)
   unsigned n_fb;                               // cells k_cells could not certify (k_refold)
-  unsigned n_fbpts;                            // their points (k_collect list length)
+  unsigned n_fbpts;                            // their points (k_refold's list length)
 };
 
-// reset description shared by k_band (lazy strips) and k_shift
+// reset description shared by k_cells / k_sort / k_smap (lazy strips) and k_shift
 struct ResetInfo {
   int n_word, n_flag, n_label;
   int label_word[kMaxGroups];
 };
 
-// Arguments of one point input, shared by k_bin, k_band and the router.
+// Arguments of one point input, shared by the point kernels and the router.
 // The call's points are split into tiles of kTile consecutive points of one map (tiles of map
 // m: [tstart[m], tstart[m+1])); the physical cells [cell_lo, cell_hi) of every map are split
 // into bands of band_cells cells (the last one shorter).
@@ -77,14 +77,14 @@ struct PassArgs {
   unsigned long long *rec;     // [n_maps][HW][4]: P, S, group words
   unsigned *cert;              // [n_maps][HW][2]: certificate slots (bf16x2: S, X; k_red.cuh)
   unsigned long long *fb;      // [2 k]: the k-th cell k_cells could not certify (m * HW + cell);
-                               // [2 k + 1]: its list offset | point count << 32 (k_collect, k_refold)
+                               // [2 k + 1]: its list offset | point count << 32 (k_refold)
   int *fbmark;                 // [n_maps][HW]: k of an uncertified cell, else -1 (reset by k_refold)
-  unsigned *fbfill;            // [k]: points k_collect has listed for cell k (reset by k_refold)
+  unsigned *fbfill;            // [k]: points listed for cell k (k_refold's collect phase) (reset by k_refold)
   unsigned *fbmap;             // [n_maps]: != 0 if the map has an uncertified cell (reset by k_refold)
   unsigned *fblist;            // point indices (relative to the map's first point) of those cells
   int t_uniform;               // > 0: every map has exactly this many tiles
   double inv_t_uniform;        // 1.0 / t_uniform (divmod_fast)
-  int tmax;                    // most tiles of one map (k_band's shared memory)
+  int tmax;                    // most tiles of one map (k_sort's shared memory)
   int cell_lo, cell_hi;        // physical cells fused (a row band when sharded)
   int band_cells, nbands, key_bits;
   double inv_band, inv_nbands;

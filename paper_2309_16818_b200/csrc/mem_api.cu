@@ -112,8 +112,6 @@ struct mem_map {
   // staging
   void *dparam = nullptr;
   size_t dparam_cap = 0;
-  void *dparam2 = nullptr;  // k_points item prefix sums of large batches
-  size_t dparam2_cap = 0;
   PinnedRing pin;
   unsigned *seen_rec = nullptr;  // pinned: in-window records of a recent point input (band sizing)
   void *din = nullptr;
@@ -122,7 +120,7 @@ struct mem_map {
   size_t dout_cap = 0;
   void *pca_buf = nullptr;  // PCA readout scratch
   size_t pca_cap = 0;
-  Control *ctl = nullptr;   // stats + work queue of k_fused (zeroed per point input)
+  Control *ctl = nullptr;   // per-call counters (two epochs) and list lengths
   size_t ctl_bytes = 0;
   int pdl = 1;               // programmatic dependent launch
   int occlusion = 0;         // image association with the Bresenham occlusion test (NEXT-1)
@@ -139,7 +137,7 @@ struct mem_map {
   void *rmark_s = nullptr, *rfill_s = nullptr, *rmapfb_s = nullptr, *rlist_s = nullptr;
   size_t rlist_cap = 0, red_all = 0;
   size_t red_cells = 0;  // cells the RED scratch holds
-  bool pending = false;     // a mem_move_to shift not yet applied (folded into the next k_fused)
+  bool pending = false;     // a mem_move_to shift not yet applied (folded into the next point pass)
   // sharded big map: 0 none, 1 NCCL, 2 local (one process, one device)
   int transport = 0, rank = 0, nranks = 1;
   int band_lo = 0, band_n = 0;          // owned physical cells [band_lo, band_lo + band_n)
@@ -495,7 +493,6 @@ void free_map(mem_map *m) {
   cudaFree(m->st.acc);
   cudaFree(m->ring);
   cudaFree(m->dparam);
-  cudaFree(m->dparam2);
   cudaFree(m->din);
   cudaFree(m->dout);
   cudaFree(m->pca_buf);
@@ -831,14 +828,7 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
   if (B <= kInlineMaps) {
     for (int i = 0; i <= B; ++i) a.psi[i] = ps[i];
     a.pstart = nullptr;
-  } else {
-    void *d = nullptr;
-    if (grow(&m->dparam2, &m->dparam2_cap, sizeof(int) * (B + 1), m->stream) != MEM_OK) return MEM_ENOMEM;
-    CU(cudaMemcpyAsync(m->dparam2, ps.data(), sizeof(int) * (B + 1), cudaMemcpyHostToDevice, m->stream));
-    CU(cudaStreamSynchronize(m->stream));  // ps is a local vector
-    d = m->dparam2;
-    a.pstart = reinterpret_cast<const int *>(d);
-  }
+  }  // else: a.pstart points into the staged parameter blob (input_points)
   HP(8);
   for (int w0 = 0; w0 < B; w0 += wmaps) {
     a.m0 = w0;
@@ -852,7 +842,7 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
 }
 
 // tiles of every map, bands of the physical cells [cell_lo, cell_hi), buffers; then k_bin and
-// k_band.  `a` carries the frames, the point offsets and the tile prefix sums
+// k_sort.  `a` carries the frames, the point offsets and the tile prefix sums
 // (inline or staged); `tiles` = all tiles of the call, `tmax` = most tiles of one map.
 static mem_status fuse_points(mem_map *m, PassArgs &a, int tiles, long long tmax, long long max_n,
                               const int64_t *offsets = nullptr, long long total = 0) {
@@ -1216,7 +1206,13 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     // parameter blob: frames [B] | offsets [B+1] (i64) | tstart [B+1] (i32)
     const size_t off_at = (sizeof(PointFrame) * B + 15) & ~(size_t)15;  // int64 alignment
     const size_t ts_at = off_at + sizeof(long long) * (B + 1);
-    std::vector<unsigned char> blob(ts_at + sizeof(int) * (B + 1));
+    const size_t ps_at = ts_at + sizeof(int) * (B + 1);
+    std::vector<unsigned char> blob(ps_at + sizeof(int) * (B + 1));
+    {  // k_points' warp-item prefix sums ride in the same blob (no second staging, no sync)
+      int *ps = reinterpret_cast<int *>(blob.data() + ps_at);
+      ps[0] = 0;
+      for (int i = 0; i < B; ++i) ps[i + 1] = ps[i] + (int)((offsets[i + 1] - offsets[i] + kWarpPoints - 1) / kWarpPoints);
+    }
     PointFrame *fr = reinterpret_cast<PointFrame *>(blob.data());
     for (int i = 0; i < B; ++i) fr[i] = frame(i);
     memcpy(blob.data() + off_at, offsets, sizeof(long long) * (B + 1));
@@ -1227,6 +1223,7 @@ static mem_status input_points(mem_map *m, const float *pts, const int64_t *offs
     a.frames = reinterpret_cast<const PointFrame *>(d);
     a.offsets = reinterpret_cast<const long long *>((char *)d + off_at);
     a.tstart = reinterpret_cast<const int *>((char *)d + ts_at);
+    a.pstart = reinterpret_cast<const int *>((char *)d + ps_at);
   }
   HP(6);
   if (m->transport != 0 && m->nranks > 1) {  // sharded map: route the shard's points to their owners
@@ -1365,7 +1362,7 @@ static mem_status move_to(mem_map *m, const double *xy) {
     any |= (sr != 0 || sc != 0);
   }
   // s = 0 everywhere: bit-identical, nothing to do.  Otherwise the strip reset is applied
-  // lazily by the next point input's k_fused (or eagerly by flush_shift before any other call).
+  // lazily by the next point input's point pass (or eagerly by flush_shift before any other call).
   m->pending = any;
   return MEM_OK;
 }

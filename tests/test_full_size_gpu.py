@@ -248,3 +248,38 @@ def test_uncertified_cells_are_refolded_exactly(rows, n, group):
         assert np.array_equal(gk, code) and np.array_equal(gc, cell)
         assert g.stats() == o.stats()
         compare_layers(g, o, where=f"refold frame {f}: ")
+
+
+def test_red_path_batch_of_more_than_128_maps():
+    """More maps than ride in the kernel parameters (kInlineMaps = 128): frames, offsets and
+    the warp-item prefix sums are staged in one parameter blob; maps too large for k_smap
+    (130 x 130 cells) take the certified-RED path.  Ragged point counts, colour group, 3
+    frames with moves; 6 maps checked against the oracle."""
+    rng = np.random.default_rng(23)
+    B, rows = 136, 130
+    res = 0.1
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5)]
+    noise = dict(a=1e-4, b=1e-5, r_min=0.0, r_max=50.0, h_min=-5.0, h_max=5.0, tau2=9.0, v_out=0.01)
+    g = M.Map(res, rows, rows, groups, n_maps=B)
+    check = [0, 1, 64, 127, 128, 135]
+    oras = {b: O.OracleMap(res, rows, rows, groups) for b in check}
+    for f in range(3):
+        counts = rng.integers(0, 3000, B)
+        offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        n = int(offsets[-1])
+        xy = rng.uniform(-7.0, 7.0, (n, 2))
+        z = 0.3 * np.sin(xy[:, 0]) + rng.normal(0, 0.02, n)
+        pts = np.stack([xy[:, 0], xy[:, 1], z - 1.0, np.zeros(n)], 1).astype(np.float32)
+        pts[:, 3] = S.pack_rgb(rng.integers(0, 256, (n, 3)).astype(np.uint8))
+        moves = rng.uniform(-0.5, 0.5, (B, 2)) + 0.013
+        R = np.tile(np.eye(3), (B, 1, 1))
+        t = np.tile([0.0, 0.0, 1.0], (B, 1))
+        g.move_to_batch(moves)
+        g.input_pointcloud_batch(torch.from_numpy(pts).cuda(), offsets, [(0, 1, 0)], R, t, noise)
+        for b in check:
+            oras[b].move_to(*moves[b])
+            oras[b].input_pointcloud(pts[offsets[b]:offsets[b + 1]], [(0, 1, 0)], np.eye(3), [0.0, 0.0, 1.0], noise)
+    for nm in g.layer_names():
+        lay = np.asarray(g.get_layer(nm))
+        for b in check:
+            assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
