@@ -21,7 +21,10 @@ __device__ __forceinline__ float4 ld_stream_f4(const float *p, unsigned long lon
                : "l"(p), "l"(pol));
   return r;
 }
-__device__ __forceinline__ bool finite3(float a, float b, float c) { return isfinite(a) && isfinite(b) && isfinite(c); }
+// branch-free: |x| < inf is false exactly for +-inf and NaN
+__device__ __forceinline__ bool finite3(float a, float b, float c) {
+  return (fabsf(a) < INFINITY) & (fabsf(b) < INFINITY) & (fabsf(c) < INFINITY);
+}
 
 __device__ __forceinline__ int stat_slot(int code) {
   // mem_stats order: n_input, nonfinite, range, height, oob, inlier, outlier, touched
