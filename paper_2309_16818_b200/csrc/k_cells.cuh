@@ -301,6 +301,65 @@ __device__ __forceinline__ void refold_fold(const float *w, const float *zw, con
   }
 }
 
+// Block-certified sequential folding.  Within a block of 32 consecutive terms the oracle's
+// sequential fp64 sum V <- V + t_1 <- ... rounds nowhere when every value involved is a multiple
+// of 2^q (q = the lowest set bit over V and the block's terms) and every partial sum is below
+// 2^(q + 53); then V + (the block's exact sum, any order) is the sequential result bit for bit.
+// The block sums and their lowest-bit / magnitude summaries are computed in parallel; only the
+// chain over blocks (and the rare block that fails the test) is sequential.
+__device__ __forceinline__ int expo64(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023; }
+__device__ __forceinline__ int lsb64(double x) {  // x normal, non-zero
+  const unsigned long long m = ((unsigned long long)__double_as_longlong(x) & 0xfffffffffffffull) | (1ull << 52);
+  return expo64(x) - 52 + __ffsll((long long)m) - 1;
+}
+__device__ __forceinline__ int lsb32(float t) {  // t non-zero (normal or subnormal)
+  const unsigned u = __float_as_uint(t) & 0x7fffffffu;
+  const int fe = (int)(u >> 23);
+  const unsigned m = (u & 0x7fffffu) | (fe ? 0x800000u : 0u);
+  return (fe ? fe - 127 : -126) - 23 + __ffs((int)m) - 1;
+}
+struct FoldBlock {
+  double t[3], a[3];  // block sums (P, S, X) and sums of magnitudes
+  int q[3];           // lowest set bit over the block's non-zero terms (INT_MAX: none)
+};
+// the block's summary from lane l's terms (all 32 lanes of a warp)
+template <int kFast>
+__device__ __forceinline__ FoldBlock fold_block(float w, float zw, float c) {
+  FoldBlock fb;
+  const float v[3] = {w, zw, c};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k == 2 && kFast != 2) {
+      fb.t[k] = fb.a[k] = 0.0;
+      fb.q[k] = 0x7fffffff;
+      continue;
+    }
+    double t = (double)v[k], aa = fabs((double)v[k]);
+    int q = v[k] != 0.0f ? lsb32(v[k]) : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      aa += __shfl_xor_sync(0xffffffffu, aa, o);
+      q = min(q, __shfl_xor_sync(0xffffffffu, q, o));
+    }
+    fb.t[k] = t;
+    fb.a[k] = aa;
+    fb.q[k] = q;
+  }
+  return fb;
+}
+// V + the block's terms, when the sequential fold provably rounds nowhere
+__device__ __forceinline__ bool fold_exact(double V, double absum, int qb) {
+  if (absum == 0.0) return true;  // only zero terms
+  int q = qb;
+  int e = expo64(absum);
+  if (V != 0.0) {
+    q = min(q, lsb64(V));
+    e = max(e, expo64(V));
+  }
+  return e + 2 <= q + 53;  // |partial| <= |V| + absum < 2^(e + 2) <= 2^(q + 53)
+}
+
 template <int kFast>
 struct RefoldSmem {
   using Sort = cub::BlockRadixSort<unsigned, kRefoldThreads, kRefoldItems>;
@@ -313,6 +372,7 @@ struct RefoldSmem {
     Bufs b;
   } u;
   unsigned idx[kRefoldCap];
+  FoldBlock blk[2][kRefoldChunk / 32];
 };
 template <int kFast>
 size_t refold_smem_bytes() { return sizeof(RefoldSmem<kFast>); }
@@ -367,25 +427,48 @@ __global__ void __launch_bounds__(kRefoldThreads) k_refold(const __grid_constant
         if (j < n) s_idx[j] = keys[q];
       }
       __syncthreads();  // s_idx complete; the sort's storage (aliasing the term buffers) is free
+      // chunk ch's 16 blocks of 32 positions: block bk is produced by warp bk % W for the first
+      // chunk (W warps), by warp 1 + bk % (W - 1) for the others (warp 0 folds meanwhile); a producing
+      // warp writes the terms (for a block that must fold sequentially) and the block summary
+      constexpr int kBlocks = kRefoldChunk / 32;
       const int nch = (int)((n + kRefoldChunk - 1) / kRefoldChunk);
-      const int len0 = n < (unsigned)kRefoldChunk ? (int)n : kRefoldChunk;
-      for (int j = threadIdx.x; j < len0; j += kRefoldThreads)
-        refold_term<kFast>(a, f, map_base, beg + s_idx[j], gc, h, s2, s_u.b.w[0][j], s_u.b.zw[0][j],
-                           s_u.b.c[0][kFast == 2 ? j : 0], t);
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      auto produce = [&](int ch, int bk) {
+        const int bb = ch & 1, j = bk * 32 + lane, pos = ch * kRefoldChunk + j;
+        float w = 0.0f, zw = 0.0f, c = 0.0f;
+        if (pos < (int)n) refold_term<kFast>(a, f, map_base, beg + s_idx[pos], gc, h, s2, w, zw, c, t);
+        s_u.b.w[bb][j] = w;
+        s_u.b.zw[bb][j] = zw;
+        if (kFast == 2) s_u.b.c[bb][j] = c;
+        const FoldBlock fb = fold_block<kFast>(w, zw, c);
+        if (lane == 0) sm.blk[bb][bk] = fb;
+      };
+      for (int bk = wid; bk < kBlocks; bk += kRefoldThreads / 32) produce(0, bk);
       __syncthreads();
       for (int ch = 0; ch < nch; ++ch) {
-        const int b = ch & 1;
-        if (threadIdx.x < 32) {  // warp 0: the fold of chunk ch
-          if (threadIdx.x == 0) {
+        const int bb = ch & 1;
+        if (wid == 0) {  // warp 0: the chain over chunk ch's blocks
+          if (lane == 0) {
             const int len = (int)n - ch * kRefoldChunk < kRefoldChunk ? (int)n - ch * kRefoldChunk : kRefoldChunk;
-            refold_fold<kFast>(s_u.b.w[b], s_u.b.zw[b], s_u.b.c[b], len, P, S, X);
+            for (int bk = 0; bk * 32 < len; ++bk) {
+              const FoldBlock &fb = sm.blk[bb][bk];
+              const int bl = len - bk * 32 < 32 ? len - bk * 32 : 32;
+              double *acc[3] = {&P, &S, &X};
+              const float *src[3] = {s_u.b.w[bb] + bk * 32, s_u.b.zw[bb] + bk * 32, s_u.b.c[bb] + bk * 32};
+#pragma unroll
+              for (int k = 0; k < (kFast == 2 ? 3 : 2); ++k) {
+                if (fold_exact(*acc[k], fb.a[k], fb.q[k])) {
+                  *acc[k] += fb.t[k];
+                } else {  // the oracle's sequential fold of this block
+                  double v = *acc[k];
+                  for (int i = 0; i < bl; ++i) v += (double)src[k][i];
+                  *acc[k] = v;
+                }
+              }
+            }
           }
-        } else if (ch + 1 < nch) {  // warps 1-15: the terms of chunk ch + 1
-          const int j0 = (ch + 1) * kRefoldChunk;
-          const int len = (int)n - j0 < kRefoldChunk ? (int)n - j0 : kRefoldChunk;
-          for (int j = threadIdx.x - 32; j < len; j += kRefoldThreads - 32)
-            refold_term<kFast>(a, f, map_base, beg + s_idx[j0 + j], gc, h, s2, s_u.b.w[b ^ 1][j],
-                               s_u.b.zw[b ^ 1][j], s_u.b.c[b ^ 1][kFast == 2 ? j : 0], t);
+        } else if (ch + 1 < nch) {  // warps 1-15: chunk ch + 1
+          for (int bk = wid - 1; bk < kBlocks; bk += (kRefoldThreads / 32) - 1) produce(ch + 1, bk);
         }
         __syncthreads();
       }
