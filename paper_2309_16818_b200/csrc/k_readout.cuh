@@ -92,18 +92,19 @@ __global__ void __launch_bounds__(kThreads) k_write(const __grid_constant__ Read
 // ---------------------------------------------------------------- PCA readout (a14, C4)
 // Moments over the observed cells of one map: sum x and the upper triangle of sum x x^T in
 // fp64 (products of fp32 values are exact in fp64).  Persistent CTAs walk tiles of kPcaTile
-// cells staged in shared memory in fp64 ([cell][channel], channels padded to a multiple of 4
-// with zeros); thread b < nb (nb + 1) / 2 owns the 4 x 4 block (bi, bj), bi <= bj, of the Gram
-// matrix in 16 fp64 registers (four 16-B shared loads per 16 FMAs) and the
+// cells staged in shared memory in fp64 by all threads ([channel][cell], channels padded to a
+// multiple of 4 with zeros, the observed flags staged first); thread b < nb (nb + 1) / 2 owns
+// the 4 x 4 block (bi, bj), bi <= bj, of the Gram matrix in 16 fp64 registers and the
 // diagonal-block threads the sums of their 4 channels; each CTA writes its partial moments to
 // its own row (no atomics), k_pca_eigen adds the rows in a fixed order.
 constexpr int kPcaTile = 128;
-__host__ __device__ inline int pca_ldc(int d) { return ((d + 3) & ~3) + 2; }  // doubles per staged cell (16-B rows)
+__host__ __device__ inline int pca_ldc(int d) { return ((d + 3) & ~3) * (kPcaTile + 1); }  // doubles of the staged tile
 __global__ void __launch_bounds__(kThreads) k_pca_moments(const __grid_constant__ PcaArgs a) {
-  extern __shared__ double s_xd[];  // [kPcaTile][ldc]: the tile's values in fp64, converted once
+  extern __shared__ double s_xd[];  // [d4][kPcaTile + 1]: the tile's values in fp64, converted once
+  __shared__ unsigned char s_obs[kPcaTile];
   __shared__ int s_n;
   const Geometry &g = a.geo;
-  const int d = a.d, d4 = (d + 3) & ~3, nb = d4 / 4, ldc = pca_ldc(d);
+  const int d = a.d, d4 = (d + 3) & ~3, nb = d4 / 4, ld = kPcaTile + 1;
   const int pairs = d * (d + 1) / 2, nv = d + pairs + 1;
   const float *vals = reinterpret_cast<const float *>(a.st.words);
   const long long mb = (long long)a.map * g.HW;
@@ -131,22 +132,31 @@ __global__ void __launch_bounds__(kThreads) k_pca_moments(const __grid_constant_
   for (int c0 = blockIdx.x * kPcaTile; c0 < g.HW; c0 += gridDim.x * kPcaTile) {
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < kPcaTile; t += kThreads) {  // physical cells: order is irrelevant
-      const int phys = c0 + t;
+    if (threadIdx.x < kPcaTile) {  // physical cells: order is irrelevant
+      const int phys = c0 + threadIdx.x;
       const bool obs = phys < g.HW && a.st.flags[(long long)a.flag * g.BHW + mb + phys];
-      for (int k = 0; k < d4; ++k)
-        s_xd[t * ldc + k] = obs && k < d ? (double)vals[(long long)(a.word0 + k) * g.BHW + mb + phys] : 0.0;
+      s_obs[threadIdx.x] = obs;
       if (obs) atomicAdd(&s_n, 1);
+    }
+    __syncthreads();
+    // every thread stages: channel k of cell t at [k][t] (coalesced loads, conflict-free stores)
+    for (int e = threadIdx.x; e < kPcaTile * d4; e += kThreads) {
+      const int k = e / kPcaTile, t = e - k * kPcaTile;
+      const int phys = c0 + t;
+      s_xd[k * ld + t] = k < d && s_obs[t] ? (double)vals[(long long)(a.word0 + k) * g.BHW + mb + phys] : 0.0;
     }
     __syncthreads();
     nobs += s_n;
     if (b < nblk) {
+      const double *xa = s_xd + 4 * bi * ld, *xb = s_xd + 4 * bj * ld;
 #pragma unroll 2
       for (int t = 0; t < kPcaTile; ++t) {
-        const double2 *pa = reinterpret_cast<const double2 *>(s_xd + t * ldc + 4 * bi);
-        const double2 *pb = reinterpret_cast<const double2 *>(s_xd + t * ldc + 4 * bj);
-        const double2 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
-        const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
+        double va[4], vb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          va[i] = xa[i * ld + t];
+          vb[i] = xb[i * ld + t];
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           sum[i] += va[i];

@@ -258,7 +258,7 @@ cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
 int pca_parts(int HW) { return (int)std::min<long long>(2 * 148, (HW + kPcaTile - 1) / kPcaTile); }
 
 cudaError_t launch_pca_moments(const PcaArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * kPcaTile * pca_ldc(a.d);
+  const size_t smem = sizeof(double) * pca_ldc(a.d);
   cudaError_t e = cudaFuncSetAttribute(k_pca_moments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_pca_moments<<<a.nparts, kThreads, smem, s>>>(a);
