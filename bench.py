@@ -672,7 +672,10 @@ def run_mem(a):
     traffic = None
     if tr and tr.get("maps") == M_ and tr.get("points_per_map") == npts:
         traffic = tr.get("k_points_dram_bytes_per_launch")
-    launches = sum(prof[k][1] for k in ("shift", "point", "cell", "image", "read", "write"))
+    # kernels per profiled call on this path: a point stage is k_points, a cell stage k_cells +
+    # k_refold (cooperative; returns at once when no cell is uncertified) -- see the ncu launch
+    # list profiles/r02z_launches_c2x64.txt: 3 kernels per step
+    launches = sum(prof[k][1] for k in ("shift", "point", "image", "read", "write")) + 2 * prof["cell"][1]
     step_bytes = bytes_pts + bytes_cells
 
     # ---- e2e: through the C-ABI with HOST (pinned) buffers, H2D + D2H inside the timed region
