@@ -29,7 +29,10 @@ constexpr int kFuseThreads = MEM_FUSE_THREADS;
 constexpr int kShortSeg = 8;           // cells of at most this many points: a thread each
 constexpr int kMidSeg = 64;            // at most this many: 8 lanes each (fast paths); longer: 16 lanes / a warp
 constexpr int kMaxTilesPerMap = 8192;   // tiles of one map per call (k_sort keeps their runs in smem)
-constexpr int kInlineMaps = 128;        // maps whose frames travel in the kernel parameters
+#ifndef MEM_INLINE_MAPS
+#define MEM_INLINE_MAPS 128
+#endif
+constexpr int kInlineMaps = MEM_INLINE_MAPS;  // maps whose frames travel in the kernel parameters
 // k_points: persistent grid-stride over 128-point warp-items (4 points per lane)
 #ifndef MEM_WARP_PTS
 #define MEM_WARP_PTS 4
