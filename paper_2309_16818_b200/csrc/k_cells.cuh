@@ -307,17 +307,6 @@ __device__ __forceinline__ void refold_fold(const float *w, const float *zw, con
 // 2^(q + 53); then V + (the block's exact sum, any order) is the sequential result bit for bit.
 // The block sums and their lowest-bit / magnitude summaries are computed in parallel; only the
 // chain over blocks (and the rare block that fails the test) is sequential.
-__device__ __forceinline__ int expo64(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023; }
-__device__ __forceinline__ int lsb64(double x) {  // x normal, non-zero
-  const unsigned long long m = ((unsigned long long)__double_as_longlong(x) & 0xfffffffffffffull) | (1ull << 52);
-  return expo64(x) - 52 + __ffsll((long long)m) - 1;
-}
-__device__ __forceinline__ int lsb32(float t) {  // t non-zero (normal or subnormal)
-  const unsigned u = __float_as_uint(t) & 0x7fffffffu;
-  const int fe = (int)(u >> 23);
-  const unsigned m = (u & 0x7fffffu) | (fe ? 0x800000u : 0u);
-  return (fe ? fe - 127 : -126) - 23 + __ffs((int)m) - 1;
-}
 struct FoldBlock {
   double t[3], a[3];  // block sums (P, S, X) and sums of magnitudes
   int q[3];           // lowest set bit over the block's non-zero terms (INT_MAX: none)
@@ -347,17 +336,6 @@ __device__ __forceinline__ FoldBlock fold_block(float w, float zw, float c) {
     fb.q[k] = q;
   }
   return fb;
-}
-// V + the block's terms, when the sequential fold provably rounds nowhere
-__device__ __forceinline__ bool fold_exact(double V, double absum, int qb) {
-  if (absum == 0.0) return true;  // only zero terms
-  int q = qb;
-  int e = expo64(absum);
-  if (V != 0.0) {
-    q = min(q, lsb64(V));
-    e = max(e, expo64(V));
-  }
-  return e + 2 <= q + 53;  // |partial| <= |V| + absum < 2^(e + 2) <= 2^(q + 53)
 }
 
 template <int kFast>

@@ -279,12 +279,18 @@ __device__ __forceinline__ void fuse_cell_group(const PassArgs &a, const uint4 s
   int nmax = n;
 #pragma unroll
   for (int d = 16; d >= G; d >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, d));
+  constexpr unsigned gmask = (unsigned)((1ull << G) - 1ull);
+  // pass 1: a7, the counts and colour sums, and the fp64 sums as group trees with the
+  // exactness certificate of the cell's terms (k_red.cuh): when it holds the trees are the
+  // oracle's sequential sums bit for bit; pass 2 (only groups whose certificate fails) folds
+  // sequentially in input order
+  unsigned ewx = 0u, ewn = 255u, ezx = 0u, ezn = 255u, ecx = 0u, ecn = 255u;
   uint4 q = make_uint4(0u, 0u, 0u, 0u);
   if (li < n) q = __ldcg(rec + li);
   for (int b0 = 0; b0 < nmax; b0 += G) {
     const int m_ = n - b0 < G ? (n - b0 > 0 ? n - b0 : 0) : G;
     const bool act = li < m_;
-    uint4 nq = make_uint4(0u, 0u, 0u, 0u);  // the next batch in flight while this one folds
+    uint4 nq = make_uint4(0u, 0u, 0u, 0u);  // the next batch in flight
     if (b0 + G + li < n) nq = __ldcg(rec + b0 + G + li);
     const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
     const float d = z - h;  // a7 (D10)
@@ -294,42 +300,132 @@ __device__ __forceinline__ void fuse_cell_group(const PassArgs &a, const uint4 s
     if (inl) {
       w = 1.0f / v;  // a8: the oracle's fp32 terms
       zw = z * w;
+      const unsigned e1 = max((__float_as_uint(w) >> 23) & 255u, 1u);
+      ewx = max(ewx, e1);
+      ewn = min(ewn, e1);
+      if (zw != 0.0f) {
+        const unsigned e2 = max((__float_as_uint(zw) >> 23) & 255u, 1u);
+        ezx = max(ezx, e2);
+        ezn = min(ezn, e2);
+      }
     }
-    constexpr unsigned gmask = (unsigned)((1ull << G) - 1ull);
-    const unsigned im = (__ballot_sync(0xffffffffu, inl) >> gsh) & gmask;
-    nin += __popc(im);
+    nin += __popc((__ballot_sync(0xffffffffu, inl) >> gsh) & gmask);
     nout += __popc((__ballot_sync(0xffffffffu, outl) >> gsh) & gmask);
     float c = 0.0f;
-    unsigned fm = 0u;
     if (kFast == 1) {  // D20: exact integer sums, order-free
       cr += group_sum<G>(act ? (q.w >> 16) & 255u : 0u);
       cg += group_sum<G>(act ? (q.w >> 8) & 255u : 0u);
       cb += group_sum<G>(act ? q.w & 255u : 0u);
       na += m_;
     } else if (kFast == 2) {  // D31
-      c = __uint_as_float(q.w);
-      fm = (__ballot_sync(0xffffffffu, act && isfinite(c)) >> gsh) & gmask;
-      na += __popc(fm);
-    }
-    for (int j0 = 0; j0 < G; j0 += 8) {  // input order; 8 lanes' terms fetched ahead of the adds
-      float wj[8], zj[8], cj[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        wj[u] = __shfl_sync(0xffffffffu, w, j0 + u, G);
-        zj[u] = __shfl_sync(0xffffffffu, zw, j0 + u, G);
-        if (kFast == 2) cj[u] = __shfl_sync(0xffffffffu, c, j0 + u, G);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (im >> (j0 + u) & 1u) {
-          P += (double)wj[u];
-          S += (double)zj[u];
+      const float cc = __uint_as_float(q.w);
+      const bool fin = act && isfinite(cc);
+      na += __popc((__ballot_sync(0xffffffffu, fin) >> gsh) & gmask);
+      if (fin) {
+        c = cc;
+        if (cc != 0.0f) {
+          const unsigned e3 = max((__float_as_uint(cc) >> 23) & 255u, 1u);
+          ecx = max(ecx, e3);
+          ecn = min(ecn, e3);
         }
-        if (kFast == 2 && (fm >> (j0 + u) & 1u)) X += (double)cj[u];
       }
     }
+    double tw = (double)w, tz = (double)zw, tc = (double)c;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      tw += __shfl_xor_sync(0xffffffffu, tw, o);
+      tz += __shfl_xor_sync(0xffffffffu, tz, o);
+      if (kFast == 2) tc += __shfl_xor_sync(0xffffffffu, tc, o);
+    }
+    P += tw;
+    S += tz;
+    if (kFast == 2) X += tc;
     if (kDebug && act) a.dbg_code[__ldcg(a.sridx + seg.y + b0 + li)] = (uint8_t)(outl ? MEM_CODE_OUTLIER : MEM_CODE_INLIER);
     q = nq;
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    ewx = max(ewx, __shfl_xor_sync(0xffffffffu, ewx, o));
+    ewn = min(ewn, __shfl_xor_sync(0xffffffffu, ewn, o));
+    ezx = max(ezx, __shfl_xor_sync(0xffffffffu, ezx, o));
+    ezn = min(ezn, __shfl_xor_sync(0xffffffffu, ezn, o));
+    if (kFast == 2) {
+      ecx = max(ecx, __shfl_xor_sync(0xffffffffu, ecx, o));
+      ecn = min(ecn, __shfl_xor_sync(0xffffffffu, ecn, o));
+    }
+  }
+  const unsigned lg = cert_ceil_log2(nin);
+  const bool exact = (nin == 0u || ewx - ewn + lg <= 29u) && (ezx < ezn || ezx - ezn + lg <= 29u) &&
+                     (kFast != 2 || ecx < ecn || ecx - ecn + cert_ceil_log2(na) <= 29u);
+  if (__any_sync(0xffffffffu, !exact)) {  // pass 2: every lane runs it (full-warp shuffles)
+    double P2 = 0.0, S2 = 0.0, X2 = 0.0;
+    if (li < n) q = __ldcg(rec + li);
+    for (int b0 = 0; b0 < nmax; b0 += G) {
+      const int m_ = n - b0 < G ? (n - b0 > 0 ? n - b0 : 0) : G;
+      const bool act = li < m_;
+      uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+      if (b0 + G + li < n) nq = __ldcg(rec + b0 + G + li);
+      const float z = __uint_as_float(q.y), v = __uint_as_float(q.z);
+      const float d = z - h;
+      const bool inl = act && !(d * d > tau2 * (s2 + v));
+      float w = 0.0f, zw = 0.0f, c = 0.0f;
+      if (inl) {
+        w = 1.0f / v;
+        zw = z * w;
+      }
+      const unsigned im = (__ballot_sync(0xffffffffu, inl) >> gsh) & gmask;
+      unsigned fm = 0u;
+      if (kFast == 2) {
+        c = __uint_as_float(q.w);
+        fm = (__ballot_sync(0xffffffffu, act && isfinite(c)) >> gsh) & gmask;
+        if (!(fm >> li & 1u)) c = 0.0f;
+      }
+      // block-certified: the batch's exact sum when adding it to the running sum provably
+      // rounds nowhere (fold_exact), else term by term in input order
+      double bs[3] = {(double)w, (double)zw, (double)c}, ba[3] = {(double)w, fabs((double)zw), fabs((double)c)};
+      int bq[3] = {w != 0.0f ? lsb32(w) : 0x7fffffff, zw != 0.0f ? lsb32(zw) : 0x7fffffff,
+                   c != 0.0f ? lsb32(c) : 0x7fffffff};
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          if (k == 2 && kFast != 2) continue;
+          bs[k] += __shfl_xor_sync(0xffffffffu, bs[k], o);
+          ba[k] += __shfl_xor_sync(0xffffffffu, ba[k], o);
+          bq[k] = min(bq[k], __shfl_xor_sync(0xffffffffu, bq[k], o));
+        }
+      }
+      const bool okP = fold_exact(P2, ba[0], bq[0]), okS = fold_exact(S2, ba[1], bq[1]);
+      const bool okX = kFast != 2 || fold_exact(X2, ba[2], bq[2]);
+      if (okP) P2 += bs[0];
+      if (okS) S2 += bs[1];
+      if (kFast == 2 && okX) X2 += bs[2];
+      if (__any_sync(0xffffffffu, !(okP && okS && okX))) {
+        for (int j0 = 0; j0 < G; j0 += 8) {  // input order; 8 lanes' terms fetched ahead of the adds
+          float wj[8], zj[8], cj[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            wj[u] = __shfl_sync(0xffffffffu, w, j0 + u, G);
+            zj[u] = __shfl_sync(0xffffffffu, zw, j0 + u, G);
+            if (kFast == 2) cj[u] = __shfl_sync(0xffffffffu, c, j0 + u, G);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (im >> (j0 + u) & 1u) {
+              if (!okP) P2 += (double)wj[u];
+              if (!okS) S2 += (double)zj[u];
+            }
+            if (kFast == 2 && !okX && (fm >> (j0 + u) & 1u)) X2 += (double)cj[u];
+          }
+        }
+      }
+      q = nq;
+    }
+    if (!exact) {
+      P = P2;
+      S = S2;
+      X = X2;
+    }
   }
   if (li == 0 && n > 0) {
     cnt[5] += nin;

@@ -37,6 +37,33 @@ __device__ __forceinline__ bool cert_ok(unsigned w, unsigned n) {
   return emax - emin + cert_ceil_log2(n) <= 29u;
 }
 
+// Block-certified sequential folding (k_refold, k_fuse): adding a block of fp32 terms to an fp64
+// running sum V rounds nowhere when every value involved is a multiple of 2^q (q = the lowest
+// set bit over V and the terms) and every partial sum is below 2^(q + 53); then V + (the block's
+// exact sum, any order) is the sequential result bit for bit.
+__device__ __forceinline__ int expo64(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023; }
+__device__ __forceinline__ int lsb64(double x) {  // x normal, non-zero
+  const unsigned long long m = ((unsigned long long)__double_as_longlong(x) & 0xfffffffffffffull) | (1ull << 52);
+  return expo64(x) - 52 + __ffsll((long long)m) - 1;
+}
+__device__ __forceinline__ int lsb32(float t) {  // t non-zero (normal or subnormal)
+  const unsigned u = __float_as_uint(t) & 0x7fffffffu;
+  const int fe = (int)(u >> 23);
+  const unsigned m = (u & 0x7fffffu) | (fe ? 0x800000u : 0u);
+  return (fe ? fe - 127 : -126) - 23 + __ffs((int)m) - 1;
+}
+// V + the block's terms, when the sequential fold provably rounds nowhere
+__device__ __forceinline__ bool fold_exact(double V, double absum, int qb) {
+  if (absum == 0.0) return true;  // only zero terms
+  int q = qb;
+  int e = expo64(absum);
+  if (V != 0.0) {
+    q = min(q, lsb64(V));
+    e = max(e, expo64(V));
+  }
+  return e + 2 <= q + 53;  // |partial| <= |V| + absum < 2^(e + 2) <= 2^(q + 53)
+}
+
 // ---------------------------------------------------------------- a7, batched gathers
 // a7 for a batch of points: issue every state gather first (one round trip), then decide.
 // The valid flag is not read: an invalid cell always holds a NaN variance (reset_cell, and

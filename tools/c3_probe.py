@@ -11,7 +11,7 @@ fr = [S.c3_frame(f) for f in range(2)]
 groups = [dict(name="sem", rule=3, n_channels=c["n_classes"], alpha0=1.0),
           dict(name="top", rule=4, n_channels=c["n_classes"])]
 binds = [(0, c["n_classes"], 0), (0, c["n_classes"], 1)]
-mp = M.Map(c["res"], c["rows"], c["cols"], groups)
+mp = M.Map(c["res"], c["rows"], c["cols"], groups, fuse_sorted=len(sys.argv) > 2 and sys.argv[2] == "sorted")
 dev = [dict(clouds=[torch.from_numpy(cl["points"]).cuda() for cl in f["clouds"]],
             img=torch.from_numpy(f["image"]["img"]).cuda()) for f in fr]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 50

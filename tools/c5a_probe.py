@@ -10,7 +10,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 c = S.C5A
 bt = [S.c5a_batch(f, 0, n) for f in range(2)]
 dev = [torch.from_numpy(b["points"]).cuda() for b in bt]
-mp = M.Map(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])], n_maps=n)
+mp = M.Map(c["res"], c["rows"], c["cols"], [dict(name="feat", rule=0, n_channels=1, w=c["w"])], n_maps=n,
+          fuse_sorted=len(sys.argv) > 2 and sys.argv[2] == "sorted")
 for i in range(6):
     b = bt[i % 2]
     mp.move_to_batch(b["move"])
