@@ -195,7 +195,11 @@ MEM_API mem_status mem_shard_local_sync(mem_map **shards, int nranks);
 /* Fuses one point cloud: n points of `stride` floats (xyz in the
  * sensor frame, then channels), AoS, host or device.  R (row-major 3x3, sensor->map) and
  * t (sensor position in the map/world frame) are host doubles.  n == 0 is legal and leaves
- * the map unchanged.  Atomic per call: on error nothing is enqueued.
+ * the map unchanged.  Atomic per call: on error nothing is enqueued.  Every result equals the
+ * sequential oracle bit for bit whatever the path: one colour group, one
+ * 1-channel average group (stride 4, 16-B aligned) or no group take the certified-atomic path
+ * when the call's 1/v terms span few binades (colour: at most 131,586 points per map per call);
+ * batches of >= 64 small maps the one-CTA-per-map kernel; everything else the sort pipeline.
  * Errors: EINVAL (n < 0, stride < 3, bad binding, a <= 0, b < 0, a + b r_max^2 not finite), EPOSE,
  * ECUDA. */
 MEM_API mem_status mem_input_pointcloud(mem_map *map, const float *pts, int64_t n, int stride, const mem_binding *bind,
