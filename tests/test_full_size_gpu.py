@@ -283,3 +283,22 @@ def test_red_path_batch_of_more_than_128_maps():
         lay = np.asarray(g.get_layer(nm))
         for b in check:
             assert np.array_equal(lay[b], oras[b].get_layer(nm), equal_nan=True), (b, nm)
+
+
+def test_colour_map_beyond_the_packed_count_limit_takes_the_sort_path():
+    """A colour call of more than 131,586 points per map cannot use the packed colour count word
+    of the RED path (b | n << 25 | n_out << 43): it is fused by the sort pipeline, with the same
+    bits as the oracle -- two LiDAR frames merged into one 262,144-point call, 3 calls."""
+    c = S.C2
+    groups = [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=c["w"])]
+    g = M.Map(c["res"], c["rows"], c["cols"], groups)
+    o = O.OracleMap(c["res"], c["rows"], c["cols"], groups)
+    for f in range(3):
+        a, b = S.c2_frame(2 * f), S.c2_frame(2 * f + 1)
+        pts = np.concatenate([a["points"], b["points"]]).astype(np.float32)
+        g.move_to(*a["move"])
+        o.move_to(*a["move"])
+        g.input_pointcloud(torch.from_numpy(pts).cuda(), [(0, 1, 0)], a["R"], a["t"], c["noise"])
+        o.input_pointcloud(pts, [(0, 1, 0)], a["R"], a["t"], c["noise"])
+        assert g.stats() == o.stats()
+    compare_layers(g, o, where="colour, 262,144 points per call: ")
