@@ -12,6 +12,24 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ unsigned long long evict_last_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 16-byte store with an L2 eviction-priority policy
+__device__ __forceinline__ void st_hint_u64x2(void *p, unsigned long long x, unsigned long long y,
+                                              unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(p), "l"(x), "l"(y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint_u64(void *p, unsigned long long x, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(x), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float ld_hint_f32(const float *p, unsigned long long pol) {
+  float r;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
 // read-once point data: no L1 allocation, evict-first in L2 so the scratch of the maps in
 // flight keeps its L2 residency
 __device__ __forceinline__ float4 ld_stream_f4(const float *p, unsigned long long pol) {

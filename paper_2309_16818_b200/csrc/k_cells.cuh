@@ -96,9 +96,18 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
     // re-zero the scratch for the next wave / point input
     const int q = (m - a.m0) * g.HW + phys[u];
     unsigned long long *r = a.rec + (long long)q * 4;
+#if MEM_SCRATCH_HINT
+    {  // evict-last: the zeroed lines should still be in L2 when the next point pass REDs into them
+      const unsigned long long pol = evict_last_policy();
+      st_hint_u64(a.cnt + q, 0ull, pol);
+      st_hint_u64x2(r, 0ull, 0ull, pol);
+      st_hint_u64x2(r + 2, 0ull, 0ull, pol);
+    }
+#else
     __stcg(a.cnt + q, 0ull);
     __stcg(reinterpret_cast<ulonglong2 *>(r), make_ulonglong2(0ull, 0ull));
     __stcg(reinterpret_cast<ulonglong2 *>(r) + 1, make_ulonglong2(0ull, 0ull));
+#endif
     if (kFast == 2) __stcg(reinterpret_cast<uint2 *>(a.cert) + q, make_uint2(0u, 0u));
   }
 }

@@ -2,6 +2,12 @@
 // D39).  Part of the single translation unit kernels.cu (included inside namespace memk, in order).
 #pragma once
 
+#ifndef MEM_SCRATCH_HINT
+#define MEM_SCRATCH_HINT 2  // L2 priorities: 1 = k_cells zeroes the RED scratch evict-last (the next
+                            // point pass REDs into it); 2 = also k_points' state gathers evict-first
+                            // (C2x64 114.4 -> 112.6 us; REDs evict-last measured slower)
+#endif
+
 // ---------------------------------------------------------------- exactness certificates
 // fp64 sums of fp32 terms are EXACT, in any order, when every partial sum is representable:
 // with e_max / e_min the largest / smallest binary exponent among the (non-zero) terms and n
@@ -78,8 +84,14 @@ __device__ __forceinline__ void mahalanobis(PointOut (&o)[N], const State &st, c
   for (int u = 0; u < N; ++u) {
     hv[u] = sv[u] = __int_as_float(0x7fc00000);
     if (o[u].test) {
+#if MEM_SCRATCH_HINT >= 2
+      const unsigned long long pf = evict_first_policy();
+      hv[u] = ld_hint_f32(elev + o[u].cell, pf);
+      sv[u] = ld_hint_f32(var + o[u].cell, pf);
+#else
       hv[u] = __ldcg(elev + o[u].cell);
       sv[u] = __ldcg(var + o[u].cell);
+#endif
     }
   }
 #pragma unroll
