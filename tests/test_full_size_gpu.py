@@ -218,13 +218,13 @@ def test_paths_give_identical_bits(case):
 
 
 @pytest.mark.parametrize("rows,n,group", [(16, 20000, "average"), (4, 100000, "average"), (8, 50000, "colour"),
-                                          (16, 20000, None), (2, 30000, None)])
+                                          (16, 20000, None), (2, 30000, None), (1, 40000, "average")])
 def test_uncertified_cells_are_refolded_exactly(rows, n, group):
     """Cells whose height terms z/v span more binades than the certificate allows (z from 1e-12
     to 1 m in one cell) cannot be summed by atomics in an order-free way: they must be
     recomputed in input order (k_collect + k_refold) and still equal the oracle bit for bit.
-    Cells of up to 4096 points take the sorted-list path, larger ones (4 x 4 map, 100k points;
-    2 x 2 map, 30k points) the whole-map walk; colour, 1-channel average and height only."""
+    Cells of up to 16384 points take the sorted-list path (block-certified fold), larger ones
+    (1 x 1 map, 40k points) the whole-map walk; colour, 1-channel average and height only."""
     rng = np.random.default_rng(11 + rows)
     cols = rows
     res = 0.1
