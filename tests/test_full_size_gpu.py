@@ -220,9 +220,20 @@ def test_paths_give_identical_bits(case):
 @pytest.mark.parametrize("rows,n,group", [(16, 20000, "average"), (4, 100000, "average"), (8, 50000, "colour"),
                                           (16, 20000, None), (2, 30000, None), (1, 40000, "average")])
 def test_uncertified_cells_are_refolded_exactly(rows, n, group):
+    run_uncertified(rows, n, group, sorted_=False)
+
+
+@pytest.mark.parametrize("rows,n,group", [(16, 20000, "average"), (8, 50000, "colour"), (2, 30000, None)])
+def test_uncertified_cells_through_the_sort_path(rows, n, group):
+    """The same inputs through the sort pipeline (MEM_FLAG_FUSE_SORTED): mid and long cells whose
+    certificate fails fold block-certified in input order (k_fuse), bit-exact."""
+    run_uncertified(rows, n, group, sorted_=True)
+
+
+def run_uncertified(rows, n, group, sorted_):
     """Cells whose height terms z/v span more binades than the certificate allows (z from 1e-12
     to 1 m in one cell) cannot be summed by atomics in an order-free way: they must be
-    recomputed in input order (k_collect + k_refold) and still equal the oracle bit for bit.
+    recomputed in input order (k_refold) and still equal the oracle bit for bit.
     Cells of up to 16384 points take the sorted-list path (block-certified fold), larger ones
     (1 x 1 map, 40k points) the whole-map walk; colour, 1-channel average and height only."""
     rng = np.random.default_rng(11 + rows)
@@ -233,7 +244,7 @@ def test_uncertified_cells_are_refolded_exactly(rows, n, group):
     groups = {"average": [dict(name="feat", rule=M.MEM_AVERAGE, n_channels=1, w=0.5)],
               "colour": [dict(name="rgb", rule=M.MEM_COLOR, n_channels=3, w=0.5)], None: []}[group]
     binds = [] if group is None else [(0, 1, 0)]
-    g = M.Map(res, rows, cols, groups, debug_points=True)
+    g = M.Map(res, rows, cols, groups, debug_points=True, fuse_sorted=sorted_)
     o = O.OracleMap(res, rows, cols, groups)
     for f in range(4):
         xy = rng.uniform(-half, half, (n, 2))
