@@ -88,6 +88,7 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 constexpr int kImgBatch = MEM_IMG_BATCH;
 constexpr int kImgLanes = MEM_IMG_LANES;
 // the group's channels k = sub, sub + L, ... of one binding fused with N_j = 1
+template <bool kSimple>
 __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW, long long cell, const GroupDesc &g,
                                                  const float *ch, long long plane, int sub, unsigned gmask) {
   float *vals = reinterpret_cast<float *>(st.words);
@@ -95,7 +96,7 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
   const bool observed = *obs != 0;
   const bool dir = g.rule == MEM_CLASS_BAYESIAN;
   constexpr int L = kImgLanes;
-  if (g.rule == MEM_GAUSSIAN) {  // two words per channel: mean at word0 + k, variance at word0 + nch + k
+  if (!kSimple && g.rule == MEM_GAUSSIAN) {  // two words per channel: mean at word0 + k, variance at word0 + nch + k
     for (int k0 = 0; k0 < g.nch; k0 += kImgBatch * L) {
       float p[kImgBatch], mu[kImgBatch], var[kImgBatch];
 #pragma unroll
@@ -146,6 +147,8 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
 #endif
 constexpr int kImgThreads = MEM_IMG_THREADS;
 constexpr int kImgCells = kImgThreads / kImgLanes;  // cells per CTA
+// kSimple: no top-k binding, no gaussian group, no occlusion walk (C3, C4): a leaner kernel
+template <bool kSimple>
 __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ ImageArgs a) {
   constexpr int L = kImgLanes;
   const Geometry &g = a.geo;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
   const float v = f.K[3] * uy + f.K[4];
   const float fu = floorf(u + 0.5f), fv = floorf(v + 0.5f);  // nearest pixel (D16)
   if (!(0.0f <= fu && fu < (float)a.IW && 0.0f <= fv && fv < (float)a.IH)) return;  // frustum
-  if (a.occlusion) {  // the walk on the group's first lane
+  if (!kSimple && a.occlusion) {  // the walk on the group's first lane
     bool vis = false;
     if (sub == 0) vis = cell_visible(a, m, row, col, f.t[0], f.t[1], f.t[2], hcell, ring);
     if (!__shfl_sync(gmask, vis, 0, L)) return;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
   for (int bi = 0; bi < a.nb; ++bi) {
     const BindDesc &b = a.b[bi];
     const float *ch = pix + (long long)b.ch_offset * plane;
-    if (b.topk > 0) {  // top-k pairs (D38): the group's first lane
+    if (!kSimple && b.topk > 0) {  // top-k pairs (D38): the group's first lane
       if (sub == 0) {
         const TopK tk{ch, plane, b.topk, b.g.nch - 1};
         if (tk.ok()) {
@@ -243,6 +246,6 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
       __syncwarp(gmask);
       continue;
     }
-    image_fuse_words(a.st, g.BHW, cell, b.g, ch, plane, sub, gmask);
+    image_fuse_words<kSimple>(a.st, g.BHW, cell, b.g, ch, plane, sub, gmask);
   }
 }

@@ -245,7 +245,12 @@ cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long l
 }
 
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
-  k_image<<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
+  bool simple = !a.occlusion;
+  for (int i = 0; i < a.nb && simple; ++i) simple = a.b[i].topk == 0 && a.b[i].g.rule != MEM_GAUSSIAN;
+  if (simple)
+    k_image<true><<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
+  else
+    k_image<false><<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
