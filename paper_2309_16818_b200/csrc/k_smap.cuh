@@ -20,6 +20,10 @@
 #define MEM_SMAP_MINB 1
 #endif
 constexpr int kSmapThreads = MEM_SMAP_THREADS;
+#ifndef MEM_SMAP_P1
+#define MEM_SMAP_P1 2  // P1: points per thread in flight (C5a: 4 -> 2: 3.18 -> 3.13 ms)
+#endif
+constexpr int kSmapP1 = MEM_SMAP_P1;
 constexpr int kSmapCells = 16384;
 constexpr int kSmapPoints = 65535;
 
@@ -87,15 +91,15 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
     if (threadIdx.x == 0) a.ring[m] = make_int2(f.r0, f.c0);
     __syncthreads();
     // P1: bin every point (a2-a6), histogram of the in-window points' cells
-    for (int i0 = threadIdx.x; i0 < np; i0 += 4 * kSmapThreads) {
-      float4 q[4];
+    for (int i0 = threadIdx.x; i0 < np; i0 += kSmapP1 * kSmapThreads) {
+      float4 q[kSmapP1];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kSmapP1; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i < np) q[u] = ld_stream_f4(reinterpret_cast<const float *>(pts4 + beg + i), pol);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kSmapP1; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
         const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, map_base, a.r2lo, a.r2hi);
@@ -149,15 +153,15 @@ __global__ void __launch_bounds__(kSmapThreads, MEM_SMAP_MINB) k_smap(const __gr
         if (c != 0xffffu) idx[(atomicAdd(&hist[c >> 1], 1u << (16 * (c & 1))) >> (16 * (c & 1))) & 0xffffu] = (uint16_t)i;
       }
     }
-    for (int i0 = threadIdx.x; i0 < (cached ? 0 : np); i0 += 4 * kSmapThreads) {  // re-binned (points in L2)
-      float4 q[4];
+    for (int i0 = threadIdx.x; i0 < (cached ? 0 : np); i0 += kSmapP1 * kSmapThreads) {  // re-binned (points in L2)
+      float4 q[kSmapP1];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kSmapP1; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i < np) q[u] = __ldg(pts4 + beg + i);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kSmapP1; ++u) {
         const int i = i0 + u * kSmapThreads;
         if (i >= np) continue;
         const PointOut o = bin_point(q[u].x, q[u].y, q[u].z, f, g, a.np, map_base, a.r2lo, a.r2hi);
