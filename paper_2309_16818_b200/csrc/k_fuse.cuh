@@ -3,6 +3,11 @@
 // memk, in order).
 #pragma once
 
+#ifndef MEM_FUSE_MINB0
+#define MEM_FUSE_MINB0 4  // k_fuse short cells, generic groups: CTAs per SM the registers are sized for
+                           // (8: spills; 4: paper sweep 3-5% faster)
+#endif
+
 // ---------------------------------------------------------------- k_fuse
 // Persistent grid-stride over the call's segments (one touched cell each: its records are
 // contiguous in the sorted array, in input order, k_sort).  One thread per cell runs the
@@ -660,7 +665,7 @@ __device__ __forceinline__ void fuse_cell_warp(const PassArgs &a, const uint4 se
 // kPart 0: the short cells (a thread each); kPart 1: long cells (16 lanes each), then mid-size
 // ones (8 lanes each).  Two kernels, so that the common short-cell kernel keeps few registers.
 template <bool kDebug, int kFast, int kPart>
-__global__ void __launch_bounds__(kFuseThreads, kPart == 0 ? 8 : 4) k_fuse(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(kFuseThreads, kPart == 0 ? (kFast == 0 ? MEM_FUSE_MINB0 : 8) : 4) k_fuse(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   pdl_wait();
