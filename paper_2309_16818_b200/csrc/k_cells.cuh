@@ -120,8 +120,11 @@ constexpr int kChunk = 32 * kChunkPerLane;        // 128-cell chunk per warp
 // scratch was touched last by k_points and is still in L2).  Each warp, independently of the
 // others (no CTA barrier): 4 count loads per lane in flight, the pending shift strips reset,
 // its touched cells compacted in its own shared-memory slice, then fused 2 per lane per round.
+#ifndef MEM_CELLS_MINB
+#define MEM_CELLS_MINB 3  // k_cells: CTAs per SM the registers are sized for
+#endif
 template <int kFast>
-__global__ void __launch_bounds__(kThreads, 3) k_cells(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid_constant__ PassArgs a) {
   __shared__ int s_phys[kThreads / 32][kChunk];
   __shared__ unsigned long long s_cntv[kThreads / 32][kChunk];
   __shared__ unsigned s_cnt[8];

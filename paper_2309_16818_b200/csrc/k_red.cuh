@@ -370,8 +370,11 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   }
 }
 
+#ifndef MEM_POINTS_MINB
+#define MEM_POINTS_MINB 3  // k_points: CTAs per SM the registers are sized for
+#endif
 template <bool kDebug, int kFast>
-__global__ void __launch_bounds__(kThreads, 3) k_points(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
