@@ -26,7 +26,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
   for (int u = 0; u < N; ++u) {  // one round of loads
     if (phys[u] < 0) continue;
     const int c = m * g.HW + phys[u];                // state
-    const int q = (m - a.m0) * g.HW + phys[u];       // scratch (this wave's maps)
+    const int q = (m - a.m0) * g.HW + phys[u] - a.sc_lo;  // scratch (this wave's maps / cells)
     const ulonglong2 *r = reinterpret_cast<const ulonglong2 *>(a.rec + (long long)q * 4);
     const ulonglong2 ps = __ldcg(r), ww = __ldcg(r + 1);
     P[u] = __longlong_as_double((long long)ps.x);
@@ -94,7 +94,7 @@ __device__ __forceinline__ void fuse_cells_red(const PassArgs &a, int m, const i
       a.fbmap[m] = 1u;
     }
     // re-zero the scratch for the next wave / point input
-    const int q = (m - a.m0) * g.HW + phys[u];
+    const int q = (m - a.m0) * g.HW + phys[u] - a.sc_lo;
     unsigned long long *r = a.rec + (long long)q * 4;
 #if MEM_SCRATCH_HINT
     {  // evict-last: the zeroed lines should still be in L2 when the next point pass REDs into them
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
     const int mi = chunk / cpm;
     const int m = a.m0 + mi;
     const int t0 = a.cell_lo + (chunk - mi * cpm) * kChunk;
-    const int sb = mi * g.HW;  // scratch
+    const int sb = mi * g.HW - a.sc_lo;  // scratch
     unsigned long long cv[kChunkPerLane];
 #pragma unroll
     for (int u = 0; u < kChunkPerLane; ++u) {  // counts first (memory-level parallelism)

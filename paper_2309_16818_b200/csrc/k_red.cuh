@@ -333,7 +333,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
   const int lane = threadIdx.x & 31;
   const PointFrame f = frame_of(a, t.m);
   const int map_base = t.m * g.HW;
-  const int sb = (t.m - a.m0) * g.HW;  // the map's scratch cells (this wave's maps)
+  const int sb = (t.m - a.m0) * g.HW - a.sc_lo;  // the map's scratch cells (this wave's maps / cells)
   // points of the item present: [0, nv) (32-bit indices within the item)
   const int nv = kFull ? kWarpPoints : t.end - t.base < kWarpPoints ? (int)(t.end - t.base) : kWarpPoints;
   PointOut o[kWarpPtsPerLane];
@@ -342,6 +342,14 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
     const bool in = u * 32 + lane < nv;
     if (in) {
       o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, map_base, a.r2lo, a.r2hi);
+      if (a.sc_hi > 0) {  // cell waves: another wave's point is skipped, a dropped one counted once
+        const int phys = o[u].cell - map_base;
+        if (o[u].cell >= 0 ? phys < a.sc_lo || phys >= a.sc_hi : !a.wave_first) {
+          o[u].code = -1;
+          o[u].cell = -1;
+          o[u].test = false;
+        }
+      }
     } else {
       o[u].code = in ? MEM_CODE_NONFINITE : -1;
       o[u].cell = -1;

@@ -82,26 +82,69 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
       if (in_strip(row, col, f, g)) reset_cell(a.st, g.BHW, gb + i, a.reset);
     }
   }
-  // 2. the runs of this band in the map's tiles, and their prefix (input order)
+  // 2. the runs of this band in the map's tiles, and their prefix (input order): all the
+  // (strided) tinfo loads in flight first, then the scan over shared memory
+  for (int tb = 0; tb < T; tb += 4 * kSortThreads) {
+    unsigned v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = tb + u * kSortThreads + tid;
+      v[u] = t < T ? __ldcg(a.tinfo + (long long)(t0 + t) * a.nbands + bb) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = tb + u * kSortThreads + tid;
+      if (t < T) tcnt_s[t] = v[u];
+    }
+  }
+  __syncthreads();
   unsigned K = 0u;
   for (int tb = 0; tb < T; tb += kSortThreads) {
     const int t = tb + tid;
-    const unsigned v = t < T ? __ldcg(a.tinfo + (long long)(t0 + t) * a.nbands + bb) : 0u;
+    const unsigned v = t < T ? tcnt_s[t] : 0u;
     unsigned tot;
     const unsigned pre = block_excl_scan<kSortThreads>(v >> 16, s_part, &tot);
-    if (t < T) {
-      tcnt_s[t] = v;
-      tpre_s[t] = K + pre;
-    }
+    if (t < T) tpre_s[t] = K + pre;
     K += tot;
   }
   if (tid == 0) tpre_s[T] = K;
   __syncthreads();
   const int nwin = (int)((K + kSortCap - 1) / kSortCap);
+  // runs of a few records (a sparse band: C5b's uniform cloud) are gathered by every thread with
+  // plain loads; longer runs by one bulk copy each (warp 0)
+  const bool short_runs = K < (unsigned)T * kSortBulkRun;
   unsigned phase = 0u;
-  // the window [p0, p0 + n) of band positions into rec_s: one bulk copy per tile run (warp 0),
-  // all in flight together; every thread waits for the lot
+  // the window [p0, p0 + n) of band positions into rec_s, all the copies in flight together;
+  // every thread waits for the lot
   auto load_window = [&](unsigned p0, unsigned n) {
+    if (short_runs) {
+      for (int tb = 0; tb < T; tb += 4 * kSortThreads) {  // 4 tiles per thread in flight
+        unsigned lo[4], hi[4];
+        const uint4 *src[4];
+        uint4 r0[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = tb + u * kSortThreads + tid;
+          lo[u] = hi[u] = 0u;
+          src[u] = a.recs;
+          if (t < T) {
+            lo[u] = tpre_s[t] > p0 ? tpre_s[t] : p0;
+            hi[u] = tpre_s[t + 1] < p0 + n ? tpre_s[t + 1] : p0 + n;
+            src[u] = a.recs + (long long)(t0 + t) * kTile + (tcnt_s[t] & 0xffffu) - tpre_s[t];
+          }
+          if (hi[u] > lo[u]) r0[u] = __ldcg(src[u] + lo[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (hi[u] > lo[u]) {
+            rec_s[lo[u] - p0] = r0[u];
+            for (unsigned r = lo[u] + 1; r < hi[u]; ++r) rec_s[r - p0] = __ldcg(src[u] + r);
+          }
+        }
+      }
+      __syncthreads();
+      return;
+    }
     if (wid == 0) {
       if (lane == 0) mbar_arrive_expect_tx(bar, 16u * n);
       __syncwarp();

@@ -19,6 +19,10 @@ constexpr int kMaxBands = 2048;         // bands per map (k_bin's per-warp band 
 #endif
 constexpr int kSortThreads = MEM_SORT_THREADS;
 constexpr int kSortCap = 1024;          // records ranked per window (shared memory)
+#ifndef MEM_SORT_BULK_RUN
+#define MEM_SORT_BULK_RUN 4
+#endif
+constexpr int kSortBulkRun = MEM_SORT_BULK_RUN;  // k_sort: mean run length from which runs are bulk-copied
 constexpr int kSortChunk = 2048;        // band sizing: records expected per band
 constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in shared memory)
 // k_fuse: persistent grid-stride over the touched cells, one thread each
@@ -73,6 +77,10 @@ struct PassArgs {
   const int *tstart;
   const int *pstart;           // k_points: prefix sums of 128-point warp-items per map (staged)
   int m0, m1;                  // k_points / k_smap: maps [m0, m1) = all maps of the call
+  int sc_lo, sc_hi;            // RED path, cell waves of one big map: k_points accumulates the points of
+                               // the physical cells [sc_lo, sc_hi) only (sc_hi 0: every cell), into scratch
+                               // cell (phys - sc_lo); k_cells fuses [cell_lo, cell_hi) = the same range
+  int wave_first;               // the first cell wave of the call (counts the dropped points)
   int smap_maxpts;             // k_smap: points of the largest map of the call (shared memory layout)
   int p_uniform;               // > 0: every map has exactly this many warp-items
   double inv_p_uniform;

@@ -769,6 +769,9 @@ static bool p_certified(const PassArgs &a, long long max_n) {
 #ifndef MEM_WAVE_MB
 #define MEM_WAVE_MB 0  // RED scratch budget: 0 = all maps of a call in one wave
 #endif
+#ifndef MEM_CELL_WAVE_MB
+#define MEM_CELL_WAVE_MB 64  // one big map: RED scratch per cell wave (0 = one wave; C5b: 48 / 64 / 100 MB -> 389 / 325 / 330 us)
+#endif
 static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offsets, long long total) {
   const int B = a.n_maps;
   const size_t HW = (size_t)m->H * m->W;
@@ -777,7 +780,16 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
   const size_t per_cell = 8 + 32 + (a.fast == 2 ? 8 : 0);
   int wmaps = B;
   if (MEM_WAVE_MB > 0) wmaps = (int)std::max<size_t>(1, std::min<size_t>(B, (size_t)MEM_WAVE_MB * 1048576 / (per_cell * HW)));
-  const size_t cells = (size_t)wmaps * HW, all = (size_t)B * HW;
+  // one big map (C5b): waves of cells whose scratch stays in L2 between the cell pass that
+  // zeroes it and the next wave's REDs; every wave re-reads the points
+  const int clo = a.cell_lo, chi = a.cell_hi;
+  const size_t band = (size_t)(chi - clo);
+  int wcells = 0;
+  if (B == 1 && a.dbg_cell == nullptr && MEM_CELL_WAVE_MB > 0 && per_cell * band > (size_t)MEM_CELL_WAVE_MB * 1048576) {
+    const size_t nw = (per_cell * band + (size_t)MEM_CELL_WAVE_MB * 1048576 - 1) / ((size_t)MEM_CELL_WAVE_MB * 1048576);
+    wcells = (int)(((band + nw - 1) / nw + 1023) / 1024 * 1024);
+  }
+  const size_t cells = wcells ? (size_t)wcells : (size_t)wmaps * HW, all = (size_t)B * HW;
   if (cells > m->red_cells || all > m->red_all) {
     CU(cudaStreamSynchronize(m->stream));
     void **bufs[] = {&m->rcnt_s, &m->rrec_s, &m->rcert_s, &m->rfb_s, &m->rmark_s, &m->rfill_s, &m->rmapfb_s};
@@ -830,6 +842,23 @@ static mem_status fuse_points_red(mem_map *m, PassArgs &a, const int64_t *offset
     a.pstart = nullptr;
   }  // else: a.pstart points into the staged parameter blob (input_points)
   HP(8);
+  if (wcells) {
+    a.m0 = 0;
+    a.m1 = 1;
+    for (int lo = clo; lo < chi; lo += wcells) {
+      a.sc_lo = a.cell_lo = lo;
+      a.sc_hi = a.cell_hi = std::min(chi, lo + wcells);
+      a.wave_first = lo == clo;
+      if (ps[1] > ps[0]) TIMED(MEM_STAGE_POINT, launch_points(a, m->stream));
+      else CU(cudaMemsetAsync(&m->ctl->n_fb, 0, sizeof(unsigned) * 2, m->stream));
+      TIMED(MEM_STAGE_CELL, launch_cells(a, m->stream));
+    }
+    a.sc_lo = a.sc_hi = 0;
+    a.cell_lo = clo;
+    a.cell_hi = chi;
+    HP(10);
+    return MEM_OK;
+  }
   for (int w0 = 0; w0 < B; w0 += wmaps) {
     a.m0 = w0;
     a.m1 = std::min(B, w0 + wmaps);
