@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
   const int nwin = (int)((K + kSortCap - 1) / kSortCap);
   // runs of a few records (a sparse band: C5b's uniform cloud) are gathered by every thread with
   // plain loads; longer runs by one bulk copy each (warp 0)
-  const bool short_runs = K < (unsigned)T * kSortBulkRun;
+  const bool short_runs = 4ull * K < (unsigned long long)T * kSortBulkRun4;
   unsigned phase = 0u;
   // the window [p0, p0 + n) of band positions into rec_s, all the copies in flight together;
   // every thread waits for the lot
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
       for (int tb = 0; tb < T; tb += 4 * kSortThreads) {  // 4 tiles per thread in flight
         unsigned lo[4], hi[4];
         const uint4 *src[4];
-        uint4 r0[4];
+        uint4 r0[4], r1[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int t = tb + u * kSortThreads + tid;
@@ -133,13 +133,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
             src[u] = a.recs + (long long)(t0 + t) * kTile + (tcnt_s[t] & 0xffffu) - tpre_s[t];
           }
           if (hi[u] > lo[u]) r0[u] = __ldcg(src[u] + lo[u]);
+          if (hi[u] > lo[u] + 1) r1[u] = __ldcg(src[u] + lo[u] + 1);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (hi[u] > lo[u]) {
-            rec_s[lo[u] - p0] = r0[u];
-            for (unsigned r = lo[u] + 1; r < hi[u]; ++r) rec_s[r - p0] = __ldcg(src[u] + r);
-          }
+          if (hi[u] > lo[u]) rec_s[lo[u] - p0] = r0[u];
+          if (hi[u] > lo[u] + 1) rec_s[lo[u] + 1 - p0] = r1[u];
+          for (unsigned r = lo[u] + 2; r < hi[u]; ++r) rec_s[r - p0] = __ldcg(src[u] + r);
         }
       }
       __syncthreads();

@@ -15,14 +15,14 @@ constexpr int kTile = kBinThreads * kBinPerThread;  // 2048
 constexpr int kMaxBands = 2048;         // bands per map (k_bin's per-warp band counters)
 // k_sort: one CTA per (map, band); the band's records counting-sorted kSortCap at a time
 #ifndef MEM_SORT_THREADS
-#define MEM_SORT_THREADS 128
+#define MEM_SORT_THREADS 256
 #endif
 constexpr int kSortThreads = MEM_SORT_THREADS;
 constexpr int kSortCap = 1024;          // records ranked per window (shared memory)
-#ifndef MEM_SORT_BULK_RUN
-#define MEM_SORT_BULK_RUN 4
+#ifndef MEM_SORT_BULK_RUN4
+#define MEM_SORT_BULK_RUN4 6
 #endif
-constexpr int kSortBulkRun = MEM_SORT_BULK_RUN;  // k_sort: mean run length from which runs are bulk-copied
+constexpr int kSortBulkRun4 = MEM_SORT_BULK_RUN4;  // k_sort: 4 x the mean run length from which runs are bulk-copied
 constexpr int kSortChunk = 2048;        // band sizing: records expected per band
 constexpr int kMaxBandCells = 4096;     // cells per band (per-cell arrays in shared memory)
 // k_fuse: persistent grid-stride over the touched cells, one thread each
