@@ -324,7 +324,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool kDebug, int kFast, bool kFull = false>
+template <bool kDebug, int kFast, bool kWave, bool kFull = false>
 __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, const float (&px)[kWarpPtsPerLane],
                                              const float (&py)[kWarpPtsPerLane], const float (&pz)[kWarpPtsPerLane],
                                              const float (&pw)[kWarpPtsPerLane],
@@ -342,7 +342,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
     const bool in = u * 32 + lane < nv;
     if (in) {
       o[u] = bin_point(px[u], py[u], pz[u], f, g, a.np, map_base, a.r2lo, a.r2hi);
-      if (a.sc_hi > 0) {  // cell waves: another wave's point is skipped, a dropped one counted once
+      if (kWave) {  // cell waves: another wave's point is skipped, a dropped one counted once
         const int phys = o[u].cell - map_base;
         if (o[u].cell >= 0 ? phys < a.sc_lo || phys >= a.sc_hi : !a.wave_first) {
           o[u].code = -1;
@@ -381,7 +381,7 @@ __device__ __forceinline__ void process_item(const PassArgs &a, const Item &t, c
 #ifndef MEM_POINTS_MINB
 #define MEM_POINTS_MINB 3  // k_points: CTAs per SM the registers are sized for
 #endif
-template <bool kDebug, int kFast>
+template <bool kDebug, int kFast, bool kWave>
 __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __grid_constant__ PassArgs a) {
   __shared__ unsigned s_cnt[8];
   __shared__ float4 s_pts[kThreads / 32][2][kWarpPoints];  // per warp: 2 stages x 128 points
@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
       }
 #if MEM_FULL_ITEMS
       if (cur.end - cur.base >= kWarpPoints)  // every lane holds 4 points: no bounds checks
-        process_item<kDebug, kFast, true>(a, cur, px, py, pz, pw, packed, npk, cnt);
+        process_item<kDebug, kFast, kWave, true>(a, cur, px, py, pz, pw, packed, npk, cnt);
       else
 #endif
-        process_item<kDebug, kFast>(a, cur, px, py, pz, pw, packed, npk, cnt);
+        process_item<kDebug, kFast, kWave>(a, cur, px, py, pz, pw, packed, npk, cnt);
       cur = nxt;
     }
   } else {
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
           px[u] = q[0]; py[u] = q[1]; pz[u] = q[2]; pw[u] = 0.0f;
         }
         __syncwarp();  // the slice is rewritten by the warp's next item
-        process_item<kDebug, kFast, MEM_FULL_ITEMS != 0>(a, t, px, py, pz, pw, packed, npk, cnt);
+        process_item<kDebug, kFast, kWave, MEM_FULL_ITEMS != 0>(a, t, px, py, pz, pw, packed, npk, cnt);
         continue;
       }
 #pragma unroll
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, MEM_POINTS_MINB) k_points(const __gr
           px[u] = __ldg(q); py[u] = __ldg(q + 1); pz[u] = __ldg(q + 2);
         }
       }
-      process_item<kDebug, kFast>(a, t, px, py, pz, pw, packed, npk, cnt);
+      process_item<kDebug, kFast, kWave>(a, t, px, py, pz, pw, packed, npk, cnt);
     }
   }
 #pragma unroll

@@ -151,17 +151,23 @@ static int resident_grid(K kernel, int threads, int slot) {
   return gd;
 }
 
-template <bool kDebug, int kFast>
+template <bool kDebug, int kFast, bool kWave = false>
 static cudaError_t launch_points_t(const PassArgs &a, cudaStream_t s) {
   const long long items = (long long)(a.pstart ? 0 : a.psi[a.m1] - a.psi[a.m0]);
-  int g = resident_grid(k_points<kDebug, kFast>, kThreads, kFast + (kDebug ? 3 : 0));
+  int g = resident_grid(k_points<kDebug, kFast, kWave>, kThreads, kWave ? 10 + kFast : kFast + (kDebug ? 3 : 0));
   if (items > 0) g = (int)std::max(1LL, std::min<long long>(g, (items + 7) / 8));
-  return launch_pdl(k_points<kDebug, kFast>, g, 0, s, a, kThreads);
+  return launch_pdl(k_points<kDebug, kFast, kWave>, g, 0, s, a, kThreads);
 }
 
 cudaError_t launch_points(const PassArgs &a, cudaStream_t s) {
   const bool dbg = a.dbg_cell != nullptr;
   const int f = a.fast == 3 ? 0 : a.fast;
+  if (a.sc_hi > 0) {  // cell waves of one big map (never with debug outputs): their own instantiation,
+                      // so that the filter costs the other calls no registers
+    if (f == 1) return launch_points_t<false, 1, true>(a, s);
+    if (f == 2) return launch_points_t<false, 2, true>(a, s);
+    return launch_points_t<false, 0, true>(a, s);
+  }
   if (f == 1) return dbg ? launch_points_t<true, 1>(a, s) : launch_points_t<false, 1>(a, s);
   if (f == 2) return dbg ? launch_points_t<true, 2>(a, s) : launch_points_t<false, 2>(a, s);
   return dbg ? launch_points_t<true, 0>(a, s) : launch_points_t<false, 0>(a, s);
