@@ -110,9 +110,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort(const __grid_constant__ P
   if (tid == 0) tpre_s[T] = K;
   __syncthreads();
   const int nwin = (int)((K + kSortCap - 1) / kSortCap);
-  // runs of a few records (a sparse band: C5b's uniform cloud) are gathered by every thread with
-  // plain loads; longer runs by one bulk copy each (warp 0)
-  const bool short_runs = 4ull * K < (unsigned long long)T * kSortBulkRun4;
+  // runs of a few records in a map of many tiles (a sparse band: C5b's uniform cloud) are gathered
+  // by every thread with plain loads; otherwise every run by one bulk copy (warp 0)
+  const bool short_runs = T > kSortThreads && 4ull * K < (unsigned long long)T * kSortBulkRun4;
   unsigned phase = 0u;
   // the window [p0, p0 + n) of band positions into rec_s, all the copies in flight together;
   // every thread waits for the lot
