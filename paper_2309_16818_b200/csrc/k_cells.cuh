@@ -123,10 +123,13 @@ constexpr int kChunk = 32 * kChunkPerLane;        // 128-cell chunk per warp
 #ifndef MEM_CELLS_MINB
 #define MEM_CELLS_MINB 3  // k_cells: CTAs per SM the registers are sized for
 #endif
-template <int kFast>
+// kCPL: cells per lane per chunk -- 4 (128-cell chunks) when the call has chunks for every
+// resident warp, else 1 (32-cell chunks: a small map spreads over more SMs, shorter chains)
+template <int kFast, int kCPL>
 __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid_constant__ PassArgs a) {
-  __shared__ int s_phys[kThreads / 32][kChunk];
-  __shared__ unsigned long long s_cntv[kThreads / 32][kChunk];
+  constexpr int kCh = 32 * kCPL;
+  __shared__ int s_phys[kThreads / 32][kCh];
+  __shared__ unsigned long long s_cntv[kThreads / 32][kCh];
   __shared__ unsigned s_cnt[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   pdl_wait();
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (kThreads / 32);
   const int gw = blockIdx.x * (kThreads / 32) + wid;
-  const int cpm = (a.cell_hi - a.cell_lo + kChunk - 1) / kChunk;  // chunks per map (band)
+  const int cpm = (a.cell_hi - a.cell_lo + kCh - 1) / kCh;  // chunks per map (band)
   const int total = (a.m1 - a.m0) * cpm;  // this wave's maps
   int *sp = s_phys[wid];
   unsigned long long *sc = s_cntv[wid];
@@ -145,11 +148,11 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
     const int chunk = total - 1 - rt;
     const int mi = chunk / cpm;
     const int m = a.m0 + mi;
-    const int t0 = a.cell_lo + (chunk - mi * cpm) * kChunk;
+    const int t0 = a.cell_lo + (chunk - mi * cpm) * kCh;
     const int sb = mi * g.HW - a.sc_lo;  // scratch
-    unsigned long long cv[kChunkPerLane];
+    unsigned long long cv[kCPL];
 #pragma unroll
-    for (int u = 0; u < kChunkPerLane; ++u) {  // counts first (memory-level parallelism)
+    for (int u = 0; u < kCPL; ++u) {  // counts first (memory-level parallelism)
       const int phys = t0 + u * 32 + lane;
       cv[u] = phys < a.cell_hi ? __ldcg(a.cnt + sb + phys) : 0ull;
     }
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, MEM_CELLS_MINB) k_cells(const __grid
     if (t0 == a.cell_lo && lane == 0) a.ring[m] = make_int2(f.r0, f.c0);
     int n = 0;
 #pragma unroll
-    for (int u = 0; u < kChunkPerLane; ++u) {
+    for (int u = 0; u < kCPL; ++u) {
       const int phys = t0 + u * 32 + lane;
       if (phys < a.cell_hi && (f.sr != 0 || f.sc != 0)) {  // lazy ring shift: reset the scrolled-in cells (a13)
         int pcol;

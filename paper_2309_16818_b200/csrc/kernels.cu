@@ -176,9 +176,16 @@ cudaError_t launch_points(const PassArgs &a, cudaStream_t s) {
 template <int kFast>
 static cudaError_t launch_cells_t(const PassArgs &a, cudaStream_t s) {
   const long long chunks = (long long)(a.m1 - a.m0) * ((a.cell_hi - a.cell_lo + kChunk - 1) / kChunk);
-  const int g = (int)std::max(1LL, std::min<long long>(resident_grid(k_cells<kFast>, kThreads, 6 + kFast),
-                                                       (chunks + 7) / 8));
-  cudaError_t e = launch_pdl(k_cells<kFast>, g, 0, s, a, kThreads);
+  const int res = resident_grid(k_cells<kFast, kChunkPerLane>, kThreads, 6 + kFast);
+  cudaError_t e;
+  if (chunks >= (long long)res * (kThreads / 32)) {  // a chunk for every resident warp
+    e = launch_pdl(k_cells<kFast, kChunkPerLane>, res, 0, s, a, kThreads);
+  } else {  // small calls (C3, single maps): 32-cell chunks
+    const long long ch1 = (long long)(a.m1 - a.m0) * ((a.cell_hi - a.cell_lo + 31) / 32);
+    const int g = (int)std::max(1LL, std::min<long long>(resident_grid(k_cells<kFast, 1>, kThreads, 13 + kFast),
+                                                         (ch1 + 7) / 8));
+    e = launch_pdl(k_cells<kFast, 1>, g, 0, s, a, kThreads);
+  }
   if (e != cudaSuccess) return e;
   // uncertified cells (none: k_refold returns at once): a cooperative launch (its collect
   // phase and its folds are separated by a grid barrier), every CTA resident
