@@ -88,7 +88,7 @@ __device__ __forceinline__ bool cell_visible(const ImageArgs &a, int m, int row,
 constexpr int kImgBatch = MEM_IMG_BATCH;
 constexpr int kImgLanes = MEM_IMG_LANES;
 // the group's channels k = sub, sub + L, ... of one binding fused with N_j = 1
-template <bool kSimple>
+template <bool kSimple, int kB>
 __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW, long long cell, const GroupDesc &g,
                                                  const float *ch, long long plane, int sub, unsigned gmask) {
   float *vals = reinterpret_cast<float *>(st.words);
@@ -97,10 +97,10 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
   const bool dir = g.rule == MEM_CLASS_BAYESIAN;
   constexpr int L = kImgLanes;
   if (!kSimple && g.rule == MEM_GAUSSIAN) {  // two words per channel: mean at word0 + k, variance at word0 + nch + k
-    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch * L) {
-      float p[kImgBatch], mu[kImgBatch], var[kImgBatch];
+    for (int k0 = 0; k0 < g.nch; k0 += kB * L) {
+      float p[kB], mu[kB], var[kB];
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) {
+      for (int u = 0; u < kB; ++u) {
         const int k = k0 + u * L + sub;
         if (k < g.nch) {
           p[u] = __ldg(ch + (long long)k * plane);
@@ -109,7 +109,7 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
         }
       }
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) {
+      for (int u = 0; u < kB; ++u) {
         const int k = k0 + u * L + sub;
         if (k < g.nch) {
           rule_gaussian(mu[u], var[u], observed, (double)p[u], 1.0, g);
@@ -119,10 +119,10 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
       }
     }
   } else {
-    for (int k0 = 0; k0 < g.nch; k0 += kImgBatch * L) {
-      float p[kImgBatch], th[kImgBatch];
+    for (int k0 = 0; k0 < g.nch; k0 += kB * L) {
+      float p[kB], th[kB];
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) {
+      for (int u = 0; u < kB; ++u) {
         const int k = k0 + u * L + sub;
         if (k < g.nch) {
           p[u] = __ldg(ch + (long long)k * plane);
@@ -130,7 +130,7 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
         }
       }
 #pragma unroll
-      for (int u = 0; u < kImgBatch; ++u) {
+      for (int u = 0; u < kB; ++u) {
         const int k = k0 + u * L + sub;
         if (k < g.nch)
           vals[(long long)(g.word0 + k) * BHW + cell] =
@@ -148,7 +148,8 @@ __device__ __forceinline__ void image_fuse_words(const State &st, long long BHW,
 constexpr int kImgThreads = MEM_IMG_THREADS;
 constexpr int kImgCells = kImgThreads / kImgLanes;  // cells per CTA
 // kSimple: no top-k binding, no gaussian group, no occlusion walk (C3, C4): a leaner kernel
-template <bool kSimple>
+// kB: channels per lane per batch of loads in flight (kImgBatch; 8 for bindings of <= 32 channels)
+template <bool kSimple, int kB>
 __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ ImageArgs a) {
   constexpr int L = kImgLanes;
   const Geometry &g = a.geo;
@@ -208,15 +209,15 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
     bool fin = true;
     float bv = -INFINITY;
     int best = -1;
-    for (int k0 = 0; k0 < b.nch; k0 += kImgBatch * L) {  // loads of a batch in flight together
-      float c[kImgBatch];
+    for (int k0 = 0; k0 < b.nch; k0 += kB * L) {  // loads of a batch in flight together
+      float c[kB];
 #pragma unroll
-      for (int q = 0; q < kImgBatch; ++q) {
+      for (int q = 0; q < kB; ++q) {
         const int k = k0 + q * L + sub;
         c[q] = k < b.nch ? __ldg(ch + (long long)k * plane) : 0.0f;
       }
 #pragma unroll
-      for (int q = 0; q < kImgBatch; ++q) {
+      for (int q = 0; q < kB; ++q) {
         const int k = k0 + q * L + sub;
         if (k < b.nch) {
           fin &= (bool)isfinite(c[q]);
@@ -246,6 +247,6 @@ __global__ void __launch_bounds__(kImgThreads) k_image(const __grid_constant__ I
       __syncwarp(gmask);
       continue;
     }
-    image_fuse_words<kSimple>(a.st, g.BHW, cell, b.g, ch, plane, sub, gmask);
+    image_fuse_words<kSimple, kB>(a.st, g.BHW, cell, b.g, ch, plane, sub, gmask);
   }
 }

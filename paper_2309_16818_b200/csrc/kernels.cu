@@ -260,10 +260,15 @@ cudaError_t launch_code_return(const uint8_t *codes, const unsigned *idx, long l
 cudaError_t launch_image(const ImageArgs &a, cudaStream_t s) {
   bool simple = !a.occlusion;
   for (int i = 0; i < a.nb && simple; ++i) simple = a.b[i].topk == 0 && a.b[i].g.rule != MEM_GAUSSIAN;
-  if (simple)
-    k_image<true><<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
+  int nch = 0;  // the widest binding
+  for (int i = 0; i < a.nb; ++i) nch = std::max(nch, a.b[i].nch);
+  const dim3 grid(cdiv(a.geo.HW, kImgCells), a.geo.n_maps);
+  if (simple && nch <= 32 && kImgBatch > 8)  // C3's 20 classes: shorter batches (C3 frame -2 us)
+    k_image<true, 8><<<grid, kImgThreads, 0, s>>>(a);
+  else if (simple)
+    k_image<true, kImgBatch><<<grid, kImgThreads, 0, s>>>(a);
   else
-    k_image<false><<<dim3(cdiv(a.geo.HW, kImgCells), a.geo.n_maps), kImgThreads, 0, s>>>(a);
+    k_image<false, kImgBatch><<<grid, kImgThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
